@@ -1,0 +1,321 @@
+"""WIPES oracle — TEST INFRASTRUCTURE ONLY.
+
+A plain, slow, double-precision CPU implementation of the WIPES rasterizer
+(arXiv 2508.12615) used to prove the CUDA path correct. Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package. The product package
+``paper_2508_12615_b200`` never imports it and shares no code with it.
+
+The arithmetic lives in ``oracle/oracle.cpp`` (see its header for the paper
+passages each function follows); this module only builds it with gcc
+(``-O2 -fopenmp -ffp-contract=off -fno-fast-math``) and marshals numpy arrays.
+
+Parity status: pinned by ``tests/test_oracle_*.py`` (closed forms, invariants,
+finite differences, DFT, brute-force compositing). The exact z-integration
+mode (``exact_proj=1``) is pinned only by 1-D quadrature of its kernel value;
+its chain rule is not implemented ("parity unpinned" for exact-mode gradients).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+GCC_FLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+             "-shared", "-std=c++17"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.cpp -> liboracle.so (idempotent)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", *GCC_FLAGS, _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class ora_cfg(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tile", C.c_int32),
+                ("prim3d", C.c_int32), ("alpha_blend", C.c_int32), ("cov2", C.c_int32),
+                ("extent", C.c_int32), ("ewa_clamp", C.c_int32), ("exact_proj", C.c_int32),
+                ("use_rect", C.c_int32),
+                ("alpha_min", C.c_double), ("alpha_max", C.c_double), ("T_min", C.c_double),
+                ("dilation", C.c_double), ("cov_eps", C.c_double), ("det_min", C.c_double),
+                ("bg", C.c_double * 3)]
+
+
+class ora_cam(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("t", C.c_double * 3), ("fx", C.c_double),
+                ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("near_z", C.c_double), ("far_z", C.c_double)]
+
+
+COV_MODES = {"sigma": 0, "cholesky": 1, "rs": 2}
+
+
+@dataclass
+class Cfg:
+    """Oracle configuration. Constants are float32-rounded where the CUDA path
+    receives float32 (so both sides decide with the same threshold values)."""
+    width: int
+    height: int
+    tile: int = 16
+    prim3d: bool = False
+    alpha_blend: bool = False
+    cov2: str = "sigma"
+    extent: str = "opacity"      # or "sigma3"
+    ewa_clamp: bool = True
+    exact_proj: bool = False
+    use_rect: bool = False
+    alpha_min: float = float(np.float32(1.0 / 255.0))
+    alpha_max: float = float(np.float32(0.99))
+    T_min: float = float(np.float32(1e-4))
+    dilation: float = 0.0
+    cov_eps: float = 0.0
+    det_min: float = float(np.float32(1e-12))
+    bg: tuple = (0.0, 0.0, 0.0)
+
+    def c(self) -> ora_cfg:
+        return ora_cfg(self.width, self.height, self.tile, int(self.prim3d),
+                       int(self.alpha_blend), COV_MODES[self.cov2],
+                       0 if self.extent == "opacity" else 1, int(self.ewa_clamp),
+                       int(self.exact_proj), int(self.use_rect),
+                       self.alpha_min, self.alpha_max, self.T_min, self.dilation,
+                       self.cov_eps, self.det_min, (C.c_double * 3)(*self.bg))
+
+
+P_FIELDS = ["mux", "muy", "a", "b", "c", "fx", "fy", "phi", "beta", "cr", "cg", "cb",
+            "alpha", "depth", "sxx", "sxy", "syy", "rmargin", "rx", "ry"]
+G_FIELDS = ["mux", "muy", "a", "b", "c", "fx", "fy", "phi", "beta", "cr", "cg", "cb", "alpha"]
+NP_ = len(P_FIELDS)
+NG_ = len(G_FIELDS)
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.ora_bin.restype = C.c_int64
+        assert _lib.ora_record_width() == NP_ and _lib.ora_grad_width() == NG_
+    return _lib
+
+
+def _d(a):
+    if a is None:
+        return None
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def cams_c(cams):
+    arr = (ora_cam * len(cams))()
+    for k, cm in enumerate(cams):
+        arr[k].R = (C.c_double * 9)(*np.asarray(cm["R"], np.float64).reshape(9))
+        arr[k].t = (C.c_double * 3)(*np.asarray(cm["t"], np.float64).reshape(3))
+        for nm in ("fx", "fy", "cx", "cy"):
+            setattr(arr[k], nm, float(cm[nm]))
+        arr[k].near_z = float(cm.get("near", 0.01))
+        arr[k].far_z = float(cm.get("far", 100.0))
+    return arr
+
+
+@dataclass
+class Projected:
+    N: int
+    B: int
+    flag: np.ndarray
+    rect: np.ndarray
+    count: np.ndarray
+    keylo: np.ndarray
+    rec: np.ndarray
+
+    def field(self, name):
+        return self.rec[:, P_FIELDS.index(name)]
+
+
+def project2d(cfg: Cfg, p: dict) -> Projected:
+    """O1 — 2D preprocess of parameter dict p (mean, cov, freq, [phase], color,
+    opacity, [depth])."""
+    N = int(np.asarray(p["mean"]).shape[0])
+    mean, cov, freq = _d(p["mean"]), _d(p["cov"]), _d(p["freq"])
+    phase, color, op = _d(p.get("phase")), _d(p["color"]), _d(p["opacity"])
+    depth = _d(p.get("depth"))
+    flag = np.zeros(N, np.int32)
+    rect = np.zeros((N, 4), np.int32)
+    count = np.zeros(N, np.int32)
+    keylo = np.zeros(N, np.uint32)
+    rec = np.zeros((N, NP_), np.float64)
+    cf = cfg.c()
+    lib().ora_project2d(C.byref(cf), C.c_int64(N), _p(mean), _p(cov), _p(freq), _p(phase),
+                        _p(color), _p(op), _p(depth), _p(flag), _p(rect), _p(count),
+                        _p(keylo), _p(rec))
+    return Projected(N, 1, flag, rect, count, keylo, rec)
+
+
+def project3d(cfg: Cfg, p: dict, cams, view_stride: int = 0) -> Projected:
+    """O2 — 3D preprocess for B cameras. view_stride (in primitives): 0 = one
+    shared parameter set, N = per-view parameter sets (6D)."""
+    B = len(cams)
+    mean = _d(p["mean"]).reshape(-1, 3)
+    N = mean.shape[0] if view_stride == 0 else int(view_stride)
+    scale, quat, freq = _d(p["scale"]), _d(p["quat"]), _d(p["freq"])
+    phase, color, op = _d(p.get("phase")), _d(p["color"]), _d(p["opacity"])
+    flag = np.zeros(B * N, np.int32)
+    rect = np.zeros((B * N, 4), np.int32)
+    count = np.zeros(B * N, np.int32)
+    keylo = np.zeros(B * N, np.uint32)
+    rec = np.zeros((B * N, NP_), np.float64)
+    cf = cfg.c()
+    cc = cams_c(cams)
+    lib().ora_project3d(C.byref(cf), C.c_int64(N), C.c_int32(B), cc, _p(mean), _p(scale),
+                        _p(quat), _p(freq), _p(phase), _p(color), _p(op),
+                        C.c_int64(view_stride), _p(flag), _p(rect), _p(count), _p(keylo),
+                        _p(rec))
+    return Projected(N, B, flag, rect, count, keylo, rec)
+
+
+def bin_sort(cfg: Cfg, pr: Projected):
+    """O6 — offsets, sorted (key, value) pairs and per-tile CSR offsets."""
+    B, N = pr.B, pr.N
+    GX = -(-cfg.width // cfg.tile)
+    GY = -(-cfg.height // cfg.tile)
+    offsets = np.zeros(B * N, np.int64)
+    total = int(lib().ora_bin(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), _p(pr.rect),
+                              _p(pr.count), _p(pr.keylo), _p(offsets), None, None, None,
+                              C.c_int64(0)))
+    keys = np.zeros(max(total, 1), np.uint64)
+    vals = np.zeros(max(total, 1), np.uint32)
+    toff = np.zeros(B * GX * GY + 1, np.int64)
+    lib().ora_bin(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), _p(pr.rect), _p(pr.count),
+                  _p(pr.keylo), _p(offsets), _p(keys), _p(vals), _p(toff),
+                  C.c_int64(total))
+    return dict(offsets=offsets, keys=keys[:total], vals=vals[:total], tile_offsets=toff,
+                total=total)
+
+
+def render(cfg: Cfg, pr: Projected, pix=None, dLdC=None, nthreads: int = 0):
+    """O3-O5 — brute-force render of the listed pixels (flat ids v*H*W+y*W+x;
+    None = all pixels of all views). Returns dict(color [npix,3], T, margin,
+    ncomp, rgrad [B*N, 13] if dLdC given (dLdC is [npix, 3]))."""
+    B, N = pr.B, pr.N
+    if pix is not None:
+        pix = np.ascontiguousarray(np.asarray(pix, np.int64))
+        npix = pix.shape[0]
+    else:
+        npix = B * cfg.height * cfg.width
+    color = np.zeros((npix, 3), np.float64)
+    T = np.zeros(npix, np.float64)
+    margin = np.zeros(npix, np.float64)
+    ncomp = np.zeros(npix, np.int32)
+    rgrad = None
+    if dLdC is not None:
+        dLdC = _d(dLdC).reshape(npix, 3)
+        rgrad = np.zeros((B * N, NG_), np.float64)
+    rec = np.ascontiguousarray(pr.rec)
+    lib().ora_render(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), _p(rec), _p(pr.flag),
+                     _p(pr.rect), _p(pr.keylo), C.c_int64(npix), _p(pix), _p(color), _p(T),
+                     _p(margin), _p(ncomp), _p(dLdC), _p(rgrad), C.c_int32(nthreads))
+    return dict(color=color, T=T, margin=margin, ncomp=ncomp, rgrad=rgrad)
+
+
+def image_pixels_to_planar(color, B, H, W):
+    """[B*H*W, 3] -> [B, 3, H, W]"""
+    return np.ascontiguousarray(color.reshape(B, H, W, 3).transpose(0, 3, 1, 2))
+
+
+def planar_to_pixels(img):
+    """[B, 3, H, W] -> [B*H*W, 3]"""
+    img = np.asarray(img)
+    return np.ascontiguousarray(img.transpose(0, 2, 3, 1).reshape(-1, 3))
+
+
+def chain2d(cfg: Cfg, p: dict, pr: Projected, rgrad):
+    N = pr.N
+    out = {k: np.zeros(s, np.float64) for k, s in
+           [("mean", (N, 2)), ("cov", (N, 3)), ("freq", (N, 2)), ("phase", (N,)),
+            ("color", (N, 3)), ("opacity", (N,))]}
+    lib().ora_chain2d(C.byref(cfg.c()), C.c_int64(N), _p(_d(p["cov"])), _p(pr.flag),
+                      _p(np.ascontiguousarray(pr.rec)), _p(_d(rgrad)), _p(out["mean"]),
+                      _p(out["cov"]), _p(out["freq"]), _p(out["phase"]), _p(out["color"]),
+                      _p(out["opacity"]))
+    return out
+
+
+def chain3d(cfg: Cfg, p: dict, cams, pr: Projected, rgrad, view_stride: int = 0):
+    N, B = pr.N, pr.B
+    NP = N if view_stride == 0 else B * N
+    out = {k: np.zeros(s, np.float64) for k, s in
+           [("mean", (NP, 3)), ("scale", (NP, 3)), ("quat", (NP, 4)), ("freq", (NP, 3)),
+            ("phase", (NP,)), ("color", (NP, 3)), ("opacity", (NP,))]}
+    lib().ora_chain3d(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), cams_c(cams),
+                      _p(_d(p["mean"])), _p(_d(p["scale"])), _p(_d(p["quat"])),
+                      _p(_d(p["freq"])), _p(pr.flag), _p(np.ascontiguousarray(pr.rec)),
+                      _p(_d(rgrad)), C.c_int64(view_stride), _p(out["mean"]),
+                      _p(out["scale"]), _p(out["quat"]), _p(out["freq"]), _p(out["phase"]),
+                      _p(out["color"]), _p(out["opacity"]))
+    return out
+
+
+# ---- small scalar helpers (wrappers of the C kernel evaluators) ------------
+def eval_wavelet2(conic, f, phi, beta, dx, dy) -> float:
+    L = lib()
+    L.ora_eval_wavelet2.restype = C.c_double
+    c = (C.c_double * 3)(*conic)
+    ff = (C.c_double * 2)(*f)
+    return L.ora_eval_wavelet2(c, ff, C.c_double(phi), C.c_double(beta), C.c_double(dx),
+                               C.c_double(dy))
+
+
+def eval_gaussian2(conic, dx, dy) -> float:
+    L = lib()
+    L.ora_eval_gaussian2.restype = C.c_double
+    c = (C.c_double * 3)(*conic)
+    return L.ora_eval_gaussian2(c, C.c_double(dx), C.c_double(dy))
+
+
+def eval_wavelet3(inv_cov, f, phi, beta, d) -> float:
+    L = lib()
+    L.ora_eval_wavelet3.restype = C.c_double
+    ic = (C.c_double * 9)(*np.asarray(inv_cov, np.float64).reshape(9))
+    ff = (C.c_double * 3)(*f)
+    dd = (C.c_double * 3)(*d)
+    return L.ora_eval_wavelet3(ic, ff, C.c_double(phi), C.c_double(beta), dd)
+
+
+def cov2d(mode: str, params) -> np.ndarray:
+    out = np.zeros(3, np.float64)
+    pp = _d(params)
+    lib().ora_cov2d(C.c_int32(COV_MODES[mode]), _p(pp), _p(out))
+    return out
+
+
+# ---- whole-pipeline conveniences used by tests and the CPU baseline --------
+def forward(cfg: Cfg, p: dict, cams=None, view_stride=0, pix=None, dLdC=None, nthreads=0):
+    pr = project3d(cfg, p, cams, view_stride) if cfg.prim3d else project2d(cfg, p)
+    out = render(cfg, pr, pix=pix, dLdC=dLdC, nthreads=nthreads)
+    out["proj"] = pr
+    return out
+
+
+def forward_backward(cfg: Cfg, p: dict, dLdC, cams=None, view_stride=0, pix=None,
+                     nthreads=0):
+    out = forward(cfg, p, cams, view_stride, pix=pix, dLdC=dLdC, nthreads=nthreads)
+    pr = out["proj"]
+    if cfg.prim3d:
+        out["grads"] = chain3d(cfg, p, cams, pr, out["rgrad"], view_stride)
+    else:
+        out["grads"] = chain2d(cfg, p, pr, out["rgrad"])
+    return out
