@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""WIPES rasterizer benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric (BASELINE.json): fwd+bwd iters/s (and render FPS) of the WIPES
+rasterizer. A step = one full pass of the hot path over one batch of synthetic
+input: preprocess -> count/scan -> duplicate -> radix sort -> tile ranges ->
+render forward -> render backward -> preprocess backward (all SURVEY §8(a)
+rows), every kernel ours (libwipes.so through the C ABI).
+
+Default workload: configs[1] (C2) — Kodak-shaped 768x512 image, 70k 2D wavelet
+primitives, weighted sum (Eq. 4). Under torchrun each rank fits
+its own Kodak-shaped image (independent problems: weak scaling, no data-path
+collective). `--config c3` runs the 3D static NVS batch (8 x 1080p views,
+1M primitives, alpha blending) with views sharded across ranks and the
+per-primitive gradients summed by an NCCL all_reduce (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FWD_WORK = {"sum": (9, 2), "alpha": (13, 2)}     # (+FP32, MUFU) per in-ellipse pair
+BWD_WORK = {"sum": (48, 3), "alpha": (66, 4)}
+CAND_FP32 = 7                                      # FP32 per tile-method candidate test
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-pixels", type=int, default=4096)
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(2)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.strip().split(", ") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows if len(r) > 8 for k in range(4)
+                          if r[5 + k].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU ---
+def cpu_oracle_sample(c, npix, seed):
+    """The oracle as it stands (double-precision brute force over ALL primitives
+    per pixel, no tiling) on a bounded random pixel sample of the workload;
+    returns (seconds for the sample, extrapolation factor, cores)."""
+    import oracle
+    H, W, B = c["H"], c["W"], c.get("B", 1)
+    rng = np.random.default_rng(seed)
+    npix = min(npix, B * H * W)
+    pix = np.sort(rng.choice(B * H * W, npix, replace=False))
+    dL = rng.uniform(-1, 1, (npix, 3))
+    kind = c["kind"]
+    cfg = oracle.Cfg(width=W, height=H, prim3d=kind != "2d", alpha_blend=c["blend"] == "alpha",
+                     dilation=float(np.float32(0.3)) if kind != "2d" else 0.0)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.forward_backward(cfg, c["params"], dL, cams=c.get("cams"),
+                            view_stride=c.get("view_stride", 0), pix=pix, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return dt, (B * H * W) / npix, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host
+    cores, same config/metric/unit; each step is a bounded pixel sample of the
+    workload, extrapolated to the full frame."""
+    if rank != 0:
+        return
+    from paper_2508_12615_b200 import gen
+    c = gen.make_config(args.config, seed=args.seed)
+    per = max(64, args.cpu_pixels // 4)
+    times = []
+    cores = os.cpu_count() or 1
+    for s in range(args.warmup + args.steps):
+        dt, fac, cores = cpu_oracle_sample(c, per, seed=1000 + s)
+        if s >= args.warmup:
+            times.append(dt * fac)
+    ms = 1e3 * statistics.mean(times)
+    value = 1e3 / ms
+    sample = (f"{per} random pixels of {c['B'] if 'B' in c else 1}x{c['H']}x{c['W']} per step, "
+              f"fwd+bwd against all {c['N']} primitives, extrapolated linearly to the full frame")
+    line = {"impl": "reference", "metric": "fwd+bwd iters/s", "value": value, "unit": "iters/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.config}: {c['desc']}"},
+            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU ---
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_2508_12615_b200 import abi, build, gen
+    from paper_2508_12615_b200.raster import Rasterizer
+    from paper_2508_12615_b200 import dist as wdist
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peaks, peak_src = load_peaks()
+
+    name = args.config
+    base = gen.CONFIGS[name]
+    shared = base["kind"] == "3d"
+    # weak scaling: every rank its own independent problem (different seed);
+    # 3D batch: one scene, views sharded across ranks + gradient all_reduce.
+    c = gen.make_config(name, seed=args.seed + (0 if shared else rank))
+    H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+    blend = c["blend"]
+    cams = c["cams"]
+    vs = c["view_stride"]
+    my_views = list(range(rank, B, world)) if shared else None
+    if shared:
+        cams = [cams[v] for v in my_views]
+    Bl = len(cams) if cams is not None else 1
+    r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev)
+    params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
+    if c["kind"] == "6d":
+        pass
+    dL_host = gen.gen_dLdC(Bl, H, W, seed=args.seed + rank)
+    dL = torch.from_numpy(dL_host).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    grads = {k: torch.empty_like(v) for k, v in params.items() if k not in ("depth",)}
+    flat = None
+    if shared and world > 1:
+        flat = wdist.GradBucket(grads)
+
+    def step(ev0=None, ev1=None, ev2=None, sync=False):
+        if ev0 is not None:
+            ev0.record(stream)
+        r.preprocess(params, cams, vs, sync=sync)
+        r.bin_sort()
+        r.render()
+        if ev1 is not None:
+            ev1.record(stream)
+        r.backward(dL, grads)
+        if flat is not None:
+            flat.all_reduce()
+        if ev2 is not None:
+            ev2.record(stream)
+
+    # first call sizes the workspace (one host sync), then warm-up
+    step(sync=True)
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    n_tot, over = r.check_overflow()
+    assert not over, "capacity overflow"
+
+    sampler = ClockSampler(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    abi.timing_enable(True)
+    l0 = abi.launch_count()
+    for k in range(args.steps):
+        flush.zero_()
+        step(*evs[k])
+    torch.cuda.synchronize()
+    launches = abi.launch_count() - l0
+    abi.timing_enable(False)
+    kt = abi.timing_collect()
+    clocks = sampler.stop()
+    n_tot2, over = r.check_overflow()
+    assert not over
+    fwd_ms = [a.elapsed_time(b) for a, b, _ in evs]
+    tot_ms = [a.elapsed_time(c_) for a, _, c_ in evs]
+    my_total = sum(tot_ms)
+    my_fwd = sum(fwd_ms)
+    t = torch.tensor([my_total, my_fwd], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, total_fwd_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    units = world * args.steps if not shared else args.steps   # iterations (problems) processed
+    value = units / (total_ms / 1e3)
+    render_fps = (world * args.steps * Bl if not shared else args.steps * B) / (total_fwd_ms / 1e3)
+
+    # ---- e2e: same metric through the public API with HOST buffers --------
+    host_params = {k: torch.from_numpy(v).pin_memory() for k, v in c["params"].items()}
+    host_dL = torch.from_numpy(dL_host).pin_memory()
+    host_grads = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in grads.items()}
+    h2d = sum(v.numel() * 4 for v in host_params.values()) + host_dL.numel() * 4
+    d2h = sum(v.numel() * 4 for v in host_grads.values())
+    e2e_ms = []
+    for k in range(max(3, args.steps // 2) + 2):
+        flush.zero_()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for kk, v in host_params.items():
+            params[kk].copy_(v, non_blocking=True)
+        dL.copy_(host_dL, non_blocking=True)
+        step()
+        for kk, v in grads.items():
+            host_grads[kk].copy_(v, non_blocking=True)
+        b_.record(stream)
+        b_.synchronize()
+        if k >= 2:
+            e2e_ms.append(a.elapsed_time(b_))
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = (world if not shared else 1) * len(e2e_ms) / (float(te[0]) / 1e3)
+
+    # ---- roofline of the dominant render kernel -----------------------------
+    n_cand, n_ell, n_con = r.render_stats()
+    clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    p32, psfu = 148 * 128 * clk, 148 * 16 * clk
+    fwd_t = kt["render_fwd"][0] / max(kt["render_fwd"][1], 1) / 1e3
+    bwd_t = kt["render_bwd"][0] / max(kt["render_bwd"][1], 1) / 1e3
+    dom = "render_bwd" if kt["render_bwd"][0] >= kt["render_fwd"][0] else "render_fwd"
+    E, m = (BWD_WORK if dom == "render_bwd" else FWD_WORK)[blend]
+    tdom = bwd_t if dom == "render_bwd" else fwd_t
+    launches_dom = kt[dom][1] / args.steps
+    work32 = (CAND_FP32 * n_cand + E * n_ell) / launches_dom if launches_dom else 0
+    worksfu = m * n_ell / launches_dom if launches_dom else 0
+    f32frac = work32 / tdom / p32 if tdom else 0
+    sfufrac = worksfu / tdom / psfu if tdom else 0
+    pipe = "fp32" if f32frac >= sfufrac else "mufu"
+    useful32 = (CAND_FP32 + E) * n_ell / max(launches_dom, 1)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{name}:{dom}")
+    roof = {"bound": "alu", "kernel": dom, "pipe": pipe,
+            "achieved": (work32 if pipe == "fp32" else worksfu) / tdom / 1e9,
+            "peak": (p32 if pipe == "fp32" else psfu) / 1e9,
+            "unit": f"G{pipe} instr/s (tile-method algorithmic work, {peak_src} clock "
+                    f"{clk / 1e6:.0f} MHz)",
+            "frac": max(f32frac, sfufrac), "frac_fp32": f32frac, "frac_mufu": sfufrac,
+            "frac_useful_fp32": useful32 / tdom / p32 if tdom else 0,
+            "kernel_ms": tdom * 1e3, "traffic": traffic,
+            "pairs": {"tile_candidates": n_cand, "in_ellipse": n_ell, "contributing": n_con}}
+
+    line = {"metric": "fwd+bwd iters/s", "value": value, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong" if shared else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{name}: {c['desc']}", "H": H, "W": W, "N": N, "views": B,
+                       "blend": blend, "dup": int(n_tot2),
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "parallelism": (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
+                                       "per-primitive gradients") if shared else
+                                      f"replicas: {world} independent image(s), one per GPU"},
+            "render_fps": render_fps,
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
+            "roofline": roof,
+            "paper_context": "render FPS on one A6000: Kodak 1708-1779 (Table 1, PAPER.md:148-149); "
+                             "Mip-NeRF360 95.7 (Table 2, PAPER.md:239)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, fac, cores = cpu_oracle_sample(c, args.cpu_pixels, seed=123)
+        line["cpu_baseline"] = {"value": 1.0 / (dt * fac), "unit": "iters/s", "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"{args.cpu_pixels} random pixels, fwd+bwd against all "
+                                          f"{N} primitives ({dt:.1f} s), extrapolated x{fac:.0f} "
+                                          "to the full frame"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/* ==========================================================================
+ * include/wipes.h — C ABI of the B200-native WIPES rasterizer (ABI version 1)
+ * ==========================================================================
+ * WIPES: Wavelet-based vIsual PrimitivES, arXiv 2508.12615 (/root/reference/
+ * PAPER.md). This library implements the paper's one data-parallel hot path,
+ * the "fast, differentiable rasterizer" (Sec. 1; PAPER.md:215,
+ * Sec. 4.1; Sec. 5): per-primitive preprocess, tile binning
+ * with a (tile | depth) key radix sort, per-pixel evaluation of the wavelet
+ * primitive W = G * 1/2 [1 + beta cos(f.(x - mu) + phi)] (PAPER.md:187-191,
+ * Eq. 6; beta, phi: DESIGN.md R1), accumulated as the weighted sum of Eq. 4
+ * or front-to-back alpha blending of Eq. 3, and
+ * analytic gradients of every primitive parameter.
+ *
+ * Conventions for every entry point
+ *  - Pointers are DEVICE pointers unless marked (host). Arrays are dense,
+ *    row-major, float32 unless noted, and 16-byte aligned (else WIPES_EINVAL).
+ *  - The CALLER owns every buffer. The library never allocates or frees device
+ *    memory, keeps no state between calls outside `ws`, and launches all work
+ *    on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - It never synchronises, except (a) wipes_preprocess when `n_dup` is
+ *    non-NULL and (b) wipes_check_overflow / wipes_timing_collect.
+ *  - Status codes only; nothing is thrown across the ABI. Arguments are
+ *    validated BEFORE any launch. CUDA launch failures return WIPES_ECUDA with
+ *    the detail in wipes_last_error() (thread-local).
+ *  - Degenerate primitives are NOT errors ("signals a degenerate
+ *    primitive to be skipped"): they are culled — no tiles, no contribution,
+ *    zero gradient — and reported in cull_flags: 1 = camera depth outside
+ *    [near, far]; 2 = det(Sigma') < det_min or non-positive variance; 3 =
+ *    opacity < alpha_min; 4 = off-screen (no tile); 5 = non-finite input.
+ *  - Reentrant: calls with distinct workspaces may run concurrently on
+ *    distinct streams (kernel timing, when enabled, is process-global).
+ * ========================================================================== */
+#ifndef WIPES_H
+#define WIPES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WIPES_ABI_VERSION 1
+#define WIPES_MAX_CAMERAS_PER_LAUNCH 128 /* more views are processed in chunks */
+#define WIPES_RECORD_GRADS 13            /* see wipes_render_bwd */
+
+typedef enum {
+  WIPES_OK = 0,
+  WIPES_EINVAL = 1,       /* bad argument; nothing launched                    */
+  WIPES_ECAPACITY = 2,    /* dup total > dup_capacity (known on the host)      */
+  WIPES_ECUDA = 3,        /* a CUDA call failed; see wipes_last_error()        */
+  WIPES_EUNSUPPORTED = 4  /* a mode this build does not implement              */
+} wipes_status;
+
+enum { WIPES_PRIM_2D = 0, WIPES_PRIM_3D = 1 };
+/* Eq. 4 weighted sum / Eq. 3 alpha blending */
+enum { WIPES_BLEND_SUM = 0, WIPES_BLEND_ALPHA = 1 };
+/* 2D covariance parameterisations ("Cholesky and RS") */
+enum { WIPES_COV2_SIGMA = 0, WIPES_COV2_CHOLESKY = 1, WIPES_COV2_RS = 2 };
+/* Eq. 7 as written (beta = 1) / exact z-marginal (NEXT-1) */
+enum { WIPES_PROJ_PAPER = 0, WIPES_PROJ_EXACT = 1 };
+/* tile extent: opacity-aware AABB (R7, default) / SPEC's 3-sigma square */
+enum { WIPES_EXTENT_OPACITY = 0, WIPES_EXTENT_SIGMA3 = 1 };
+
+/* Pinhole camera, (host) memory. World -> camera x_c = R x_w + t (R row-major),
+ * camera axes x right, y down, z forward (the ray-space z of PAPER.md:116-122);
+ * pixel (j, i) has centre (j + 0.5, i + 0.5) (R11). */
+typedef struct {
+  float R[9];
+  float t[3];
+  float fx, fy, cx, cy;   /* pixels */
+  float near_z, far_z;    /* primitives with z outside [near, far] are culled */
+} wipes_camera;
+
+typedef struct {
+  int32_t width, height;  /* pixels, each in [1, 16384]                        */
+  int32_t tile;           /* 8, 16 or 32 (default 16)                          */
+  int32_t prim;           /* WIPES_PRIM_*                                      */
+  int32_t blend;          /* WIPES_BLEND_*                                     */
+  int32_t cov2;           /* WIPES_COV2_* (2D only)                            */
+  int32_t proj;           /* WIPES_PROJ_* (3D only)                            */
+  int32_t extent;         /* WIPES_EXTENT_*                                    */
+  float alpha_min;        /* skip contributions with alpha*W < alpha_min (1/255) */
+  float alpha_max;        /* ALPHA: clamp a = min(alpha_max, alpha*W) (0.99)   */
+  float T_min;            /* ALPHA: stop when T (1 - a) < T_min (1e-4)         */
+  float dilation;         /* added to diag(Sigma') (0.3 px^2 in 3D, 0 in 2D)   */
+  float cov_eps;          /* added to diag(Sigma') too (default 0)             */
+  float det_min;          /* cull if det(Sigma') < det_min (1e-12)             */
+  int32_t ewa_clamp;      /* 1: clamp x/z, y/z at 1.3 x half-FOV inside J      */
+  float background[3];    /* ALPHA only                                        */
+  int32_t deterministic;  /* reserved (must be 0 in ABI v1)                    */
+} wipes_config;
+
+/* Primitive parameters (device). Shapes, with N primitives:
+ *   2D: mean [N,2] px, cov [N,3] = (sxx, sxy, syy) | (l1, l2, l3) Cholesky
+ *       L = [[l1,0],[l2,l3]] | (theta, sx, sy) RS, freq [N,2] rad/px,
+ *       depth [N] (ALPHA only: the compositing order key).
+ *   3D: mean [N,3], scale [N,3] (activated), quat [N,4] (w,x,y,z; normalised
+ *       inside), freq [N,3] rad/world-unit.
+ *   both: phase [N] rad (NULL = 0), color [N,3], opacity [N] (activated).
+ * view_stride (3D, counted in PRIMITIVES): view v reads row v*view_stride + i;
+ * 0 = one shared set for all B views (static scene), N = per-view sets
+ * (6D per-frame parameters, Eq. 8). Gradients are w.r.t. these
+ * activated values; activations belong to the caller's autograd. */
+typedef struct {
+  const float *mean, *cov, *scale, *quat, *freq, *phase, *color, *opacity, *depth;
+  int64_t view_stride;
+} wipes_params;
+
+/* Gradient outputs, same shapes as wipes_params (rows [B*N] when view_stride
+ * = N). Overwritten (never accumulated into). NULL = group not written. */
+typedef struct {
+  float *mean, *cov, *scale, *quat, *freq, *phase, *color, *opacity;
+} wipes_grads;
+
+/* Bytes of opaque workspace for N primitives, B views and room for
+ * dup_capacity (view, primitive, tile) intersections. */
+size_t wipes_workspace_bytes(const wipes_config* cfg, int64_t N, int32_t B,
+                             int64_t dup_capacity);
+
+/* Step 1: per (view, primitive) preprocess — covariance
+ * (2D modes / 3D EWA projection PAPER.md:122 + frequency transform :212),
+ * conic, opacity-aware extent, tile rect (FP64 decisions, DESIGN.md "Pinned
+ * preprocess arithmetic"), 64-byte render record, depth key; then the
+ * exclusive scan of tile counts. cams: (host) [B] for 3D, NULL for 2D (B must
+ * be 1). n_dup: (host) out, total intersections — when non-NULL the call
+ * synchronises `stream` once; NULL keeps it sync-free (capacity protocol).
+ * cull_flags: [B*N] uint8 out or NULL. */
+wipes_status wipes_preprocess(const wipes_config* cfg, const wipes_params* params,
+                              int64_t N, const wipes_camera* cams, int32_t B,
+                              void* ws, size_t ws_bytes, int64_t dup_capacity,
+                              int64_t* n_dup, uint8_t* cull_flags, void* stream);
+
+/* Step 2 (a4-a6): duplicate each primitive once per overlapped tile under the
+ * key ((view*T + tile) << 32) | depth_bits (depth_bits = 0 in SUM mode),
+ * stable LSD radix sort of the significant key bits, per-tile CSR ranges.
+ * Optional copies for parity tests: keys_out/vals_out [dup_capacity],
+ * tile_offsets_out [B*T + 1] int32 (T = ceil(W/tile) * ceil(H/tile)).
+ * If the total exceeds dup_capacity nothing past the capacity is written and
+ * a device overflow flag is set (see wipes_check_overflow). */
+wipes_status wipes_bin_sort(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                            size_t ws_bytes, int64_t dup_capacity, uint64_t* keys_out,
+                            uint32_t* vals_out, int32_t* tile_offsets_out, void* stream);
+
+/* Reads the device total and overflow flag; synchronises `stream`. */
+wipes_status wipes_check_overflow(const void* ws, size_t ws_bytes, int64_t* n_dup,
+                                  int32_t* overflowed, void* stream);
+
+/* Copies of the preprocess artefacts for parity tests (device outputs, each
+ * optional): rect [B*N,4] int32 (tx0, ty0, tx1, ty1), count [B*N] int32,
+ * offsets [B*N] int64 (exclusive scan), depth_key [B*N] uint32,
+ * records [B*N,16] float32 (the render record). */
+wipes_status wipes_get_preprocess(const wipes_config* cfg, int64_t N, int32_t B,
+                                  const void* ws, size_t ws_bytes, int64_t dup_capacity,
+                                  int32_t* rect, int32_t* count, int64_t* offsets,
+                                  uint32_t* depth_key, float* records, void* stream);
+
+/* Step 3 (a7/a8): render. image [B,3,H,W] (planar); ALPHA mode also writes
+ * T_final [B,H,W] and n_contrib [B,H,W] int32 (one past the tile-list index of
+ * the last composited entry), both needed by wipes_render_bwd. */
+wipes_status wipes_render_fwd(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                              size_t ws_bytes, int64_t dup_capacity, float* image,
+                              float* T_final, int32_t* n_contrib, void* stream);
+
+/* Step 4 (a9-a12): gradients of L given dL/dimage [B,3,H,W] w.r.t. every
+ * parameter group ("explicit gradients for all parameters"):
+ * per-pair analytic terms reduced per warp with shuffles, then one atomic per
+ * (warp, record, value) into the workspace's record gradients, then the
+ * preprocess chain rule (FP64) into `grads`. The same params/cams as the
+ * forward call must be passed. */
+wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* params,
+                              int64_t N, const wipes_camera* cams, int32_t B, void* ws,
+                              size_t ws_bytes, int64_t dup_capacity,
+                              const float* dL_dimage, const float* T_final,
+                              const int32_t* n_contrib, wipes_grads* grads, void* stream);
+
+/* Record-space gradients [B*N, 13] (float32) of the last wipes_render_bwd, for
+ * parity tests: d/d(mu'x, mu'y, conic a, b, c, f'x, f'y, phi, beta, c_r, c_g,
+ * c_b, alpha). */
+wipes_status wipes_get_record_grads(const wipes_config* cfg, int64_t N, int32_t B,
+                                    const void* ws, size_t ws_bytes, int64_t dup_capacity,
+                                    float* out, void* stream);
+
+/* Measurement only (not on the hot path): runs a counting variant of the
+ * forward render kernel over the workspace of the last preprocess/bin_sort
+ * and writes stats3 (device, 3 x uint64): [0] tile-method candidate pairs
+ * (tile-list entries x in-image pixels, up to each pixel's termination in
+ * ALPHA mode), [1] in-ellipse pairs (alpha*G >= alpha_min), [2] contributing
+ * pairs (alpha*W >= alpha_min; composited in ALPHA mode). These are the
+ * algorithmic work units of the render roofline. */
+wipes_status wipes_render_stats(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                                size_t ws_bytes, int64_t dup_capacity, uint64_t* stats3,
+                                void* stream);
+
+/* Instrumentation: per-kernel CUDA-event timing (process-global, not for use
+ * during graph capture) and a launch counter. */
+int          wipes_num_kernels(void);
+const char*  wipes_kernel_name(int kernel_id);
+void         wipes_timing_enable(int on);
+/* Synchronises on the recorded events; fills ms[k] (summed device time) and
+ * launches[k] per kernel id since the last collect, then resets. */
+wipes_status wipes_timing_collect(double* ms, int64_t* launches, int n);
+int64_t      wipes_launch_count(void);
+
+const char*  wipes_status_string(wipes_status s);
+const char*  wipes_last_error(void);
+int          wipes_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WIPES_H */

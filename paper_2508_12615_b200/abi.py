@@ -1,0 +1,233 @@
+"""Thin ctypes binding of libwipes.so (include/wipes.h) — argument marshalling only.
+
+Every step of the rasterizer runs in the CUDA kernels behind these calls;
+PyTorch only supplies device memory, the current stream and process groups.
+There is NO CPU fallback: if libwipes.so is missing or no CUDA device is
+present, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwipes.so")
+
+WIPES_OK, WIPES_EINVAL, WIPES_ECAPACITY, WIPES_ECUDA, WIPES_EUNSUPPORTED = range(5)
+PRIM = {"2d": 0, "3d": 1}
+BLEND = {"sum": 0, "alpha": 1}
+COV2 = {"sigma": 0, "cholesky": 1, "rs": 2}
+PROJ = {"paper": 0, "exact": 1}
+EXTENT = {"opacity": 0, "sigma3": 1}
+RECORD_GRADS = 13
+MAX_CAMS_PER_LAUNCH = 128
+
+
+class wipes_camera(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float),
+                ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("near_z", C.c_float), ("far_z", C.c_float)]
+
+
+class wipes_config(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tile", C.c_int32),
+                ("prim", C.c_int32), ("blend", C.c_int32), ("cov2", C.c_int32),
+                ("proj", C.c_int32), ("extent", C.c_int32),
+                ("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float),
+                ("dilation", C.c_float), ("cov_eps", C.c_float), ("det_min", C.c_float),
+                ("ewa_clamp", C.c_int32), ("background", C.c_float * 3),
+                ("deterministic", C.c_int32)]
+
+
+class wipes_params(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "cov", "scale", "quat", "freq", "phase",
+                                          "color", "opacity", "depth")] + \
+               [("view_stride", C.c_int64)]
+
+
+class wipes_grads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "cov", "scale", "quat", "freq", "phase",
+                                          "color", "opacity")]
+
+
+class WipesError(RuntimeError):
+    def __init__(self, status, where, detail):
+        super().__init__(f"{where}: {status_name(status)}: {detail}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libwipes.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libwipes.so not built at {LIB_PATH}: run "
+                           "`python -m paper_2508_12615_b200.build` (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+    P = C.POINTER
+    L.wipes_workspace_bytes.argtypes = [P(wipes_config), i64, i32, i64]
+    L.wipes_workspace_bytes.restype = sz
+    L.wipes_preprocess.argtypes = [P(wipes_config), P(wipes_params), i64, P(wipes_camera), i32,
+                                   vp, sz, i64, P(C.c_int64), vp, vp]
+    L.wipes_bin_sort.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp, vp]
+    L.wipes_check_overflow.argtypes = [vp, sz, P(C.c_int64), P(C.c_int32), vp]
+    L.wipes_get_preprocess.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp, vp,
+                                       vp, vp]
+    L.wipes_render_fwd.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp, vp]
+    L.wipes_render_bwd.argtypes = [P(wipes_config), P(wipes_params), i64, P(wipes_camera), i32,
+                                   vp, sz, i64, vp, vp, vp, P(wipes_grads), vp]
+    L.wipes_get_record_grads.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
+    L.wipes_render_stats.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
+    L.wipes_num_kernels.restype = C.c_int
+    L.wipes_kernel_name.argtypes = [C.c_int]
+    L.wipes_kernel_name.restype = C.c_char_p
+    L.wipes_timing_enable.argtypes = [C.c_int]
+    L.wipes_timing_collect.argtypes = [P(C.c_double), P(C.c_int64), C.c_int]
+    L.wipes_launch_count.restype = C.c_int64
+    L.wipes_status_string.argtypes = [C.c_int]
+    L.wipes_status_string.restype = C.c_char_p
+    L.wipes_last_error.restype = C.c_char_p
+    L.wipes_abi_version.restype = C.c_int
+    for fn in ("wipes_preprocess", "wipes_bin_sort", "wipes_check_overflow",
+               "wipes_get_preprocess", "wipes_render_fwd", "wipes_render_bwd",
+               "wipes_get_record_grads", "wipes_timing_collect", "wipes_render_stats"):
+        getattr(L, fn).restype = C.c_int
+    _lib = L
+    return L
+
+
+EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
+            "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
+            "wipes_render_bwd", "wipes_get_record_grads", "wipes_render_stats",
+            "wipes_num_kernels",
+            "wipes_kernel_name", "wipes_timing_enable", "wipes_timing_collect",
+            "wipes_launch_count", "wipes_status_string", "wipes_last_error",
+            "wipes_abi_version"]
+
+
+def status_name(s: int) -> str:
+    return lib().wipes_status_string(s).decode()
+
+
+def check(status: int, where: str):
+    if status != WIPES_OK:
+        raise WipesError(status, where, lib().wipes_last_error().decode())
+
+
+def make_config(width, height, tile=16, prim="2d", blend="sum", cov2="sigma", proj="paper",
+                extent="opacity", alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4,
+                dilation=None, cov_eps=0.0, det_min=1e-12, ewa_clamp=True,
+                background=(0.0, 0.0, 0.0), deterministic=0) -> wipes_config:
+    if dilation is None:
+        dilation = 0.3 if prim == "3d" else 0.0
+    return wipes_config(int(width), int(height), int(tile), PRIM[prim], BLEND[blend], COV2[cov2],
+                        PROJ[proj], EXTENT[extent], alpha_min, alpha_max, T_min, dilation,
+                        cov_eps, det_min, int(bool(ewa_clamp)), (C.c_float * 3)(*background),
+                        int(deterministic))
+
+
+def cameras(cams) -> "C.Array":
+    arr = (wipes_camera * max(len(cams), 1))()
+    for k, cm in enumerate(cams):
+        R = [float(x) for x in list(_flat(cm["R"]))]
+        t = [float(x) for x in list(_flat(cm["t"]))]
+        arr[k].R = (C.c_float * 9)(*R)
+        arr[k].t = (C.c_float * 3)(*t)
+        arr[k].fx, arr[k].fy = float(cm["fx"]), float(cm["fy"])
+        arr[k].cx, arr[k].cy = float(cm["cx"]), float(cm["cy"])
+        arr[k].near_z = float(cm.get("near", 0.01))
+        arr[k].far_z = float(cm.get("far", 100.0))
+    return arr
+
+
+def _flat(x):
+    try:
+        import numpy as np
+        return np.asarray(x, dtype=np.float64).reshape(-1)
+    except Exception:  # pragma: no cover
+        return x
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None passes NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+# ---- same-name wrappers: marshalling only --------------------------------
+def wipes_workspace_bytes(cfg, N, B, cap) -> int:
+    return int(lib().wipes_workspace_bytes(C.byref(cfg), N, B, cap))
+
+
+def wipes_preprocess(cfg, params, N, cams, B, ws, ws_bytes, cap, n_dup_out, cull_flags, stream):
+    n = C.c_int64(0)
+    st = lib().wipes_preprocess(C.byref(cfg), C.byref(params), N,
+                                cams if cams is not None else None, B, ws, ws_bytes, cap,
+                                C.byref(n) if n_dup_out else None, cull_flags, stream)
+    return st, n.value
+
+
+def wipes_bin_sort(cfg, N, B, ws, ws_bytes, cap, keys_out, vals_out, toff_out, stream):
+    return lib().wipes_bin_sort(C.byref(cfg), N, B, ws, ws_bytes, cap, keys_out, vals_out,
+                                toff_out, stream)
+
+
+def wipes_check_overflow(ws, ws_bytes, stream):
+    n, o = C.c_int64(0), C.c_int32(0)
+    st = lib().wipes_check_overflow(ws, ws_bytes, C.byref(n), C.byref(o), stream)
+    return st, n.value, o.value
+
+
+def wipes_get_preprocess(cfg, N, B, ws, ws_bytes, cap, rect, count, offsets, dkey, records,
+                         stream):
+    return lib().wipes_get_preprocess(C.byref(cfg), N, B, ws, ws_bytes, cap, rect, count,
+                                      offsets, dkey, records, stream)
+
+
+def wipes_render_fwd(cfg, N, B, ws, ws_bytes, cap, image, T_final, n_contrib, stream):
+    return lib().wipes_render_fwd(C.byref(cfg), N, B, ws, ws_bytes, cap, image, T_final,
+                                  n_contrib, stream)
+
+
+def wipes_render_bwd(cfg, params, N, cams, B, ws, ws_bytes, cap, dLdC, T_final, n_contrib,
+                     grads, stream):
+    return lib().wipes_render_bwd(C.byref(cfg), C.byref(params), N,
+                                  cams if cams is not None else None, B, ws, ws_bytes, cap,
+                                  dLdC, T_final, n_contrib, C.byref(grads), stream)
+
+
+def wipes_get_record_grads(cfg, N, B, ws, ws_bytes, cap, out, stream):
+    return lib().wipes_get_record_grads(C.byref(cfg), N, B, ws, ws_bytes, cap, out, stream)
+
+
+def wipes_render_stats(cfg, N, B, ws, ws_bytes, cap, stats3, stream):
+    return lib().wipes_render_stats(C.byref(cfg), N, B, ws, ws_bytes, cap, stats3, stream)
+
+
+def kernel_names():
+    L = lib()
+    return [L.wipes_kernel_name(k).decode() for k in range(L.wipes_num_kernels())]
+
+
+def timing_enable(on: bool):
+    lib().wipes_timing_enable(1 if on else 0)
+
+
+def timing_collect():
+    L = lib()
+    n = L.wipes_num_kernels()
+    ms = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    check(L.wipes_timing_collect(ms, cnt, n), "wipes_timing_collect")
+    names = kernel_names()
+    return {names[k]: (ms[k], cnt[k]) for k in range(n)}
+
+
+def launch_count() -> int:
+    return int(lib().wipes_launch_count())

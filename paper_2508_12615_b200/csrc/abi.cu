@@ -1,0 +1,381 @@
+// C-ABI entry points of libwipes.so (include/wipes.h): argument validation
+// before any launch, workspace carving, kernel sequencing on the caller's
+// stream, optional per-kernel CUDA-event timing and a launch counter.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace wipes {
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+// ---- timing: a pool of event pairs recorded around each launch ------------
+struct TimedLaunch {
+  int kid;
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<cudaEvent_t> g_pool;
+std::vector<TimedLaunch> g_log;
+cudaEvent_t g_pending = nullptr;
+
+cudaEvent_t take_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+const char* kNames[K_NUM] = {
+    "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
+    "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
+    "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset"};
+
+wipes_status fail(wipes_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+wipes_status cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return WIPES_ECUDA;
+}
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
+  if (!c) return fail(WIPES_EINVAL, "cfg is NULL");
+  if (c->width < 1 || c->width > 16384 || c->height < 1 || c->height > 16384)
+    return fail(WIPES_EINVAL, "width/height must be in [1, 16384]");
+  if (c->tile != 8 && c->tile != 16 && c->tile != 32)
+    return fail(WIPES_EINVAL, "tile must be 8, 16 or 32");
+  if (c->prim != WIPES_PRIM_2D && c->prim != WIPES_PRIM_3D) return fail(WIPES_EINVAL, "prim");
+  if (c->blend != WIPES_BLEND_SUM && c->blend != WIPES_BLEND_ALPHA)
+    return fail(WIPES_EINVAL, "blend");
+  if (c->cov2 < 0 || c->cov2 > 2) return fail(WIPES_EINVAL, "cov2");
+  if (c->proj != WIPES_PROJ_PAPER && c->proj != WIPES_PROJ_EXACT) return fail(WIPES_EINVAL, "proj");
+  if (c->extent != WIPES_EXTENT_OPACITY && c->extent != WIPES_EXTENT_SIGMA3)
+    return fail(WIPES_EINVAL, "extent");
+  if (c->proj == WIPES_PROJ_EXACT)
+    return fail(WIPES_EUNSUPPORTED, "exact z-integration projection is not built (NEXT-1)");
+  if (c->deterministic != 0)
+    return fail(WIPES_EUNSUPPORTED, "deterministic reduction is not built in ABI v1");
+  if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
+    return fail(WIPES_EINVAL, "need 0 <= alpha_min < alpha_max <= 1");
+  if (!(c->T_min >= 0.f) || !(c->T_min < 1.f)) return fail(WIPES_EINVAL, "T_min");
+  if (N < 0 || N > ((int64_t)1 << 31) - 1) return fail(WIPES_EINVAL, "N out of range");
+  if (B < 1) return fail(WIPES_EINVAL, "B must be >= 1");
+  if (c->prim == WIPES_PRIM_2D && B != 1) return fail(WIPES_EINVAL, "2D primitives need B == 1");
+  int64_t GX = (c->width + c->tile - 1) / c->tile, GY = (c->height + c->tile - 1) / c->tile;
+  if (GX * GY * (int64_t)B >= ((int64_t)1 << 31)) return fail(WIPES_EINVAL, "B*T >= 2^31");
+  return WIPES_OK;
+}
+
+wipes_status check_ws(const Layout& L, const void* ws, size_t ws_bytes, int64_t cap) {
+  if (cap < 0 || cap >= ((int64_t)1 << 31)) return fail(WIPES_EINVAL, "dup_capacity out of range");
+  if (!ws) return fail(WIPES_EINVAL, "ws is NULL");
+  if (!aligned(ws, 256)) return fail(WIPES_EINVAL, "ws must be 256-byte aligned");
+  if (ws_bytes < L.total) return fail(WIPES_EINVAL, "ws_bytes smaller than wipes_workspace_bytes");
+  return WIPES_OK;
+}
+
+#define REQ(ptr, name)                                                        \
+  do {                                                                        \
+    if (!(ptr)) return fail(WIPES_EINVAL, std::string(name) + " is NULL");    \
+    if (!aligned((ptr), 4)) return fail(WIPES_EINVAL, std::string(name) + " misaligned"); \
+  } while (0)
+
+wipes_status check_params(const wipes_config* c, const wipes_params* p, int64_t N, int32_t B) {
+  if (!p) return fail(WIPES_EINVAL, "params is NULL");
+  if (N == 0) return WIPES_OK;
+  REQ(p->mean, "mean");
+  REQ(p->freq, "freq");
+  REQ(p->color, "color");
+  REQ(p->opacity, "opacity");
+  if (p->phase && !aligned(p->phase, 4)) return fail(WIPES_EINVAL, "phase misaligned");
+  if (c->prim == WIPES_PRIM_2D) {
+    REQ(p->cov, "cov");
+    if (c->blend == WIPES_BLEND_ALPHA) REQ(p->depth, "depth (2D alpha blending)");
+  } else {
+    REQ(p->scale, "scale");
+    REQ(p->quat, "quat");
+    if (p->view_stride != 0 && p->view_stride != N)
+      return fail(WIPES_EINVAL, "view_stride must be 0 or N");
+    (void)B;
+  }
+  return WIPES_OK;
+}
+
+}  // namespace
+
+void launch_begin(int kid, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_pending = take_event();
+  cudaEventRecord(g_pending, s);
+  (void)kid;
+}
+
+void launch_end(int kid, cudaStream_t s) {
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, s);
+  g_log.push_back({kid, g_pending, b});
+  g_pending = nullptr;
+}
+
+}  // namespace wipes
+
+using namespace wipes;
+
+extern "C" {
+
+size_t wipes_workspace_bytes(const wipes_config* cfg, int64_t N, int32_t B, int64_t cap) {
+  if (!cfg || check_cfg(cfg, N, B) != WIPES_OK) return 0;
+  return make_layout(*cfg, N, B, cap).total;
+}
+
+wipes_status wipes_preprocess(const wipes_config* cfg, const wipes_params* params, int64_t N,
+                              const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
+                              int64_t dup_capacity, int64_t* n_dup, uint8_t* cull_flags,
+                              void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  st = check_params(cfg, params, N, B);
+  if (st != WIPES_OK) return st;
+  if (cfg->prim == WIPES_PRIM_3D && !cams) return fail(WIPES_EINVAL, "cams is NULL (3D)");
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  cudaError_t e = cfg->prim == WIPES_PRIM_2D
+                      ? launch_preprocess2d(*cfg, *params, L, w, cull_flags, s)
+                      : launch_preprocess3d(*cfg, *params, L, cams, w, cull_flags, s);
+  if (e != cudaSuccess) return cuda_fail(e, "preprocess launch");
+  e = launch_scan_counts(L, w, s);
+  if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+  if (n_dup) {
+    WsHeader h;
+    e = cudaMemcpyAsync(&h, w + L.hdr, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "n_dup readback");
+    *n_dup = h.total;
+    if (h.total > dup_capacity)
+      return fail(WIPES_ECAPACITY, "tile intersections exceed dup_capacity");
+  }
+  return WIPES_OK;
+}
+
+wipes_status wipes_bin_sort(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                            size_t ws_bytes, int64_t dup_capacity, uint64_t* keys_out,
+                            uint32_t* vals_out, int32_t* tile_offsets_out, void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int fb = 0;
+  cudaError_t e = launch_bin_sort(*cfg, L, w, s, &fb);
+  if (e != cudaSuccess) return cuda_fail(e, "bin_sort launch");
+  if (keys_out && L.cap)
+    e = cudaMemcpyAsync(keys_out, w + (fb ? L.keysB : L.keysA), 8 * L.cap,
+                        cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && vals_out && L.cap)
+    e = cudaMemcpyAsync(vals_out, w + (fb ? L.valsB : L.valsA), 4 * L.cap,
+                        cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && tile_offsets_out)
+    e = cudaMemcpyAsync(tile_offsets_out, w + L.toff, 4 * (L.BT + 1), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "bin_sort copies");
+  return WIPES_OK;
+}
+
+wipes_status wipes_check_overflow(const void* ws, size_t ws_bytes, int64_t* n_dup,
+                                  int32_t* overflowed, void* stream) {
+  if (!ws || ws_bytes < sizeof(WsHeader)) return fail(WIPES_EINVAL, "ws");
+  cudaStream_t s = (cudaStream_t)stream;
+  WsHeader h;
+  cudaError_t e = cudaMemcpyAsync(&h, ws, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "check_overflow");
+  if (n_dup) *n_dup = h.total;
+  if (overflowed) *overflowed = h.overflow;
+  return WIPES_OK;
+}
+
+wipes_status wipes_get_preprocess(const wipes_config* cfg, int64_t N, int32_t B, const void* ws,
+                                  size_t ws_bytes, int64_t dup_capacity, int32_t* rect,
+                                  int32_t* count, int64_t* offsets, uint32_t* depth_key,
+                                  float* records, void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const char* w = (const char*)ws;
+  cudaError_t e = cudaSuccess;
+  if (L.BN == 0) return WIPES_OK;
+  if (rect) e = cudaMemcpyAsync(rect, w + L.rect, 16 * L.BN, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && count)
+    e = cudaMemcpyAsync(count, w + L.count, 4 * L.BN, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && depth_key)
+    e = cudaMemcpyAsync(depth_key, w + L.dkey, 4 * L.BN, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && records)
+    e = cudaMemcpyAsync(records, w + L.rec, 64 * L.BN, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && offsets) e = launch_offsets_copy(L, w, offsets, s);
+  if (e != cudaSuccess) return cuda_fail(e, "get_preprocess copies");
+  return WIPES_OK;
+}
+
+wipes_status wipes_render_fwd(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                              size_t ws_bytes, int64_t dup_capacity, float* image, float* T_final,
+                              int32_t* n_contrib, void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  if (!image || !aligned(image, 4)) return fail(WIPES_EINVAL, "image NULL or misaligned");
+  if (cfg->blend == WIPES_BLEND_ALPHA && (!T_final || !n_contrib))
+    return fail(WIPES_EINVAL, "ALPHA mode needs T_final and n_contrib");
+  cudaError_t e = launch_render_fwd(*cfg, L, (char*)ws, final_buffer_is_b(L), image, T_final,
+                                    n_contrib, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "render_fwd launch");
+  return WIPES_OK;
+}
+
+wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* params, int64_t N,
+                              const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
+                              int64_t dup_capacity, const float* dL_dimage, const float* T_final,
+                              const int32_t* n_contrib, wipes_grads* grads, void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  st = check_params(cfg, params, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  if (!dL_dimage || !aligned(dL_dimage, 4)) return fail(WIPES_EINVAL, "dL_dimage");
+  if (cfg->blend == WIPES_BLEND_ALPHA && (!T_final || !n_contrib))
+    return fail(WIPES_EINVAL, "ALPHA mode needs T_final and n_contrib");
+  if (!grads) return fail(WIPES_EINVAL, "grads is NULL");
+  if (cfg->prim == WIPES_PRIM_3D && !cams) return fail(WIPES_EINVAL, "cams is NULL (3D)");
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  cudaError_t e = cudaSuccess;
+  if (L.BN > 0) {
+    launch_begin(K_MEMSET, s);
+    e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kRecGrads * L.BN, s);
+    launch_end(K_MEMSET, s);
+    if (e != cudaSuccess) return cuda_fail(e, "rgrad memset");
+  }
+  e = launch_render_bwd(*cfg, L, w, final_buffer_is_b(L), dL_dimage, T_final, n_contrib, s);
+  if (e != cudaSuccess) return cuda_fail(e, "render_bwd launch");
+  e = cfg->prim == WIPES_PRIM_2D ? launch_preprocess2d_bwd(*cfg, *params, L, w, *grads, s)
+                                 : launch_preprocess3d_bwd(*cfg, *params, L, cams, w, *grads, s);
+  if (e != cudaSuccess) return cuda_fail(e, "preprocess_bwd launch");
+  return WIPES_OK;
+}
+
+wipes_status wipes_get_record_grads(const wipes_config* cfg, int64_t N, int32_t B, const void* ws,
+                                    size_t ws_bytes, int64_t dup_capacity, float* out,
+                                    void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  if (!out) return fail(WIPES_EINVAL, "out is NULL");
+  if (L.BN == 0) return WIPES_OK;
+  cudaError_t e = cudaMemcpyAsync(out, (const char*)ws + L.rgrad, 4 * kRecGrads * L.BN,
+                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "get_record_grads");
+  return WIPES_OK;
+}
+
+wipes_status wipes_render_stats(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                                size_t ws_bytes, int64_t dup_capacity, uint64_t* stats3,
+                                void* stream) {
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  if (!stats3 || !aligned(stats3, 8)) return fail(WIPES_EINVAL, "stats3");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(stats3, 0, 3 * sizeof(uint64_t), s);
+  if (e == cudaSuccess)
+    e = launch_render_fwd(*cfg, L, (char*)ws, final_buffer_is_b(L), nullptr, nullptr, nullptr, s,
+                          (unsigned long long*)stats3);
+  if (e != cudaSuccess) return cuda_fail(e, "render_stats");
+  return WIPES_OK;
+}
+
+int wipes_num_kernels(void) { return K_NUM; }
+
+const char* wipes_kernel_name(int k) { return (k >= 0 && k < K_NUM) ? kNames[k] : "?"; }
+
+void wipes_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+}
+
+wipes_status wipes_timing_collect(double* ms, int64_t* launches, int n) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (int k = 0; k < n; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+  }
+  cudaError_t e = cudaSuccess;
+  if (!g_log.empty()) e = cudaEventSynchronize(g_log.back().b);
+  for (auto& t : g_log) {
+    float dt = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&dt, t.a, t.b);
+    if (t.kid < n) {
+      if (ms) ms[t.kid] += dt;
+      if (launches) launches[t.kid] += 1;
+    }
+    g_pool.push_back(t.a);
+    g_pool.push_back(t.b);
+  }
+  g_log.clear();
+  if (e != cudaSuccess) return cuda_fail(e, "timing_collect");
+  return WIPES_OK;
+}
+
+int64_t wipes_launch_count(void) { return g_launches.load(); }
+
+const char* wipes_status_string(wipes_status s) {
+  switch (s) {
+    case WIPES_OK: return "WIPES_OK";
+    case WIPES_EINVAL: return "WIPES_EINVAL";
+    case WIPES_ECAPACITY: return "WIPES_ECAPACITY";
+    case WIPES_ECUDA: return "WIPES_ECUDA";
+    case WIPES_EUNSUPPORTED: return "WIPES_EUNSUPPORTED";
+  }
+  return "WIPES_UNKNOWN";
+}
+
+const char* wipes_last_error(void) { return g_last_error.c_str(); }
+
+int wipes_abi_version(void) { return WIPES_ABI_VERSION; }
+
+}  // extern "C"

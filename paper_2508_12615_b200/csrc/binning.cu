@@ -1,0 +1,314 @@
+// Tile binning: exclusive scan of per-(view, primitive)
+// tile counts, duplication under the 64-bit key ((view*T + tile) << 32 |
+// depth bits), a stable LSD radix sort over the significant key bits only,
+// and per-tile CSR ranges. PAPER.md:64 ("an efficient GPU sorting algorithm").
+//
+// Radix sort design (sm_100a, no CUB): per 8-bit digit one histogram kernel
+// (per-WARP sub-block histograms, match_any-aggregated shared atomics), one
+// device-wide exclusive scan of the digit-major [256 x nsub] count matrix,
+// and one stable scatter kernel in which each warp walks its own contiguous
+// sub-block in order, ranking equal digits with __match_any_sync. Stability
+// follows from sub-block order = input order and lane order = input order.
+#include "common.cuh"
+
+namespace wipes {
+
+namespace {
+
+__device__ __forceinline__ int64_t clamp_n(const WsHeader* h, int64_t cap) {
+  int64_t t = h->total;
+  return t < cap ? t : cap;
+}
+
+// ---------------------------------------------------------------- scan ----
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const TIn* in, int64_t n,
+                                                           TOut* loc, TOut* blk_sum) {
+  __shared__ TOut warp_tot[kScanBlock / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * kScanItems;
+  TOut v[kScanItems];
+  TOut s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t idx = base + k;
+    v[k] = idx < n ? (TOut)in[idx] : (TOut)0;
+    s += v[k];
+  }
+  // inclusive warp scan of thread sums
+  TOut inc = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    TOut t = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += t;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    TOut t = lane < kScanBlock / 32 ? warp_tot[lane] : (TOut)0;
+    TOut ti = t;
+#pragma unroll
+    for (int off = 1; off < kScanBlock / 32; off <<= 1) {
+      TOut u = __shfl_up_sync(0xffffffffu, ti, off);
+      if (lane >= off) ti += u;
+    }
+    if (lane < kScanBlock / 32) warp_tot[lane] = ti - t;  // exclusive
+    if (lane == kScanBlock / 32 - 1) blk_sum[blockIdx.x] = ti;
+  }
+  __syncthreads();
+  TOut run = warp_tot[wid] + inc - s;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t idx = base + k;
+    if (idx < n) loc[idx] = run;
+    run += v[k];
+  }
+}
+
+// Exclusive scan of the block sums in place (one block). Optionally publishes
+// the grand total and the capacity-overflow flag into the workspace header.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_sums(T* blk, int64_t nblk, WsHeader* hdr,
+                                                   int64_t cap) {
+  __shared__ T wt[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (nblk + 1023) / 1024;
+  const int64_t b0 = (int64_t)tid * per;
+  T s = 0;
+  for (int64_t k = 0; k < per; ++k)
+    if (b0 + k < nblk) s += blk[b0 + k];
+  T inc = s;
+  for (int off = 1; off < 32; off <<= 1) {
+    T t = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += t;
+  }
+  if (lane == 31) wt[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T t = wt[lane];
+    T ti = t;
+    for (int off = 1; off < 32; off <<= 1) {
+      T u = __shfl_up_sync(0xffffffffu, ti, off);
+      if (lane >= off) ti += u;
+    }
+    wt[lane] = ti - t;
+    if (lane == 31 && hdr) {
+      hdr->total = (int64_t)ti;
+      hdr->overflow = (int64_t)ti > cap ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  T run = wt[wid] + inc - s;
+  for (int64_t k = 0; k < per; ++k)
+    if (b0 + k < nblk) {
+      T v = blk[b0 + k];
+      blk[b0 + k] = run;
+      run += v;
+    }
+}
+
+// ----------------------------------------------------------- duplicate ----
+struct DupArgs {
+  const int4* rect;
+  const int32_t* count;
+  const uint32_t* dkey;
+  const int64_t* loc;
+  const int64_t* blk;
+  int64_t BN, N, T, cap;
+  int32_t GX, alpha;
+  uint64_t* keys;
+  uint32_t* vals;
+};
+
+__global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= a.BN) return;
+  int32_t n = a.count[o];
+  if (n == 0) return;
+  int64_t j = a.loc[o] + a.blk[o / kScanTile];
+  int64_t v = o / a.N, i = o - v * a.N;
+  int4 r = a.rect[o];
+  uint64_t lo = a.alpha ? (uint64_t)a.dkey[o] : 0ull;
+  uint64_t vt = (uint64_t)(v * a.T);
+  for (int ty = r.y; ty < r.w; ++ty) {
+    uint64_t rowt = vt + (uint64_t)ty * a.GX;
+    for (int tx = r.x; tx < r.z; ++tx, ++j) {
+      if (j >= a.cap) return;
+      a.keys[j] = ((rowt + tx) << 32) | lo;
+      a.vals[j] = (uint32_t)i;
+    }
+  }
+}
+
+// -------------------------------------------------------------- radix -----
+struct RadixArgs {
+  const uint64_t* kin;
+  const uint32_t* vin;
+  uint64_t* kout;
+  uint32_t* vout;
+  const WsHeader* hdr;
+  int64_t cap, nsub;
+  int32_t shift, items;
+  int32_t* counts;  // [256][nsub] digit-major; after the scan: local exclusive
+  const int32_t* rblk;
+};
+
+__global__ void __launch_bounds__(kRadixWarps * 32) k_radix_hist(RadixArgs a) {
+  __shared__ int32_t hist[kRadixWarps][kRadixBins];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wid;
+  for (int d = lane; d < kRadixBins; d += 32) hist[wid][d] = 0;
+  __syncwarp();
+  const int64_t n = clamp_n(a.hdr, a.cap);
+  const int64_t base = w * 32 * (int64_t)a.items;
+  for (int it = 0; it < a.items; ++it) {
+    int64_t idx = base + (int64_t)it * 32 + lane;
+    if (base + (int64_t)it * 32 >= n) break;  // warp-uniform
+    bool valid = idx < n;
+    uint32_t d = valid ? (uint32_t)(a.kin[idx] >> a.shift) & (kRadixBins - 1) : kRadixBins;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    int leader = __ffs(peers) - 1;
+    if (valid && lane == leader) hist[wid][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int d = lane; d < kRadixBins; d += 32) a.counts[(int64_t)d * a.nsub + w] = hist[wid][d];
+}
+
+__global__ void __launch_bounds__(kRadixWarps * 32) k_radix_scatter(RadixArgs a) {
+  __shared__ int32_t off[kRadixWarps][kRadixBins];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wid;
+  const int64_t n = clamp_n(a.hdr, a.cap);
+  const int64_t base = w * 32 * (int64_t)a.items;
+  if (base >= n) return;  // whole warp idle (no shared state across warps)
+  for (int d = lane; d < kRadixBins; d += 32) {
+    int64_t ci = (int64_t)d * a.nsub + w;
+    off[wid][d] = a.counts[ci] + a.rblk[ci / kScanTile];
+  }
+  __syncwarp();
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int it = 0; it < a.items; ++it) {
+    int64_t idx = base + (int64_t)it * 32 + lane;
+    if (base + (int64_t)it * 32 >= n) break;
+    bool valid = idx < n;
+    uint64_t key = valid ? a.kin[idx] : 0ull;
+    uint32_t val = valid ? a.vin[idx] : 0u;
+    uint32_t d = valid ? (uint32_t)(key >> a.shift) & (kRadixBins - 1) : kRadixBins;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    int rank = __popc(peers & lt);
+    if (valid) {
+      int pos = off[wid][d] + rank;
+      a.kout[pos] = key;
+      a.vout[pos] = val;
+    }
+    __syncwarp();
+    if (valid && rank == 0) off[wid][d] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------- tile ranges ----
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint64_t* keys, const WsHeader* hdr,
+                                                     int64_t cap, int64_t BT, int32_t* toff) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = clamp_n(hdr, cap);
+  if (i > n) return;
+  int64_t tp = i == 0 ? -1 : (int64_t)(keys[i - 1] >> 32);
+  int64_t tc = i == n ? BT : (int64_t)(keys[i] >> 32);
+  if (tc > BT) tc = BT;
+  for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
+}
+
+__global__ void k_offsets(const int64_t* loc, const int64_t* blk, int64_t BN, int64_t* out) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o < BN) out[o] = loc[o] + blk[o / kScanTile];
+}
+
+}  // namespace
+
+cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s) {
+  if (L.BN == 0) return cudaSuccess;
+  k_offsets<<<(unsigned)((L.BN + 255) / 256), 256, 0, s>>>(
+      (const int64_t*)(ws + L.loc_off), (const int64_t*)(ws + L.blk_sum), L.BN, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s) {
+  WsHeader* hdr = (WsHeader*)(ws + L.hdr);
+  int64_t* blk = (int64_t*)(ws + L.blk_sum);
+  if (L.BN > 0) {
+    launch_begin(K_SCAN_BLOCKS, s);
+    k_scan_blocks<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
+        (const int32_t*)(ws + L.count), L.BN, (int64_t*)(ws + L.loc_off), blk);
+    launch_end(K_SCAN_BLOCKS, s);
+  } else {
+    cudaMemsetAsync(blk, 0, sizeof(int64_t), s);
+  }
+  launch_begin(K_SCAN_SUMS, s);
+  k_scan_sums<int64_t><<<1, 1024, 0, s>>>(blk, L.nblk_scan, hdr, L.cap);
+  launch_end(K_SCAN_SUMS, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
+                            int* final_in_b) {
+  WsHeader* hdr = (WsHeader*)(ws + L.hdr);
+  uint64_t* kA = (uint64_t*)(ws + L.keysA);
+  uint64_t* kB = (uint64_t*)(ws + L.keysB);
+  uint32_t* vA = (uint32_t*)(ws + L.valsA);
+  uint32_t* vB = (uint32_t*)(ws + L.valsB);
+  *final_in_b = final_buffer_is_b(L);
+  if (L.cap > 0 && L.BN > 0) {
+    DupArgs d;
+    d.rect = (const int4*)(ws + L.rect);
+    d.count = (const int32_t*)(ws + L.count);
+    d.dkey = (const uint32_t*)(ws + L.dkey);
+    d.loc = (const int64_t*)(ws + L.loc_off);
+    d.blk = (const int64_t*)(ws + L.blk_sum);
+    d.BN = L.BN; d.N = L.N; d.T = L.T; d.cap = L.cap;
+    d.GX = L.GX; d.alpha = c.blend == WIPES_BLEND_ALPHA;
+    d.keys = kA; d.vals = vA;
+    launch_begin(K_DUPLICATE, s);
+    k_duplicate<<<(unsigned)((L.BN + 255) / 256), 256, 0, s>>>(d);
+    launch_end(K_DUPLICATE, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // LSD passes: depth bits (ALPHA) then the view|tile bits.
+    RadixArgs r;
+    r.hdr = hdr; r.cap = L.cap; r.nsub = L.nsub; r.items = L.items;
+    r.counts = (int32_t*)(ws + L.rcounts);
+    r.rblk = (const int32_t*)(ws + L.rblk);
+    const unsigned nblk = (unsigned)(L.nsub / kRadixWarps);
+    for (int p = 0; p < L.passes; ++p) {
+      int shift = p < L.lo_passes ? 8 * p : 32 + 8 * (p - L.lo_passes);
+      bool from_a = (p & 1) == 0;
+      r.kin = from_a ? kA : kB; r.vin = from_a ? vA : vB;
+      r.kout = from_a ? kB : kA; r.vout = from_a ? vB : vA;
+      r.shift = shift;
+      launch_begin(K_RADIX_HIST, s);
+      k_radix_hist<<<nblk, kRadixWarps * 32, 0, s>>>(r);
+      launch_end(K_RADIX_HIST, s);
+      launch_begin(K_RADIX_SCAN_BLOCKS, s);
+      k_scan_blocks<int32_t, int32_t><<<(unsigned)L.nblk_rscan, kScanBlock, 0, s>>>(
+          r.counts, L.nrc, r.counts, (int32_t*)(ws + L.rblk));
+      launch_end(K_RADIX_SCAN_BLOCKS, s);
+      launch_begin(K_RADIX_SCAN_SUMS, s);
+      k_scan_sums<int32_t><<<1, 1024, 0, s>>>((int32_t*)(ws + L.rblk), L.nblk_rscan, nullptr, 0);
+      launch_end(K_RADIX_SCAN_SUMS, s);
+      launch_begin(K_RADIX_SCATTER, s);
+      k_radix_scatter<<<nblk, kRadixWarps * 32, 0, s>>>(r);
+      launch_end(K_RADIX_SCATTER, s);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+  }
+  const uint64_t* kf = *final_in_b ? kB : kA;
+  launch_begin(K_TILE_RANGES, s);
+  k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(kf, hdr, L.cap, L.BT,
+                                                                  (int32_t*)(ws + L.toff));
+  launch_end(K_TILE_RANGES, s);
+  return cudaGetLastError();
+}
+
+}  // namespace wipes

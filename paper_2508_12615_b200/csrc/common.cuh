@@ -1,0 +1,149 @@
+// Shared definitions of the WIPES CUDA library (sm_100a): workspace layout,
+// render-record layout, kernel ids, launch helpers. Product code only — no
+// oracle code or header is included anywhere under csrc/.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/wipes.h"
+
+namespace wipes {
+
+constexpr int kRecGrads = WIPES_RECORD_GRADS;  // 13 record-gradient slots
+constexpr int kScanBlock = 256;                // threads per scan block
+constexpr int kScanItems = 8;                  // items per thread
+constexpr int kScanTile = kScanBlock * kScanItems;
+constexpr int kRadixBits = 8;
+constexpr int kRadixBins = 1 << kRadixBits;
+constexpr int kRadixWarps = 8;                 // warps per radix block
+constexpr int32_t kWsMagic = 0x57495053;       // "WIPS"
+
+// Record-gradient slot order (matches the oracle's documented layout, written
+// independently): mu'x, mu'y, a, b, c, f'x, f'y, phi, beta, cr, cg, cb, alpha.
+enum { RG_MUX = 0, RG_MUY, RG_A, RG_B, RG_C, RG_FX, RG_FY, RG_PHI, RG_BETA, RG_CR, RG_CG,
+       RG_CB, RG_ALPHA };
+
+// 64-byte render record (4 x float4), one per (view, primitive):
+//  r0 = {mu'x - ax, mu'y - ay, A, B}   A,B,C = -1/2 log2(e) (a, 2b, c), conic (a,b;b,c)
+//  r1 = {C, log2(alpha), f'x, f'y}
+//  r2 = {phi, beta/2, c_r, c_g}
+//  r3 = {c_b, ax, ay, half2(rx, ry)}   (ax, ay) = integer anchor floor(mu') as float;
+//                                      (rx, ry) = opacity-extent half widths (fp16, rounded
+//                                      up) used only for conservative sub-tile culling
+struct WsHeader {
+  int64_t total;       // number of (view, primitive, tile) intersections
+  int32_t overflow;    // 1 if total > capacity
+  int32_t magic;
+  int64_t N, cap, bytes;
+  int32_t B, pad;
+};
+
+struct Layout {
+  int64_t N = 0, BN = 0, cap = 0, BT = 0, T = 0;
+  int32_t B = 0, GX = 0, GY = 0;
+  int32_t hi_bits = 0, passes = 0, lo_passes = 0;
+  int64_t nsub = 0;        // radix sub-blocks (one warp each)
+  int32_t items = 0;       // keys per lane per sub-block
+  int64_t nblk_scan = 0;   // blocks of the count scan
+  int64_t nrc = 0;         // radix counts = 256 * nsub
+  int64_t nblk_rscan = 0;  // blocks of the radix-count scan
+  size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
+         blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, rcounts = 0, rblk = 0,
+         toff = 0, rgrad = 0, total = 0;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t cap) {
+  Layout L;
+  L.N = N; L.B = B; L.BN = N * (int64_t)B; L.cap = cap < 0 ? 0 : cap;
+  L.GX = (c.width + c.tile - 1) / c.tile;
+  L.GY = (c.height + c.tile - 1) / c.tile;
+  L.T = (int64_t)L.GX * L.GY;
+  L.BT = L.T * B;
+  int hb = 0;
+  while (((int64_t)1 << hb) < L.BT) ++hb;
+  L.hi_bits = hb;
+  L.lo_passes = (c.blend == WIPES_BLEND_ALPHA) ? 4 : 0;
+  L.passes = L.lo_passes + (hb + kRadixBits - 1) / kRadixBits;
+  // radix sub-blocks: aim for ~148 SMs x 16 warps, at least 4 items per lane
+  int64_t target_warps = 148 * 16;
+  int64_t items = (L.cap + 32 * target_warps - 1) / (32 * target_warps);
+  if (items < 4) items = 4;
+  items = (items + 3) / 4 * 4;
+  L.items = (int32_t)items;
+  L.nsub = (L.cap + 32 * items - 1) / (32 * items);
+  if (L.nsub < 1) L.nsub = 1;
+  L.nsub = (L.nsub + kRadixWarps - 1) / kRadixWarps * kRadixWarps;
+  L.nrc = (int64_t)kRadixBins * L.nsub;
+  L.nblk_rscan = (L.nrc + kScanTile - 1) / kScanTile;
+  L.nblk_scan = (L.BN + kScanTile - 1) / kScanTile;
+  if (L.nblk_scan < 1) L.nblk_scan = 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  L.hdr = take(256);
+  L.rect = take(sizeof(int4) * L.BN);
+  L.count = take(sizeof(int32_t) * L.BN);
+  L.flag = take(sizeof(uint8_t) * L.BN);
+  L.dkey = take(sizeof(uint32_t) * L.BN);
+  L.rec = take(64 * L.BN);
+  L.loc_off = take(sizeof(int64_t) * L.BN);
+  L.blk_sum = take(sizeof(int64_t) * (L.nblk_scan + 1));
+  L.keysA = take(sizeof(uint64_t) * L.cap);
+  L.keysB = take(sizeof(uint64_t) * L.cap);
+  L.valsA = take(sizeof(uint32_t) * L.cap);
+  L.valsB = take(sizeof(uint32_t) * L.cap);
+  L.rcounts = take(sizeof(int32_t) * L.nrc);
+  L.rblk = take(sizeof(int32_t) * (L.nblk_rscan + 1));
+  L.toff = take(sizeof(int32_t) * (L.BT + 1));
+  L.rgrad = take(sizeof(float) * kRecGrads * L.BN);
+  L.total = o;
+  return L;
+}
+
+// Kernel ids for the timing instrumentation (wipes_kernel_name).
+enum KernelId {
+  K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
+  K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_NUM
+};
+
+// Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph
+// capturable). 18 floats per camera: R[9], t[3], fx, fy, cx, cy, near, far.
+struct CamBlock {
+  float v[WIPES_MAX_CAMERAS_PER_LAUNCH][18];
+  int32_t nv;    // cameras in this block
+  int32_t v0;    // first view index of this block
+};
+
+// ---- host-side launch bookkeeping (defined in abi.cu) ----------------------
+void launch_begin(int kid, cudaStream_t s);
+void launch_end(int kid, cudaStream_t s);
+
+// ---- launchers (defined in the .cu files) ----------------------------------
+cudaError_t launch_preprocess2d(const wipes_config& c, const wipes_params& p, const Layout& L,
+                                char* ws, uint8_t* cull_flags, cudaStream_t s);
+cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, const Layout& L,
+                                const wipes_camera* cams, char* ws, uint8_t* cull_flags,
+                                cudaStream_t s);
+cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
+cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);
+cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
+                            int* final_in_b);
+cudaError_t launch_render_fwd(const wipes_config& c, const Layout& L, char* ws, int final_in_b,
+                              float* image, float* T_final, int32_t* n_contrib,
+                              cudaStream_t s, unsigned long long* stats = nullptr);
+cudaError_t launch_render_bwd(const wipes_config& c, const Layout& L, char* ws, int final_in_b,
+                              const float* dLdC, const float* T_final,
+                              const int32_t* n_contrib, cudaStream_t s);
+cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p,
+                                    const Layout& L, char* ws, const wipes_grads& g,
+                                    cudaStream_t s);
+cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p,
+                                    const Layout& L, const wipes_camera* cams, char* ws,
+                                    const wipes_grads& g, cudaStream_t s);
+
+inline int final_buffer_is_b(const Layout& L) { return L.passes & 1; }
+
+}  // namespace wipes

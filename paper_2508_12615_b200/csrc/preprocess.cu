@@ -1,0 +1,643 @@
+// Preprocess kernels — compiled with
+// --fmad=false so every FP64 expression rounds exactly as written, in the
+// pinned order of DESIGN.md "Pinned preprocess arithmetic" (the integer
+// decisions — tile rects and counts — must match the CPU oracle bit for bit).
+//
+//  k_pre2d      : PAPER.md:299 (Cholesky / RS covariances), Eq. 4 inputs.
+//  k_pre3d      : PAPER.md:106 (Sigma = R S S^T R^T), :116-122 (Eq. 2, J W),
+//                 :194-198 (Eq. 7), :212 (frequency transform, R3).
+//  k_pre2d_bwd / k_pre3d_bwd : chain rule of the above ("explicit gradients
+//                 for all parameters"), in FP64.
+#include <cfloat>
+#include <cmath>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace wipes {
+
+namespace {
+
+constexpr double kLog2e = 1.4426950408889634;
+
+struct PreOut {
+  int4* rect;
+  int32_t* count;
+  uint8_t* flag;
+  uint32_t* dkey;
+  float4* rec;
+  uint8_t* cull_flags;
+};
+
+__device__ __forceinline__ bool fin(double x) { return isfinite(x); }
+
+__device__ __forceinline__ uint32_t orderable(float v) {
+  uint32_t u = __float_as_uint(v);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+
+struct Cfg2 {
+  int32_t W, H, tile, GX, GY, extent, alpha_blend;
+  double alpha_min, det_min, diag;  // diag = cov_eps + dilation
+};
+
+// Steps 3-7 of O1 on Sigma' (diag offset already added) and the
+// render record. Returns the cull flag.
+__device__ int finish2d(const Cfg2& c, double mux, double muy, double sxx, double sxy,
+                        double syy, double alpha, int4* rect, int32_t* count, double* conic,
+                        double* ext) {
+  *rect = make_int4(0, 0, 0, 0);
+  *count = 0;
+  double det = sxx * syy - sxy * sxy;
+  if (!(det >= c.det_min) || !(sxx > 0.0) || !(syy > 0.0)) return 2;
+  if (!(alpha >= c.alpha_min)) return 3;
+  conic[0] = syy / det;
+  conic[1] = -sxy / det;
+  conic[2] = sxx / det;
+  double rx, ry;
+  // opacity-aware extent: alpha*W >= alpha_min  =>  |dx| <= k sqrt(sxx), |dy| <= k sqrt(syy)
+  double k = (c.alpha_min > 0.0) ? sqrt(2.0 * log(alpha / c.alpha_min)) : (double)INFINITY;
+  ext[0] = k * sqrt(sxx);
+  ext[1] = k * sqrt(syy);
+  if (c.extent == WIPES_EXTENT_OPACITY) {
+    rx = ext[0];
+    ry = ext[1];
+  } else {
+    double m = 0.5 * (sxx + syy);
+    double lam = m + sqrt(fmax(m * m - det, 0.0));
+    rx = 3.0 * sqrt(lam);
+    ry = rx;
+  }
+  const double ts = (double)c.tile;
+  double fx0 = floor((mux - rx) / ts), fx1 = floor((mux + rx) / ts) + 1.0;
+  double fy0 = floor((muy - ry) / ts), fy1 = floor((muy + ry) / ts) + 1.0;
+  fx0 = fmin(fmax(fx0, 0.0), (double)c.GX);
+  fx1 = fmin(fmax(fx1, 0.0), (double)c.GX);
+  fy0 = fmin(fmax(fy0, 0.0), (double)c.GY);
+  fy1 = fmin(fmax(fy1, 0.0), (double)c.GY);
+  int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
+  int n = max(0, x1 - x0) * max(0, y1 - y0);
+  *rect = make_int4(x0, y0, x1, y1);
+  *count = n;
+  return n == 0 ? 4 : 0;
+}
+
+__device__ void write_record(float4* rec, double mux, double muy, const double* conic,
+                             double alpha, double fpx, double fpy, double phi, double beta,
+                             double cr, double cg, double cb, const double* ext) {
+  double ax = fmin(fmax(floor(mux), -1073741824.0), 1073741824.0);
+  double ay = fmin(fmax(floor(muy), -1073741824.0), 1073741824.0);
+  float4 r0, r1, r2, r3;
+  r0.x = (float)(mux - ax);
+  r0.y = (float)(muy - ay);
+  r0.z = (float)(-0.5 * kLog2e * conic[0]);
+  r0.w = (float)(-kLog2e * conic[1]);
+  r1.x = (float)(-0.5 * kLog2e * conic[2]);
+  r1.y = (float)log2(alpha);
+  r1.z = (float)fpx;
+  r1.w = (float)fpy;
+  r2.x = (float)phi;
+  r2.y = (float)(0.5 * beta);
+  r2.z = (float)cr;
+  r2.w = (float)cg;
+  r3.x = (float)cb;
+  r3.y = (float)ax;
+  r3.z = (float)ay;
+  // opacity-extent half widths as fp16, rounded UP (sub-tile culling only)
+  __half2 e2 = __halves2half2(__float2half_ru((float)ext[0] * 1.0001f),
+                              __float2half_ru((float)ext[1] * 1.0001f));
+  r3.w = *reinterpret_cast<float*>(&e2);
+  rec[0] = r0; rec[1] = r1; rec[2] = r2; rec[3] = r3;
+}
+
+__device__ __forceinline__ void zero_record(float4* rec) {
+  float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  rec[0] = z; rec[1] = z; rec[2] = z; rec[3] = z;
+}
+
+// 2D covariance by mode (O1 step 1, pinned order).
+__device__ __forceinline__ void cov2d(int mode, double p0, double p1, double p2, double* s) {
+  if (mode == WIPES_COV2_SIGMA) {
+    s[0] = p0; s[1] = p1; s[2] = p2;
+  } else if (mode == WIPES_COV2_CHOLESKY) {
+    s[0] = p0 * p0;
+    s[1] = p0 * p1;
+    s[2] = (p1 * p1) + (p2 * p2);
+  } else {
+    double cs = cos(p0), sn = sin(p0);
+    double sx2 = p1 * p1, sy2 = p2 * p2;
+    s[0] = (cs * cs) * sx2 + (sn * sn) * sy2;
+    s[1] = (cs * sn) * (sx2 - sy2);
+    s[2] = (sn * sn) * sx2 + (cs * cs) * sy2;
+  }
+}
+
+struct Pre2DArgs {
+  Cfg2 c;
+  int32_t cov2;
+  int64_t N;
+  const float *mean, *cov, *freq, *phase, *color, *opacity, *depth;
+  PreOut o;
+};
+
+__global__ void __launch_bounds__(256) k_pre2d(Pre2DArgs a) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const Cfg2& c = a.c;
+  double mux = a.mean[2 * i], muy = a.mean[2 * i + 1];
+  double p0 = a.cov[3 * i], p1 = a.cov[3 * i + 1], p2 = a.cov[3 * i + 2];
+  double fx = a.freq[2 * i], fy = a.freq[2 * i + 1];
+  double phi = a.phase ? (double)a.phase[i] : 0.0;
+  double cr = a.color[3 * i], cg = a.color[3 * i + 1], cb = a.color[3 * i + 2];
+  double al = a.opacity[i];
+  double dep = (c.alpha_blend && a.depth) ? (double)a.depth[i] : 0.0;
+  int4 rect = make_int4(0, 0, 0, 0);
+  int32_t cnt = 0;
+  int flag;
+  double conic[3] = {0, 0, 0}, ext[2] = {0, 0};
+  bool ok = fin(mux) && fin(muy) && fin(p0) && fin(p1) && fin(p2) && fin(fx) && fin(fy) &&
+            fin(phi) && fin(cr) && fin(cg) && fin(cb) && fin(al) && fin(dep);
+  if (!ok) {
+    flag = 5;
+  } else {
+    double s[3];
+    cov2d(a.cov2, p0, p1, p2, s);
+    flag = finish2d(c, mux, muy, s[0] + c.diag, s[1], s[2] + c.diag, al, &rect, &cnt, conic,
+                    ext);
+  }
+  a.o.rect[i] = rect;
+  a.o.count[i] = cnt;
+  a.o.flag[i] = (uint8_t)flag;
+  a.o.dkey[i] = c.alpha_blend ? orderable((float)dep) : 0u;
+  if (a.o.cull_flags) a.o.cull_flags[i] = (uint8_t)flag;
+  if (flag == 0)
+    write_record(a.o.rec + 4 * i, mux, muy, conic, al, fx, fy, phi, 1.0, cr, cg, cb, ext);
+  else
+    zero_record(a.o.rec + 4 * i);
+}
+
+// ---------------------------------------------------------------- 3D ------
+struct Proj3 {
+  double p[3];
+  double Rq[9], qn[4], qnorm;
+  double S3[6];  // 00 01 02 11 12 22
+  double j00, j02, j11, j12, thx, thy;
+  bool clx, cly;
+  double M[6];
+  double g[3];
+  double Sp[3];
+};
+
+__device__ __forceinline__ double s3at(const double* S, int i, int j) {
+  int k = (i <= j) ? (i == 0 ? j : (i == 1 ? 2 + j : 5)) : (j == 0 ? i : (j == 1 ? 2 + i : 5));
+  return S[k];
+}
+
+// O2 steps 1-9 in the pinned order.
+__device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_clamp,
+                         const double* mu, const double* s, const double* q, const double* f,
+                         Proj3& P) {
+  double Rv[9];
+  for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
+  double t0 = cam[9], t1 = cam[10], t2 = cam[11];
+  double fx = cam[12], fy = cam[13];
+  P.p[0] = ((Rv[0] * mu[0] + Rv[1] * mu[1]) + Rv[2] * mu[2]) + t0;
+  P.p[1] = ((Rv[3] * mu[0] + Rv[4] * mu[1]) + Rv[5] * mu[2]) + t1;
+  P.p[2] = ((Rv[6] * mu[0] + Rv[7] * mu[1]) + Rv[8] * mu[2]) + t2;
+  double x = P.p[0], y = P.p[1], z = P.p[2];
+  double w = q[0], qx = q[1], qy = q[2], qz = q[3];
+  double n = sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
+  w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+  P.qn[0] = w; P.qn[1] = qx; P.qn[2] = qy; P.qn[3] = qz; P.qnorm = n;
+  double* R = P.Rq;
+  R[0] = 1.0 - 2.0 * ((qy * qy) + (qz * qz));
+  R[1] = 2.0 * ((qx * qy) - (w * qz));
+  R[2] = 2.0 * ((qx * qz) + (w * qy));
+  R[3] = 2.0 * ((qx * qy) + (w * qz));
+  R[4] = 1.0 - 2.0 * ((qx * qx) + (qz * qz));
+  R[5] = 2.0 * ((qy * qz) - (w * qx));
+  R[6] = 2.0 * ((qx * qz) - (w * qy));
+  R[7] = 2.0 * ((qy * qz) + (w * qx));
+  R[8] = 1.0 - 2.0 * ((qx * qx) + (qy * qy));
+  double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+  int k = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = i; j < 3; ++j)
+      P.S3[k++] = (((R[3 * i] * s2[0]) * R[3 * j] + (R[3 * i + 1] * s2[1]) * R[3 * j + 1]) +
+                   (R[3 * i + 2] * s2[2]) * R[3 * j + 2]);
+  double tx = x / z, ty = y / z;
+  P.clx = P.cly = false;
+  if (ewa_clamp) {
+    double limx = (1.3 * (double)W) / (2.0 * fx);
+    double limy = (1.3 * (double)H) / (2.0 * fy);
+    P.clx = (tx < -limx || tx > limx);
+    P.cly = (ty < -limy || ty > limy);
+    tx = fmin(fmax(tx, -limx), limx);
+    ty = fmin(fmax(ty, -limy), limy);
+  }
+  P.thx = tx; P.thy = ty;
+  P.j00 = fx / z;
+  P.j11 = fy / z;
+  P.j02 = -(fx * tx) / z;
+  P.j12 = -(fy * ty) / z;
+  for (int jj = 0; jj < 3; ++jj) {
+    P.M[jj] = P.j00 * Rv[jj] + P.j02 * Rv[6 + jj];
+    P.M[3 + jj] = P.j11 * Rv[3 + jj] + P.j12 * Rv[6 + jj];
+  }
+  double T[2][3];
+  for (int i = 0; i < 2; ++i)
+    for (int kk = 0; kk < 3; ++kk)
+      T[i][kk] = ((P.M[3 * i] * s3at(P.S3, 0, kk) + P.M[3 * i + 1] * s3at(P.S3, 1, kk)) +
+                  P.M[3 * i + 2] * s3at(P.S3, 2, kk));
+  P.Sp[0] = ((T[0][0] * P.M[0] + T[0][1] * P.M[1]) + T[0][2] * P.M[2]);
+  P.Sp[1] = ((T[0][0] * P.M[3] + T[0][1] * P.M[4]) + T[0][2] * P.M[5]);
+  P.Sp[2] = ((T[1][0] * P.M[3] + T[1][1] * P.M[4]) + T[1][2] * P.M[5]);
+  P.g[0] = ((Rv[0] * f[0] + Rv[1] * f[1]) + Rv[2] * f[2]);
+  P.g[1] = ((Rv[3] * f[0] + Rv[4] * f[1]) + Rv[5] * f[2]);
+  P.g[2] = ((Rv[6] * f[0] + Rv[7] * f[1]) + Rv[8] * f[2]);
+}
+
+struct Pre3DArgs {
+  Cfg2 c;
+  int32_t ewa_clamp;
+  int64_t N, view_stride;
+  const float *mean, *scale, *quat, *freq, *phase, *color, *opacity;
+  PreOut o;
+  CamBlock cams;
+};
+
+__global__ void __launch_bounds__(128) k_pre3d(const __grid_constant__ Pre3DArgs a) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)a.cams.nv * a.N) return;
+  int vl = (int)(gid / a.N);
+  int64_t i = gid - (int64_t)vl * a.N;
+  int v = a.cams.v0 + vl;
+  int64_t o = (int64_t)v * a.N + i;
+  int64_t pi = (int64_t)v * a.view_stride + i;
+  const float* cam = a.cams.v[vl];
+  const Cfg2& c = a.c;
+  double mu[3] = {a.mean[3 * pi], a.mean[3 * pi + 1], a.mean[3 * pi + 2]};
+  double s[3] = {a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2]};
+  double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
+  double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
+  double phi = a.phase ? (double)a.phase[pi] : 0.0;
+  double cr = a.color[3 * pi], cg = a.color[3 * pi + 1], cb = a.color[3 * pi + 2];
+  double al = a.opacity[pi];
+  int4 rect = make_int4(0, 0, 0, 0);
+  int32_t cnt = 0;
+  int flag = 0;
+  uint32_t dk = 0;
+  double conic[3] = {0, 0, 0}, ext[2] = {0, 0};
+  double mux = 0, muy = 0, fpx = 0, fpy = 0;
+  double qq = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+  bool ok = fin(mu[0]) && fin(mu[1]) && fin(mu[2]) && fin(s[0]) && fin(s[1]) && fin(s[2]) &&
+            fin(q[0]) && fin(q[1]) && fin(q[2]) && fin(q[3]) && fin(f[0]) && fin(f[1]) &&
+            fin(f[2]) && fin(phi) && fin(al) && fin(cr) && fin(cg) && fin(cb) && (qq > 0.0);
+  if (!ok) {
+    flag = 5;
+  } else {
+    Proj3 P;
+    project3(cam, c.W, c.H, a.ewa_clamp, mu, s, q, f, P);
+    double x = P.p[0], y = P.p[1], z = P.p[2];
+    double nz = cam[16], fz = cam[17];
+    if (!(z >= nz && z <= fz)) {
+      flag = 1;
+    } else {
+      double fx = cam[12], fy = cam[13], cx = cam[14], cy = cam[15];
+      mux = (fx * (x / z)) + cx;
+      muy = (fy * (y / z)) + cy;
+      fpx = (z * P.g[0]) / fx;
+      fpy = (z * P.g[1]) / fy;
+      float dz = (float)z;
+      dk = orderable(dz);
+      flag = finish2d(c, mux, muy, P.Sp[0] + c.diag, P.Sp[1], P.Sp[2] + c.diag, al, &rect,
+                      &cnt, conic, ext);
+    }
+  }
+  a.o.rect[o] = rect;
+  a.o.count[o] = cnt;
+  a.o.flag[o] = (uint8_t)flag;
+  a.o.dkey[o] = dk;
+  if (a.o.cull_flags) a.o.cull_flags[o] = (uint8_t)flag;
+  if (flag == 0)
+    write_record(a.o.rec + 4 * o, mux, muy, conic, al, fpx, fpy, phi, 1.0, cr, cg, cb, ext);
+  else
+    zero_record(a.o.rec + 4 * o);
+}
+
+// ------------------------------------------------------------- backward ----
+// conic -> covariance: G_Sigma = -A G_A A, G_A = [[ga, gb/2],[gb/2, gc]];
+// returns (g_xx, g_xy (off-diagonal counted twice), g_yy).
+__device__ __forceinline__ void conic_grad_to_cov(const double* A, double ga, double gb,
+                                                  double gc, double* gs) {
+  double a = A[0], b = A[1], c = A[2];
+  double h = 0.5 * gb;
+  // T1 = A Ga
+  double t00 = a * ga + b * h, t01 = a * h + b * gc;
+  double t10 = b * ga + c * h, t11 = b * h + c * gc;
+  // T2 = -T1 A
+  double s00 = -(t00 * a + t01 * b), s01 = -(t00 * b + t01 * c);
+  double s10 = -(t10 * a + t11 * b), s11 = -(t10 * b + t11 * c);
+  gs[0] = s00;
+  gs[1] = s01 + s10;
+  gs[2] = s11;
+}
+
+struct Bwd2DArgs {
+  Cfg2 c;
+  int32_t cov2;
+  int64_t N;
+  const float *cov;
+  const uint8_t* flag;
+  const float* rgrad;
+  wipes_grads g;
+};
+
+__global__ void __launch_bounds__(256) k_pre2d_bwd(Bwd2DArgs a) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const float* rg = a.rgrad + kRecGrads * i;
+  bool live = a.flag[i] == 0;
+  double g[kRecGrads];
+  for (int k = 0; k < kRecGrads; ++k) g[k] = live ? (double)rg[k] : 0.0;
+  if (a.g.mean) { a.g.mean[2 * i] = (float)g[RG_MUX]; a.g.mean[2 * i + 1] = (float)g[RG_MUY]; }
+  if (a.g.freq) { a.g.freq[2 * i] = (float)g[RG_FX]; a.g.freq[2 * i + 1] = (float)g[RG_FY]; }
+  if (a.g.phase) a.g.phase[i] = (float)g[RG_PHI];
+  if (a.g.color) {
+    a.g.color[3 * i] = (float)g[RG_CR];
+    a.g.color[3 * i + 1] = (float)g[RG_CG];
+    a.g.color[3 * i + 2] = (float)g[RG_CB];
+  }
+  if (a.g.opacity) a.g.opacity[i] = (float)g[RG_ALPHA];
+  if (!a.g.cov) return;
+  float* gc = a.g.cov + 3 * i;
+  if (!live) { gc[0] = gc[1] = gc[2] = 0.f; return; }
+  double p0 = a.cov[3 * i], p1 = a.cov[3 * i + 1], p2 = a.cov[3 * i + 2];
+  double s[3];
+  cov2d(a.cov2, p0, p1, p2, s);
+  double sxx = s[0] + a.c.diag, sxy = s[1], syy = s[2] + a.c.diag;
+  double det = sxx * syy - sxy * sxy;
+  double A[3] = {syy / det, -sxy / det, sxx / det};
+  double gs[3];
+  conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gs);
+  if (a.cov2 == WIPES_COV2_SIGMA) {
+    gc[0] = (float)gs[0]; gc[1] = (float)gs[1]; gc[2] = (float)gs[2];
+  } else if (a.cov2 == WIPES_COV2_CHOLESKY) {
+    gc[0] = (float)(2.0 * p0 * gs[0] + p1 * gs[1]);
+    gc[1] = (float)(p0 * gs[1] + 2.0 * p1 * gs[2]);
+    gc[2] = (float)(2.0 * p2 * gs[2]);
+  } else {
+    double cs = cos(p0), sn = sin(p0);
+    double sx = p1, sy = p2;
+    gc[0] = (float)((sx * sx - sy * sy) *
+                    (-2.0 * cs * sn * gs[0] + (cs * cs - sn * sn) * gs[1] + 2.0 * cs * sn * gs[2]));
+    gc[1] = (float)(2.0 * sx * (cs * cs * gs[0] + cs * sn * gs[1] + sn * sn * gs[2]));
+    gc[2] = (float)(2.0 * sy * (sn * sn * gs[0] - cs * sn * gs[1] + cs * cs * gs[2]));
+  }
+}
+
+struct Bwd3DArgs {
+  Cfg2 c;
+  int32_t ewa_clamp, accumulate;
+  int64_t N, view_stride, nrows;
+  const float *mean, *scale, *quat, *freq;
+  const uint8_t* flag;
+  const float* rgrad;
+  wipes_grads g;
+  CamBlock cams;  // views [v0, v0 + nv) of this launch
+};
+
+// One thread per OUTPUT parameter row. With view_stride = 0 it sums the
+// contributions of the launch's views in view order (deterministic); launches
+// after the first (B > 128 views) add to the rows written before.
+__global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3DArgs a) {
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= a.nrows) return;
+  int v_lo, v_hi;
+  int64_t i, pi;
+  if (a.view_stride == 0) { v_lo = a.cams.v0; v_hi = a.cams.v0 + a.cams.nv; i = row; pi = row; }
+  else {
+    int vl = (int)(row / a.N);
+    v_lo = a.cams.v0 + vl; v_hi = v_lo + 1; i = row - (int64_t)vl * a.N;
+    pi = (int64_t)v_lo * a.view_stride + i;
+  }
+  double gmu[3] = {0, 0, 0}, gs_[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gf[3] = {0, 0, 0};
+  double gphi = 0, gcol[3] = {0, 0, 0}, gal = 0;
+  double mu[3] = {a.mean[3 * pi], a.mean[3 * pi + 1], a.mean[3 * pi + 2]};
+  double s[3] = {a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2]};
+  double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
+  double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
+  for (int v = v_lo; v < v_hi; ++v) {
+    const int64_t o = (int64_t)v * a.N + i;
+    if (a.flag[o] != 0) continue;
+    const float* rg = a.rgrad + kRecGrads * o;
+    double g[kRecGrads];
+    for (int k = 0; k < kRecGrads; ++k) g[k] = rg[k];
+    gphi += g[RG_PHI];
+    gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
+    gal += g[RG_ALPHA];
+    const float* cam = a.cams.v[v - a.cams.v0];
+    Proj3 P;
+    project3(cam, a.c.W, a.c.H, a.ewa_clamp, mu, s, q, f, P);
+    double x = P.p[0], y = P.p[1], z = P.p[2];
+    double fx = cam[12], fy = cam[13];
+    double Rv[9];
+    for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
+    double dp[3] = {0, 0, 0};
+    dp[0] += g[RG_MUX] * fx / z;
+    dp[1] += g[RG_MUY] * fy / z;
+    dp[2] += -g[RG_MUX] * fx * x / (z * z) - g[RG_MUY] * fy * y / (z * z);
+    dp[2] += g[RG_FX] * P.g[0] / fx + g[RG_FY] * P.g[1] / fy;
+    double dg0 = g[RG_FX] * z / fx, dg1 = g[RG_FY] * z / fy;
+    for (int k = 0; k < 3; ++k) gf[k] += Rv[k] * dg0 + Rv[3 + k] * dg1;
+    // conic of the (diag-offset) Sigma'
+    double sxx = P.Sp[0] + a.c.diag, sxy = P.Sp[1], syy = P.Sp[2] + a.c.diag;
+    double det = sxx * syy - sxy * sxy;
+    double A[3] = {syy / det, -sxy / det, sxx / det};
+    double gsv[3];
+    conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gsv);
+    double GS[2][2] = {{gsv[0], 0.5 * gsv[1]}, {0.5 * gsv[1], gsv[2]}};
+    double M[2][3] = {{P.M[0], P.M[1], P.M[2]}, {P.M[3], P.M[4], P.M[5]}};
+    double GM[2][3];
+    for (int r = 0; r < 2; ++r)
+      for (int cc = 0; cc < 3; ++cc) GM[r][cc] = GS[r][0] * M[0][cc] + GS[r][1] * M[1][cc];
+    double dM[2][3];
+    for (int r = 0; r < 2; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += GM[r][k] * s3at(P.S3, k, cc);
+        dM[r][cc] = 2.0 * acc;
+      }
+    double dS3[3][3];
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) dS3[r][cc] = M[0][r] * GM[0][cc] + M[1][r] * GM[1][cc];
+    double dj00 = dM[0][0] * Rv[0] + dM[0][1] * Rv[1] + dM[0][2] * Rv[2];
+    double dj02 = dM[0][0] * Rv[6] + dM[0][1] * Rv[7] + dM[0][2] * Rv[8];
+    double dj11 = dM[1][0] * Rv[3] + dM[1][1] * Rv[4] + dM[1][2] * Rv[5];
+    double dj12 = dM[1][0] * Rv[6] + dM[1][1] * Rv[7] + dM[1][2] * Rv[8];
+    dp[2] += dj00 * (-fx / (z * z)) + dj11 * (-fy / (z * z));
+    double dtx_dx = P.clx ? 0.0 : 1.0 / z, dtx_dz = P.clx ? 0.0 : -x / (z * z);
+    double dty_dy = P.cly ? 0.0 : 1.0 / z, dty_dz = P.cly ? 0.0 : -y / (z * z);
+    dp[0] += dj02 * (-(fx / z) * dtx_dx);
+    dp[2] += dj02 * (fx * P.thx / (z * z) - (fx / z) * dtx_dz);
+    dp[1] += dj12 * (-(fy / z) * dty_dy);
+    dp[2] += dj12 * (fy * P.thy / (z * z) - (fy / z) * dty_dz);
+    for (int k = 0; k < 3; ++k) gmu[k] += Rv[k] * dp[0] + Rv[3 + k] * dp[1] + Rv[6 + k] * dp[2];
+    const double* R = P.Rq;
+    double dRq[9];
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) {
+        double acc = 0.0;
+        for (int b = 0; b < 3; ++b) acc += dS3[r][b] * R[3 * b + k];
+        dRq[3 * r + k] = 2.0 * acc * s[k] * s[k];
+      }
+    for (int k = 0; k < 3; ++k) {
+      double Wkk = 0.0;
+      for (int r = 0; r < 3; ++r)
+        for (int b = 0; b < 3; ++b) Wkk += R[3 * r + k] * dS3[r][b] * R[3 * b + k];
+      gs_[k] += 2.0 * s[k] * Wkk;
+    }
+    double w = P.qn[0], qx = P.qn[1], qy = P.qn[2], qz = P.qn[3];
+    double dqn[4];
+    dqn[0] = dRq[1] * (-2 * qz) + dRq[2] * (2 * qy) + dRq[3] * (2 * qz) + dRq[5] * (-2 * qx) +
+             dRq[6] * (-2 * qy) + dRq[7] * (2 * qx);
+    dqn[1] = dRq[1] * (2 * qy) + dRq[2] * (2 * qz) + dRq[3] * (2 * qy) + dRq[4] * (-4 * qx) +
+             dRq[5] * (-2 * w) + dRq[6] * (2 * qz) + dRq[7] * (2 * w) + dRq[8] * (-4 * qx);
+    dqn[2] = dRq[0] * (-4 * qy) + dRq[1] * (2 * qx) + dRq[2] * (2 * w) + dRq[3] * (2 * qx) +
+             dRq[5] * (2 * qz) + dRq[6] * (-2 * w) + dRq[7] * (2 * qz) + dRq[8] * (-4 * qy);
+    dqn[3] = dRq[0] * (-4 * qz) + dRq[1] * (-2 * w) + dRq[2] * (2 * qx) + dRq[3] * (2 * w) +
+             dRq[4] * (-4 * qz) + dRq[5] * (2 * qy) + dRq[6] * (2 * qx) + dRq[7] * (2 * qy);
+    double dot = dqn[0] * P.qn[0] + dqn[1] * P.qn[1] + dqn[2] * P.qn[2] + dqn[3] * P.qn[3];
+    for (int k = 0; k < 4; ++k) gq[k] += (dqn[k] - P.qn[k] * dot) / P.qnorm;
+  }
+  auto put = [&](float* dst, double v) { *dst = a.accumulate ? *dst + (float)v : (float)v; };
+  if (a.g.mean) for (int k = 0; k < 3; ++k) put(&a.g.mean[3 * pi + k], gmu[k]);
+  if (a.g.scale) for (int k = 0; k < 3; ++k) put(&a.g.scale[3 * pi + k], gs_[k]);
+  if (a.g.quat) for (int k = 0; k < 4; ++k) put(&a.g.quat[4 * pi + k], gq[k]);
+  if (a.g.freq) for (int k = 0; k < 3; ++k) put(&a.g.freq[3 * pi + k], gf[k]);
+  if (a.g.phase) put(&a.g.phase[pi], gphi);
+  if (a.g.color) for (int k = 0; k < 3; ++k) put(&a.g.color[3 * pi + k], gcol[k]);
+  if (a.g.opacity) put(&a.g.opacity[pi], gal);
+}
+
+Cfg2 make_cfg2(const wipes_config& c, const Layout& L) {
+  Cfg2 r;
+  r.W = c.width; r.H = c.height; r.tile = c.tile; r.GX = L.GX; r.GY = L.GY;
+  r.extent = c.extent; r.alpha_blend = c.blend == WIPES_BLEND_ALPHA;
+  r.alpha_min = (double)c.alpha_min;
+  r.det_min = (double)c.det_min;
+  r.diag = (double)c.cov_eps + (double)c.dilation;
+  return r;
+}
+
+PreOut make_out(const Layout& L, char* ws, uint8_t* cull) {
+  PreOut o;
+  o.rect = (int4*)(ws + L.rect);
+  o.count = (int32_t*)(ws + L.count);
+  o.flag = (uint8_t*)(ws + L.flag);
+  o.dkey = (uint32_t*)(ws + L.dkey);
+  o.rec = (float4*)(ws + L.rec);
+  o.cull_flags = cull;
+  return o;
+}
+
+void fill_cams(CamBlock& cb, const wipes_camera* cams, int v0, int nv) {
+  cb.v0 = v0; cb.nv = nv;
+  for (int k = 0; k < nv; ++k) {
+    const wipes_camera& c = cams[v0 + k];
+    for (int j = 0; j < 9; ++j) cb.v[k][j] = c.R[j];
+    for (int j = 0; j < 3; ++j) cb.v[k][9 + j] = c.t[j];
+    cb.v[k][12] = c.fx; cb.v[k][13] = c.fy; cb.v[k][14] = c.cx; cb.v[k][15] = c.cy;
+    cb.v[k][16] = c.near_z; cb.v[k][17] = c.far_z;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_preprocess2d(const wipes_config& c, const wipes_params& p, const Layout& L,
+                                char* ws, uint8_t* cull_flags, cudaStream_t s) {
+  if (L.N == 0) return cudaSuccess;
+  Pre2DArgs a;
+  a.c = make_cfg2(c, L);
+  a.cov2 = c.cov2;
+  a.N = L.N;
+  a.mean = p.mean; a.cov = p.cov; a.freq = p.freq; a.phase = p.phase; a.color = p.color;
+  a.opacity = p.opacity; a.depth = p.depth;
+  a.o = make_out(L, ws, cull_flags);
+  launch_begin(K_PRE2D, s);
+  k_pre2d<<<(unsigned)((L.N + 255) / 256), 256, 0, s>>>(a);
+  launch_end(K_PRE2D, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, const Layout& L,
+                                const wipes_camera* cams, char* ws, uint8_t* cull_flags,
+                                cudaStream_t s) {
+  if (L.N == 0) return cudaSuccess;
+  static thread_local Pre3DArgs a;  // ~9 KB: keep off the host stack
+  a.c = make_cfg2(c, L);
+  a.ewa_clamp = c.ewa_clamp;
+  a.N = L.N;
+  a.view_stride = p.view_stride;
+  a.mean = p.mean; a.scale = p.scale; a.quat = p.quat; a.freq = p.freq; a.phase = p.phase;
+  a.color = p.color; a.opacity = p.opacity;
+  a.o = make_out(L, ws, cull_flags);
+  for (int v0 = 0; v0 < L.B; v0 += WIPES_MAX_CAMERAS_PER_LAUNCH) {
+    int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;
+    fill_cams(a.cams, cams, v0, nv);
+    int64_t n = (int64_t)nv * L.N;
+    launch_begin(K_PRE3D, s);
+    k_pre3d<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+    launch_end(K_PRE3D, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p,
+                                    const Layout& L, char* ws, const wipes_grads& g,
+                                    cudaStream_t s) {
+  if (L.N == 0) return cudaSuccess;
+  Bwd2DArgs a;
+  a.c = make_cfg2(c, L);
+  a.cov2 = c.cov2;
+  a.N = L.N;
+  a.cov = p.cov;
+  a.flag = (const uint8_t*)(ws + L.flag);
+  a.rgrad = (const float*)(ws + L.rgrad);
+  a.g = g;
+  launch_begin(K_PRE2D_BWD, s);
+  k_pre2d_bwd<<<(unsigned)((L.N + 255) / 256), 256, 0, s>>>(a);
+  launch_end(K_PRE2D_BWD, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p,
+                                    const Layout& L, const wipes_camera* cams, char* ws,
+                                    const wipes_grads& g, cudaStream_t s) {
+  if (L.N == 0) return cudaSuccess;
+  static thread_local Bwd3DArgs a;  // ~9 KB: keep off the host stack
+  a.c = make_cfg2(c, L);
+  a.ewa_clamp = c.ewa_clamp;
+  a.N = L.N;
+  a.view_stride = p.view_stride;
+  a.mean = p.mean; a.scale = p.scale; a.quat = p.quat; a.freq = p.freq;
+  a.flag = (const uint8_t*)(ws + L.flag);
+  a.rgrad = (const float*)(ws + L.rgrad);
+  a.g = g;
+  for (int v0 = 0; v0 < L.B; v0 += WIPES_MAX_CAMERAS_PER_LAUNCH) {
+    int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;
+    fill_cams(a.cams, cams, v0, nv);
+    a.accumulate = (p.view_stride == 0 && v0 > 0) ? 1 : 0;
+    a.nrows = p.view_stride == 0 ? L.N : (int64_t)nv * L.N;
+    launch_begin(K_PRE3D_BWD, s);
+    k_pre3d_bwd<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+    launch_end(K_PRE3D_BWD, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace wipes

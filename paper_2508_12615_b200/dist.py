@@ -1,0 +1,46 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed.
+
+Partitioning of the hot path:
+  * views / frames of a 3D batch are sharded round-robin across ranks
+    (view v -> rank v mod world); each rank runs the whole rasterizer on its
+    views; the per-primitive gradients of a SHARED parameter set are then
+    summed across ranks with one all_reduce over a single flat bucket (NCCL
+    over NVLink/NVSwitch on the GPU box; gloo in the CPU tests);
+  * independent 2D images (one primitive set each) need no exchange at all.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_views(B: int, rank: int, world: int) -> list[int]:
+    """Round-robin view assignment (view v -> rank v mod world)."""
+    return list(range(rank, B, world))
+
+
+def tile_rows(GY: int, rank: int, world: int) -> list[int]:
+    """Cyclic tile-row assignment for image-space sharding of one large image."""
+    return list(range(rank, GY, world))
+
+
+class GradBucket:
+    """Rebinds the tensors of `grads` (dict name -> tensor) to views of one flat
+    float32 buffer so the cross-rank gradient sum is a single collective."""
+
+    def __init__(self, grads: dict, group=None):
+        self.keys = list(grads.keys())
+        total = sum(grads[k].numel() for k in self.keys)
+        dev = grads[self.keys[0]].device
+        self.flat = torch.zeros(total, dtype=torch.float32, device=dev)
+        off = 0
+        for k in self.keys:
+            n = grads[k].numel()
+            grads[k] = self.flat[off:off + n].view(grads[k].shape)
+            off += n
+        self.group = group
+
+    def all_reduce(self):
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+        return self.flat

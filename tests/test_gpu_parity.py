@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the double-precision
+oracle on the same seeded float32 inputs (run with `pytest -m gpu` on a B200).
+
+Integer artefacts (tile rects, counts, offsets, sorted keys/values, per-tile
+CSR ranges, cull flags) must be bit-exact. Pixels: |g - o| <= max(1e-5,
+1e-4 |o|); gradients: |g - o| <= max(1e-5, 1e-3 |o|) (north_star; DESIGN.md
+R23), with threshold-ambiguous pixels (decision margin < 1e-5) masked and
+counted (R24).
+"""
+import numpy as np
+import pytest
+
+from paper_2508_12615_b200 import gen
+from parity_util import (oracle_cfg, gpu_rasterizer, to_dev, pixel_violations,
+                         grad_violations, f32)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2508_12615_b200 import build
+    build.build()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _check_integers(ora, cfg_o, pr, r, B, N):
+    pre = r.get_preprocess()
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(pre["rect"]), pr.rect.reshape(B * N, 4)), "tile rects differ"
+    assert np.array_equal(_np(pre["count"]), pr.count), "tile counts differ"
+    b = ora.bin_sort(cfg_o, pr)
+    assert np.array_equal(_np(pre["offsets"]), b["offsets"]), "offsets differ"
+    if cfg_o.alpha_blend:
+        dk = _np(pre["depth_key"]).view(np.uint32)
+        live = pr.flag == 0
+        assert np.array_equal(dk[live], pr.keylo[live]), "depth keys differ"
+    keys, vals, toff = r.bin_sort_outputs()
+    torch.cuda.synchronize()
+    assert keys.shape[0] == b["total"]
+    assert np.array_equal(_np(keys).view(np.uint64), b["keys"]), "sorted keys differ"
+    assert np.array_equal(_np(vals).view(np.uint32), b["vals"]), "sorted values differ"
+    assert np.array_equal(_np(toff).astype(np.int64), b["tile_offsets"]), "tile ranges differ"
+    return b
+
+
+def _pixels(arr_bchw):
+    a = np.asarray(arr_bchw)
+    return a.transpose(0, 2, 3, 1).reshape(-1, 3)
+
+
+# --------------------------------------------------------------------- 2D --
+@pytest.mark.parametrize("cov2", ["sigma", "cholesky", "rs"])
+@pytest.mark.parametrize("blend", ["sum", "alpha"])
+def test_c1_2d_full_parity(ora, cov2, blend):
+    """configs[0] (C1): 64x64, 256 primitives — every integer artefact
+    bit-exact, every pixel and every gradient within tolerance."""
+    H = W = 64
+    N = 256
+    p = gen.gen2d(H, W, N, seed=0, cov_mode=cov2, freq_std=0.5, phase=True,
+                  alpha=(0.2, 1.0) if blend == "alpha" else 1.0,
+                  color_max=1.0 if blend == "alpha" else 0.1, depth=(blend == "alpha"))
+    cfg_o = oracle_cfg(ora, "2d", H, W, blend, cov2=cov2)
+    pr = ora.project2d(cfg_o, p)
+    r = gpu_rasterizer("2d", H, W, blend, cov2=cov2)
+    dp = to_dev(p)
+    out = r.forward(dp)
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, 1, N)
+    dL = gen.gen_dLdC(1, H, W, seed=0)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    img = _pixels(_np(out["image"]))
+    nbad, namb = pixel_violations(img, ro["color"], ro["margin"])
+    assert nbad == 0, (nbad, namb)
+    assert namb <= 4
+    if blend == "alpha":
+        nbad, _ = pixel_violations(_np(out["T_final"]).reshape(-1), ro["T"], ro["margin"])
+        assert nbad == 0
+    grads = r.backward(torch.from_numpy(dL).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain2d(cfg_o, p, pr, ro["rgrad"])
+    amb_prims = set()
+    if namb:
+        # primitives touching an ambiguous pixel may legitimately differ
+        yy, xx = np.nonzero(ro["margin"].reshape(H, W) < 1e-5)
+        for (y, x) in zip(yy, xx):
+            for i in range(N):
+                x0, y0, x1, y1 = pr.rect[i]
+                if pr.flag[i] == 0 and x0 <= x // 16 < x1 and y0 <= y // 16 < y1:
+                    amb_prims.add(i)
+    keep = np.array([i not in amb_prims for i in range(N)])
+    for k in ("mean", "cov", "freq", "phase", "color", "opacity"):
+        nbad, worst = grad_violations(_np(grads[k])[keep], og[k][keep])
+        assert nbad == 0, (k, nbad, worst)
+
+
+@pytest.mark.parametrize("tile", [8, 32])
+def test_tile_size_invariance_bitwise(tile):
+    """Lemma O3 on the GPU: images rendered with 8/16/32-pixel tiles are bit
+    for bit identical (same per-pixel contributor set and order, R7)."""
+    H, W = 96, 80
+    for blend in ("sum", "alpha"):
+        p = gen.gen2d(H, W, 500, seed=3, freq_std=0.5, phase=True, alpha=(0.2, 1.0),
+                      depth=(blend == "alpha"))
+        dp = to_dev(p)
+        a = gpu_rasterizer("2d", H, W, blend, tile=16).forward(dp)["image"]
+        b = gpu_rasterizer("2d", H, W, blend, tile=tile).forward(dp)["image"]
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), (blend, tile)
+
+
+def test_c2_kodak_integer_and_sampled_parity(ora):
+    """configs[1] (C2, the bench workload): 768x512, 70k primitives. Integer
+    artefacts bit-exact; pixels and gradients on 4096 sampled pixels (dL/dC is
+    non-zero only there, so the oracle's subset gradient is the full one)."""
+    c = gen.make_config("c2", seed=0)
+    H, W, N = c["H"], c["W"], c["N"]
+    p = c["params"]
+    cfg_o = oracle_cfg(ora, "2d", H, W, "sum", use_rect=True)
+    pr = ora.project2d(cfg_o, p)
+    r = gpu_rasterizer("2d", H, W, "sum")
+    out = r.forward(to_dev(p))
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, 1, N)
+    rng = np.random.default_rng(7)
+    pix = np.sort(rng.choice(H * W, 4096, replace=False))
+    dLfull = np.zeros((1, 3, H, W), np.float32)
+    dLs = rng.uniform(-1, 1, (4096, 3)).astype(np.float32)
+    dLfull[0, :, pix // W, pix % W] = dLs
+    ro = ora.render(cfg_o, pr, pix=pix, dLdC=dLs)
+    img = _pixels(_np(out["image"]))[pix]
+    nbad, namb = pixel_violations(img, ro["color"], ro["margin"])
+    assert nbad == 0, (nbad, namb)
+    grads = r.backward(torch.from_numpy(dLfull).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain2d(cfg_o, p, pr, ro["rgrad"])
+    for k in ("mean", "cov", "freq", "color", "opacity"):
+        nbad, worst = grad_violations(_np(grads[k]), og[k])
+        assert nbad <= 2 * max(namb, 1), (k, nbad, worst)
+
+
+# --------------------------------------------------------------------- 3D --
+@pytest.mark.parametrize("name", ["p3d", "p6d"])
+def test_mini_3d_6d_parity(ora, name):
+    """Parity-only mini configs: 3D static (2 views, shared
+    params) and 6D per-frame params (view_stride = N)."""
+    c = gen.make_config(name, seed=0)
+    H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+    p, cams, vs = c["params"], c["cams"], c["view_stride"]
+    cfg_o = oracle_cfg(ora, "3d", H, W, "alpha", use_rect=True)
+    pr = ora.project3d(cfg_o, p, cams, view_stride=vs)
+    r = gpu_rasterizer("3d", H, W, "alpha")
+    cull = torch.zeros(B * N, dtype=torch.uint8, device="cuda")
+    r.preprocess(to_dev(p), cams, view_stride=vs, cull_flags=cull)
+    r.bin_sort()
+    img, T, nc = r.render()
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(cull), pr.flag.astype(np.uint8)), "cull flags differ"
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    dL = gen.gen_dLdC(B, H, W, seed=1)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    nbad, namb = pixel_violations(_pixels(_np(img)), ro["color"], ro["margin"])
+    assert nbad == 0, (nbad, namb)
+    assert namb <= 0.002 * B * H * W
+    grads = r.backward(torch.from_numpy(dL).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain3d(cfg_o, p, cams, pr, ro["rgrad"], view_stride=vs)
+    for k in ("mean", "scale", "quat", "freq", "color", "opacity"):
+        nbad, worst = grad_violations(_np(grads[k]), og[k])
+        frac = nbad / og[k].size
+        assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
+
+
+# --------------------------------------------------------------- contract --
+def test_capacity_protocol_overflow_then_retry():
+    H = W = 64
+    p = to_dev(gen.gen2d(H, W, 256, seed=1))
+    r = gpu_rasterizer("2d", H, W, "sum")
+    ref = r.forward(p)["image"].clone()
+    total = r.n_dup
+    r2 = gpu_rasterizer("2d", H, W, "sum")
+    r2._alloc(256, 1, total // 2)
+    r2.preprocess(p, sync=False)
+    r2.bin_sort()
+    r2.render()
+    n, over = r2.check_overflow()
+    assert n == total and over
+    r2._alloc(256, 1, total)
+    img = r2.forward(p, sync=False)["image"]
+    n, over = r2.check_overflow()
+    assert not over
+    assert torch.equal(img, ref)
+
+
+def test_empty_scene_and_all_culled():
+    H = W = 32
+    for blend, bg in (("sum", (0, 0, 0)), ("alpha", (0.1, 0.2, 0.3))):
+        p = to_dev(gen.gen2d(H, W, 4, seed=2, depth=True))
+        empty = {k: v[:0].contiguous() for k, v in p.items()}
+        r = gpu_rasterizer("2d", H, W, blend, background=bg)
+        out = r.forward(empty)
+        torch.cuda.synchronize()
+        for ch in range(3):
+            assert torch.all(out["image"][0, ch] == f32(bg[ch]))
+        # non-finite inputs are culled (flag 5), not errors
+        bad = {k: v.clone() for k, v in p.items()}
+        bad["mean"][:] = float("nan")
+        cull = torch.zeros(4, dtype=torch.uint8, device="cuda")
+        r2 = gpu_rasterizer("2d", H, W, blend, background=bg)
+        r2.preprocess(bad, cull_flags=cull)
+        torch.cuda.synchronize()
+        assert torch.all(cull == 5)
