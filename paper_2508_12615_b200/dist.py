@@ -36,7 +36,9 @@ class GradBucket:
         off = 0
         for k in self.keys:
             n = grads[k].numel()
-            grads[k] = self.flat[off:off + n].view(grads[k].shape)
+            view = self.flat[off:off + n].view(grads[k].shape)
+            view.copy_(grads[k])  # keep current values
+            grads[k] = view
             off += n
         self.group = group
 

@@ -1,0 +1,85 @@
+"""World-size-2 gloo tests of the multi-GPU path (CPU).
+
+The kernels cannot run here, so the per-rank work is done by the oracle as a
+test harness stand-in (never a product fallback); what is tested is the
+product's partitioning (dist.shard_views) and its exchange step
+(dist.GradBucket: one flat all_reduce of the per-primitive gradients)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2508_12615_b200 import dist as wdist
+from paper_2508_12615_b200 import gen
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    c = gen.make_config("p3d", seed=0, N=300, H=48, W=48, B=5)
+    views = wdist.shard_views(c["B"], rank, world)
+    cams = [c["cams"][v] for v in views]
+    cfg = oracle.Cfg(width=48, height=48, prim3d=True, alpha_blend=True,
+                     dilation=float(np.float32(0.3)))
+    dL = gen.gen_dLdC(c["B"], 48, 48, seed=3)[views]
+    dLp = dL.transpose(0, 2, 3, 1).reshape(-1, 3)
+    out = oracle.forward_backward(cfg, c["params"], dLp, cams=cams)
+    grads = {k: torch.from_numpy(v.astype(np.float32)) for k, v in out["grads"].items()}
+    bucket = wdist.GradBucket(grads)
+    bucket.all_reduce()
+    if rank == 0:
+        q.put({k: v.numpy().copy() for k, v in grads.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_views_partition():
+    for B in (1, 5, 8, 100):
+        for world in (1, 2, 4, 8):
+            got = sorted(v for r in range(world) for v in wdist.shard_views(B, r, world))
+            assert got == list(range(B))
+
+
+def test_gradbucket_views_share_storage():
+    g = {"a": torch.zeros(3, 2), "b": torch.zeros(5)}
+    b = wdist.GradBucket(g)
+    g["a"] += 1
+    g["b"][2] = 7
+    assert b.flat.numel() == 11 and b.flat[:6].sum() == 6 and b.flat[8] == 7
+
+
+@pytest.mark.timeout(300)
+def test_view_sharded_gradients_equal_single_process(ora):
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    c = gen.make_config("p3d", seed=0, N=300, H=48, W=48, B=5)
+    cfg = ora.Cfg(width=48, height=48, prim3d=True, alpha_blend=True,
+                  dilation=float(np.float32(0.3)))
+    dL = gen.gen_dLdC(c["B"], 48, 48, seed=3).transpose(0, 2, 3, 1).reshape(-1, 3)
+    ref = ora.forward_backward(cfg, c["params"], dL, cams=c["cams"])["grads"]
+    for k, v in ref.items():
+        np.testing.assert_allclose(got[k], v.astype(np.float32), rtol=1e-5, atol=1e-6)
