@@ -42,7 +42,7 @@ extern "C" {
 
 #define WIPES_ABI_VERSION 1
 #define WIPES_MAX_CAMERAS_PER_LAUNCH 128 /* more views are processed in chunks */
-#define WIPES_RECORD_GRADS 13            /* see wipes_render_bwd */
+#define WIPES_GRAD_MOMENTS 12            /* see wipes_get_grad_moments */
 
 typedef enum {
   WIPES_OK = 0,
@@ -164,9 +164,9 @@ wipes_status wipes_render_fwd(const wipes_config* cfg, int64_t N, int32_t B, voi
 
 /* Step 4 (a9-a12): gradients of L given dL/dimage [B,3,H,W] w.r.t. every
  * parameter group ("explicit gradients for all parameters"):
- * per-pair analytic terms reduced per warp with shuffles, then one atomic per
- * (warp, record, value) into the workspace's record gradients, then the
- * preprocess chain rule (FP64) into `grads`. The same params/cams as the
+ * per-pair analytic terms accumulated as 12 per-record moments, reduced per
+ * warp with shuffles, then one atomic per (warp, record, moment) into the
+ * workspace; then the preprocess chain rule (FP64) into `grads`. The same params/cams as the
  * forward call must be passed. */
 wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* params,
                               int64_t N, const wipes_camera* cams, int32_t B, void* ws,
@@ -174,10 +174,14 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
                               const float* dL_dimage, const float* T_final,
                               const int32_t* n_contrib, wipes_grads* grads, void* stream);
 
-/* Record-space gradients [B*N, 13] (float32) of the last wipes_render_bwd, for
- * parity tests: d/d(mu'x, mu'y, conic a, b, c, f'x, f'y, phi, beta, c_r, c_g,
- * c_b, alpha). */
-wipes_status wipes_get_record_grads(const wipes_config* cfg, int64_t N, int32_t B,
+/* The 12 per-record gradient MOMENTS [B*N, 12] (float32) accumulated by the
+ * last wipes_render_bwd, for tests and inspection. With gw = dL/dw of a valid
+ * (pixel, record) pair, w = alpha W, ag = alpha G, d = pixel - mu', sums over
+ * the record's pairs: M0 = gw w, M1 = gw w dx, M2 = gw w dy, M3 = gw w dx^2,
+ * M4 = gw w dx dy, M5 = gw w dy^2, M6 = gw ag sin(theta), M7 = M6 dx,
+ * M8 = M6 dy, M9..M11 = dL/dc (w g, or a T g in ALPHA mode). The record
+ * gradients are linear in them. */
+wipes_status wipes_get_grad_moments(const wipes_config* cfg, int64_t N, int32_t B,
                                     const void* ws, size_t ws_bytes, int64_t dup_capacity,
                                     float* out, void* stream);
 

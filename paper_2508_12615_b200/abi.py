@@ -19,7 +19,7 @@ BLEND = {"sum": 0, "alpha": 1}
 COV2 = {"sigma": 0, "cholesky": 1, "rs": 2}
 PROJ = {"paper": 0, "exact": 1}
 EXTENT = {"opacity": 0, "sigma3": 1}
-RECORD_GRADS = 13
+GRAD_MOMENTS = 12
 MAX_CAMS_PER_LAUNCH = 128
 
 
@@ -81,7 +81,7 @@ def lib():
     L.wipes_render_fwd.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp, vp]
     L.wipes_render_bwd.argtypes = [P(wipes_config), P(wipes_params), i64, P(wipes_camera), i32,
                                    vp, sz, i64, vp, vp, vp, P(wipes_grads), vp]
-    L.wipes_get_record_grads.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
+    L.wipes_get_grad_moments.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
     L.wipes_render_stats.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
     L.wipes_num_kernels.restype = C.c_int
     L.wipes_kernel_name.argtypes = [C.c_int]
@@ -95,7 +95,7 @@ def lib():
     L.wipes_abi_version.restype = C.c_int
     for fn in ("wipes_preprocess", "wipes_bin_sort", "wipes_check_overflow",
                "wipes_get_preprocess", "wipes_render_fwd", "wipes_render_bwd",
-               "wipes_get_record_grads", "wipes_timing_collect", "wipes_render_stats"):
+               "wipes_get_grad_moments", "wipes_timing_collect", "wipes_render_stats"):
         getattr(L, fn).restype = C.c_int
     _lib = L
     return L
@@ -103,7 +103,7 @@ def lib():
 
 EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
             "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
-            "wipes_render_bwd", "wipes_get_record_grads", "wipes_render_stats",
+            "wipes_render_bwd", "wipes_get_grad_moments", "wipes_render_stats",
             "wipes_num_kernels",
             "wipes_kernel_name", "wipes_timing_enable", "wipes_timing_collect",
             "wipes_launch_count", "wipes_status_string", "wipes_last_error",
@@ -202,8 +202,8 @@ def wipes_render_bwd(cfg, params, N, cams, B, ws, ws_bytes, cap, dLdC, T_final, 
                                   dLdC, T_final, n_contrib, C.byref(grads), stream)
 
 
-def wipes_get_record_grads(cfg, N, B, ws, ws_bytes, cap, out, stream):
-    return lib().wipes_get_record_grads(C.byref(cfg), N, B, ws, ws_bytes, cap, out, stream)
+def wipes_get_grad_moments(cfg, N, B, ws, ws_bytes, cap, out, stream):
+    return lib().wipes_get_grad_moments(C.byref(cfg), N, B, ws, ws_bytes, cap, out, stream)
 
 
 def wipes_render_stats(cfg, N, B, ws, ws_bytes, cap, stats3, stream):

@@ -283,7 +283,7 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
   cudaError_t e = cudaSuccess;
   if (L.BN > 0) {
     launch_begin(K_MEMSET, s);
-    e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kRecGrads * L.BN, s);
+    e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kMoments * L.BN, s);
     launch_end(K_MEMSET, s);
     if (e != cudaSuccess) return cuda_fail(e, "rgrad memset");
   }
@@ -295,7 +295,7 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
   return WIPES_OK;
 }
 
-wipes_status wipes_get_record_grads(const wipes_config* cfg, int64_t N, int32_t B, const void* ws,
+wipes_status wipes_get_grad_moments(const wipes_config* cfg, int64_t N, int32_t B, const void* ws,
                                     size_t ws_bytes, int64_t dup_capacity, float* out,
                                     void* stream) {
   wipes_status st = check_cfg(cfg, N, B);
@@ -305,9 +305,9 @@ wipes_status wipes_get_record_grads(const wipes_config* cfg, int64_t N, int32_t 
   if (st != WIPES_OK) return st;
   if (!out) return fail(WIPES_EINVAL, "out is NULL");
   if (L.BN == 0) return WIPES_OK;
-  cudaError_t e = cudaMemcpyAsync(out, (const char*)ws + L.rgrad, 4 * kRecGrads * L.BN,
+  cudaError_t e = cudaMemcpyAsync(out, (const char*)ws + L.rgrad, 4 * kMoments * L.BN,
                                   cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "get_record_grads");
+  if (e != cudaSuccess) return cuda_fail(e, "get_grad_moments");
   return WIPES_OK;
 }
 

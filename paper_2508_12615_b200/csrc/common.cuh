@@ -10,7 +10,8 @@
 
 namespace wipes {
 
-constexpr int kRecGrads = WIPES_RECORD_GRADS;  // 13 record-gradient slots
+constexpr int kRecGrads = 13;                  // record-gradient slots (FP64, in registers)
+constexpr int kMoments = WIPES_GRAD_MOMENTS;   // 12 per-record gradient moments (HBM)
 constexpr int kScanBlock = 256;                // threads per scan block
 constexpr int kScanItems = 8;                  // items per thread
 constexpr int kScanTile = kScanBlock * kScanItems;
@@ -25,12 +26,12 @@ enum { RG_MUX = 0, RG_MUY, RG_A, RG_B, RG_C, RG_FX, RG_FY, RG_PHI, RG_BETA, RG_C
        RG_CB, RG_ALPHA };
 
 // 64-byte render record (4 x float4), one per (view, primitive):
-//  r0 = {mu'x - ax, mu'y - ay, A, B}   A,B,C = -1/2 log2(e) (a, 2b, c), conic (a,b;b,c)
-//  r1 = {C, log2(alpha), f'x, f'y}
-//  r2 = {phi, beta/2, c_r, c_g}
-//  r3 = {c_b, ax, ay, half2(rx, ry)}   (ax, ay) = integer anchor floor(mu') as float;
-//                                      (rx, ry) = opacity-extent half widths (fp16, rounded
-//                                      up) used only for conservative sub-tile culling
+//  r0 = {ax, ay, mu'x - ax, mu'y - ay}  (ax, ay) = integer anchor floor(mu') as float
+//  r1 = {A, B, C, log2(alpha)}          A,B,C = -1/2 log2(e) (a, 2b, c), conic (a,b;b,c)
+//  r2 = {f'x, f'y, phi, beta/2}
+//  r3 = {c_r, c_g, c_b, half2(rx, ry)}  (rx, ry) = opacity-extent half widths (fp16,
+//                                       rounded up), only for conservative sub-tile culling
+// The candidate test needs r0, r1 only (two broadcast LDS.128).
 struct WsHeader {
   int64_t total;       // number of (view, primitive, tile) intersections
   int32_t overflow;    // 1 if total > capacity
@@ -97,7 +98,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.rcounts = take(sizeof(int32_t) * L.nrc);
   L.rblk = take(sizeof(int32_t) * (L.nblk_rscan + 1));
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
-  L.rgrad = take(sizeof(float) * kRecGrads * L.BN);
+  L.rgrad = take(sizeof(float) * kMoments * L.BN);
   L.total = o;
   return L;
 }

@@ -88,21 +88,21 @@ __device__ void write_record(float4* rec, double mux, double muy, const double* 
   double ax = fmin(fmax(floor(mux), -1073741824.0), 1073741824.0);
   double ay = fmin(fmax(floor(muy), -1073741824.0), 1073741824.0);
   float4 r0, r1, r2, r3;
-  r0.x = (float)(mux - ax);
-  r0.y = (float)(muy - ay);
-  r0.z = (float)(-0.5 * kLog2e * conic[0]);
-  r0.w = (float)(-kLog2e * conic[1]);
-  r1.x = (float)(-0.5 * kLog2e * conic[2]);
-  r1.y = (float)log2(alpha);
-  r1.z = (float)fpx;
-  r1.w = (float)fpy;
-  r2.x = (float)phi;
-  r2.y = (float)(0.5 * beta);
-  r2.z = (float)cr;
-  r2.w = (float)cg;
-  r3.x = (float)cb;
-  r3.y = (float)ax;
-  r3.z = (float)ay;
+  r0.x = (float)ax;
+  r0.y = (float)ay;
+  r0.z = (float)(mux - ax);
+  r0.w = (float)(muy - ay);
+  r1.x = (float)(-0.5 * kLog2e * conic[0]);
+  r1.y = (float)(-kLog2e * conic[1]);
+  r1.z = (float)(-0.5 * kLog2e * conic[2]);
+  r1.w = (float)log2(alpha);
+  r2.x = (float)fpx;
+  r2.y = (float)fpy;
+  r2.z = (float)phi;
+  r2.w = (float)(0.5 * beta);
+  r3.x = (float)cr;
+  r3.y = (float)cg;
+  r3.z = (float)cb;
   // opacity-extent half widths as fp16, rounded UP (sub-tile culling only)
   __half2 e2 = __halves2half2(__float2half_ru((float)ext[0] * 1.0001f),
                               __float2half_ru((float)ext[1] * 1.0001f));
@@ -343,23 +343,57 @@ __device__ __forceinline__ void conic_grad_to_cov(const double* A, double ga, do
   gs[2] = s11;
 }
 
+// Record gradients from the render kernel's 12 per-record moments (DESIGN.md
+// §5): with hb = beta/2 and the FP64 conic (a, b, c), frequency f' and alpha,
+//   dphi = -hb M6, df' = -hb (M7, M8), dmu' = A (M1, M2) + hb f' M6,
+//   d(a, b, c) = (-M3/2, -M4, -M5/2), dalpha = M0 / alpha, dc = (M9, M10, M11).
+__device__ __forceinline__ void moments_to_grads(const float* mom, const double* A, double fx,
+                                                 double fy, double hb, double alpha,
+                                                 double* g) {
+  double m[kMoments];
+  for (int k = 0; k < kMoments; ++k) m[k] = mom[k];
+  g[RG_PHI] = -hb * m[6];
+  g[RG_FX] = -hb * m[7];
+  g[RG_FY] = -hb * m[8];
+  g[RG_MUX] = A[0] * m[1] + A[1] * m[2] + hb * fx * m[6];
+  g[RG_MUY] = A[1] * m[1] + A[2] * m[2] + hb * fy * m[6];
+  g[RG_A] = -0.5 * m[3];
+  g[RG_B] = -m[4];
+  g[RG_C] = -0.5 * m[5];
+  g[RG_BETA] = 0.0;
+  g[RG_ALPHA] = m[0] / alpha;
+  g[RG_CR] = m[9];
+  g[RG_CG] = m[10];
+  g[RG_CB] = m[11];
+}
+
 struct Bwd2DArgs {
   Cfg2 c;
   int32_t cov2;
   int64_t N;
-  const float *cov;
+  const float *cov, *freq, *opacity;
   const uint8_t* flag;
-  const float* rgrad;
+  const float* mom;
   wipes_grads g;
 };
 
 __global__ void __launch_bounds__(256) k_pre2d_bwd(Bwd2DArgs a) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
-  const float* rg = a.rgrad + kRecGrads * i;
   bool live = a.flag[i] == 0;
   double g[kRecGrads];
-  for (int k = 0; k < kRecGrads; ++k) g[k] = live ? (double)rg[k] : 0.0;
+  for (int k = 0; k < kRecGrads; ++k) g[k] = 0.0;
+  double A[3] = {0, 0, 0};
+  double p0 = a.cov[3 * i], p1 = a.cov[3 * i + 1], p2 = a.cov[3 * i + 2];
+  if (live) {
+    double s[3];
+    cov2d(a.cov2, p0, p1, p2, s);
+    double sxx = s[0] + a.c.diag, sxy = s[1], syy = s[2] + a.c.diag;
+    double det = sxx * syy - sxy * sxy;
+    A[0] = syy / det; A[1] = -sxy / det; A[2] = sxx / det;
+    moments_to_grads(a.mom + kMoments * i, A, a.freq[2 * i], a.freq[2 * i + 1], 0.5,
+                     a.opacity[i], g);
+  }
   if (a.g.mean) { a.g.mean[2 * i] = (float)g[RG_MUX]; a.g.mean[2 * i + 1] = (float)g[RG_MUY]; }
   if (a.g.freq) { a.g.freq[2 * i] = (float)g[RG_FX]; a.g.freq[2 * i + 1] = (float)g[RG_FY]; }
   if (a.g.phase) a.g.phase[i] = (float)g[RG_PHI];
@@ -372,12 +406,6 @@ __global__ void __launch_bounds__(256) k_pre2d_bwd(Bwd2DArgs a) {
   if (!a.g.cov) return;
   float* gc = a.g.cov + 3 * i;
   if (!live) { gc[0] = gc[1] = gc[2] = 0.f; return; }
-  double p0 = a.cov[3 * i], p1 = a.cov[3 * i + 1], p2 = a.cov[3 * i + 2];
-  double s[3];
-  cov2d(a.cov2, p0, p1, p2, s);
-  double sxx = s[0] + a.c.diag, sxy = s[1], syy = s[2] + a.c.diag;
-  double det = sxx * syy - sxy * sxy;
-  double A[3] = {syy / det, -sxy / det, sxx / det};
   double gs[3];
   conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gs);
   if (a.cov2 == WIPES_COV2_SIGMA) {
@@ -401,8 +429,9 @@ struct Bwd3DArgs {
   int32_t ewa_clamp, accumulate;
   int64_t N, view_stride, nrows;
   const float *mean, *scale, *quat, *freq;
+  const float* opacity;
   const uint8_t* flag;
-  const float* rgrad;
+  const float* mom;
   wipes_grads g;
   CamBlock cams;  // views [v0, v0 + nv) of this launch
 };
@@ -430,12 +459,6 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
   for (int v = v_lo; v < v_hi; ++v) {
     const int64_t o = (int64_t)v * a.N + i;
     if (a.flag[o] != 0) continue;
-    const float* rg = a.rgrad + kRecGrads * o;
-    double g[kRecGrads];
-    for (int k = 0; k < kRecGrads; ++k) g[k] = rg[k];
-    gphi += g[RG_PHI];
-    gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
-    gal += g[RG_ALPHA];
     const float* cam = a.cams.v[v - a.cams.v0];
     Proj3 P;
     project3(cam, a.c.W, a.c.H, a.ewa_clamp, mu, s, q, f, P);
@@ -443,6 +466,16 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
     double fx = cam[12], fy = cam[13];
     double Rv[9];
     for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
+    // conic of the (diag-offset) Sigma' and the record gradients from moments
+    double sxx = P.Sp[0] + a.c.diag, sxy = P.Sp[1], syy = P.Sp[2] + a.c.diag;
+    double det = sxx * syy - sxy * sxy;
+    double A[3] = {syy / det, -sxy / det, sxx / det};
+    double g[kRecGrads];
+    moments_to_grads(a.mom + kMoments * o, A, (z * P.g[0]) / fx, (z * P.g[1]) / fy, 0.5,
+                     a.opacity[pi], g);
+    gphi += g[RG_PHI];
+    gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
+    gal += g[RG_ALPHA];
     double dp[3] = {0, 0, 0};
     dp[0] += g[RG_MUX] * fx / z;
     dp[1] += g[RG_MUY] * fy / z;
@@ -450,10 +483,6 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
     dp[2] += g[RG_FX] * P.g[0] / fx + g[RG_FY] * P.g[1] / fy;
     double dg0 = g[RG_FX] * z / fx, dg1 = g[RG_FY] * z / fy;
     for (int k = 0; k < 3; ++k) gf[k] += Rv[k] * dg0 + Rv[3 + k] * dg1;
-    // conic of the (diag-offset) Sigma'
-    double sxx = P.Sp[0] + a.c.diag, sxy = P.Sp[1], syy = P.Sp[2] + a.c.diag;
-    double det = sxx * syy - sxy * sxy;
-    double A[3] = {syy / det, -sxy / det, sxx / det};
     double gsv[3];
     conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gsv);
     double GS[2][2] = {{gsv[0], 0.5 * gsv[1]}, {0.5 * gsv[1], gsv[2]}};
@@ -604,8 +633,10 @@ cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p
   a.cov2 = c.cov2;
   a.N = L.N;
   a.cov = p.cov;
+  a.freq = p.freq;
+  a.opacity = p.opacity;
   a.flag = (const uint8_t*)(ws + L.flag);
-  a.rgrad = (const float*)(ws + L.rgrad);
+  a.mom = (const float*)(ws + L.rgrad);
   a.g = g;
   launch_begin(K_PRE2D_BWD, s);
   k_pre2d_bwd<<<(unsigned)((L.N + 255) / 256), 256, 0, s>>>(a);
@@ -623,8 +654,9 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
   a.N = L.N;
   a.view_stride = p.view_stride;
   a.mean = p.mean; a.scale = p.scale; a.quat = p.quat; a.freq = p.freq;
+  a.opacity = p.opacity;
   a.flag = (const uint8_t*)(ws + L.flag);
-  a.rgrad = (const float*)(ws + L.rgrad);
+  a.mom = (const float*)(ws + L.rgrad);
   a.g = g;
   for (int v0 = 0; v0 < L.B; v0 += WIPES_MAX_CAMERAS_PER_LAUNCH) {
     int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;

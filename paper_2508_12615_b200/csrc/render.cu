@@ -4,16 +4,20 @@
 //             blending), with the Gaussian G' replaced by the wavelet W'
 //             (PAPER.md:215, :272): w = alpha * G * 1/2 [1 + beta cos(f.d + phi)].
 //  backward : analytic per-pair gradients ("explicit gradients for all
-//             parameters"), reduced per warp with a 16-value
-//             transpose-reduce of shuffles, then one atomic per (warp, record,
-//             value) into the record-gradient buffer.
+//             parameters") accumulated as 12 per-record MOMENTS
+//              that the FP64 preprocess-backward turns into the
+//             record gradients exactly (they are linear in the moments with
+//             per-record coefficients). Moments are reduced per warp with a
+//             12-slot transpose-reduce of shuffles, then one atomic per (warp,
+//             record, moment).
 //
-// One CTA per (view, tile); TS x TS threads, one pixel each. Warps own 8 x 4
-// pixel sub-tiles; every staged record carries a sub-tile mask computed from
-// its opacity extent (conservative), so a warp skips records that cannot
-// reach its pixels (warp-uniform branch). Records are staged in shared memory
-// in batches of up to 256 (one coalesced 64-byte record per loading thread).
-// The exp is a single MUFU.EX2 (the -1/2 log2(e) scale and log2(alpha) are
+// One CTA per (view, tile). Each warp owns an 8x8-pixel sub-tile, each lane two
+// pixels (rows y and y+4). Records are staged in shared memory in batches
+// (structure-of-float4 layout, conflict-free stores, broadcast loads); every
+// staged record carries a sub-tile mask from its conservative opacity extent,
+// and each warp compacts the batch into its own ordered list of records that
+// can reach its pixels (ballot + popc), so a warp never visits a record that
+// cannot touch it. exp is one MUFU.EX2 (the -1/2 log2(e) scale and log2(alpha)
 // folded into the record); cos / sin are MUFU.COS / MUFU.SIN.
 #include <cuda_fp16.h>
 
@@ -24,9 +28,7 @@ namespace wipes {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr float kLn2 = 0.6931471805599453f;
-// unscaled conic = scaled / (-1/2 log2 e)
-constexpr float kInvHalfLog2e = -1.3862943611198906f;  // = -2 ln 2
+constexpr int kMom = kMoments;  // 12
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -63,217 +65,307 @@ struct RenderArgs {
   const float* dLdC;     // [B,3,H,W]
   const float* T_in;
   const int32_t* nc_in;
-  float* rgrad;          // [B*N, 13]
+  float* mom;            // [B*N, 12] gradient moments
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
-// Sub-tile mask of a record for tile origin (X0, Y0): bit (sy * NSX + sx) set
-// when the record's opacity-extent AABB (padded) may touch the 8x4 sub-tile.
+// Sub-tile mask of a record for tile origin (X0, Y0): bit (sy * NS + sx) set
+// when the record's opacity-extent AABB (padded) may touch 8x8 sub-tile (sx, sy).
 template <int TS>
 __device__ __forceinline__ uint32_t subtile_mask(const float4& r0, const float4& r3, int X0,
                                                  int Y0) {
-  constexpr int NSX = TS / 8, NSY = TS / 4;
+  constexpr int NS = TS / 8;
   __half2 e2 = *reinterpret_cast<const __half2*>(&r3.w);
   float rx = __low2float(e2) + 0.02f, ry = __high2float(e2) + 0.02f;
-  float cx = (r3.y - (float)X0) + r0.x;  // centre relative to the tile origin
-  float cy = (r3.z - (float)Y0) + r0.y;
-  // sub-tile sx covers pixel centres [8 sx + 0.5, 8 sx + 7.5]
+  float cx = (r0.x - (float)X0) + r0.z;  // centre relative to the tile origin
+  float cy = (r0.y - (float)Y0) + r0.w;
+  // sub-tile s covers pixel centres [8 s + 0.5, 8 s + 7.5]
   float fx0 = ceilf((cx - rx - 7.5f) * 0.125f), fx1 = floorf((cx + rx - 0.5f) * 0.125f);
-  float fy0 = ceilf((cy - ry - 3.5f) * 0.25f), fy1 = floorf((cy + ry - 0.5f) * 0.25f);
-  int sx0 = (int)fmaxf(fx0, 0.f), sx1 = (int)fminf(fx1, (float)(NSX - 1));
-  int sy0 = (int)fmaxf(fy0, 0.f), sy1 = (int)fminf(fy1, (float)(NSY - 1));
-  if (!(fx0 <= fx1) || !(fy0 <= fy1) || sx0 > sx1 || sy0 > sy1) return 0u;
+  float fy0 = ceilf((cy - ry - 7.5f) * 0.125f), fy1 = floorf((cy + ry - 0.5f) * 0.125f);
+  fx0 = fmaxf(fx0, 0.f); fy0 = fmaxf(fy0, 0.f);
+  fx1 = fminf(fx1, (float)(NS - 1)); fy1 = fminf(fy1, (float)(NS - 1));
+  if (!(fx0 <= fx1) || !(fy0 <= fy1)) return 0u;
+  int sx0 = (int)fx0, sx1 = (int)fx1, sy0 = (int)fy0, sy1 = (int)fy1;
   uint32_t row = ((2u << sx1) - 1u) & ~((1u << sx0) - 1u);
   uint32_t m = 0;
 #pragma unroll
-  for (int sy = 0; sy < NSY; ++sy)
-    if (sy >= sy0 && sy <= sy1) m |= row << (sy * NSX);
+  for (int sy = 0; sy < NS; ++sy)
+    if (sy >= sy0 && sy <= sy1) m |= row << (sy * NS);
   return m;
 }
 
-// Shared exp/cos evaluation of one (pixel, record) pair, identical in forward
-// and backward so both take the same alpha_min decisions.
-struct PairEval {
-  float dx, dy, ag, th, w;
-  bool ok;
-};
-
-__device__ __forceinline__ void eval_pair(const float4& r0, const float4& r1, const float4& r2,
-                                          const float4& r3, float px, float py, float skip_e,
-                                          float alpha_min, PairEval& e, float& cs) {
-  e.dx = __fsub_rn(__fsub_rn(px, r3.y), r0.x);
-  e.dy = __fsub_rn(__fsub_rn(py, r3.z), r0.y);
-  float t = __fmaf_rn(r0.z, e.dx, __fmul_rn(r0.w, e.dy));
-  float u = __fmaf_rn(__fmul_rn(r1.x, e.dy), e.dy, r1.y);
-  float ex = __fmaf_rn(t, e.dx, u);
-  e.ok = ex >= skip_e;
-  if (!e.ok) return;
-  e.ag = ex2(ex);
-  e.th = __fmaf_rn(r1.z, e.dx, __fmaf_rn(r1.w, e.dy, r2.x));
-  cs = cos_a(e.th);
-  e.w = __fmul_rn(e.ag, __fmaf_rn(r2.y, cs, 0.5f));
-  e.ok = e.w >= alpha_min;
+// Exponent of alpha*G for one (pixel, record) pair — identical arithmetic in
+// every kernel so all take the same alpha_min decisions.
+__device__ __forceinline__ float pair_exponent(const float4& r0, const float4& r1, float px,
+                                               float py, float& dx, float& dy) {
+  dx = __fsub_rn(__fsub_rn(px, r0.x), r0.z);
+  dy = __fsub_rn(__fsub_rn(py, r0.y), r0.w);
+  float t = __fmaf_rn(r1.x, dx, __fmul_rn(r1.y, dy));
+  float u = __fmaf_rn(__fmul_rn(r1.z, dy), dy, r1.w);
+  return __fmaf_rn(t, dx, u);
 }
 
-constexpr int kBatch = 256;
+__device__ __forceinline__ float pair_theta(const float4& r2, float dx, float dy) {
+  return __fmaf_rn(r2.x, dx, __fmaf_rn(r2.y, dy, r2.z));
+}
+
+__device__ __forceinline__ float pair_weight(float ag, float cs, const float4& r2) {
+  return __fmul_rn(ag, __fmaf_rn(r2.w, cs, 0.5f));
+}
+
+template <int TS>
+struct Geo {
+  static constexpr int NS = TS / 8;           // sub-tiles per side
+  static constexpr int NW = NS * NS;          // warps per CTA
+  static constexpr int NT = 32 * NW;          // threads per CTA
+  static constexpr int NB = NT < 128 ? 128 : NT;  // records per staged batch
+};
+
+// Stage records [b0, b0 + nb) of the tile list into shared memory and build
+// each warp's compacted list. Returns this warp's list length.
+template <int TS>
+__device__ __forceinline__ int stage_batch(const RenderArgs& a, const float4* recv, int b0,
+                                           int nb, int X0, int Y0, float4 (*s_rec)[Geo<TS>::NB],
+                                           uint32_t* s_mask, uint8_t (*s_list)[Geo<TS>::NB],
+                                           int32_t* s_pid, int tid, int lane, int wid) {
+  constexpr int NB = Geo<TS>::NB, NT = Geo<TS>::NT;
+#pragma unroll
+  for (int t = tid; t < NB; t += NT) {
+    uint32_t m = 0;
+    if (t < nb) {
+      const uint32_t pid = a.vals[b0 + t];
+      const float4* r = recv + 4 * (int64_t)pid;
+      float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3);
+      s_rec[0][t] = r0; s_rec[1][t] = r1; s_rec[2][t] = r2; s_rec[3][t] = r3;
+      s_pid[t] = (int32_t)pid;
+      m = subtile_mask<TS>(r0, r3, X0, Y0);
+    }
+    s_mask[t] = m;
+  }
+  __syncthreads();
+  int cnt = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int c = 0; c < NB / 32; ++c) {
+    const int j = c * 32 + lane;
+    const bool hit = (s_mask[j] >> wid) & 1u;
+    const uint32_t bal = __ballot_sync(kFull, hit);
+    if (hit) s_list[wid][cnt + __popc(bal & lt)] = (uint8_t)j;
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  return cnt;
+}
 
 template <int TS, bool ALPHA, bool STATS>
-__global__ void __launch_bounds__(TS* TS) k_render_fwd(RenderArgs a) {
-  constexpr int NT = TS * TS;
-  constexpr int NB = NT < kBatch ? NT : kBatch;
-  constexpr int NSX = TS / 8;
-  __shared__ float4 s_rec[NB][4];
+__global__ void __launch_bounds__(Geo<TS>::NT) k_render_fwd(RenderArgs a) {
+  using G = Geo<TS>;
+  constexpr int NB = G::NB;
+  __shared__ float4 s_rec[4][NB];
   __shared__ uint32_t s_mask[NB];
+  __shared__ uint8_t s_list[G::NW][NB];
+  __shared__ int32_t s_pid[NB];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t tile = blockIdx.x;
   const int64_t v = tile / a.T;
   const int64_t t_in_v = tile - v * a.T;
   const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
   const int X0 = tx * TS, Y0 = ty * TS;
-  const int sx = wid % NSX, sy = wid / NSX;
-  const int x = X0 + sx * 8 + (lane & 7), y = Y0 + sy * 4 + (lane >> 3);
-  const bool inside = x < a.W && y < a.H;
-  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const int x = X0 + (wid % G::NS) * 8 + (lane & 7);
+  const int y0 = Y0 + (wid / G::NS) * 8 + (lane >> 3), y1 = y0 + 4;
+  const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
+  const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f, py1 = (float)y1 + 0.5f;
   const int start = a.toff[tile], end = a.toff[tile + 1];
   const float4* recv = a.rec + 4 * (v * a.N);
-  float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f;
-  int last = 0;
-  bool done = ALPHA ? !inside : false;
-  bool warp_done = ALPHA ? __all_sync(kFull, done) : false;
-  const uint32_t mybit = 1u << wid;
-  int n_ell = 0, n_con = 0, stop_pos = end - start;  // STATS only
+  float C00 = 0.f, C01 = 0.f, C02 = 0.f, C10 = 0.f, C11 = 0.f, C12 = 0.f;
+  float T0 = 1.f, T1 = 1.f;
+  int last0 = 0, last1 = 0;
+  bool done0 = ALPHA ? !in0 : false, done1 = ALPHA ? !in1 : false;
+  int n_ell = 0, n_con = 0, stop0 = end - start, stop1 = end - start;  // STATS only
   for (int b0 = start; b0 < end; b0 += NB) {
     const int nb = min(NB, end - b0);
     __syncthreads();
-    if (tid < nb) {
-      const uint32_t pid = a.vals[b0 + tid];
-      const float4* r = recv + 4 * (int64_t)pid;
-      float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-      s_rec[tid][0] = r0; s_rec[tid][1] = r1; s_rec[tid][2] = r2; s_rec[tid][3] = r3;
-      s_mask[tid] = subtile_mask<TS>(r0, r3, X0, Y0);
-    }
-    __syncthreads();
-    if (!warp_done) {
-      for (int j = 0; j < nb; ++j) {
-        if (!(s_mask[j] & mybit)) continue;  // warp-uniform
-        if (!done) {
-          const float4 r0 = s_rec[j][0], r1 = s_rec[j][1], r2 = s_rec[j][2], r3 = s_rec[j][3];
-          PairEval e;
-          float cs;
-          eval_pair(r0, r1, r2, r3, px, py, a.skip_e, a.alpha_min, e, cs);
-          if (STATS && inside) {
-            const float4 q0 = r0, q1 = r1;
-            float t = __fmaf_rn(q0.z, e.dx, __fmul_rn(q0.w, e.dy));
-            float u = __fmaf_rn(__fmul_rn(q1.x, e.dy), e.dy, q1.y);
-            if (__fmaf_rn(t, e.dx, u) >= a.skip_e) ++n_ell;
-          }
-          if (e.ok) {
+    const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, s_rec, s_mask, s_list, s_pid,
+                                    tid, lane, wid);
+    if (!ALPHA || !__all_sync(kFull, done0 && done1)) {
+      for (int i = 0; i < cnt; ++i) {
+        const int j = s_list[wid][i];
+        const float4 r0 = s_rec[0][j], r1 = s_rec[1][j];
+        float dx0, dy0, dx1, dy1;
+        const float e0 = pair_exponent(r0, r1, px, py0, dx0, dy0);
+        const float e1 = pair_exponent(r0, r1, px, py1, dx1, dy1);
+        bool h0 = e0 >= a.skip_e && !done0, h1 = e1 >= a.skip_e && !done1;
+        if (STATS) { n_ell += (h0 && in0) + (h1 && in1); }
+        if (!__any_sync(kFull, h0 || h1)) continue;
+        const float4 r2 = s_rec[2][j], r3 = s_rec[3][j];
+        const int pos = b0 + j - start + 1;
+        // pixel 0
+        if (h0) {
+          const float w = pair_weight(ex2(e0), cos_a(pair_theta(r2, dx0, dy0)), r2);
+          if (w >= a.alpha_min) {
             if (!ALPHA) {
-              if (STATS && inside) ++n_con;
-              C0 = __fmaf_rn(r2.z, e.w, C0);
-              C1 = __fmaf_rn(r2.w, e.w, C1);
-              C2 = __fmaf_rn(r3.x, e.w, C2);
+              if (STATS) n_con += in0;
+              C00 = __fmaf_rn(r3.x, w, C00);
+              C01 = __fmaf_rn(r3.y, w, C01);
+              C02 = __fmaf_rn(r3.z, w, C02);
             } else {
-              const float al = fminf(a.alpha_max, e.w);
-              const float Tn = __fmul_rn(T, __fsub_rn(1.f, al));
+              const float al = fminf(a.alpha_max, w);
+              const float Tn = __fmul_rn(T0, __fsub_rn(1.f, al));
               if (Tn < a.T_min) {
-                done = true;
-                if (STATS) stop_pos = b0 + j - start + 1;
+                done0 = true;
+                if (STATS) stop0 = pos;
               } else {
                 if (STATS) ++n_con;
-                const float aT = __fmul_rn(al, T);
-                C0 = __fmaf_rn(r2.z, aT, C0);
-                C1 = __fmaf_rn(r2.w, aT, C1);
-                C2 = __fmaf_rn(r3.x, aT, C2);
-                T = Tn;
-                last = b0 + j - start + 1;
+                const float aT = __fmul_rn(al, T0);
+                C00 = __fmaf_rn(r3.x, aT, C00);
+                C01 = __fmaf_rn(r3.y, aT, C01);
+                C02 = __fmaf_rn(r3.z, aT, C02);
+                T0 = Tn;
+                last0 = pos;
               }
             }
           }
         }
-        if (ALPHA && __all_sync(kFull, done)) { warp_done = true; break; }
+        // pixel 1
+        if (h1) {
+          const float w = pair_weight(ex2(e1), cos_a(pair_theta(r2, dx1, dy1)), r2);
+          if (w >= a.alpha_min) {
+            if (!ALPHA) {
+              if (STATS) n_con += in1;
+              C10 = __fmaf_rn(r3.x, w, C10);
+              C11 = __fmaf_rn(r3.y, w, C11);
+              C12 = __fmaf_rn(r3.z, w, C12);
+            } else {
+              const float al = fminf(a.alpha_max, w);
+              const float Tn = __fmul_rn(T1, __fsub_rn(1.f, al));
+              if (Tn < a.T_min) {
+                done1 = true;
+                if (STATS) stop1 = pos;
+              } else {
+                if (STATS) ++n_con;
+                const float aT = __fmul_rn(al, T1);
+                C10 = __fmaf_rn(r3.x, aT, C10);
+                C11 = __fmaf_rn(r3.y, aT, C11);
+                C12 = __fmaf_rn(r3.z, aT, C12);
+                T1 = Tn;
+                last1 = pos;
+              }
+            }
+          }
+        }
+        if (ALPHA && __all_sync(kFull, done0 && done1)) break;
       }
     }
     if (ALPHA) {
-      if (__syncthreads_count(!done) == 0) break;
+      if (__syncthreads_count(!(done0 && done1)) == 0) break;
     }
   }
   if (STATS) {
-    unsigned long long c3[3] = {inside ? (unsigned long long)stop_pos : 0ull,
-                                (unsigned long long)n_ell, (unsigned long long)n_con};
+    unsigned long long c3[3] = {
+        (in0 ? (unsigned long long)stop0 : 0ull) + (in1 ? (unsigned long long)stop1 : 0ull),
+        (unsigned long long)n_ell, (unsigned long long)n_con};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      unsigned long long v = c3[k];
+      unsigned long long s = c3[k];
 #pragma unroll
-      for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-      if (lane == 0) atomicAdd(a.stats + k, v);
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+      if (lane == 0) atomicAdd(a.stats + k, s);
     }
     return;
   }
-  if (!inside) return;
   const int64_t HW = (int64_t)a.H * a.W;
-  const int64_t pix = (int64_t)y * a.W + x;
-  if (ALPHA) {
-    C0 = __fmaf_rn(T, a.bg0, C0);
-    C1 = __fmaf_rn(T, a.bg1, C1);
-    C2 = __fmaf_rn(T, a.bg2, C2);
-    a.T_final[v * HW + pix] = T;
-    a.n_contrib[v * HW + pix] = last;
+  float* img = a.image + v * 3 * HW;
+  if (in0) {
+    const int64_t p = (int64_t)y0 * a.W + x;
+    if (ALPHA) {
+      C00 = __fmaf_rn(T0, a.bg0, C00);
+      C01 = __fmaf_rn(T0, a.bg1, C01);
+      C02 = __fmaf_rn(T0, a.bg2, C02);
+      a.T_final[v * HW + p] = T0;
+      a.n_contrib[v * HW + p] = last0;
+    }
+    img[p] = C00; img[HW + p] = C01; img[2 * HW + p] = C02;
   }
-  float* img = a.image + v * 3 * HW + pix;
-  img[0] = C0;
-  img[HW] = C1;
-  img[2 * HW] = C2;
+  if (in1) {
+    const int64_t p = (int64_t)y1 * a.W + x;
+    if (ALPHA) {
+      C10 = __fmaf_rn(T1, a.bg0, C10);
+      C11 = __fmaf_rn(T1, a.bg1, C11);
+      C12 = __fmaf_rn(T1, a.bg2, C12);
+      a.T_final[v * HW + p] = T1;
+      a.n_contrib[v * HW + p] = last1;
+    }
+    img[p] = C10; img[HW + p] = C11; img[2 * HW + p] = C12;
+  }
 }
 
-// 16-value warp transpose-reduce: returns, in every lane L, the warp-wide sum
-// of value index (L >> 1) & 15.
-__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+// 12-slot warp transpose-reduce. On return lane L holds the warp-wide sum of
+// moment index 6*b4 + 3*b3 + q (b_k = bit k of L, q = (L >> 1) & 3) when q < 3.
+__device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) {
   {
     const bool up = lane & 16;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float send = up ? v[k] : v[k + 8];
-      float keep = up ? v[k + 8] : v[k];
+    for (int k = 0; k < 6; ++k) {
+      float send = up ? v[k] : v[k + 6];
+      float keep = up ? v[k + 6] : v[k];
       v[k] = keep + __shfl_xor_sync(kFull, send, 16);
     }
   }
   {
     const bool up = lane & 8;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float send = up ? v[k] : v[k + 4];
-      float keep = up ? v[k + 4] : v[k];
+    for (int k = 0; k < 3; ++k) {
+      float send = up ? v[k] : v[k + 3];
+      float keep = up ? v[k + 3] : v[k];
       v[k] = keep + __shfl_xor_sync(kFull, send, 8);
     }
   }
   {
-    const bool up = lane & 4;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      float send = up ? v[k] : v[k + 2];
-      float keep = up ? v[k + 2] : v[k];
-      v[k] = keep + __shfl_xor_sync(kFull, send, 4);
-    }
+    const bool up = lane & 4;  // pairs (0, 2) and (1, pad)
+    float s0 = up ? v[0] : v[2], k0 = up ? v[2] : v[0];
+    float s1 = up ? v[1] : 0.f, k1 = up ? 0.f : v[1];
+    v[0] = k0 + __shfl_xor_sync(kFull, s0, 4);
+    v[1] = k1 + __shfl_xor_sync(kFull, s1, 4);
   }
   {
     const bool up = lane & 2;
-    float send = up ? v[0] : v[1];
-    float keep = up ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(kFull, send, 2);
+    float s = up ? v[0] : v[1], k = up ? v[1] : v[0];
+    v[0] = k + __shfl_xor_sync(kFull, s, 2);
   }
   return v[0] + __shfl_xor_sync(kFull, v[0], 1);
 }
 
+// Moments of one valid pair: with gw = dL/dw,
+//   M0 = gw w, M1 = gw w dx, M2 = gw w dy, M3 = gw w dx^2, M4 = gw w dx dy,
+//   M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx, M8 = M6 dy, M9..11 = colour terms.
+__device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w, float ag,
+                                            float sn, float dx, float dy, float c0, float c1,
+                                            float c2) {
+  const float gww = gw * w;
+  const float m1 = gww * dx, m2 = gww * dy;
+  const float m6 = gw * ag * sn;
+  m[0] += gww;
+  m[1] += m1;
+  m[2] += m2;
+  m[3] = __fmaf_rn(m1, dx, m[3]);
+  m[4] = __fmaf_rn(m1, dy, m[4]);
+  m[5] = __fmaf_rn(m2, dy, m[5]);
+  m[6] += m6;
+  m[7] = __fmaf_rn(m6, dx, m[7]);
+  m[8] = __fmaf_rn(m6, dy, m[8]);
+  m[9] += c0;
+  m[10] += c1;
+  m[11] += c2;
+}
+
 template <int TS, bool ALPHA>
-__global__ void __launch_bounds__(TS* TS) k_render_bwd(RenderArgs a) {
-  constexpr int NT = TS * TS;
-  constexpr int NB = NT < kBatch ? NT : kBatch;
-  constexpr int NSX = TS / 8;
-  __shared__ float4 s_rec[NB][4];
-  __shared__ float4 s_aux[NB];  // unscaled conic (a, b, c), 1/alpha
+__global__ void __launch_bounds__(Geo<TS>::NT) k_render_bwd(RenderArgs a) {
+  using G = Geo<TS>;
+  constexpr int NB = G::NB;
+  __shared__ float4 s_rec[4][NB];
   __shared__ uint32_t s_mask[NB];
-  __shared__ int32_t s_rid[NB];
+  __shared__ uint8_t s_list[G::NW][NB];
+  __shared__ int32_t s_pid[NB];
   __shared__ int32_t s_maxlast;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t tile = blockIdx.x;
@@ -281,137 +373,152 @@ __global__ void __launch_bounds__(TS* TS) k_render_bwd(RenderArgs a) {
   const int64_t t_in_v = tile - v * a.T;
   const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
   const int X0 = tx * TS, Y0 = ty * TS;
-  const int sx = wid % NSX, sy = wid / NSX;
-  const int x = X0 + sx * 8 + (lane & 7), y = Y0 + sy * 4 + (lane >> 3);
-  const bool inside = x < a.W && y < a.H;
-  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const int x = X0 + (wid % G::NS) * 8 + (lane & 7);
+  const int y0 = Y0 + (wid / G::NS) * 8 + (lane >> 3), y1 = y0 + 4;
+  const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
+  const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f, py1 = (float)y1 + 0.5f;
   const int start = a.toff[tile];
   int end = a.toff[tile + 1];
   const int64_t HW = (int64_t)a.H * a.W;
-  const int64_t pix = v * HW + (int64_t)y * a.W + x;
-  float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-  float T = 1.f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-  int last = 0;
-  if (inside) {
-    const float* gp = a.dLdC + v * 3 * HW + (int64_t)y * a.W + x;
-    g0 = gp[0]; g1 = gp[HW]; g2 = gp[2 * HW];
+  const int64_t p0 = v * HW + (int64_t)y0 * a.W + x, p1 = v * HW + (int64_t)y1 * a.W + x;
+  float g00 = 0.f, g01 = 0.f, g02 = 0.f, g10 = 0.f, g11 = 0.f, g12 = 0.f;
+  float T0 = 1.f, T1 = 1.f, S00 = 0.f, S01 = 0.f, S02 = 0.f, S10 = 0.f, S11 = 0.f, S12 = 0.f;
+  int last0 = 0, last1 = 0;
+  const float* gp = a.dLdC + v * 3 * HW;
+  if (in0) {
+    const int64_t q = (int64_t)y0 * a.W + x;
+    g00 = gp[q]; g01 = gp[HW + q]; g02 = gp[2 * HW + q];
     if (ALPHA) {
-      T = a.T_in[pix];
-      last = a.nc_in[pix];
-      S0 = T * a.bg0; S1 = T * a.bg1; S2 = T * a.bg2;
+      T0 = a.T_in[p0]; last0 = a.nc_in[p0];
+      S00 = T0 * a.bg0; S01 = T0 * a.bg1; S02 = T0 * a.bg2;
+    }
+  }
+  if (in1) {
+    const int64_t q = (int64_t)y1 * a.W + x;
+    g10 = gp[q]; g11 = gp[HW + q]; g12 = gp[2 * HW + q];
+    if (ALPHA) {
+      T1 = a.T_in[p1]; last1 = a.nc_in[p1];
+      S10 = T1 * a.bg0; S11 = T1 * a.bg1; S12 = T1 * a.bg2;
     }
   }
   if (ALPHA) {
     if (tid == 0) s_maxlast = 0;
     __syncthreads();
-    if (last > 0) atomicMax(&s_maxlast, last);
+    const int ml = max(last0, last1);
+    if (ml > 0) atomicMax(&s_maxlast, ml);
     __syncthreads();
     end = start + s_maxlast;
   }
-  const uint32_t mybit = 1u << wid;
+  const float4* recv = a.rec + 4 * (v * a.N);
   const int64_t vN = v * a.N;
-  const float4* recv = a.rec + 4 * vN;
   const int nbatch = (end - start + NB - 1) / NB;
+  const int q3 = (lane >> 1) & 3;
+  const int my_m = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
+  const bool writer = !(lane & 1) && q3 < 3;
   for (int bi = 0; bi < nbatch; ++bi) {
     // ALPHA walks batches back to front; SUM front to back (order-free).
     const int b0 = ALPHA ? max(start, end - (bi + 1) * NB) : start + bi * NB;
     const int nb = ALPHA ? (end - bi * NB) - b0 : min(NB, end - b0);
     __syncthreads();
-    if (tid < nb) {
-      const uint32_t pid = a.vals[b0 + tid];
-      const float4* r = recv + 4 * (int64_t)pid;
-      float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-      s_rec[tid][0] = r0; s_rec[tid][1] = r1; s_rec[tid][2] = r2; s_rec[tid][3] = r3;
-      s_aux[tid] = make_float4(r0.z * kInvHalfLog2e, r0.w * (0.5f * kInvHalfLog2e),
-                               r1.x * kInvHalfLog2e, ex2(-r1.y));
-      s_mask[tid] = subtile_mask<TS>(r0, r3, X0, Y0);
-      s_rid[tid] = (int32_t)pid;
-    }
-    __syncthreads();
-    for (int jj = 0; jj < nb; ++jj) {
-      const int j = ALPHA ? nb - 1 - jj : jj;
-      if (!(s_mask[j] & mybit)) continue;  // warp-uniform
-      const int pos = b0 + j - start;      // index within the tile list
-      const float4 r0 = s_rec[j][0], r1 = s_rec[j][1], r2 = s_rec[j][2], r3 = s_rec[j][3];
-      PairEval e;
-      float cs = 0.f;
-      bool valid = inside && (!ALPHA || pos < last);
-      if (valid) {
-        eval_pair(r0, r1, r2, r3, px, py, a.skip_e, a.alpha_min, e, cs);
-        valid = e.ok;
-      }
-      if (!__any_sync(kFull, valid)) continue;
-      float vals[16];
+    const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, s_rec, s_mask, s_list, s_pid,
+                                    tid, lane, wid);
+    for (int ii = 0; ii < cnt; ++ii) {
+      const int j = s_list[wid][ALPHA ? cnt - 1 - ii : ii];
+      const int pos = b0 + j - start;  // index within the tile list
+      const float4 r0 = s_rec[0][j], r1 = s_rec[1][j];
+      float dx0, dy0, dx1, dy1;
+      const float e0 = pair_exponent(r0, r1, px, py0, dx0, dy0);
+      const float e1 = pair_exponent(r0, r1, px, py1, dx1, dy1);
+      bool h0 = in0 && e0 >= a.skip_e && (!ALPHA || pos < last0);
+      bool h1 = in1 && e1 >= a.skip_e && (!ALPHA || pos < last1);
+      if (!__any_sync(kFull, h0 || h1)) continue;
+      const float4 r2 = s_rec[2][j], r3 = s_rec[3][j];
+      float m[kMom];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) vals[k] = 0.f;
-      if (valid) {
-        const float4 aux = s_aux[j];
-        const float sn = sin_a(e.th);
-        const float gdc = __fmaf_rn(r2.z, g0, __fmaf_rn(r2.w, g1, __fmul_rn(r3.x, g2)));
-        float gw;
-        if (!ALPHA) {
-          gw = gdc;
-          vals[RG_CR] = e.w * g0;
-          vals[RG_CG] = e.w * g1;
-          vals[RG_CB] = e.w * g2;
-        } else {
-          const float al = fminf(a.alpha_max, e.w);
-          const float ri = rcp_a(1.f - al);
-          const float Tk = T * ri;
-          const float sdg = __fmaf_rn(S0, g0, __fmaf_rn(S1, g1, __fmul_rn(S2, g2)));
-          const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
-          const float aT = al * Tk;
-          vals[RG_CR] = aT * g0;
-          vals[RG_CG] = aT * g1;
-          vals[RG_CB] = aT * g2;
-          S0 = __fmaf_rn(r2.z, aT, S0);
-          S1 = __fmaf_rn(r2.w, aT, S1);
-          S2 = __fmaf_rn(r3.x, aT, S2);
-          T = Tk;
-          gw = (e.w < a.alpha_max) ? dLda : 0.f;
+      for (int k = 0; k < kMom; ++k) m[k] = 0.f;
+      bool any = false;
+      if (h0) {
+        const float ag = ex2(e0);
+        const float th = pair_theta(r2, dx0, dy0);
+        const float cs = cos_a(th);
+        const float w = pair_weight(ag, cs, r2);
+        if (w >= a.alpha_min) {
+          any = true;
+          const float sn = sin_a(th);
+          const float gdc = __fmaf_rn(r3.x, g00, __fmaf_rn(r3.y, g01, __fmul_rn(r3.z, g02)));
+          if (!ALPHA) {
+            add_moments(m, gdc, w, ag, sn, dx0, dy0, w * g00, w * g01, w * g02);
+          } else {
+            const float al = fminf(a.alpha_max, w);
+            const float ri = rcp_a(1.f - al);
+            const float Tk = T0 * ri;
+            const float sdg = __fmaf_rn(S00, g00, __fmaf_rn(S01, g01, __fmul_rn(S02, g02)));
+            const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
+            const float aT = al * Tk;
+            S00 = __fmaf_rn(r3.x, aT, S00);
+            S01 = __fmaf_rn(r3.y, aT, S01);
+            S02 = __fmaf_rn(r3.z, aT, S02);
+            T0 = Tk;
+            add_moments(m, (w < a.alpha_max) ? dLda : 0.f, w, ag, sn, dx0, dy0, aT * g00,
+                        aT * g01, aT * g02);
+          }
         }
-        const float s = -r2.y * e.ag * sn;    // dw/dtheta
-        const float gs = gw * s;
-        const float gww = gw * e.w;
-        vals[RG_FX] = gs * e.dx;
-        vals[RG_FY] = gs * e.dy;
-        vals[RG_PHI] = gs;
-        vals[RG_MUX] = __fmaf_rn(gww, __fmaf_rn(aux.x, e.dx, aux.y * e.dy), -gs * r1.z);
-        vals[RG_MUY] = __fmaf_rn(gww, __fmaf_rn(aux.y, e.dx, aux.z * e.dy), -gs * r1.w);
-        const float hg = -0.5f * gww;
-        vals[RG_A] = hg * e.dx * e.dx;
-        vals[RG_B] = -gww * e.dx * e.dy;
-        vals[RG_C] = hg * e.dy * e.dy;
-        vals[RG_BETA] = gw * 0.5f * e.ag * cs;
-        vals[RG_ALPHA] = gww * aux.w;
       }
-      const float red = transpose_reduce16(vals, lane);
-      const int k = lane >> 1;
-      if (!(lane & 1) && k < kRecGrads)
-        atomicAdd(a.rgrad + (vN + s_rid[j]) * kRecGrads + k, red);
+      if (h1) {
+        const float ag = ex2(e1);
+        const float th = pair_theta(r2, dx1, dy1);
+        const float cs = cos_a(th);
+        const float w = pair_weight(ag, cs, r2);
+        if (w >= a.alpha_min) {
+          any = true;
+          const float sn = sin_a(th);
+          const float gdc = __fmaf_rn(r3.x, g10, __fmaf_rn(r3.y, g11, __fmul_rn(r3.z, g12)));
+          if (!ALPHA) {
+            add_moments(m, gdc, w, ag, sn, dx1, dy1, w * g10, w * g11, w * g12);
+          } else {
+            const float al = fminf(a.alpha_max, w);
+            const float ri = rcp_a(1.f - al);
+            const float Tk = T1 * ri;
+            const float sdg = __fmaf_rn(S10, g10, __fmaf_rn(S11, g11, __fmul_rn(S12, g12)));
+            const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
+            const float aT = al * Tk;
+            S10 = __fmaf_rn(r3.x, aT, S10);
+            S11 = __fmaf_rn(r3.y, aT, S11);
+            S12 = __fmaf_rn(r3.z, aT, S12);
+            T1 = Tk;
+            add_moments(m, (w < a.alpha_max) ? dLda : 0.f, w, ag, sn, dx1, dy1, aT * g10,
+                        aT * g11, aT * g12);
+          }
+        }
+      }
+      if (!__any_sync(kFull, any)) continue;
+      const float red = transpose_reduce12(m, lane);
+      if (writer) atomicAdd(a.mom + (vN + s_pid[j]) * kMom + my_m, red);
     }
   }
 }
 
 template <int TS>
 cudaError_t launch_fwd_ts(bool alpha, const RenderArgs& ra, unsigned grid, cudaStream_t s) {
+  constexpr int NT = Geo<TS>::NT;
   if (ra.stats) {
-    if (alpha) k_render_fwd<TS, true, true><<<grid, TS * TS, 0, s>>>(ra);
-    else k_render_fwd<TS, false, true><<<grid, TS * TS, 0, s>>>(ra);
+    if (alpha) k_render_fwd<TS, true, true><<<grid, NT, 0, s>>>(ra);
+    else k_render_fwd<TS, false, true><<<grid, NT, 0, s>>>(ra);
     return cudaGetLastError();
   }
   launch_begin(K_RENDER_FWD, s);
-  if (alpha) k_render_fwd<TS, true, false><<<grid, TS * TS, 0, s>>>(ra);
-  else k_render_fwd<TS, false, false><<<grid, TS * TS, 0, s>>>(ra);
+  if (alpha) k_render_fwd<TS, true, false><<<grid, NT, 0, s>>>(ra);
+  else k_render_fwd<TS, false, false><<<grid, NT, 0, s>>>(ra);
   launch_end(K_RENDER_FWD, s);
   return cudaGetLastError();
 }
 
 template <int TS>
 cudaError_t launch_bwd_ts(bool alpha, const RenderArgs& ra, unsigned grid, cudaStream_t s) {
+  constexpr int NT = Geo<TS>::NT;
   launch_begin(K_RENDER_BWD, s);
-  if (alpha) k_render_bwd<TS, true><<<grid, TS * TS, 0, s>>>(ra);
-  else k_render_bwd<TS, false><<<grid, TS * TS, 0, s>>>(ra);
+  if (alpha) k_render_bwd<TS, true><<<grid, NT, 0, s>>>(ra);
+  else k_render_bwd<TS, false><<<grid, NT, 0, s>>>(ra);
   launch_end(K_RENDER_BWD, s);
   return cudaGetLastError();
 }
@@ -433,7 +540,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.bg0 = c.background[0]; ra.bg1 = c.background[1]; ra.bg2 = c.background[2];
   ra.image = nullptr; ra.T_final = nullptr; ra.n_contrib = nullptr;
   ra.dLdC = nullptr; ra.T_in = nullptr; ra.nc_in = nullptr;
-  ra.rgrad = (float*)(ws + L.rgrad);
+  ra.mom = (float*)(ws + L.rgrad);
   ra.stats = nullptr;
   return ra;
 }

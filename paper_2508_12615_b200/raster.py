@@ -197,12 +197,12 @@ class Rasterizer:
                                          self.cap, abi.ptr(out), _stream()), "wipes_render_stats")
         return tuple(int(x) for x in out.cpu())
 
-    def get_record_grads(self):
-        out = torch.empty((self.B * self.N, abi.RECORD_GRADS), dtype=torch.float32,
+    def get_grad_moments(self):
+        out = torch.empty((self.B * self.N, abi.GRAD_MOMENTS), dtype=torch.float32,
                           device=self.device)
-        abi.check(abi.wipes_get_record_grads(self.cfg, self.N, self.B, self._ws_ptr(),
+        abi.check(abi.wipes_get_grad_moments(self.cfg, self.N, self.B, self._ws_ptr(),
                                              self.ws_bytes, self.cap, abi.ptr(out), _stream()),
-                  "wipes_get_record_grads")
+                  "wipes_get_grad_moments")
         return out
 
     def bin_sort_outputs(self):
