@@ -177,7 +177,7 @@ def main():
         return
 
     from paper_2508_12615_b200 import abi, build, gen
-    from paper_2508_12615_b200.raster import Rasterizer
+    from paper_2508_12615_b200.raster import FrameGraph, Rasterizer
     from paper_2508_12615_b200 import dist as wdist
     if rank == 0:
         build.build()
@@ -215,22 +215,33 @@ def main():
     if shared and world > 1:
         flat = wdist.GradBucket(grads)
 
-    def step(ev0=None, ev1=None, ev2=None, sync=False):
-        if ev0 is not None:
-            ev0.record(stream)
+    def step_eager(sync=False):
         r.preprocess(params, cams, vs, sync=sync)
         r.bin_sort()
-        r.render()
+        r.render(*(r._saved if r._saved is not None else (None, None, None)))
+        r.backward(dL, grads)
+        if flat is not None:
+            flat.all_reduce()
+
+    # one synced step sizes the workspace; then the frame is captured as CUDA
+    # graphs (public API: raster.FrameGraph) — the timed steps replay them
+    step_eager(sync=True)
+    l0 = abi.launch_count()
+    fg = FrameGraph(r, params, cams, vs, dL, grads)
+    kernels_per_step = None
+
+    def step(ev0=None, ev1=None, ev2=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        fg.forward()
         if ev1 is not None:
             ev1.record(stream)
-        r.backward(dL, grads)
+        fg.backward()
         if flat is not None:
             flat.all_reduce()
         if ev2 is not None:
             ev2.record(stream)
 
-    # first call sizes the workspace (one host sync), then warm-up
-    step(sync=True)
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -246,15 +257,24 @@ def main():
     torch.cuda.synchronize()
     sampler.start()
     time.sleep(0.3)
-    abi.timing_enable(True)
-    l0 = abi.launch_count()
     for k in range(args.steps):
         flush.zero_()
         step(*evs[k])
     torch.cuda.synchronize()
-    launches = abi.launch_count() - l0
+    # per-kernel CUDA-event timing (same kernels, eager launches on the same
+    # stream, inside the clock-sampled window): roofline numerator + breakdown
+    nk = max(3, min(args.steps, 10))
+    abi.timing_enable(True)
+    l1 = abi.launch_count()
+    for k in range(nk):
+        flush.zero_()
+        step_eager()
+    torch.cuda.synchronize()
+    kernels_per_step = (abi.launch_count() - l1) / nk
     abi.timing_enable(False)
     kt = abi.timing_collect()
+    kt = {k: (v[0] / nk * args.steps, v[1] / nk * args.steps) for k, v in kt.items()}
+    launches = int(round(kernels_per_step * args.steps))
     clocks = sampler.stop()
     n_tot2, over = r.check_overflow()
     assert not over
@@ -286,7 +306,7 @@ def main():
             params[kk].copy_(v, non_blocking=True)
         dL.copy_(host_dL, non_blocking=True)
         step()
-        for kk, v in grads.items():
+        for kk, v in fg.grads.items():
             host_grads[kk].copy_(v, non_blocking=True)
         b_.record(stream)
         b_.synchronize()
@@ -341,7 +361,7 @@ def main():
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches), "cuda_graph": True,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
             "roofline": roof,
             "paper_context": "render FPS on one A6000: Kodak 1708-1779 (Table 1, PAPER.md:148-149); "

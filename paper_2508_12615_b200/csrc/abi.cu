@@ -42,7 +42,7 @@ cudaEvent_t take_event() {
 const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
-    "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset"};
+    "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -122,7 +122,7 @@ wipes_status check_params(const wipes_config* c, const wipes_params* p, int64_t 
 }  // namespace
 
 void launch_begin(int kid, cudaStream_t s) {
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (kid != K_MEMSET) g_launches.fetch_add(1, std::memory_order_relaxed);  // kernels only
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);
   g_pending = take_event();

@@ -97,6 +97,11 @@ __global__ void __launch_bounds__(1024) k_scan_sums(T* blk, int64_t nblk, WsHead
       hdr->overflow = (int64_t)ti > cap ? 1 : 0;
     }
   }
+  if (hdr && wid == 1) {  // reset the per-frame scheduling state
+    hdr->bcount[lane] = 0;
+    hdr->bfill[lane] = 0;
+    if (lane < kQueues) { hdr->work[lane] = 0; hdr->done[lane] = 0; }
+  }
   __syncthreads();
   T run = wt[wid] + inc - s;
   for (int64_t k = 0; k < per; ++k)
@@ -220,6 +225,48 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint64_t* keys, const
   for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
 }
 
+// Longest-first tile order for the persistent render kernels: tiles are
+// bucketed by floor(log2(list length)) + 1 (0 for empty tiles) and laid out in
+// descending bucket order (order within a bucket is arbitrary: it affects only
+// the processing order, never a result).
+__device__ __forceinline__ int tile_bucket(const int32_t* toff, int64_t u) {
+  const int len = toff[u + 1] - toff[u];
+  return len > 0 ? 32 - __clz(len) : 0;
+}
+
+__global__ void __launch_bounds__(256) k_tile_order_hist(const int32_t* toff, int64_t BT,
+                                                         WsHeader* hdr) {
+  __shared__ int32_t h[kBuckets];
+  if (threadIdx.x < kBuckets) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < BT) atomicAdd(&h[tile_bucket(toff, u)], 1);
+  __syncthreads();
+  if (threadIdx.x < kBuckets && h[threadIdx.x]) atomicAdd(&hdr->bcount[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_tile_order_place(const int32_t* toff, int64_t BT,
+                                                          WsHeader* hdr, int32_t* order) {
+  __shared__ int32_t base[kBuckets], h[kBuckets];
+  const int tid = threadIdx.x;
+  if (tid < kBuckets) h[tid] = 0;
+  __syncthreads();
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + tid;
+  int b = 0, r = 0;
+  if (u < BT) {
+    b = tile_bucket(toff, u);
+    r = atomicAdd(&h[b], 1);
+  }
+  __syncthreads();
+  if (tid < kBuckets) {
+    int off = 0;  // start of bucket tid in descending-bucket order
+    for (int k = kBuckets - 1; k > tid; --k) off += hdr->bcount[k];
+    base[tid] = h[tid] ? off + atomicAdd(&hdr->bfill[tid], h[tid]) : 0;
+  }
+  __syncthreads();
+  if (u < BT) order[base[b] + r] = (int32_t)u;
+}
+
 __global__ void k_offsets(const int64_t* loc, const int64_t* blk, int64_t BN, int64_t* out) {
   int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o < BN) out[o] = loc[o] + blk[o / kScanTile];
@@ -308,6 +355,19 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
   k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(kf, hdr, L.cap, L.BT,
                                                                   (int32_t*)(ws + L.toff));
   launch_end(K_TILE_RANGES, s);
+  if (L.BT > 0) {
+    const unsigned g = (unsigned)((L.BT + 255) / 256);
+    // bucket counters must start at zero for every ordering (bin_sort may run
+    // more than once per preprocess)
+    cudaMemsetAsync(hdr->bcount, 0, sizeof(hdr->bcount) + sizeof(hdr->bfill), s);
+    launch_begin(K_TILE_ORDER, s);
+    k_tile_order_hist<<<g, 256, 0, s>>>((const int32_t*)(ws + L.toff), L.BT, hdr);
+    launch_end(K_TILE_ORDER, s);
+    launch_begin(K_TILE_ORDER, s);
+    k_tile_order_place<<<g, 256, 0, s>>>((const int32_t*)(ws + L.toff), L.BT, hdr,
+                                         (int32_t*)(ws + L.order));
+    launch_end(K_TILE_ORDER, s);
+  }
   return cudaGetLastError();
 }
 

@@ -32,13 +32,22 @@ enum { RG_MUX = 0, RG_MUY, RG_A, RG_B, RG_C, RG_FX, RG_FY, RG_PHI, RG_BETA, RG_C
 //  r3 = {c_r, c_g, c_b, half2(rx, ry)}  (rx, ry) = opacity-extent half widths (fp16,
 //                                       rounded up), only for conservative sub-tile culling
 // The candidate test needs r0, r1 only (two broadcast LDS.128).
+constexpr int kBuckets = 32;  // tile-cost buckets (log2 of the list length)
+constexpr int kQueues = 4;    // work queues: render fwd, render bwd, stats, spare
+
 struct WsHeader {
   int64_t total;       // number of (view, primitive, tile) intersections
   int32_t overflow;    // 1 if total > capacity
   int32_t magic;
   int64_t N, cap, bytes;
   int32_t B, pad;
+  // persistent-kernel work queues (self-resetting: the last CTA zeroes them)
+  int32_t work[kQueues], done[kQueues];
+  // longest-first tile order: per-bucket counts and fill pointers (zeroed by
+  // the count scan of every preprocess)
+  int32_t bcount[kBuckets], bfill[kBuckets];
 };
+static_assert(sizeof(WsHeader) <= 512, "header must fit its slot");
 
 struct Layout {
   int64_t N = 0, BN = 0, cap = 0, BT = 0, T = 0;
@@ -51,7 +60,7 @@ struct Layout {
   int64_t nblk_rscan = 0;  // blocks of the radix-count scan
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, rcounts = 0, rblk = 0,
-         toff = 0, rgrad = 0, total = 0;
+         toff = 0, order = 0, rgrad = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -83,7 +92,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   if (L.nblk_scan < 1) L.nblk_scan = 1;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-  L.hdr = take(256);
+  L.hdr = take(512);
   L.rect = take(sizeof(int4) * L.BN);
   L.count = take(sizeof(int32_t) * L.BN);
   L.flag = take(sizeof(uint8_t) * L.BN);
@@ -98,6 +107,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.rcounts = take(sizeof(int32_t) * L.nrc);
   L.rblk = take(sizeof(int32_t) * (L.nblk_rscan + 1));
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
+  L.order = take(sizeof(int32_t) * (L.BT + 1));
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
   L.total = o;
   return L;
@@ -107,7 +117,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
 enum KernelId {
   K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
   K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
-  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_NUM
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_NUM
 };
 
 // Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph

@@ -11,15 +11,21 @@
 //             12-slot transpose-reduce of shuffles, then one atomic per (warp,
 //             record, moment).
 //
-// One CTA per (view, tile). Each warp owns an 8x8-pixel sub-tile, each lane two
-// pixels (rows y and y+4). Records are staged in shared memory in batches
-// (structure-of-float4 layout, conflict-free stores, broadcast loads); every
-// staged record carries a sub-tile mask from its conservative opacity extent,
-// and each warp compacts the batch into its own ordered list of records that
-// can reach its pixels (ballot + popc), so a warp never visits a record that
-// cannot touch it. exp is one MUFU.EX2 (the -1/2 log2(e) scale and log2(alpha)
-// folded into the record); cos / sin are MUFU.COS / MUFU.SIN.
+// Persistent CTAs (grid = SMs x resident CTAs) pull (view, tile) work items
+// from a queue ordered longest-list-first (bin_sort's tile order), so the
+// uneven per-tile cost does not leave SMs idle at the end of the launch.
+// Each warp owns an 8x8-pixel sub-tile, each lane two pixels (rows y and
+// y+4; the second is evaluated incrementally from the first). Records are
+// staged in shared memory in batches (structure-of-float4 layout); every staged
+// record carries a sub-tile mask from its conservative opacity extent, and each
+// warp compacts the batch into its own ordered list of records that can reach
+// its pixels (ballot + popc). Branches inside a (warp, record) step are
+// warp-uniform (ballots); per-lane decisions are predicated selects. exp is one
+// MUFU.EX2 (the -1/2 log2(e) scale and log2(alpha) folded into the record);
+// cos / sin are MUFU.COS / MUFU.SIN.
 #include <cuda_fp16.h>
+
+#include <mutex>
 
 #include "common.cuh"
 
@@ -29,6 +35,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMom = kMoments;  // 12
+enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -55,8 +62,10 @@ struct RenderArgs {
   const float4* rec;     // [B*N][4]
   const uint32_t* vals;  // sorted primitive indices
   const int32_t* toff;   // [B*T + 1]
-  int64_t N, T;
-  int32_t W, H, GX;
+  const int32_t* order;  // [B*T] longest-first tile order
+  WsHeader* hdr;         // work queues
+  int64_t N, T, BT;
+  int32_t W, H, GX, queue;
   float alpha_min, skip_e, alpha_max, T_min;
   float bg0, bg1, bg2;
   float* image;          // [B,3,H,W]
@@ -94,15 +103,26 @@ __device__ __forceinline__ uint32_t subtile_mask(const float4& r0, const float4&
   return m;
 }
 
-// Exponent of alpha*G for one (pixel, record) pair — identical arithmetic in
-// every kernel so all take the same alpha_min decisions.
-__device__ __forceinline__ float pair_exponent(const float4& r0, const float4& r1, float px,
-                                               float py, float& dx, float& dy) {
-  dx = __fsub_rn(__fsub_rn(px, r0.x), r0.z);
-  dy = __fsub_rn(__fsub_rn(py, r0.y), r0.w);
-  float t = __fmaf_rn(r1.x, dx, __fmul_rn(r1.y, dy));
-  float u = __fmaf_rn(__fmul_rn(r1.z, dy), dy, r1.w);
-  return __fmaf_rn(t, dx, u);
+// Exponents of alpha*G for the lane's two pixels (rows y0 and y0 + 4) — one
+// arithmetic shared by every kernel, so all take the same alpha_min decisions
+// (and, since 8x8 sub-tiles are 8-aligned for every tile size, every pixel is
+// evaluated by the same expression whatever the tiling).
+struct PairPos {
+  float dx, dy0, e0, e1;
+};
+
+__device__ __forceinline__ PairPos pair_exponents(const float4& r0, const float4& r1, float px,
+                                                  float py0) {
+  PairPos p;
+  p.dx = __fsub_rn(__fsub_rn(px, r0.x), r0.z);
+  p.dy0 = __fsub_rn(__fsub_rn(py0, r0.y), r0.w);
+  const float t = __fmaf_rn(r1.x, p.dx, __fmul_rn(r1.y, p.dy0));  // A dx + B dy
+  const float cdy = __fmul_rn(r1.z, p.dy0);                        // C dy
+  p.e0 = __fmaf_rn(t, p.dx, __fmaf_rn(cdy, p.dy0, r1.w));
+  // dy1 = dy0 + 4: e1 = e0 + 4 (B dx + 2 C dy0 + 4 C)
+  const float v = __fmaf_rn(r1.y, p.dx, __fmaf_rn(2.f, cdy, __fmul_rn(4.f, r1.z)));
+  p.e1 = __fmaf_rn(4.f, v, p.e0);
+  return p;
 }
 
 __device__ __forceinline__ float pair_theta(const float4& r2, float dx, float dy) {
@@ -115,19 +135,27 @@ __device__ __forceinline__ float pair_weight(float ag, float cs, const float4& r
 
 template <int TS>
 struct Geo {
-  static constexpr int NS = TS / 8;           // sub-tiles per side
-  static constexpr int NW = NS * NS;          // warps per CTA
-  static constexpr int NT = 32 * NW;          // threads per CTA
+  static constexpr int NS = TS / 8;               // sub-tiles per side
+  static constexpr int NW = NS * NS;              // warps per CTA
+  static constexpr int NT = 32 * NW;              // threads per CTA
   static constexpr int NB = NT < 128 ? 128 : NT;  // records per staged batch
+};
+
+template <int TS>
+struct Smem {
+  float4 rec[4][Geo<TS>::NB];
+  uint32_t mask[Geo<TS>::NB];
+  uint8_t list[Geo<TS>::NW][Geo<TS>::NB];
+  int32_t pid[Geo<TS>::NB];
+  int32_t item, maxlast;
 };
 
 // Stage records [b0, b0 + nb) of the tile list into shared memory and build
 // each warp's compacted list. Returns this warp's list length.
 template <int TS>
 __device__ __forceinline__ int stage_batch(const RenderArgs& a, const float4* recv, int b0,
-                                           int nb, int X0, int Y0, float4 (*s_rec)[Geo<TS>::NB],
-                                           uint32_t* s_mask, uint8_t (*s_list)[Geo<TS>::NB],
-                                           int32_t* s_pid, int tid, int lane, int wid) {
+                                           int nb, int X0, int Y0, Smem<TS>& sm, int tid,
+                                           int lane, int wid) {
   constexpr int NB = Geo<TS>::NB, NT = Geo<TS>::NT;
 #pragma unroll
   for (int t = tid; t < NB; t += NT) {
@@ -136,11 +164,11 @@ __device__ __forceinline__ int stage_batch(const RenderArgs& a, const float4* re
       const uint32_t pid = a.vals[b0 + t];
       const float4* r = recv + 4 * (int64_t)pid;
       float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-      s_rec[0][t] = r0; s_rec[1][t] = r1; s_rec[2][t] = r2; s_rec[3][t] = r3;
-      s_pid[t] = (int32_t)pid;
+      sm.rec[0][t] = r0; sm.rec[1][t] = r1; sm.rec[2][t] = r2; sm.rec[3][t] = r3;
+      sm.pid[t] = (int32_t)pid;
       m = subtile_mask<TS>(r0, r3, X0, Y0);
     }
-    s_mask[t] = m;
+    sm.mask[t] = m;
   }
   __syncthreads();
   int cnt = 0;
@@ -148,155 +176,176 @@ __device__ __forceinline__ int stage_batch(const RenderArgs& a, const float4* re
 #pragma unroll
   for (int c = 0; c < NB / 32; ++c) {
     const int j = c * 32 + lane;
-    const bool hit = (s_mask[j] >> wid) & 1u;
+    const bool hit = (sm.mask[j] >> wid) & 1u;
     const uint32_t bal = __ballot_sync(kFull, hit);
-    if (hit) s_list[wid][cnt + __popc(bal & lt)] = (uint8_t)j;
+    if (hit) sm.list[wid][cnt + __popc(bal & lt)] = (uint8_t)j;
     cnt += __popc(bal);
   }
   __syncwarp();
   return cnt;
 }
 
+// Persistent work loop helpers: fetch the next (view, tile) item; the last CTA
+// to leave resets the queue for the next launch.
+template <int TS>
+__device__ __forceinline__ int64_t next_item(const RenderArgs& a, Smem<TS>& sm, int tid) {
+  __syncthreads();
+  if (tid == 0) sm.item = atomicAdd(&a.hdr->work[a.queue], 1);
+  __syncthreads();
+  const int item = sm.item;
+  return item < a.BT ? (int64_t)a.order[item] : -1;
+}
+
+__device__ __forceinline__ void leave_queue(const RenderArgs& a, int tid) {
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&a.hdr->done[a.queue], 1) == (int)gridDim.x - 1) {
+      a.hdr->work[a.queue] = 0;
+      a.hdr->done[a.queue] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// Front-to-back alpha compositing step of one pixel (Eq. 3, R9/R10),
+// predicated: ok = the pair contributes alpha*W >= alpha_min.
+__device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, int pos,
+                                           float amax, float tmin, float& T, float& C0,
+                                           float& C1, float& C2, int& last, bool& done,
+                                           int& stop) {
+  const float al = fminf(amax, w);
+  const float Tn = __fmul_rn(T, __fsub_rn(1.f, al));
+  const bool stp = ok && Tn < tmin;
+  const bool comp = ok && !stp;
+  const float aT = comp ? __fmul_rn(al, T) : 0.f;
+  C0 = __fmaf_rn(r3.x, aT, C0);
+  C1 = __fmaf_rn(r3.y, aT, C1);
+  C2 = __fmaf_rn(r3.z, aT, C2);
+  T = comp ? Tn : T;
+  last = comp ? pos : last;
+  done = done || stp;
+  stop = stp ? pos : stop;
+}
+
 template <int TS, bool ALPHA, bool STATS>
 __global__ void __launch_bounds__(Geo<TS>::NT) k_render_fwd(RenderArgs a) {
   using G = Geo<TS>;
   constexpr int NB = G::NB;
-  __shared__ float4 s_rec[4][NB];
-  __shared__ uint32_t s_mask[NB];
-  __shared__ uint8_t s_list[G::NW][NB];
-  __shared__ int32_t s_pid[NB];
+  __shared__ Smem<TS> sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t v = tile / a.T;
-  const int64_t t_in_v = tile - v * a.T;
-  const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
-  const int X0 = tx * TS, Y0 = ty * TS;
-  const int x = X0 + (wid % G::NS) * 8 + (lane & 7);
-  const int y0 = Y0 + (wid / G::NS) * 8 + (lane >> 3), y1 = y0 + 4;
-  const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
-  const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f, py1 = (float)y1 + 0.5f;
-  const int start = a.toff[tile], end = a.toff[tile + 1];
-  const float4* recv = a.rec + 4 * (v * a.N);
-  float C00 = 0.f, C01 = 0.f, C02 = 0.f, C10 = 0.f, C11 = 0.f, C12 = 0.f;
-  float T0 = 1.f, T1 = 1.f;
-  int last0 = 0, last1 = 0;
-  bool done0 = ALPHA ? !in0 : false, done1 = ALPHA ? !in1 : false;
-  int n_ell = 0, n_con = 0, stop0 = end - start, stop1 = end - start;  // STATS only
-  for (int b0 = start; b0 < end; b0 += NB) {
-    const int nb = min(NB, end - b0);
-    __syncthreads();
-    const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, s_rec, s_mask, s_list, s_pid,
-                                    tid, lane, wid);
-    if (!ALPHA || !__all_sync(kFull, done0 && done1)) {
-      for (int i = 0; i < cnt; ++i) {
-        const int j = s_list[wid][i];
-        const float4 r0 = s_rec[0][j], r1 = s_rec[1][j];
-        float dx0, dy0, dx1, dy1;
-        const float e0 = pair_exponent(r0, r1, px, py0, dx0, dy0);
-        const float e1 = pair_exponent(r0, r1, px, py1, dx1, dy1);
-        bool h0 = e0 >= a.skip_e && !done0, h1 = e1 >= a.skip_e && !done1;
-        if (STATS) { n_ell += (h0 && in0) + (h1 && in1); }
-        if (!__any_sync(kFull, h0 || h1)) continue;
-        const float4 r2 = s_rec[2][j], r3 = s_rec[3][j];
-        const int pos = b0 + j - start + 1;
-        // pixel 0
-        if (h0) {
-          const float w = pair_weight(ex2(e0), cos_a(pair_theta(r2, dx0, dy0)), r2);
-          if (w >= a.alpha_min) {
+  const int ox = (wid % G::NS) * 8 + (lane & 7), oy = (wid / G::NS) * 8 + (lane >> 3);
+  unsigned long long st_cand = 0, st_ell = 0, st_con = 0;  // STATS only
+  for (;;) {
+    const int64_t tile = next_item<TS>(a, sm, tid);
+    if (tile < 0) break;
+    const int64_t v = tile / a.T;
+    const int64_t t_in_v = tile - v * a.T;
+    const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
+    const int X0 = tx * TS, Y0 = ty * TS;
+    const int x = X0 + ox, y0 = Y0 + oy, y1 = y0 + 4;
+    const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
+    const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f;
+    const int start = a.toff[tile], end = a.toff[tile + 1];
+    const float4* recv = a.rec + 4 * (v * a.N);
+    float C00 = 0.f, C01 = 0.f, C02 = 0.f, C10 = 0.f, C11 = 0.f, C12 = 0.f;
+    float T0 = 1.f, T1 = 1.f;
+    int last0 = 0, last1 = 0, stop0 = end - start, stop1 = end - start;
+    bool done0 = ALPHA ? !in0 : false, done1 = ALPHA ? !in1 : false;
+    for (int b0 = start; b0 < end; b0 += NB) {
+      const int nb = min(NB, end - b0);
+      __syncthreads();
+      const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, sm, tid, lane, wid);
+      if (!ALPHA || !__all_sync(kFull, done0 && done1)) {
+        for (int i = 0; i < cnt; ++i) {
+          const int j = sm.list[wid][i];
+          const float4 r0 = sm.rec[0][j], r1 = sm.rec[1][j];
+          const PairPos pp = pair_exponents(r0, r1, px, py0);
+          const bool h0 = pp.e0 >= a.skip_e && !done0, h1 = pp.e1 >= a.skip_e && !done1;
+          if (STATS) st_ell += (h0 && in0) + (h1 && in1);
+          const uint32_t b0m = __ballot_sync(kFull, h0), b1m = __ballot_sync(kFull, h1);
+          if (!(b0m | b1m)) continue;
+          const float4 r2 = sm.rec[2][j], r3 = sm.rec[3][j];
+          const int pos = b0 + j - start + 1;
+          if (b0m) {
+            const float w = pair_weight(ex2(pp.e0), cos_a(pair_theta(r2, pp.dx, pp.dy0)), r2);
+            const bool ok = h0 && w >= a.alpha_min;
             if (!ALPHA) {
-              if (STATS) n_con += in0;
-              C00 = __fmaf_rn(r3.x, w, C00);
-              C01 = __fmaf_rn(r3.y, w, C01);
-              C02 = __fmaf_rn(r3.z, w, C02);
+              const float we = ok ? w : 0.f;
+              if (STATS) st_con += ok && in0;
+              C00 = __fmaf_rn(r3.x, we, C00);
+              C01 = __fmaf_rn(r3.y, we, C01);
+              C02 = __fmaf_rn(r3.z, we, C02);
             } else {
-              const float al = fminf(a.alpha_max, w);
-              const float Tn = __fmul_rn(T0, __fsub_rn(1.f, al));
-              if (Tn < a.T_min) {
-                done0 = true;
-                if (STATS) stop0 = pos;
-              } else {
-                if (STATS) ++n_con;
-                const float aT = __fmul_rn(al, T0);
-                C00 = __fmaf_rn(r3.x, aT, C00);
-                C01 = __fmaf_rn(r3.y, aT, C01);
-                C02 = __fmaf_rn(r3.z, aT, C02);
-                T0 = Tn;
-                last0 = pos;
-              }
+              if (STATS) st_con += ok;
+              alpha_step(ok, w, r3, pos, a.alpha_max, a.T_min, T0, C00, C01, C02, last0,
+                         done0, stop0);
+              if (STATS) st_con -= ok && done0 && stop0 == pos;
             }
           }
-        }
-        // pixel 1
-        if (h1) {
-          const float w = pair_weight(ex2(e1), cos_a(pair_theta(r2, dx1, dy1)), r2);
-          if (w >= a.alpha_min) {
+          if (b1m) {
+            const float dy1 = __fadd_rn(pp.dy0, 4.f);
+            const float w = pair_weight(ex2(pp.e1), cos_a(pair_theta(r2, pp.dx, dy1)), r2);
+            const bool ok = h1 && w >= a.alpha_min;
             if (!ALPHA) {
-              if (STATS) n_con += in1;
-              C10 = __fmaf_rn(r3.x, w, C10);
-              C11 = __fmaf_rn(r3.y, w, C11);
-              C12 = __fmaf_rn(r3.z, w, C12);
+              const float we = ok ? w : 0.f;
+              if (STATS) st_con += ok && in1;
+              C10 = __fmaf_rn(r3.x, we, C10);
+              C11 = __fmaf_rn(r3.y, we, C11);
+              C12 = __fmaf_rn(r3.z, we, C12);
             } else {
-              const float al = fminf(a.alpha_max, w);
-              const float Tn = __fmul_rn(T1, __fsub_rn(1.f, al));
-              if (Tn < a.T_min) {
-                done1 = true;
-                if (STATS) stop1 = pos;
-              } else {
-                if (STATS) ++n_con;
-                const float aT = __fmul_rn(al, T1);
-                C10 = __fmaf_rn(r3.x, aT, C10);
-                C11 = __fmaf_rn(r3.y, aT, C11);
-                C12 = __fmaf_rn(r3.z, aT, C12);
-                T1 = Tn;
-                last1 = pos;
-              }
+              if (STATS) st_con += ok;
+              alpha_step(ok, w, r3, pos, a.alpha_max, a.T_min, T1, C10, C11, C12, last1,
+                         done1, stop1);
+              if (STATS) st_con -= ok && done1 && stop1 == pos;
             }
           }
+          if (ALPHA && __all_sync(kFull, done0 && done1)) break;
         }
-        if (ALPHA && __all_sync(kFull, done0 && done1)) break;
+      }
+      if (ALPHA) {
+        if (__syncthreads_count(!(done0 && done1)) == 0) break;
       }
     }
-    if (ALPHA) {
-      if (__syncthreads_count(!(done0 && done1)) == 0) break;
+    if (STATS) {
+      st_cand += (in0 ? (unsigned long long)stop0 : 0ull) + (in1 ? (unsigned long long)stop1 : 0ull);
+      continue;
+    }
+    const int64_t HW = (int64_t)a.H * a.W;
+    float* img = a.image + v * 3 * HW;
+    if (in0) {
+      const int64_t p = (int64_t)y0 * a.W + x;
+      if (ALPHA) {
+        C00 = __fmaf_rn(T0, a.bg0, C00);
+        C01 = __fmaf_rn(T0, a.bg1, C01);
+        C02 = __fmaf_rn(T0, a.bg2, C02);
+        a.T_final[v * HW + p] = T0;
+        a.n_contrib[v * HW + p] = last0;
+      }
+      img[p] = C00; img[HW + p] = C01; img[2 * HW + p] = C02;
+    }
+    if (in1) {
+      const int64_t p = (int64_t)y1 * a.W + x;
+      if (ALPHA) {
+        C10 = __fmaf_rn(T1, a.bg0, C10);
+        C11 = __fmaf_rn(T1, a.bg1, C11);
+        C12 = __fmaf_rn(T1, a.bg2, C12);
+        a.T_final[v * HW + p] = T1;
+        a.n_contrib[v * HW + p] = last1;
+      }
+      img[p] = C10; img[HW + p] = C11; img[2 * HW + p] = C12;
     }
   }
   if (STATS) {
-    unsigned long long c3[3] = {
-        (in0 ? (unsigned long long)stop0 : 0ull) + (in1 ? (unsigned long long)stop1 : 0ull),
-        (unsigned long long)n_ell, (unsigned long long)n_con};
+    unsigned long long c3[3] = {st_cand, st_ell, st_con};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       unsigned long long s = c3[k];
 #pragma unroll
       for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-      if (lane == 0) atomicAdd(a.stats + k, s);
+      if (lane == 0 && s) atomicAdd(a.stats + k, s);
     }
-    return;
   }
-  const int64_t HW = (int64_t)a.H * a.W;
-  float* img = a.image + v * 3 * HW;
-  if (in0) {
-    const int64_t p = (int64_t)y0 * a.W + x;
-    if (ALPHA) {
-      C00 = __fmaf_rn(T0, a.bg0, C00);
-      C01 = __fmaf_rn(T0, a.bg1, C01);
-      C02 = __fmaf_rn(T0, a.bg2, C02);
-      a.T_final[v * HW + p] = T0;
-      a.n_contrib[v * HW + p] = last0;
-    }
-    img[p] = C00; img[HW + p] = C01; img[2 * HW + p] = C02;
-  }
-  if (in1) {
-    const int64_t p = (int64_t)y1 * a.W + x;
-    if (ALPHA) {
-      C10 = __fmaf_rn(T1, a.bg0, C10);
-      C11 = __fmaf_rn(T1, a.bg1, C11);
-      C12 = __fmaf_rn(T1, a.bg2, C12);
-      a.T_final[v * HW + p] = T1;
-      a.n_contrib[v * HW + p] = last1;
-    }
-    img[p] = C10; img[HW + p] = C11; img[2 * HW + p] = C12;
-  }
+  leave_queue(a, tid);
 }
 
 // 12-slot warp transpose-reduce. On return lane L holds the warp-wide sum of
@@ -335,9 +384,10 @@ __device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) 
   return v[0] + __shfl_xor_sync(kFull, v[0], 1);
 }
 
-// Moments of one valid pair: with gw = dL/dw,
-//   M0 = gw w, M1 = gw w dx, M2 = gw w dy, M3 = gw w dx^2, M4 = gw w dx dy,
-//   M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx, M8 = M6 dy, M9..11 = colour terms.
+// Moments of one pair, gw = dL/dw and w already zeroed when the
+// pair does not contribute: M0 = gw w, M1 = gw w dx, M2 = gw w dy,
+// M3 = gw w dx^2, M4 = gw w dx dy, M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx,
+// M8 = M6 dy, M9..11 = dL/dc terms.
 __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w, float ag,
                                             float sn, float dx, float dy, float c0, float c1,
                                             float c2) {
@@ -358,167 +408,191 @@ __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w,
   m[11] += c2;
 }
 
+// Backward of one pixel for one record (predicated on `h`).
+template <bool ALPHA>
+__device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, const float4& r2,
+                                          const float4& r3, float g0, float g1, float g2,
+                                          float amin, float amax, float& T, float& S0,
+                                          float& S1, float& S2, float (&m)[kMom], bool& any) {
+  const float ag = ex2(e);
+  const float th = pair_theta(r2, dx, dy);
+  const float cs = cos_a(th), sn = sin_a(th);
+  const float w = pair_weight(ag, cs, r2);
+  const bool ok = h && w >= amin;
+  any = any || ok;
+  const float gdc = __fmaf_rn(r3.x, g0, __fmaf_rn(r3.y, g1, __fmul_rn(r3.z, g2)));
+  if (!ALPHA) {
+    const float we = ok ? w : 0.f;
+    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g0, we * g1, we * g2);
+  } else {
+    const float al = fminf(amax, w);
+    const float ri = rcp_a(1.f - al);
+    const float Tk = T * ri;
+    const float sdg = __fmaf_rn(S0, g0, __fmaf_rn(S1, g1, __fmul_rn(S2, g2)));
+    const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
+    const float aT = ok ? al * Tk : 0.f;
+    S0 = __fmaf_rn(r3.x, aT, S0);
+    S1 = __fmaf_rn(r3.y, aT, S1);
+    S2 = __fmaf_rn(r3.z, aT, S2);
+    T = ok ? Tk : T;
+    add_moments(m, (ok && w < amax) ? dLda : 0.f, ok ? w : 0.f, ag, sn, dx, dy, aT * g0,
+                aT * g1, aT * g2);
+  }
+}
+
 template <int TS, bool ALPHA>
 __global__ void __launch_bounds__(Geo<TS>::NT) k_render_bwd(RenderArgs a) {
   using G = Geo<TS>;
   constexpr int NB = G::NB;
-  __shared__ float4 s_rec[4][NB];
-  __shared__ uint32_t s_mask[NB];
-  __shared__ uint8_t s_list[G::NW][NB];
-  __shared__ int32_t s_pid[NB];
-  __shared__ int32_t s_maxlast;
+  __shared__ Smem<TS> sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t v = tile / a.T;
-  const int64_t t_in_v = tile - v * a.T;
-  const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
-  const int X0 = tx * TS, Y0 = ty * TS;
-  const int x = X0 + (wid % G::NS) * 8 + (lane & 7);
-  const int y0 = Y0 + (wid / G::NS) * 8 + (lane >> 3), y1 = y0 + 4;
-  const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
-  const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f, py1 = (float)y1 + 0.5f;
-  const int start = a.toff[tile];
-  int end = a.toff[tile + 1];
-  const int64_t HW = (int64_t)a.H * a.W;
-  const int64_t p0 = v * HW + (int64_t)y0 * a.W + x, p1 = v * HW + (int64_t)y1 * a.W + x;
-  float g00 = 0.f, g01 = 0.f, g02 = 0.f, g10 = 0.f, g11 = 0.f, g12 = 0.f;
-  float T0 = 1.f, T1 = 1.f, S00 = 0.f, S01 = 0.f, S02 = 0.f, S10 = 0.f, S11 = 0.f, S12 = 0.f;
-  int last0 = 0, last1 = 0;
-  const float* gp = a.dLdC + v * 3 * HW;
-  if (in0) {
-    const int64_t q = (int64_t)y0 * a.W + x;
-    g00 = gp[q]; g01 = gp[HW + q]; g02 = gp[2 * HW + q];
-    if (ALPHA) {
-      T0 = a.T_in[p0]; last0 = a.nc_in[p0];
-      S00 = T0 * a.bg0; S01 = T0 * a.bg1; S02 = T0 * a.bg2;
-    }
-  }
-  if (in1) {
-    const int64_t q = (int64_t)y1 * a.W + x;
-    g10 = gp[q]; g11 = gp[HW + q]; g12 = gp[2 * HW + q];
-    if (ALPHA) {
-      T1 = a.T_in[p1]; last1 = a.nc_in[p1];
-      S10 = T1 * a.bg0; S11 = T1 * a.bg1; S12 = T1 * a.bg2;
-    }
-  }
-  if (ALPHA) {
-    if (tid == 0) s_maxlast = 0;
-    __syncthreads();
-    const int ml = max(last0, last1);
-    if (ml > 0) atomicMax(&s_maxlast, ml);
-    __syncthreads();
-    end = start + s_maxlast;
-  }
-  const float4* recv = a.rec + 4 * (v * a.N);
-  const int64_t vN = v * a.N;
-  const int nbatch = (end - start + NB - 1) / NB;
+  const int ox = (wid % G::NS) * 8 + (lane & 7), oy = (wid / G::NS) * 8 + (lane >> 3);
   const int q3 = (lane >> 1) & 3;
   const int my_m = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
   const bool writer = !(lane & 1) && q3 < 3;
-  for (int bi = 0; bi < nbatch; ++bi) {
-    // ALPHA walks batches back to front; SUM front to back (order-free).
-    const int b0 = ALPHA ? max(start, end - (bi + 1) * NB) : start + bi * NB;
-    const int nb = ALPHA ? (end - bi * NB) - b0 : min(NB, end - b0);
-    __syncthreads();
-    const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, s_rec, s_mask, s_list, s_pid,
-                                    tid, lane, wid);
-    for (int ii = 0; ii < cnt; ++ii) {
-      const int j = s_list[wid][ALPHA ? cnt - 1 - ii : ii];
-      const int pos = b0 + j - start;  // index within the tile list
-      const float4 r0 = s_rec[0][j], r1 = s_rec[1][j];
-      float dx0, dy0, dx1, dy1;
-      const float e0 = pair_exponent(r0, r1, px, py0, dx0, dy0);
-      const float e1 = pair_exponent(r0, r1, px, py1, dx1, dy1);
-      bool h0 = in0 && e0 >= a.skip_e && (!ALPHA || pos < last0);
-      bool h1 = in1 && e1 >= a.skip_e && (!ALPHA || pos < last1);
-      if (!__any_sync(kFull, h0 || h1)) continue;
-      const float4 r2 = s_rec[2][j], r3 = s_rec[3][j];
-      float m[kMom];
+  for (;;) {
+    const int64_t tile = next_item<TS>(a, sm, tid);
+    if (tile < 0) break;
+    const int64_t v = tile / a.T;
+    const int64_t t_in_v = tile - v * a.T;
+    const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
+    const int X0 = tx * TS, Y0 = ty * TS;
+    const int x = X0 + ox, y0 = Y0 + oy, y1 = y0 + 4;
+    const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
+    const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f;
+    const int start = a.toff[tile];
+    int end = a.toff[tile + 1];
+    const int64_t HW = (int64_t)a.H * a.W;
+    const int64_t p0 = v * HW + (int64_t)y0 * a.W + x, p1 = v * HW + (int64_t)y1 * a.W + x;
+    float g00 = 0.f, g01 = 0.f, g02 = 0.f, g10 = 0.f, g11 = 0.f, g12 = 0.f;
+    float T0 = 1.f, T1 = 1.f, S00 = 0.f, S01 = 0.f, S02 = 0.f, S10 = 0.f, S11 = 0.f, S12 = 0.f;
+    int last0 = 0, last1 = 0;
+    const float* gp = a.dLdC + v * 3 * HW;
+    if (in0) {
+      const int64_t q = (int64_t)y0 * a.W + x;
+      g00 = gp[q]; g01 = gp[HW + q]; g02 = gp[2 * HW + q];
+      if (ALPHA) {
+        T0 = a.T_in[p0]; last0 = a.nc_in[p0];
+        S00 = T0 * a.bg0; S01 = T0 * a.bg1; S02 = T0 * a.bg2;
+      }
+    }
+    if (in1) {
+      const int64_t q = (int64_t)y1 * a.W + x;
+      g10 = gp[q]; g11 = gp[HW + q]; g12 = gp[2 * HW + q];
+      if (ALPHA) {
+        T1 = a.T_in[p1]; last1 = a.nc_in[p1];
+        S10 = T1 * a.bg0; S11 = T1 * a.bg1; S12 = T1 * a.bg2;
+      }
+    }
+    if (ALPHA) {
+      if (tid == 0) sm.maxlast = 0;
+      __syncthreads();
+      const int ml = max(last0, last1);
+      if (ml > 0) atomicMax(&sm.maxlast, ml);
+      __syncthreads();
+      end = start + sm.maxlast;
+    }
+    const float4* recv = a.rec + 4 * (v * a.N);
+    const int64_t vN = v * a.N;
+    const int nbatch = (end - start + NB - 1) / NB;
+    for (int bi = 0; bi < nbatch; ++bi) {
+      // ALPHA walks batches back to front; SUM front to back (order-free).
+      const int b0 = ALPHA ? max(start, end - (bi + 1) * NB) : start + bi * NB;
+      const int nb = ALPHA ? (end - bi * NB) - b0 : min(NB, end - b0);
+      __syncthreads();
+      const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, sm, tid, lane, wid);
+      for (int ii = 0; ii < cnt; ++ii) {
+        const int j = sm.list[wid][ALPHA ? cnt - 1 - ii : ii];
+        const int pos = b0 + j - start;  // index within the tile list
+        const float4 r0 = sm.rec[0][j], r1 = sm.rec[1][j];
+        const PairPos pp = pair_exponents(r0, r1, px, py0);
+        const bool h0 = in0 && pp.e0 >= a.skip_e && (!ALPHA || pos < last0);
+        const bool h1 = in1 && pp.e1 >= a.skip_e && (!ALPHA || pos < last1);
+        const uint32_t b0m = __ballot_sync(kFull, h0), b1m = __ballot_sync(kFull, h1);
+        if (!(b0m | b1m)) continue;
+        const float4 r2 = sm.rec[2][j], r3 = sm.rec[3][j];
+        float m[kMom];
 #pragma unroll
-      for (int k = 0; k < kMom; ++k) m[k] = 0.f;
-      bool any = false;
-      if (h0) {
-        const float ag = ex2(e0);
-        const float th = pair_theta(r2, dx0, dy0);
-        const float cs = cos_a(th);
-        const float w = pair_weight(ag, cs, r2);
-        if (w >= a.alpha_min) {
-          any = true;
-          const float sn = sin_a(th);
-          const float gdc = __fmaf_rn(r3.x, g00, __fmaf_rn(r3.y, g01, __fmul_rn(r3.z, g02)));
-          if (!ALPHA) {
-            add_moments(m, gdc, w, ag, sn, dx0, dy0, w * g00, w * g01, w * g02);
-          } else {
-            const float al = fminf(a.alpha_max, w);
-            const float ri = rcp_a(1.f - al);
-            const float Tk = T0 * ri;
-            const float sdg = __fmaf_rn(S00, g00, __fmaf_rn(S01, g01, __fmul_rn(S02, g02)));
-            const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
-            const float aT = al * Tk;
-            S00 = __fmaf_rn(r3.x, aT, S00);
-            S01 = __fmaf_rn(r3.y, aT, S01);
-            S02 = __fmaf_rn(r3.z, aT, S02);
-            T0 = Tk;
-            add_moments(m, (w < a.alpha_max) ? dLda : 0.f, w, ag, sn, dx0, dy0, aT * g00,
-                        aT * g01, aT * g02);
-          }
-        }
+        for (int k = 0; k < kMom; ++k) m[k] = 0.f;
+        bool any = false;
+        if (b0m)
+          bwd_pixel<ALPHA>(h0, pp.e0, pp.dx, pp.dy0, r2, r3, g00, g01, g02, a.alpha_min,
+                           a.alpha_max, T0, S00, S01, S02, m, any);
+        if (b1m)
+          bwd_pixel<ALPHA>(h1, pp.e1, pp.dx, __fadd_rn(pp.dy0, 4.f), r2, r3, g10, g11, g12,
+                           a.alpha_min, a.alpha_max, T1, S10, S11, S12, m, any);
+        if (!__any_sync(kFull, any)) continue;
+        const float red = transpose_reduce12(m, lane);
+        if (writer) atomicAdd(a.mom + (vN + sm.pid[j]) * kMom + my_m, red);
       }
-      if (h1) {
-        const float ag = ex2(e1);
-        const float th = pair_theta(r2, dx1, dy1);
-        const float cs = cos_a(th);
-        const float w = pair_weight(ag, cs, r2);
-        if (w >= a.alpha_min) {
-          any = true;
-          const float sn = sin_a(th);
-          const float gdc = __fmaf_rn(r3.x, g10, __fmaf_rn(r3.y, g11, __fmul_rn(r3.z, g12)));
-          if (!ALPHA) {
-            add_moments(m, gdc, w, ag, sn, dx1, dy1, w * g10, w * g11, w * g12);
-          } else {
-            const float al = fminf(a.alpha_max, w);
-            const float ri = rcp_a(1.f - al);
-            const float Tk = T1 * ri;
-            const float sdg = __fmaf_rn(S10, g10, __fmaf_rn(S11, g11, __fmul_rn(S12, g12)));
-            const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
-            const float aT = al * Tk;
-            S10 = __fmaf_rn(r3.x, aT, S10);
-            S11 = __fmaf_rn(r3.y, aT, S11);
-            S12 = __fmaf_rn(r3.z, aT, S12);
-            T1 = Tk;
-            add_moments(m, (w < a.alpha_max) ? dLda : 0.f, w, ag, sn, dx1, dy1, aT * g10,
-                        aT * g11, aT * g12);
-          }
-        }
-      }
-      if (!__any_sync(kFull, any)) continue;
-      const float red = transpose_reduce12(m, lane);
-      if (writer) atomicAdd(a.mom + (vN + s_pid[j]) * kMom + my_m, red);
     }
   }
+  leave_queue(a, tid);
+}
+
+// Persistent grid: SMs x resident CTAs of this kernel (cached per kernel).
+unsigned persistent_grid(void (*kernel)(RenderArgs), int threads, int64_t items) {
+  struct Entry { const void* k; int dev, ctas; };
+  static std::mutex mu;
+  static Entry cache[64];
+  static int n = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int ctas = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < n; ++i)
+      if (cache[i].k == (const void*)kernel && cache[i].dev == dev) ctas = cache[i].ctas;
+    if (!ctas) {
+      int sms = 0, per_sm = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+      ctas = sms * (per_sm < 1 ? 1 : per_sm);
+      if (n < 64) cache[n++] = {(const void*)kernel, dev, ctas};
+    }
+  }
+  return (unsigned)(ctas < items ? ctas : (items > 0 ? items : 1));
 }
 
 template <int TS>
-cudaError_t launch_fwd_ts(bool alpha, const RenderArgs& ra, unsigned grid, cudaStream_t s) {
+cudaError_t launch_fwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   constexpr int NT = Geo<TS>::NT;
   if (ra.stats) {
-    if (alpha) k_render_fwd<TS, true, true><<<grid, NT, 0, s>>>(ra);
-    else k_render_fwd<TS, false, true><<<grid, NT, 0, s>>>(ra);
+    ra.queue = Q_STATS;
+    if (alpha) {
+      auto k = k_render_fwd<TS, true, true>;
+      k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+    } else {
+      auto k = k_render_fwd<TS, false, true>;
+      k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+    }
     return cudaGetLastError();
   }
+  ra.queue = Q_FWD;
   launch_begin(K_RENDER_FWD, s);
-  if (alpha) k_render_fwd<TS, true, false><<<grid, NT, 0, s>>>(ra);
-  else k_render_fwd<TS, false, false><<<grid, NT, 0, s>>>(ra);
+  if (alpha) {
+    auto k = k_render_fwd<TS, true, false>;
+    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+  } else {
+    auto k = k_render_fwd<TS, false, false>;
+    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+  }
   launch_end(K_RENDER_FWD, s);
   return cudaGetLastError();
 }
 
 template <int TS>
-cudaError_t launch_bwd_ts(bool alpha, const RenderArgs& ra, unsigned grid, cudaStream_t s) {
+cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   constexpr int NT = Geo<TS>::NT;
+  ra.queue = Q_BWD;
   launch_begin(K_RENDER_BWD, s);
-  if (alpha) k_render_bwd<TS, true><<<grid, NT, 0, s>>>(ra);
-  else k_render_bwd<TS, false><<<grid, NT, 0, s>>>(ra);
+  if (alpha) {
+    auto k = k_render_bwd<TS, true>;
+    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+  } else {
+    auto k = k_render_bwd<TS, false>;
+    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
+  }
   launch_end(K_RENDER_BWD, s);
   return cudaGetLastError();
 }
@@ -528,9 +602,13 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.rec = (const float4*)(ws + L.rec);
   ra.vals = (const uint32_t*)(ws + (final_in_b ? L.valsB : L.valsA));
   ra.toff = (const int32_t*)(ws + L.toff);
+  ra.order = (const int32_t*)(ws + L.order);
+  ra.hdr = (WsHeader*)(ws + L.hdr);
   ra.N = L.N;
   ra.T = L.T;
+  ra.BT = L.BT;
   ra.W = c.width; ra.H = c.height; ra.GX = L.GX;
+  ra.queue = 0;
   ra.alpha_min = c.alpha_min;
   // conservative early-out on the exponent: e < log2(alpha_min) - 1e-4 implies
   // alpha*W < alpha_min after the MUFU roundings
@@ -555,11 +633,10 @@ cudaError_t launch_render_fwd(const wipes_config& c, const Layout& L, char* ws, 
   ra.image = image; ra.T_final = T_final; ra.n_contrib = n_contrib;
   ra.stats = stats;
   const bool alpha = c.blend == WIPES_BLEND_ALPHA;
-  const unsigned grid = (unsigned)L.BT;
   switch (c.tile) {
-    case 8: return launch_fwd_ts<8>(alpha, ra, grid, s);
-    case 16: return launch_fwd_ts<16>(alpha, ra, grid, s);
-    default: return launch_fwd_ts<32>(alpha, ra, grid, s);
+    case 8: return launch_fwd_ts<8>(alpha, ra, s);
+    case 16: return launch_fwd_ts<16>(alpha, ra, s);
+    default: return launch_fwd_ts<32>(alpha, ra, s);
   }
 }
 
@@ -570,11 +647,10 @@ cudaError_t launch_render_bwd(const wipes_config& c, const Layout& L, char* ws, 
   RenderArgs ra = make_args(c, L, ws, final_in_b);
   ra.dLdC = dLdC; ra.T_in = T_final; ra.nc_in = n_contrib;
   const bool alpha = c.blend == WIPES_BLEND_ALPHA;
-  const unsigned grid = (unsigned)L.BT;
   switch (c.tile) {
-    case 8: return launch_bwd_ts<8>(alpha, ra, grid, s);
-    case 16: return launch_bwd_ts<16>(alpha, ra, grid, s);
-    default: return launch_bwd_ts<32>(alpha, ra, grid, s);
+    case 8: return launch_bwd_ts<8>(alpha, ra, s);
+    case 16: return launch_bwd_ts<16>(alpha, ra, s);
+    default: return launch_bwd_ts<32>(alpha, ra, s);
   }
 }
 

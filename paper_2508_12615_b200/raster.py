@@ -235,3 +235,73 @@ def rasterize(r: Rasterizer, params: dict, cams=None, view_stride: int = 0) -> t
     """Differentiable render: returns image [B,3,H,W]; gradients flow to params."""
     keys = tuple(k for k in (PARAM_KEYS_3D if r.prim == "3d" else PARAM_KEYS_2D) if k in params)
     return _RasterizeFn.apply(r, cams, view_stride, keys, *[params[k] for k in keys])
+
+
+class FrameGraph:
+    """CUDA-graph capture of one frame of a Rasterizer on fixed device buffers.
+
+    The forward (preprocess -> bin_sort -> render) and the backward (render
+    backward -> preprocess backward [-> optional hook, e.g. a gradient
+    all_reduce]) are captured as two graphs and replayed with ``forward()`` /
+    ``backward()``: no host work or host sync per frame. The intersection
+    capacity is sized by one synced forward before capture (x growth); if the
+    parameters later change so much that the capacity overflows,
+    ``check_overflow()`` reports it and ``recapture()`` re-sizes.
+    """
+
+    def __init__(self, r: Rasterizer, params: dict, cams=None, view_stride: int = 0,
+                 dL_dimage: Optional[torch.Tensor] = None, grads: Optional[dict] = None,
+                 backward_hook=None):
+        self.r, self.params, self.cams, self.vs = r, params, cams, view_stride
+        self.dL, self.grads, self.hook = dL_dimage, grads, backward_hook
+        self.recapture()
+
+    def recapture(self):
+        r = self.r
+        r.forward(self.params, self.cams, self.vs, sync=True)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm the captured path once on a side stream
+            self._fwd()
+            if self.dL is not None:
+                self._bwd()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.g_fwd = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_fwd):
+            self._fwd()
+        self.g_bwd = None
+        if self.dL is not None:
+            self.g_bwd = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g_bwd):
+                self._bwd()
+        torch.cuda.synchronize()
+
+    def _fwd(self):
+        r = self.r
+        r.preprocess(self.params, self.cams, self.vs, sync=False)
+        r.bin_sort()
+        img, T, nc = r._saved if r._saved is not None else (None, None, None)
+        self.out = r.render(img, T, nc)
+
+    def _bwd(self):
+        self.grads = self.r.backward(self.dL, self.grads)
+        if self.hook is not None:
+            self.hook(self.grads)
+
+    def forward(self):
+        self.g_fwd.replay()
+        return self.out
+
+    def backward(self):
+        self.g_bwd.replay()
+        return self.grads
+
+    def step(self):
+        self.g_fwd.replay()
+        if self.g_bwd is not None:
+            self.g_bwd.replay()
+
+    def check_overflow(self):
+        return self.r.check_overflow()

@@ -74,23 +74,40 @@ def kernel(rep):
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
-    hi = next(i for i, x in enumerate(rows) if x and x[0] == "Address")
-    h = rows[hi]
-    ia, ie, iss = h.index("Source"), h.index("Instructions Executed"), \
-        h.index("Warp Stall Sampling (All Samples)")
-    by, st = collections.Counter(), collections.Counter()
-    for x in rows[hi + 1:]:
-        if len(x) <= max(ia, ie, iss) or not x[ia].strip():
-            continue
-        toks = x[ia].strip().split()
-        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
-        op = op.split(".")[0]
-        by[op] += int(x[ie] or 0)
-        st[op] += int(x[iss] or 0)
-    T, S = sum(by.values()) or 1, sum(st.values()) or 1
-    print(f"\n# SASS opcode mix: {T} warp instructions executed")
-    for op, n in by.most_common(25):
-        print(f"{op:12s} {n:12d} {100 * n / T:6.1f}%   stall-samples {100 * st[op] / S:5.1f}%")
+    kernels = []
+    for x in rows:
+        if x and x[0] == "Kernel Name":
+            kernels.append([x[1] if len(x) > 1 else "?", None, []])
+        elif x and x[0] == "Address" and kernels:
+            kernels[-1][1] = x
+        elif kernels and kernels[-1][1] is not None:
+            kernels[-1][2].append(x)
+    for name, h, body in kernels:
+        ia, ie, iss = h.index("Source"), h.index("Instructions Executed"), \
+            h.index("Warp Stall Sampling (All Samples)")
+        by, st = collections.Counter(), collections.Counter()
+        for x in body:
+            if len(x) <= max(ia, ie, iss) or not x[ia].strip():
+                continue
+            toks = x[ia].strip().split()
+            op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+            op = op.split(".")[0]
+            by[op] += int(x[ie] or 0)
+            st[op] += int(x[iss] or 0)
+        T, S = sum(by.values()) or 1, sum(st.values()) or 1
+        print(f"\n# SASS opcode mix of {name[:80]}: {T} warp instructions executed")
+        for op, n in by.most_common(25):
+            print(f"{op:12s} {n:12d} {100 * n / T:6.1f}%   stall-samples {100 * st[op] / S:5.1f}%")
+    for row in r[2:]:
+        d = dict(zip(hdr, row))
+        stalls = {k.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", ""):
+                  d[k] for k in hdr if k.startswith("smsp__average_warp_latency_issue_stalled_")
+                  and k.endswith(".ratio")}
+        if stalls:
+            top = sorted(stalls.items(), key=lambda kv: -float(kv[1] or 0))[:8]
+            print(f"\n# top warp stall reasons (cycles per issued instruction) {d.get('Kernel Name', '')[:60]}")
+            for k, v in top:
+                print(f"  {k:40s} {v}")
 
 
 if __name__ == "__main__":
