@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwipes.so")
+# WIPES_LIB overrides the library path (kernel-variant experiments only)
+LIB_PATH = os.environ.get("WIPES_LIB") or os.path.join(_HERE, "libwipes.so")
 
 WIPES_OK, WIPES_EINVAL, WIPES_ECAPACITY, WIPES_ECUDA, WIPES_EUNSUPPORTED = range(5)
 PRIM = {"2d": 0, "3d": 1}

@@ -85,7 +85,7 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
 }
 
 wipes_status check_ws(const Layout& L, const void* ws, size_t ws_bytes, int64_t cap) {
-  if (cap < 0 || cap >= ((int64_t)1 << 31)) return fail(WIPES_EINVAL, "dup_capacity out of range");
+  if (cap < 0 || cap >= ((int64_t)1 << 30)) return fail(WIPES_EINVAL, "dup_capacity must be in [0, 2^30)");
   if (!ws) return fail(WIPES_EINVAL, "ws is NULL");
   if (!aligned(ws, 256)) return fail(WIPES_EINVAL, "ws must be 256-byte aligned");
   if (ws_bytes < L.total) return fail(WIPES_EINVAL, "ws_bytes smaller than wipes_workspace_bytes");

@@ -3,12 +3,7 @@
 // depth bits), a stable LSD radix sort over the significant key bits only,
 // and per-tile CSR ranges. PAPER.md:64 ("an efficient GPU sorting algorithm").
 //
-// Radix sort design (sm_100a, no CUB): per 8-bit digit one histogram kernel
-// (per-WARP sub-block histograms, match_any-aggregated shared atomics), one
-// device-wide exclusive scan of the digit-major [256 x nsub] count matrix,
-// and one stable scatter kernel in which each warp walks its own contiguous
-// sub-block in order, ranking equal digits with __match_any_sync. Stability
-// follows from sub-block order = input order and lane order = input order.
+// The radix sort itself is the onesweep implementation in sort.cu.
 #include "common.cuh"
 
 namespace wipes {
@@ -145,74 +140,6 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   }
 }
 
-// -------------------------------------------------------------- radix -----
-struct RadixArgs {
-  const uint64_t* kin;
-  const uint32_t* vin;
-  uint64_t* kout;
-  uint32_t* vout;
-  const WsHeader* hdr;
-  int64_t cap, nsub;
-  int32_t shift, items;
-  int32_t* counts;  // [256][nsub] digit-major; after the scan: local exclusive
-  const int32_t* rblk;
-};
-
-__global__ void __launch_bounds__(kRadixWarps * 32) k_radix_hist(RadixArgs a) {
-  __shared__ int32_t hist[kRadixWarps][kRadixBins];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wid;
-  for (int d = lane; d < kRadixBins; d += 32) hist[wid][d] = 0;
-  __syncwarp();
-  const int64_t n = clamp_n(a.hdr, a.cap);
-  const int64_t base = w * 32 * (int64_t)a.items;
-  for (int it = 0; it < a.items; ++it) {
-    int64_t idx = base + (int64_t)it * 32 + lane;
-    if (base + (int64_t)it * 32 >= n) break;  // warp-uniform
-    bool valid = idx < n;
-    uint32_t d = valid ? (uint32_t)(a.kin[idx] >> a.shift) & (kRadixBins - 1) : kRadixBins;
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    int leader = __ffs(peers) - 1;
-    if (valid && lane == leader) hist[wid][d] += __popc(peers);
-    __syncwarp();
-  }
-  __syncwarp();
-  for (int d = lane; d < kRadixBins; d += 32) a.counts[(int64_t)d * a.nsub + w] = hist[wid][d];
-}
-
-__global__ void __launch_bounds__(kRadixWarps * 32) k_radix_scatter(RadixArgs a) {
-  __shared__ int32_t off[kRadixWarps][kRadixBins];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wid;
-  const int64_t n = clamp_n(a.hdr, a.cap);
-  const int64_t base = w * 32 * (int64_t)a.items;
-  if (base >= n) return;  // whole warp idle (no shared state across warps)
-  for (int d = lane; d < kRadixBins; d += 32) {
-    int64_t ci = (int64_t)d * a.nsub + w;
-    off[wid][d] = a.counts[ci] + a.rblk[ci / kScanTile];
-  }
-  __syncwarp();
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int it = 0; it < a.items; ++it) {
-    int64_t idx = base + (int64_t)it * 32 + lane;
-    if (base + (int64_t)it * 32 >= n) break;
-    bool valid = idx < n;
-    uint64_t key = valid ? a.kin[idx] : 0ull;
-    uint32_t val = valid ? a.vin[idx] : 0u;
-    uint32_t d = valid ? (uint32_t)(key >> a.shift) & (kRadixBins - 1) : kRadixBins;
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    int rank = __popc(peers & lt);
-    if (valid) {
-      int pos = off[wid][d] + rank;
-      a.kout[pos] = key;
-      a.vout[pos] = val;
-    }
-    __syncwarp();
-    if (valid && rank == 0) off[wid][d] += __popc(peers);
-    __syncwarp();
-  }
-}
-
 // --------------------------------------------------------- tile ranges ----
 __global__ void __launch_bounds__(256) k_tile_ranges(const uint64_t* keys, const WsHeader* hdr,
                                                      int64_t cap, int64_t BT, int32_t* toff) {
@@ -322,33 +249,11 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // LSD passes: depth bits (ALPHA) then the view|tile bits.
-    RadixArgs r;
-    r.hdr = hdr; r.cap = L.cap; r.nsub = L.nsub; r.items = L.items;
-    r.counts = (int32_t*)(ws + L.rcounts);
-    r.rblk = (const int32_t*)(ws + L.rblk);
-    const unsigned nblk = (unsigned)(L.nsub / kRadixWarps);
-    for (int p = 0; p < L.passes; ++p) {
-      int shift = p < L.lo_passes ? 8 * p : 32 + 8 * (p - L.lo_passes);
-      bool from_a = (p & 1) == 0;
-      r.kin = from_a ? kA : kB; r.vin = from_a ? vA : vB;
-      r.kout = from_a ? kB : kA; r.vout = from_a ? vB : vA;
-      r.shift = shift;
-      launch_begin(K_RADIX_HIST, s);
-      k_radix_hist<<<nblk, kRadixWarps * 32, 0, s>>>(r);
-      launch_end(K_RADIX_HIST, s);
-      launch_begin(K_RADIX_SCAN_BLOCKS, s);
-      k_scan_blocks<int32_t, int32_t><<<(unsigned)L.nblk_rscan, kScanBlock, 0, s>>>(
-          r.counts, L.nrc, r.counts, (int32_t*)(ws + L.rblk));
-      launch_end(K_RADIX_SCAN_BLOCKS, s);
-      launch_begin(K_RADIX_SCAN_SUMS, s);
-      k_scan_sums<int32_t><<<1, 1024, 0, s>>>((int32_t*)(ws + L.rblk), L.nblk_rscan, nullptr, 0);
-      launch_end(K_RADIX_SCAN_SUMS, s);
-      launch_begin(K_RADIX_SCATTER, s);
-      k_radix_scatter<<<nblk, kRadixWarps * 32, 0, s>>>(r);
-      launch_end(K_RADIX_SCATTER, s);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-    }
+    int shifts[kMaxPasses];
+    for (int p = 0; p < L.passes; ++p)
+      shifts[p] = p < L.lo_passes ? 8 * p : 32 + 8 * (p - L.lo_passes);
+    e = launch_sort(L, ws, kA, vA, kB, vB, shifts, L.passes, s);
+    if (e != cudaSuccess) return e;
   }
   const uint64_t* kf = *final_in_b ? kB : kA;
   launch_begin(K_TILE_RANGES, s);

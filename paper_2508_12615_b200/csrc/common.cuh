@@ -16,8 +16,10 @@ constexpr int kScanBlock = 256;                // threads per scan block
 constexpr int kScanItems = 8;                  // items per thread
 constexpr int kScanTile = kScanBlock * kScanItems;
 constexpr int kRadixBits = 8;
-constexpr int kRadixBins = 1 << kRadixBits;
-constexpr int kRadixWarps = 8;                 // warps per radix block
+constexpr int kSortThreads = 256;              // onesweep CTA (one digit per thread)
+constexpr int kSortItems = 8;                  // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxPasses = 8;
 constexpr int32_t kWsMagic = 0x57495053;       // "WIPS"
 
 // Record-gradient slot order (matches the oracle's documented layout, written
@@ -53,14 +55,11 @@ struct Layout {
   int64_t N = 0, BN = 0, cap = 0, BT = 0, T = 0;
   int32_t B = 0, GX = 0, GY = 0;
   int32_t hi_bits = 0, passes = 0, lo_passes = 0;
-  int64_t nsub = 0;        // radix sub-blocks (one warp each)
-  int32_t items = 0;       // keys per lane per sub-block
   int64_t nblk_scan = 0;   // blocks of the count scan
-  int64_t nrc = 0;         // radix counts = 256 * nsub
-  int64_t nblk_rscan = 0;  // blocks of the radix-count scan
+  int64_t sort_tiles = 0;  // onesweep tiles of kSortTile keys
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
-         blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, rcounts = 0, rblk = 0,
-         toff = 0, order = 0, rgrad = 0, total = 0;
+         blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, sort_hist = 0,
+         sort_status = 0, toff = 0, order = 0, rgrad = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -77,17 +76,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.hi_bits = hb;
   L.lo_passes = (c.blend == WIPES_BLEND_ALPHA) ? 4 : 0;
   L.passes = L.lo_passes + (hb + kRadixBits - 1) / kRadixBits;
-  // radix sub-blocks: aim for ~148 SMs x 16 warps, at least 4 items per lane
-  int64_t target_warps = 148 * 16;
-  int64_t items = (L.cap + 32 * target_warps - 1) / (32 * target_warps);
-  if (items < 4) items = 4;
-  items = (items + 3) / 4 * 4;
-  L.items = (int32_t)items;
-  L.nsub = (L.cap + 32 * items - 1) / (32 * items);
-  if (L.nsub < 1) L.nsub = 1;
-  L.nsub = (L.nsub + kRadixWarps - 1) / kRadixWarps * kRadixWarps;
-  L.nrc = (int64_t)kRadixBins * L.nsub;
-  L.nblk_rscan = (L.nrc + kScanTile - 1) / kScanTile;
+  L.sort_tiles = (L.cap + kSortTile - 1) / kSortTile;
   L.nblk_scan = (L.BN + kScanTile - 1) / kScanTile;
   if (L.nblk_scan < 1) L.nblk_scan = 1;
   size_t o = 0;
@@ -104,8 +93,8 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.keysB = take(sizeof(uint64_t) * L.cap);
   L.valsA = take(sizeof(uint32_t) * L.cap);
   L.valsB = take(sizeof(uint32_t) * L.cap);
-  L.rcounts = take(sizeof(int32_t) * L.nrc);
-  L.rblk = take(sizeof(int32_t) * (L.nblk_rscan + 1));
+  L.sort_hist = take(sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses));
+  L.sort_status = take(sizeof(uint32_t) * 256 * (L.sort_tiles > 0 ? L.sort_tiles : 1));
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
   L.order = take(sizeof(int32_t) * (L.BT + 1));
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
@@ -139,6 +128,8 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
                                 const wipes_camera* cams, char* ws, uint8_t* cull_flags,
                                 cudaStream_t s);
 cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
+cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, uint64_t* kB,
+                        uint32_t* vB, const int* shifts, int npass, cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);
 cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
                             int* final_in_b);

@@ -11,15 +11,16 @@
 //             12-slot transpose-reduce of shuffles, then one atomic per (warp,
 //             record, moment).
 //
-// Persistent CTAs (grid = SMs x resident CTAs) pull (view, tile) work items
-// from a queue ordered longest-list-first (bin_sort's tile order), so the
-// uneven per-tile cost does not leave SMs idle at the end of the launch.
-// Each warp owns an 8x8-pixel sub-tile, each lane two pixels (rows y and
-// y+4; the second is evaluated incrementally from the first). Records are
-// staged in shared memory in batches (structure-of-float4 layout); every staged
-// record carries a sub-tile mask from its conservative opacity extent, and each
-// warp compacts the batch into its own ordered list of records that can reach
-// its pixels (ballot + popc). Branches inside a (warp, record) step are
+// Every WARP is an independent persistent worker (no CTA barriers): it pulls
+// work items (view, tile, warp footprint [, record chunk]) from a queue ordered
+// longest-tile-list first, walks the tile's sorted record list 32 records at a
+// time — each lane loads one 64-byte record, tests it against the warp's
+// footprint with the record's conservative opacity extent, and the hits are
+// compacted in order (ballot + popc) into warp-private shared memory. A warp
+// footprint is G stacked 8x8 blocks (G = 2 for 16/32-pixel tiles, 1 for 8);
+// each lane owns 2G pixels: rows y + 8g and y + 8g + 4 of every block g (the
+// +4 row evaluated incrementally — the same arithmetic for a given pixel
+// whatever the tile size). Branches inside a (warp, record) step are
 // warp-uniform (ballots); per-lane decisions are predicated selects. exp is one
 // MUFU.EX2 (the -1/2 log2(e) scale and log2(alpha) folded into the record);
 // cos / sin are MUFU.COS / MUFU.SIN.
@@ -35,6 +36,14 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMom = kMoments;  // 12
+#ifndef WIPES_MINB_FWD
+#define WIPES_MINB_FWD 8  // __launch_bounds__ min CTAs per SM (register cap), forward
+#endif
+#ifndef WIPES_MINB_BWD
+#define WIPES_MINB_BWD 6  // ... backward
+#endif
+constexpr int kWarpsPerCta = 4;
+constexpr int kCta = 32 * kWarpsPerCta;
 enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -57,6 +66,12 @@ __device__ __forceinline__ float rcp_a(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float4 ldg_nc(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 
 struct RenderArgs {
   const float4* rec;     // [B*N][4]
@@ -66,6 +81,7 @@ struct RenderArgs {
   WsHeader* hdr;         // work queues
   int64_t N, T, BT;
   int32_t W, H, GX, queue;
+  int32_t chunks;        // SUM backward: each footprint's list is split into this many items
   float alpha_min, skip_e, alpha_max, T_min;
   float bg0, bg1, bg2;
   float* image;          // [B,3,H,W]
@@ -78,49 +94,46 @@ struct RenderArgs {
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
-// Sub-tile mask of a record for tile origin (X0, Y0): bit (sy * NS + sx) set
-// when the record's opacity-extent AABB (padded) may touch 8x8 sub-tile (sx, sy).
 template <int TS>
-__device__ __forceinline__ uint32_t subtile_mask(const float4& r0, const float4& r3, int X0,
-                                                 int Y0) {
-  constexpr int NS = TS / 8;
-  __half2 e2 = *reinterpret_cast<const __half2*>(&r3.w);
-  float rx = __low2float(e2) + 0.02f, ry = __high2float(e2) + 0.02f;
-  float cx = (r0.x - (float)X0) + r0.z;  // centre relative to the tile origin
-  float cy = (r0.y - (float)Y0) + r0.w;
-  // sub-tile s covers pixel centres [8 s + 0.5, 8 s + 7.5]
-  float fx0 = ceilf((cx - rx - 7.5f) * 0.125f), fx1 = floorf((cx + rx - 0.5f) * 0.125f);
-  float fy0 = ceilf((cy - ry - 7.5f) * 0.125f), fy1 = floorf((cy + ry - 0.5f) * 0.125f);
-  fx0 = fmaxf(fx0, 0.f); fy0 = fmaxf(fy0, 0.f);
-  fx1 = fminf(fx1, (float)(NS - 1)); fy1 = fminf(fy1, (float)(NS - 1));
-  if (!(fx0 <= fx1) || !(fy0 <= fy1)) return 0u;
-  int sx0 = (int)fx0, sx1 = (int)fx1, sy0 = (int)fy0, sy1 = (int)fy1;
-  uint32_t row = ((2u << sx1) - 1u) & ~((1u << sx0) - 1u);
-  uint32_t m = 0;
-#pragma unroll
-  for (int sy = 0; sy < NS; ++sy)
-    if (sy >= sy0 && sy <= sy1) m |= row << (sy * NS);
-  return m;
-}
-
-// Exponents of alpha*G for the lane's two pixels (rows y0 and y0 + 4) — one
-// arithmetic shared by every kernel, so all take the same alpha_min decisions
-// (and, since 8x8 sub-tiles are 8-aligned for every tile size, every pixel is
-// evaluated by the same expression whatever the tiling).
-struct PairPos {
-  float dx, dy0, e0, e1;
+struct Geo {
+  static constexpr int G = TS >= 16 ? 2 : 1;  // 8x8 blocks per warp footprint (stacked)
+  static constexpr int P = 2 * G;             // pixels per lane
+  static constexpr int FX = TS / 8;           // footprints per tile row
+  static constexpr int FY = TS / (8 * G);     // footprints per tile column
+  static constexpr int S = FX * FY;           // footprints (work items) per tile
 };
 
-__device__ __forceinline__ PairPos pair_exponents(const float4& r0, const float4& r1, float px,
+// Conservative test: can the record's opacity-extent AABB (padded) touch the
+// footprint whose pixel centres span [sx0 + 0.5, sx0 + 7.5] x [sy0 + 0.5, sy0 + h - 0.5]?
+__device__ __forceinline__ bool hits_footprint(const float4& r0, const float4& r3, float sx0,
+                                               float sy0, float h) {
+  __half2 e2 = *reinterpret_cast<const __half2*>(&r3.w);
+  const float rx = __low2float(e2) + 0.02f, ry = __high2float(e2) + 0.02f;
+  const float cx = (r0.x - sx0) + r0.z, cy = (r0.y - sy0) + r0.w;
+  return cx + rx >= 0.5f && cx - rx <= 7.5f && cy + ry >= 0.5f && cy - ry <= h - 0.5f;
+}
+
+// Exponents of alpha*G for a lane's pixel pair (rows y0 and y0 + 4) — one
+// arithmetic shared by every kernel, so all take the same alpha_min decisions
+// (and, since 8x8 blocks are 8-aligned for every tile size, every pixel is
+// evaluated by the same expression whatever the tiling).
+struct PairPos {
+  float dy0, e0, e1;
+};
+
+__device__ __forceinline__ float pair_dx(const float4& r0, float px) {
+  return __fsub_rn(__fsub_rn(px, r0.x), r0.z);
+}
+
+__device__ __forceinline__ PairPos pair_exponents(const float4& r0, const float4& r1, float dx,
                                                   float py0) {
   PairPos p;
-  p.dx = __fsub_rn(__fsub_rn(px, r0.x), r0.z);
   p.dy0 = __fsub_rn(__fsub_rn(py0, r0.y), r0.w);
-  const float t = __fmaf_rn(r1.x, p.dx, __fmul_rn(r1.y, p.dy0));  // A dx + B dy
-  const float cdy = __fmul_rn(r1.z, p.dy0);                        // C dy
-  p.e0 = __fmaf_rn(t, p.dx, __fmaf_rn(cdy, p.dy0, r1.w));
+  const float t = __fmaf_rn(r1.x, dx, __fmul_rn(r1.y, p.dy0));  // A dx + B dy
+  const float cdy = __fmul_rn(r1.z, p.dy0);                      // C dy
+  p.e0 = __fmaf_rn(t, dx, __fmaf_rn(cdy, p.dy0, r1.w));
   // dy1 = dy0 + 4: e1 = e0 + 4 (B dx + 2 C dy0 + 4 C)
-  const float v = __fmaf_rn(r1.y, p.dx, __fmaf_rn(2.f, cdy, __fmul_rn(4.f, r1.z)));
+  const float v = __fmaf_rn(r1.y, dx, __fmaf_rn(2.f, cdy, __fmul_rn(4.f, r1.z)));
   p.e1 = __fmaf_rn(4.f, v, p.e0);
   return p;
 }
@@ -133,70 +146,56 @@ __device__ __forceinline__ float pair_weight(float ag, float cs, const float4& r
   return __fmul_rn(ag, __fmaf_rn(r2.w, cs, 0.5f));
 }
 
-template <int TS>
-struct Geo {
-  static constexpr int NS = TS / 8;               // sub-tiles per side
-  static constexpr int NW = NS * NS;              // warps per CTA
-  static constexpr int NT = 32 * NW;              // threads per CTA
-  static constexpr int NB = NT < 128 ? 128 : NT;  // records per staged batch
+// Warp-private staging area: the compacted hits of the current 32-record chunk.
+struct WarpSmem {
+  float4 rec[4][32];
+  int32_t pid[32];
+  int32_t pos[32];
+};
+
+// One work item of a warp.
+struct Item {
+  int64_t v, tile;
+  int x, y0;       // the lane's column and first row
+  float sx0, sy0;  // footprint origin (pixels)
+  int start, end;  // record range in the tile list
+  int lstart;      // start of the whole tile list (for list positions)
 };
 
 template <int TS>
-struct Smem {
-  float4 rec[4][Geo<TS>::NB];
-  uint32_t mask[Geo<TS>::NB];
-  uint8_t list[Geo<TS>::NW][Geo<TS>::NB];
-  int32_t pid[Geo<TS>::NB];
-  int32_t item, maxlast;
-};
-
-// Stage records [b0, b0 + nb) of the tile list into shared memory and build
-// each warp's compacted list. Returns this warp's list length.
-template <int TS>
-__device__ __forceinline__ int stage_batch(const RenderArgs& a, const float4* recv, int b0,
-                                           int nb, int X0, int Y0, Smem<TS>& sm, int tid,
-                                           int lane, int wid) {
-  constexpr int NB = Geo<TS>::NB, NT = Geo<TS>::NT;
-#pragma unroll
-  for (int t = tid; t < NB; t += NT) {
-    uint32_t m = 0;
-    if (t < nb) {
-      const uint32_t pid = a.vals[b0 + t];
-      const float4* r = recv + 4 * (int64_t)pid;
-      float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-      sm.rec[0][t] = r0; sm.rec[1][t] = r1; sm.rec[2][t] = r2; sm.rec[3][t] = r3;
-      sm.pid[t] = (int32_t)pid;
-      m = subtile_mask<TS>(r0, r3, X0, Y0);
-    }
-    sm.mask[t] = m;
+__device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chunks, Item& it) {
+  using Gm = Geo<TS>;
+  int item = 0;
+  if (lane == 0) item = atomicAdd(&a.hdr->work[a.queue], 1);
+  item = __shfl_sync(kFull, item, 0);
+  if ((int64_t)item >= a.BT * Gm::S * chunks) return false;
+  const int chunk = item % chunks;
+  const int sub = (item / chunks) % Gm::S;
+  it.tile = a.order[item / (chunks * Gm::S)];
+  it.v = it.tile / a.T;
+  const int64_t t_in_v = it.tile - it.v * a.T;
+  const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
+  const int X0 = tx * TS + (sub % Gm::FX) * 8, Y0 = ty * TS + (sub / Gm::FX) * (8 * Gm::G);
+  it.sx0 = (float)X0;
+  it.sy0 = (float)Y0;
+  it.x = X0 + (lane & 7);
+  it.y0 = Y0 + (lane >> 3);
+  it.lstart = a.toff[it.tile];
+  int end = a.toff[it.tile + 1];
+  if (chunks > 1) {
+    const int per = (end - it.lstart + chunks - 1) / chunks;
+    const int s0 = it.lstart + chunk * per;
+    it.end = min(end, s0 + per);
+    it.start = min(s0, it.end);
+  } else {
+    it.start = it.lstart;
+    it.end = end;
   }
-  __syncthreads();
-  int cnt = 0;
-  const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int c = 0; c < NB / 32; ++c) {
-    const int j = c * 32 + lane;
-    const bool hit = (sm.mask[j] >> wid) & 1u;
-    const uint32_t bal = __ballot_sync(kFull, hit);
-    if (hit) sm.list[wid][cnt + __popc(bal & lt)] = (uint8_t)j;
-    cnt += __popc(bal);
-  }
-  __syncwarp();
-  return cnt;
-}
-
-// Persistent work loop helpers: fetch the next (view, tile) item; the last CTA
-// to leave resets the queue for the next launch.
-template <int TS>
-__device__ __forceinline__ int64_t next_item(const RenderArgs& a, Smem<TS>& sm, int tid) {
-  __syncthreads();
-  if (tid == 0) sm.item = atomicAdd(&a.hdr->work[a.queue], 1);
-  __syncthreads();
-  const int item = sm.item;
-  return item < a.BT ? (int64_t)a.order[item] : -1;
+  return true;
 }
 
 __device__ __forceinline__ void leave_queue(const RenderArgs& a, int tid) {
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(&a.hdr->done[a.queue], 1) == (int)gridDim.x - 1) {
@@ -207,20 +206,46 @@ __device__ __forceinline__ void leave_queue(const RenderArgs& a, int tid) {
   }
 }
 
+// Load list entry `idx` (one per lane), test it against the footprint and
+// compact the hits into `ws` in list order; returns their count.
+template <int G>
+__device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* recv, int idx,
+                                           bool valid, int pos, const Item& it, WarpSmem& ws,
+                                           int lane) {
+  float4 r0, r1, r2, r3;
+  int32_t pid = 0;
+  bool hit = false;
+  if (valid) {
+    pid = (int32_t)a.vals[idx];
+    const float4* r = recv + 4 * (int64_t)pid;
+    r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
+    hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G);
+    if (hit) { r1 = ldg_nc(r + 1); r2 = ldg_nc(r + 2); }
+  }
+  const uint32_t bal = __ballot_sync(kFull, hit);
+  if (hit) {
+    const int k = __popc(bal & ((1u << lane) - 1u));
+    ws.rec[0][k] = r0; ws.rec[1][k] = r1; ws.rec[2][k] = r2; ws.rec[3][k] = r3;
+    ws.pid[k] = pid;
+    ws.pos[k] = pos;
+  }
+  __syncwarp();
+  return __popc(bal);
+}
+
 // Front-to-back alpha compositing step of one pixel (Eq. 3, R9/R10),
 // predicated: ok = the pair contributes alpha*W >= alpha_min.
 __device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, int pos,
-                                           float amax, float tmin, float& T, float& C0,
-                                           float& C1, float& C2, int& last, bool& done,
-                                           int& stop) {
+                                           float amax, float tmin, float& T, float (&C)[3],
+                                           int& last, bool& done, int& stop) {
   const float al = fminf(amax, w);
   const float Tn = __fmul_rn(T, __fsub_rn(1.f, al));
   const bool stp = ok && Tn < tmin;
   const bool comp = ok && !stp;
   const float aT = comp ? __fmul_rn(al, T) : 0.f;
-  C0 = __fmaf_rn(r3.x, aT, C0);
-  C1 = __fmaf_rn(r3.y, aT, C1);
-  C2 = __fmaf_rn(r3.z, aT, C2);
+  C[0] = __fmaf_rn(r3.x, aT, C[0]);
+  C[1] = __fmaf_rn(r3.y, aT, C[1]);
+  C[2] = __fmaf_rn(r3.z, aT, C[2]);
   T = comp ? Tn : T;
   last = comp ? pos : last;
   done = done || stp;
@@ -228,111 +253,108 @@ __device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, i
 }
 
 template <int TS, bool ALPHA, bool STATS>
-__global__ void __launch_bounds__(Geo<TS>::NT) k_render_fwd(RenderArgs a) {
-  using G = Geo<TS>;
-  constexpr int NB = G::NB;
-  __shared__ Smem<TS> sm;
+__global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs a) {
+  using Gm = Geo<TS>;
+  constexpr int G = Gm::G, P = Gm::P;
+  __shared__ WarpSmem sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int ox = (wid % G::NS) * 8 + (lane & 7), oy = (wid / G::NS) * 8 + (lane >> 3);
+  WarpSmem& ws = sm_all[wid];
   unsigned long long st_cand = 0, st_ell = 0, st_con = 0;  // STATS only
-  for (;;) {
-    const int64_t tile = next_item<TS>(a, sm, tid);
-    if (tile < 0) break;
-    const int64_t v = tile / a.T;
-    const int64_t t_in_v = tile - v * a.T;
-    const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
-    const int X0 = tx * TS, Y0 = ty * TS;
-    const int x = X0 + ox, y0 = Y0 + oy, y1 = y0 + 4;
-    const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
-    const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f;
-    const int start = a.toff[tile], end = a.toff[tile + 1];
-    const float4* recv = a.rec + 4 * (v * a.N);
-    float C00 = 0.f, C01 = 0.f, C02 = 0.f, C10 = 0.f, C11 = 0.f, C12 = 0.f;
-    float T0 = 1.f, T1 = 1.f;
-    int last0 = 0, last1 = 0, stop0 = end - start, stop1 = end - start;
-    bool done0 = ALPHA ? !in0 : false, done1 = ALPHA ? !in1 : false;
-    for (int b0 = start; b0 < end; b0 += NB) {
-      const int nb = min(NB, end - b0);
-      __syncthreads();
-      const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, sm, tid, lane, wid);
-      if (!ALPHA || !__all_sync(kFull, done0 && done1)) {
-        for (int i = 0; i < cnt; ++i) {
-          const int j = sm.list[wid][i];
-          const float4 r0 = sm.rec[0][j], r1 = sm.rec[1][j];
-          const PairPos pp = pair_exponents(r0, r1, px, py0);
-          const bool h0 = pp.e0 >= a.skip_e && !done0, h1 = pp.e1 >= a.skip_e && !done1;
-          if (STATS) st_ell += (h0 && in0) + (h1 && in1);
-          const uint32_t b0m = __ballot_sync(kFull, h0), b1m = __ballot_sync(kFull, h1);
-          if (!(b0m | b1m)) continue;
-          const float4 r2 = sm.rec[2][j], r3 = sm.rec[3][j];
-          const int pos = b0 + j - start + 1;
-          if (b0m) {
-            const float w = pair_weight(ex2(pp.e0), cos_a(pair_theta(r2, pp.dx, pp.dy0)), r2);
-            const bool ok = h0 && w >= a.alpha_min;
-            if (!ALPHA) {
-              const float we = ok ? w : 0.f;
-              if (STATS) st_con += ok && in0;
-              C00 = __fmaf_rn(r3.x, we, C00);
-              C01 = __fmaf_rn(r3.y, we, C01);
-              C02 = __fmaf_rn(r3.z, we, C02);
-            } else {
-              if (STATS) st_con += ok;
-              alpha_step(ok, w, r3, pos, a.alpha_max, a.T_min, T0, C00, C01, C02, last0,
-                         done0, stop0);
-              if (STATS) st_con -= ok && done0 && stop0 == pos;
-            }
+  Item it;
+  while (next_item<TS>(a, lane, 1, it)) {
+    bool in[P], done[P];
+    float C[P][3], T[P];
+    int last[P], stop[P];
+    const int len = it.end - it.start;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int y = it.y0 + 8 * (p >> 1) + 4 * (p & 1);
+      in[p] = it.x < a.W && y < a.H;
+      done[p] = ALPHA ? !in[p] : false;
+      C[p][0] = C[p][1] = C[p][2] = 0.f;
+      T[p] = 1.f;
+      last[p] = 0;
+      stop[p] = len;
+    }
+    const float px = (float)it.x + 0.5f, py0 = (float)it.y0 + 0.5f;
+    const float4* recv = a.rec + 4 * (it.v * a.N);
+    for (int b0 = it.start; b0 < it.end; b0 += 32) {
+      if (ALPHA) {
+        bool all = true;
+#pragma unroll
+        for (int p = 0; p < P; ++p) all = all && done[p];
+        if (__all_sync(kFull, all)) break;
+      }
+      const bool valid = b0 + lane < it.end;
+      const int cnt = stage_chunk<G>(a, recv, b0 + lane, valid, b0 - it.start + lane + 1, it, ws,
+                                     lane);
+      for (int i = 0; i < cnt; ++i) {
+        const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
+        const float dx = pair_dx(r0, px);
+        float e[P], dy[P];
+        bool h[P];
+        uint32_t any = 0, bm[P];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * g);
+          e[2 * g] = pp.e0; e[2 * g + 1] = pp.e1;
+          dy[2 * g] = pp.dy0; dy[2 * g + 1] = pp.dy0 + 4.f;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          h[p] = e[p] >= a.skip_e && !done[p];
+          if (STATS) st_ell += h[p] && in[p];
+          bm[p] = __ballot_sync(kFull, h[p]);
+          any |= bm[p];
+        }
+        if (!any) continue;
+        const float4 r2 = ws.rec[2][i], r3 = ws.rec[3][i];
+        const int pos = ws.pos[i];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          if (!bm[p]) continue;
+          const float w = pair_weight(ex2(e[p]), cos_a(pair_theta(r2, dx, dy[p])), r2);
+          const bool ok = h[p] && w >= a.alpha_min;
+          if (!ALPHA) {
+            const float we = ok ? w : 0.f;
+            if (STATS) st_con += ok && in[p];
+            C[p][0] = __fmaf_rn(r3.x, we, C[p][0]);
+            C[p][1] = __fmaf_rn(r3.y, we, C[p][1]);
+            C[p][2] = __fmaf_rn(r3.z, we, C[p][2]);
+          } else {
+            alpha_step(ok, w, r3, pos, a.alpha_max, a.T_min, T[p], C[p], last[p], done[p],
+                       stop[p]);
+            if (STATS) st_con += ok && !(done[p] && stop[p] == pos);
           }
-          if (b1m) {
-            const float dy1 = __fadd_rn(pp.dy0, 4.f);
-            const float w = pair_weight(ex2(pp.e1), cos_a(pair_theta(r2, pp.dx, dy1)), r2);
-            const bool ok = h1 && w >= a.alpha_min;
-            if (!ALPHA) {
-              const float we = ok ? w : 0.f;
-              if (STATS) st_con += ok && in1;
-              C10 = __fmaf_rn(r3.x, we, C10);
-              C11 = __fmaf_rn(r3.y, we, C11);
-              C12 = __fmaf_rn(r3.z, we, C12);
-            } else {
-              if (STATS) st_con += ok;
-              alpha_step(ok, w, r3, pos, a.alpha_max, a.T_min, T1, C10, C11, C12, last1,
-                         done1, stop1);
-              if (STATS) st_con -= ok && done1 && stop1 == pos;
-            }
-          }
-          if (ALPHA && __all_sync(kFull, done0 && done1)) break;
+        }
+        if (ALPHA) {
+          bool all = true;
+#pragma unroll
+          for (int p = 0; p < P; ++p) all = all && done[p];
+          if (__all_sync(kFull, all)) break;
         }
       }
-      if (ALPHA) {
-        if (__syncthreads_count(!(done0 && done1)) == 0) break;
-      }
+      __syncwarp();
     }
     if (STATS) {
-      st_cand += (in0 ? (unsigned long long)stop0 : 0ull) + (in1 ? (unsigned long long)stop1 : 0ull);
+#pragma unroll
+      for (int p = 0; p < P; ++p) st_cand += in[p] ? (unsigned long long)stop[p] : 0ull;
       continue;
     }
     const int64_t HW = (int64_t)a.H * a.W;
-    float* img = a.image + v * 3 * HW;
-    if (in0) {
-      const int64_t p = (int64_t)y0 * a.W + x;
+    float* img = a.image + it.v * 3 * HW;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (!in[p]) continue;
+      const int64_t q = (int64_t)(it.y0 + 8 * (p >> 1) + 4 * (p & 1)) * a.W + it.x;
       if (ALPHA) {
-        C00 = __fmaf_rn(T0, a.bg0, C00);
-        C01 = __fmaf_rn(T0, a.bg1, C01);
-        C02 = __fmaf_rn(T0, a.bg2, C02);
-        a.T_final[v * HW + p] = T0;
-        a.n_contrib[v * HW + p] = last0;
+        C[p][0] = __fmaf_rn(T[p], a.bg0, C[p][0]);
+        C[p][1] = __fmaf_rn(T[p], a.bg1, C[p][1]);
+        C[p][2] = __fmaf_rn(T[p], a.bg2, C[p][2]);
+        a.T_final[it.v * HW + q] = T[p];
+        a.n_contrib[it.v * HW + q] = last[p];
       }
-      img[p] = C00; img[HW + p] = C01; img[2 * HW + p] = C02;
-    }
-    if (in1) {
-      const int64_t p = (int64_t)y1 * a.W + x;
-      if (ALPHA) {
-        C10 = __fmaf_rn(T1, a.bg0, C10);
-        C11 = __fmaf_rn(T1, a.bg1, C11);
-        C12 = __fmaf_rn(T1, a.bg2, C12);
-        a.T_final[v * HW + p] = T1;
-        a.n_contrib[v * HW + p] = last1;
-      }
-      img[p] = C10; img[HW + p] = C11; img[2 * HW + p] = C12;
+      img[q] = C[p][0]; img[HW + q] = C[p][1]; img[2 * HW + q] = C[p][2];
     }
   }
   if (STATS) {
@@ -411,127 +433,131 @@ __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w,
 // Backward of one pixel for one record (predicated on `h`).
 template <bool ALPHA>
 __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, const float4& r2,
-                                          const float4& r3, float g0, float g1, float g2,
-                                          float amin, float amax, float& T, float& S0,
-                                          float& S1, float& S2, float (&m)[kMom], bool& any) {
+                                          const float4& r3, const float (&g)[3], float amin,
+                                          float amax, float& T, float (&S)[3], float (&m)[kMom],
+                                          bool& any) {
   const float ag = ex2(e);
   const float th = pair_theta(r2, dx, dy);
   const float cs = cos_a(th), sn = sin_a(th);
   const float w = pair_weight(ag, cs, r2);
   const bool ok = h && w >= amin;
   any = any || ok;
-  const float gdc = __fmaf_rn(r3.x, g0, __fmaf_rn(r3.y, g1, __fmul_rn(r3.z, g2)));
+  const float gdc = __fmaf_rn(r3.x, g[0], __fmaf_rn(r3.y, g[1], __fmul_rn(r3.z, g[2])));
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
-    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g0, we * g1, we * g2);
+    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g[0], we * g[1], we * g[2]);
   } else {
     const float al = fminf(amax, w);
     const float ri = rcp_a(1.f - al);
     const float Tk = T * ri;
-    const float sdg = __fmaf_rn(S0, g0, __fmaf_rn(S1, g1, __fmul_rn(S2, g2)));
+    const float sdg = __fmaf_rn(S[0], g[0], __fmaf_rn(S[1], g[1], __fmul_rn(S[2], g[2])));
     const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
     const float aT = ok ? al * Tk : 0.f;
-    S0 = __fmaf_rn(r3.x, aT, S0);
-    S1 = __fmaf_rn(r3.y, aT, S1);
-    S2 = __fmaf_rn(r3.z, aT, S2);
+    S[0] = __fmaf_rn(r3.x, aT, S[0]);
+    S[1] = __fmaf_rn(r3.y, aT, S[1]);
+    S[2] = __fmaf_rn(r3.z, aT, S[2]);
     T = ok ? Tk : T;
-    add_moments(m, (ok && w < amax) ? dLda : 0.f, ok ? w : 0.f, ag, sn, dx, dy, aT * g0,
-                aT * g1, aT * g2);
+    add_moments(m, (ok && w < amax) ? dLda : 0.f, ok ? w : 0.f, ag, sn, dx, dy, aT * g[0],
+                aT * g[1], aT * g[2]);
   }
 }
 
 template <int TS, bool ALPHA>
-__global__ void __launch_bounds__(Geo<TS>::NT) k_render_bwd(RenderArgs a) {
-  using G = Geo<TS>;
-  constexpr int NB = G::NB;
-  __shared__ Smem<TS> sm;
+__global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs a) {
+  using Gm = Geo<TS>;
+  constexpr int G = Gm::G, P = Gm::P;
+  __shared__ WarpSmem sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int ox = (wid % G::NS) * 8 + (lane & 7), oy = (wid / G::NS) * 8 + (lane >> 3);
+  WarpSmem& ws = sm_all[wid];
   const int q3 = (lane >> 1) & 3;
   const int my_m = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
   const bool writer = !(lane & 1) && q3 < 3;
-  for (;;) {
-    const int64_t tile = next_item<TS>(a, sm, tid);
-    if (tile < 0) break;
-    const int64_t v = tile / a.T;
-    const int64_t t_in_v = tile - v * a.T;
-    const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
-    const int X0 = tx * TS, Y0 = ty * TS;
-    const int x = X0 + ox, y0 = Y0 + oy, y1 = y0 + 4;
-    const bool in0 = x < a.W && y0 < a.H, in1 = x < a.W && y1 < a.H;
-    const float px = (float)x + 0.5f, py0 = (float)y0 + 0.5f;
-    const int start = a.toff[tile];
-    int end = a.toff[tile + 1];
+  Item it;
+  while (next_item<TS>(a, lane, ALPHA ? 1 : a.chunks, it)) {
     const int64_t HW = (int64_t)a.H * a.W;
-    const int64_t p0 = v * HW + (int64_t)y0 * a.W + x, p1 = v * HW + (int64_t)y1 * a.W + x;
-    float g00 = 0.f, g01 = 0.f, g02 = 0.f, g10 = 0.f, g11 = 0.f, g12 = 0.f;
-    float T0 = 1.f, T1 = 1.f, S00 = 0.f, S01 = 0.f, S02 = 0.f, S10 = 0.f, S11 = 0.f, S12 = 0.f;
-    int last0 = 0, last1 = 0;
-    const float* gp = a.dLdC + v * 3 * HW;
-    if (in0) {
-      const int64_t q = (int64_t)y0 * a.W + x;
-      g00 = gp[q]; g01 = gp[HW + q]; g02 = gp[2 * HW + q];
-      if (ALPHA) {
-        T0 = a.T_in[p0]; last0 = a.nc_in[p0];
-        S00 = T0 * a.bg0; S01 = T0 * a.bg1; S02 = T0 * a.bg2;
+    const float* gp = a.dLdC + it.v * 3 * HW;
+    bool in[P];
+    float g[P][3], T[P], S[P][3];
+    int last[P];
+    int ml = 0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int y = it.y0 + 8 * (p >> 1) + 4 * (p & 1);
+      in[p] = it.x < a.W && y < a.H;
+      g[p][0] = g[p][1] = g[p][2] = 0.f;
+      T[p] = 1.f;
+      S[p][0] = S[p][1] = S[p][2] = 0.f;
+      last[p] = 0;
+      if (in[p]) {
+        const int64_t q = (int64_t)y * a.W + it.x;
+        g[p][0] = gp[q]; g[p][1] = gp[HW + q]; g[p][2] = gp[2 * HW + q];
+        if (ALPHA) {
+          T[p] = a.T_in[it.v * HW + q];
+          last[p] = a.nc_in[it.v * HW + q];
+          S[p][0] = T[p] * a.bg0; S[p][1] = T[p] * a.bg1; S[p][2] = T[p] * a.bg2;
+          ml = max(ml, last[p]);
+        }
       }
     }
-    if (in1) {
-      const int64_t q = (int64_t)y1 * a.W + x;
-      g10 = gp[q]; g11 = gp[HW + q]; g12 = gp[2 * HW + q];
-      if (ALPHA) {
-        T1 = a.T_in[p1]; last1 = a.nc_in[p1];
-        S10 = T1 * a.bg0; S11 = T1 * a.bg1; S12 = T1 * a.bg2;
-      }
+    int start = it.start, end = it.end;
+    if (ALPHA) {  // only entries before this warp's last composited one matter
+#pragma unroll
+      for (int off = 16; off; off >>= 1) ml = max(ml, __shfl_xor_sync(kFull, ml, off));
+      end = it.lstart + ml;
     }
-    if (ALPHA) {
-      if (tid == 0) sm.maxlast = 0;
-      __syncthreads();
-      const int ml = max(last0, last1);
-      if (ml > 0) atomicMax(&sm.maxlast, ml);
-      __syncthreads();
-      end = start + sm.maxlast;
-    }
-    const float4* recv = a.rec + 4 * (v * a.N);
-    const int64_t vN = v * a.N;
-    const int nbatch = (end - start + NB - 1) / NB;
-    for (int bi = 0; bi < nbatch; ++bi) {
-      // ALPHA walks batches back to front; SUM front to back (order-free).
-      const int b0 = ALPHA ? max(start, end - (bi + 1) * NB) : start + bi * NB;
-      const int nb = ALPHA ? (end - bi * NB) - b0 : min(NB, end - b0);
-      __syncthreads();
-      const int cnt = stage_batch<TS>(a, recv, b0, nb, X0, Y0, sm, tid, lane, wid);
+    const float px = (float)it.x + 0.5f, py0 = (float)it.y0 + 0.5f;
+    const float4* recv = a.rec + 4 * (it.v * a.N);
+    const int64_t vN = it.v * a.N;
+    // ALPHA walks 32-record chunks back to front; SUM front to back.
+    const int nchunk = (end - start + 31) / 32;
+    for (int ci = 0; ci < nchunk; ++ci) {
+      const int b0 = ALPHA ? end - 32 * (ci + 1) : start + 32 * ci;
+      const bool valid = b0 + lane >= start && b0 + lane < end;
+      const int cnt = stage_chunk<G>(a, recv, b0 + lane, valid, b0 + lane - it.lstart, it, ws,
+                                     lane);
       for (int ii = 0; ii < cnt; ++ii) {
-        const int j = sm.list[wid][ALPHA ? cnt - 1 - ii : ii];
-        const int pos = b0 + j - start;  // index within the tile list
-        const float4 r0 = sm.rec[0][j], r1 = sm.rec[1][j];
-        const PairPos pp = pair_exponents(r0, r1, px, py0);
-        const bool h0 = in0 && pp.e0 >= a.skip_e && (!ALPHA || pos < last0);
-        const bool h1 = in1 && pp.e1 >= a.skip_e && (!ALPHA || pos < last1);
-        const uint32_t b0m = __ballot_sync(kFull, h0), b1m = __ballot_sync(kFull, h1);
-        if (!(b0m | b1m)) continue;
-        const float4 r2 = sm.rec[2][j], r3 = sm.rec[3][j];
+        const int i = ALPHA ? cnt - 1 - ii : ii;
+        const int pos = ws.pos[i];  // index within the tile list
+        const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
+        const float dx = pair_dx(r0, px);
+        float e[P], dy[P];
+        bool h[P];
+        uint32_t any_h = 0, bm[P];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * gg);
+          e[2 * gg] = pp.e0; e[2 * gg + 1] = pp.e1;
+          dy[2 * gg] = pp.dy0; dy[2 * gg + 1] = pp.dy0 + 4.f;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          h[p] = in[p] && e[p] >= a.skip_e && (!ALPHA || pos < last[p]);
+          bm[p] = __ballot_sync(kFull, h[p]);
+          any_h |= bm[p];
+        }
+        if (!any_h) continue;
+        const float4 r2 = ws.rec[2][i], r3 = ws.rec[3][i];
         float m[kMom];
 #pragma unroll
         for (int k = 0; k < kMom; ++k) m[k] = 0.f;
         bool any = false;
-        if (b0m)
-          bwd_pixel<ALPHA>(h0, pp.e0, pp.dx, pp.dy0, r2, r3, g00, g01, g02, a.alpha_min,
-                           a.alpha_max, T0, S00, S01, S02, m, any);
-        if (b1m)
-          bwd_pixel<ALPHA>(h1, pp.e1, pp.dx, __fadd_rn(pp.dy0, 4.f), r2, r3, g10, g11, g12,
-                           a.alpha_min, a.alpha_max, T1, S10, S11, S12, m, any);
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          if (bm[p])
+            bwd_pixel<ALPHA>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min, a.alpha_max,
+                             T[p], S[p], m, any);
         if (!__any_sync(kFull, any)) continue;
         const float red = transpose_reduce12(m, lane);
-        if (writer) atomicAdd(a.mom + (vN + sm.pid[j]) * kMom + my_m, red);
+        if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
       }
+      __syncwarp();
     }
   }
   leave_queue(a, tid);
 }
 
 // Persistent grid: SMs x resident CTAs of this kernel (cached per kernel).
-unsigned persistent_grid(void (*kernel)(RenderArgs), int threads, int64_t items) {
+unsigned persistent_grid(void (*kernel)(RenderArgs), int64_t items) {
   struct Entry { const void* k; int dev, ctas; };
   static std::mutex mu;
   static Entry cache[64];
@@ -546,53 +572,40 @@ unsigned persistent_grid(void (*kernel)(RenderArgs), int threads, int64_t items)
     if (!ctas) {
       int sms = 0, per_sm = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCta, 0);
       ctas = sms * (per_sm < 1 ? 1 : per_sm);
       if (n < 64) cache[n++] = {(const void*)kernel, dev, ctas};
     }
   }
-  return (unsigned)(ctas < items ? ctas : (items > 0 ? items : 1));
+  const int64_t need = (items + kWarpsPerCta - 1) / kWarpsPerCta;
+  return (unsigned)(ctas < need ? ctas : (need > 0 ? need : 1));
 }
 
 template <int TS>
 cudaError_t launch_fwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
-  constexpr int NT = Geo<TS>::NT;
+  const int64_t items = ra.BT * Geo<TS>::S;
+  void (*k)(RenderArgs);
   if (ra.stats) {
     ra.queue = Q_STATS;
-    if (alpha) {
-      auto k = k_render_fwd<TS, true, true>;
-      k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-    } else {
-      auto k = k_render_fwd<TS, false, true>;
-      k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-    }
+    k = alpha ? k_render_fwd<TS, true, true> : k_render_fwd<TS, false, true>;
+    k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
     return cudaGetLastError();
   }
   ra.queue = Q_FWD;
+  k = alpha ? k_render_fwd<TS, true, false> : k_render_fwd<TS, false, false>;
   launch_begin(K_RENDER_FWD, s);
-  if (alpha) {
-    auto k = k_render_fwd<TS, true, false>;
-    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-  } else {
-    auto k = k_render_fwd<TS, false, false>;
-    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-  }
+  k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
   launch_end(K_RENDER_FWD, s);
   return cudaGetLastError();
 }
 
 template <int TS>
 cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
-  constexpr int NT = Geo<TS>::NT;
+  const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   ra.queue = Q_BWD;
+  void (*k)(RenderArgs) = alpha ? k_render_bwd<TS, true> : k_render_bwd<TS, false>;
   launch_begin(K_RENDER_BWD, s);
-  if (alpha) {
-    auto k = k_render_bwd<TS, true>;
-    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-  } else {
-    auto k = k_render_bwd<TS, false>;
-    k<<<persistent_grid(k, NT, ra.BT), NT, 0, s>>>(ra);
-  }
+  k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
   launch_end(K_RENDER_BWD, s);
   return cudaGetLastError();
 }
@@ -609,6 +622,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.BT = L.BT;
   ra.W = c.width; ra.H = c.height; ra.GX = L.GX;
   ra.queue = 0;
+  ra.chunks = 4;
   ra.alpha_min = c.alpha_min;
   // conservative early-out on the exponent: e < log2(alpha_min) - 1e-4 implies
   // alpha*W < alpha_min after the MUFU roundings

@@ -1,0 +1,223 @@
+// Onesweep LSD radix sort of (uint64 key, uint32 value) pairs over selected
+// 8-bit digits ("an efficient GPU sorting
+// algorithm"), hand-written for sm_100a (no CUB):
+//
+//  1. k_sort_hist  : one read of the keys builds the global 256-bin histogram
+//                    of EVERY pass at once (shared-memory atomics, then one
+//                    global atomic per (block, pass, digit)).
+//  2. k_sort_pass  : one launch per digit. Each CTA takes the next tile of
+//                    kTile keys (tile id from an atomic counter, so tiles are
+//                    assigned in launch order), ranks them stably in shared
+//                    memory (warp-striped layout, __match_any_sync per step),
+//                    publishes its per-digit counts, resolves its per-digit
+//                    global offsets by DECOUPLED LOOK-BACK over the preceding
+//                    tiles, stages the pairs in shared memory in sorted order
+//                    and writes them out with coalesced runs.
+//
+// Per pass the keys/values are read once and written once (12 + 12 B per
+// pair) — the HBM floor of an LSD pass. Stability: within a tile the rank
+// follows input order (warp-major, then step, then lane); across tiles the
+// look-back prefix follows tile order.
+#include "common.cuh"
+
+namespace wipes {
+
+namespace {
+
+constexpr int kWarps = kSortThreads / 32;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ int64_t n_keys(const WsHeader* h, int64_t cap) {
+  int64_t t = h->total;
+  return t < cap ? t : cap;
+}
+
+struct SortArgs {
+  const uint64_t* kin;
+  const uint32_t* vin;
+  uint64_t* kout;
+  uint32_t* vout;
+  const WsHeader* hdr;
+  int64_t cap;
+  uint32_t* ghist;     // [kMaxPasses][256]
+  uint32_t* counter;   // [kMaxPasses] tile counters
+  uint32_t* status;    // [tiles][256] look-back words of this pass
+  int32_t shifts[kMaxPasses];
+  int32_t npass, pass, shift;
+};
+
+__global__ void __launch_bounds__(256) k_sort_hist(SortArgs a) {
+  __shared__ uint32_t h[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t n = n_keys(a.hdr, a.cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = a.kin[i];
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p)
+      if (p < a.npass) atomicAdd(&h[p][(uint32_t)(k >> a.shifts[p]) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.npass * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(a.ghist + i, c);
+  }
+}
+
+struct SortSmem {
+  uint64_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+  uint32_t wcnt[kWarps][256];  // per-warp running counts, then warp-exclusive prefixes
+  uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
+  uint32_t gofs[256];          // global output offset of the tile's first key per digit
+  uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t n = n_keys(a.hdr, a.cap);
+  if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
+  for (int i = tid; i < kWarps * 256; i += kSortThreads) (&sm.wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = sm.tile;
+  const int64_t base = (int64_t)tile * kSortTile;
+  if (base >= n) return;  // beyond the data: nobody waits on this tile
+  const int shift = a.shift;
+  const uint32_t lt = (1u << lane) - 1u;
+  // ---- load (warp-striped) and rank stably within the tile ----------------
+  uint64_t key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t dig[kSortItems], rank[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
+    const bool valid = idx < n;
+    key[i] = valid ? a.kin[idx] : 0ull;
+    val[i] = valid ? a.vin[idx] : 0u;
+    dig[i] = valid ? ((uint32_t)(key[i] >> shift) & 255u) : 256u;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t d = dig[i];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;
+    rank[i] = before + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256u && (peers & lt) == 0) sm.wcnt[wid][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- per digit (thread tid = digit): warp prefixes, tile count ---------
+  const int d = tid;  // kSortThreads == 256
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t c = sm.wcnt[w][d];
+    sm.wcnt[w][d] = cnt;
+    cnt += c;
+  }
+  // publish the tile aggregate, then look back for the exclusive prefix
+  volatile uint32_t* st = a.status;
+  st[(int64_t)tile * 256 + d] = kFlagAgg | cnt;
+  uint32_t prefix = 0;
+  for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+    const uint32_t s = st[t * 256 + d];
+    const uint32_t f = s & ~kValMask;
+    if (f == 0u) continue;  // not yet published: spin
+    prefix += s & kValMask;
+    if (f == kFlagInc) break;
+    --t;
+  }
+  __threadfence();
+  st[(int64_t)tile * 256 + d] = kFlagInc | (prefix + cnt);
+  // global digit base = exclusive scan of the pass histogram (block scan)
+  const uint32_t gh = a.ghist[a.pass * 256 + d];
+  uint32_t incl_g = gh, incl_b = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t tg = __shfl_up_sync(0xffffffffu, incl_g, off);
+    const uint32_t tb = __shfl_up_sync(0xffffffffu, incl_b, off);
+    if (lane >= off) { incl_g += tg; incl_b += tb; }
+  }
+  __shared__ uint32_t wg[kWarps], wb[kWarps];
+  if (lane == 31) { wg[wid] = incl_g; wb[wid] = incl_b; }
+  __syncthreads();
+  uint32_t og = 0, ob = 0;
+  for (int w = 0; w < wid; ++w) { og += wg[w]; ob += wb[w]; }
+  const uint32_t excl_g = og + incl_g - gh, excl_b = ob + incl_b - cnt;
+  sm.bexcl[d] = excl_b;
+  sm.gofs[d] = excl_g + prefix;
+  __syncthreads();
+  // ---- stage in tile-sorted order, then coalesced write-out -----------------
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t dd = dig[i];
+    if (dd < 256u) {
+      const uint32_t loc = sm.bexcl[dd] + sm.wcnt[wid][dd] + rank[i];
+      sm.keys[loc] = key[i];
+      sm.vals[loc] = val[i];
+    }
+  }
+  __syncthreads();
+  const int64_t rem = n - base;
+  const int tn = rem < kSortTile ? (int)rem : kSortTile;
+  for (int j = tid; j < tn; j += kSortThreads) {
+    const uint64_t k = sm.keys[j];
+    const uint32_t dd = (uint32_t)(k >> shift) & 255u;
+    const int64_t pos = (int64_t)sm.gofs[dd] + (j - (int64_t)sm.bexcl[dd]);
+    a.kout[pos] = k;
+    a.vout[pos] = sm.vals[j];
+  }
+}
+
+}  // namespace
+
+size_t sort_smem_bytes() { return sizeof(SortSmem); }
+
+cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, uint64_t* kB,
+                        uint32_t* vB, const int* shifts, int npass, cudaStream_t s) {
+  if (npass == 0 || L.cap == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SortSmem));
+    attr = true;
+  }
+  SortArgs a;
+  a.hdr = (const WsHeader*)(ws + L.hdr);
+  a.cap = L.cap;
+  a.ghist = (uint32_t*)(ws + L.sort_hist);
+  a.counter = a.ghist + kMaxPasses * 256;
+  a.status = (uint32_t*)(ws + L.sort_status);
+  a.npass = npass;
+  for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
+  cudaError_t e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
+  if (e != cudaSuccess) return e;
+  a.kin = kA; a.vin = vA; a.pass = 0;
+  const int64_t hist_blocks = (L.cap + 4095) / 4096;
+  launch_begin(K_RADIX_HIST, s);
+  k_sort_hist<<<(unsigned)(hist_blocks < 1184 ? (hist_blocks > 0 ? hist_blocks : 1) : 1184), 256, 0,
+                s>>>(a);
+  launch_end(K_RADIX_HIST, s);
+  const int64_t tiles = (L.cap + kSortTile - 1) / kSortTile;
+  for (int p = 0; p < npass; ++p) {
+    const bool from_a = (p & 1) == 0;
+    a.kin = from_a ? kA : kB; a.vin = from_a ? vA : vB;
+    a.kout = from_a ? kB : kA; a.vout = from_a ? vB : vA;
+    a.pass = p;
+    a.shift = shifts[p];
+    e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * 256 * (size_t)tiles, s);
+    if (e != cudaSuccess) return e;
+    launch_begin(K_RADIX_SCATTER, s);
+    k_sort_pass<<<(unsigned)tiles, kSortThreads, sizeof(SortSmem), s>>>(a);
+    launch_end(K_RADIX_SCATTER, s);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace wipes
