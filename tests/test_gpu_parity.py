@@ -217,3 +217,17 @@ def test_empty_scene_and_all_culled():
         r2.preprocess(bad, cull_flags=cull)
         torch.cuda.synchronize()
         assert torch.all(cull == 5)
+
+
+def test_forward_run_to_run_deterministic():
+    """The forward has no atomics (each pixel accumulates its list in order):
+    repeated runs are bit-identical whatever the work scheduling."""
+    H, W = 96, 80
+    for blend in ("sum", "alpha"):
+        dp = to_dev(gen.gen2d(H, W, 500, seed=4, freq_std=0.5, phase=True, depth=True))
+        r = gpu_rasterizer("2d", H, W, blend)
+        a = r.forward(dp)["image"].clone()
+        for _ in range(3):
+            b = r.forward(dp)["image"]
+            torch.cuda.synchronize()
+            assert torch.equal(a, b)
