@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pixels", type=int, default=4096)
+    ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -139,7 +139,7 @@ def run_reference(args, rank, world):
         return
     from paper_2508_12615_b200 import gen
     c = gen.make_config(args.config, seed=args.seed)
-    per = max(64, args.cpu_pixels // 4)
+    per = max(64, args.cpu_pixels // 8)
     times = []
     cores = os.cpu_count() or 1
     for s in range(args.warmup + args.steps):
