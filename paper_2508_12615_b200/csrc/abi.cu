@@ -195,9 +195,7 @@ wipes_status wipes_bin_sort(const wipes_config* cfg, int64_t N, int32_t B, void*
   int fb = 0;
   cudaError_t e = launch_bin_sort(*cfg, L, w, s, &fb);
   if (e != cudaSuccess) return cuda_fail(e, "bin_sort launch");
-  if (keys_out && L.cap)
-    e = cudaMemcpyAsync(keys_out, w + (fb ? L.keysB : L.keysA), 8 * L.cap,
-                        cudaMemcpyDeviceToDevice, s);
+  if (keys_out && L.cap) e = launch_keys64(L, w, fb, keys_out, s);
   if (e == cudaSuccess && vals_out && L.cap)
     e = cudaMemcpyAsync(vals_out, w + (fb ? L.valsB : L.valsA), 4 * L.cap,
                         cudaMemcpyDeviceToDevice, s);

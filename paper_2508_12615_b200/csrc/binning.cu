@@ -108,48 +108,80 @@ __global__ void __launch_bounds__(1024) k_scan_sums(T* blk, int64_t nblk, WsHead
 }
 
 // ----------------------------------------------------------- duplicate ----
+// Each (view, primitive) record with n tiles writes n pairs (key = view*T +
+// tile, value = primitive) at its offset, row-major over its rect. SUM walks
+// records in index order; ALPHA walks them in the depth-presorted order
+// `order` with offsets scanned in that order, so each tile's list comes out in
+// (depth, index) order and only the tile bits need sorting.
 struct DupArgs {
   const int4* rect;
   const int32_t* count;
-  const uint32_t* dkey;
+  const uint32_t* order;  // ALPHA: presorted (view, primitive) ids; SUM: nullptr
   const int64_t* loc;
   const int64_t* blk;
   int64_t BN, N, T, cap;
-  int32_t GX, alpha;
-  uint64_t* keys;
+  int32_t GX;
+  uint32_t* keys;
   uint32_t* vals;
 };
 
 __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
-  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= a.BN) return;
-  int32_t n = a.count[o];
+  const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j0 >= a.BN) return;
+  const int64_t o = a.order ? (int64_t)a.order[j0] : j0;
+  const int32_t n = a.count[o];
   if (n == 0) return;
-  int64_t j = a.loc[o] + a.blk[o / kScanTile];
-  int64_t v = o / a.N, i = o - v * a.N;
-  int4 r = a.rect[o];
-  uint64_t lo = a.alpha ? (uint64_t)a.dkey[o] : 0ull;
-  uint64_t vt = (uint64_t)(v * a.T);
+  int64_t j = a.loc[j0] + a.blk[j0 / kScanTile];
+  const int64_t v = o / a.N, i = o - v * a.N;
+  const int4 r = a.rect[o];
+  const uint32_t vt = (uint32_t)(v * a.T);
   for (int ty = r.y; ty < r.w; ++ty) {
-    uint64_t rowt = vt + (uint64_t)ty * a.GX;
+    const uint32_t rowt = vt + (uint32_t)ty * (uint32_t)a.GX;
     for (int tx = r.x; tx < r.z; ++tx, ++j) {
       if (j >= a.cap) return;
-      a.keys[j] = ((rowt + tx) << 32) | lo;
+      a.keys[j] = rowt + (uint32_t)tx;
       a.vals[j] = (uint32_t)i;
     }
   }
 }
 
+// ALPHA depth presort inputs: key = (view << 32) | orderable depth bits.
+__global__ void __launch_bounds__(256) k_presort_keys(const uint32_t* dkey, int64_t BN, int64_t N,
+                                                      uint64_t* pk, uint32_t* pv) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= BN) return;
+  pk[o] = ((uint64_t)(o / N) << 32) | (uint64_t)dkey[o];
+  pv[o] = (uint32_t)o;
+}
+
+__global__ void __launch_bounds__(256) k_gather_counts(const uint32_t* order, const int32_t* count,
+                                                       int64_t BN, int32_t* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < BN) out[j] = count[order[j]];
+}
+
 // --------------------------------------------------------- tile ranges ----
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint64_t* keys, const WsHeader* hdr,
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, const WsHeader* hdr,
                                                      int64_t cap, int64_t BT, int32_t* toff) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = clamp_n(hdr, cap);
   if (i > n) return;
-  int64_t tp = i == 0 ? -1 : (int64_t)(keys[i - 1] >> 32);
-  int64_t tc = i == n ? BT : (int64_t)(keys[i] >> 32);
+  int64_t tp = i == 0 ? -1 : (int64_t)keys[i - 1];
+  int64_t tc = i == n ? BT : (int64_t)keys[i];
   if (tc > BT) tc = BT;
   for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
+}
+
+// 64-bit (tile << 32 | depth bits) keys of the sorted pairs, for parity copies.
+__global__ void __launch_bounds__(256) k_keys64(const uint32_t* keys, const uint32_t* vals,
+                                                const uint32_t* dkey, const WsHeader* hdr,
+                                                int64_t cap, int64_t N, int64_t T, int32_t alpha,
+                                                uint64_t* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= clamp_n(hdr, cap)) return;
+  const uint32_t k = keys[j];
+  const uint64_t lo = alpha ? (uint64_t)dkey[(int64_t)(k / T) * N + vals[j]] : 0ull;
+  out[j] = ((uint64_t)k << 32) | lo;
 }
 
 // Longest-first tile order for the persistent render kernels: tiles are
@@ -201,6 +233,16 @@ __global__ void k_offsets(const int64_t* loc, const int64_t* blk, int64_t BN, in
 
 }  // namespace
 
+cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
+                          cudaStream_t s) {
+  if (L.cap == 0) return cudaSuccess;
+  k_keys64<<<(unsigned)((L.cap + 255) / 256), 256, 0, s>>>(
+      (const uint32_t*)(ws + (final_in_b ? L.keysB : L.keysA)),
+      (const uint32_t*)(ws + (final_in_b ? L.valsB : L.valsA)), (const uint32_t*)(ws + L.dkey),
+      (const WsHeader*)(ws + L.hdr), L.cap, L.N, L.T, L.alpha, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s) {
   if (L.BN == 0) return cudaSuccess;
   k_offsets<<<(unsigned)((L.BN + 255) / 256), 256, 0, s>>>(
@@ -228,34 +270,66 @@ cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s) {
 cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
                             int* final_in_b) {
   WsHeader* hdr = (WsHeader*)(ws + L.hdr);
-  uint64_t* kA = (uint64_t*)(ws + L.keysA);
-  uint64_t* kB = (uint64_t*)(ws + L.keysB);
+  uint32_t* kA = (uint32_t*)(ws + L.keysA);
+  uint32_t* kB = (uint32_t*)(ws + L.keysB);
   uint32_t* vA = (uint32_t*)(ws + L.valsA);
   uint32_t* vB = (uint32_t*)(ws + L.valsB);
   *final_in_b = final_buffer_is_b(L);
   if (L.cap > 0 && L.BN > 0) {
+    const unsigned gBN = (unsigned)((L.BN + 255) / 256);
+    const uint32_t* order = nullptr;
+    const int64_t* loc = (const int64_t*)(ws + L.loc_off);
+    const int64_t* blk = (const int64_t*)(ws + L.blk_sum);
+    cudaError_t e;
+    if (L.alpha) {
+      // depth presort of the (view, primitive) records, then offsets in that order
+      uint64_t* pkA = (uint64_t*)(ws + L.pkA);
+      uint64_t* pkB = (uint64_t*)(ws + L.pkB);
+      uint32_t* pvA = (uint32_t*)(ws + L.pvA);
+      uint32_t* pvB = (uint32_t*)(ws + L.pvB);
+      launch_begin(K_DUPLICATE, s);
+      k_presort_keys<<<gBN, 256, 0, s>>>((const uint32_t*)(ws + L.dkey), L.BN, L.N, pkA, pvA);
+      launch_end(K_DUPLICATE, s);
+      int shifts[kMaxPasses];
+      for (int p = 0; p < L.pre_passes; ++p) shifts[p] = 8 * p;  // depth bytes, then view bytes
+      e = launch_sort<uint64_t>(L, ws, pkA, pvA, pkB, pvB, shifts, L.pre_passes, L.BN, L.BN, s);
+      if (e != cudaSuccess) return e;
+      order = (L.pre_passes & 1) ? pvB : pvA;
+      launch_begin(K_DUPLICATE, s);
+      k_gather_counts<<<gBN, 256, 0, s>>>(order, (const int32_t*)(ws + L.count), L.BN,
+                                          (int32_t*)(ws + L.cnt2));
+      launch_end(K_DUPLICATE, s);
+      launch_begin(K_SCAN_BLOCKS, s);
+      k_scan_blocks<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
+          (const int32_t*)(ws + L.cnt2), L.BN, (int64_t*)(ws + L.loc2), (int64_t*)(ws + L.blk2));
+      launch_end(K_SCAN_BLOCKS, s);
+      launch_begin(K_SCAN_SUMS, s);
+      k_scan_sums<int64_t><<<1, 1024, 0, s>>>((int64_t*)(ws + L.blk2), L.nblk_scan, nullptr, 0);
+      launch_end(K_SCAN_SUMS, s);
+      loc = (const int64_t*)(ws + L.loc2);
+      blk = (const int64_t*)(ws + L.blk2);
+    }
     DupArgs d;
     d.rect = (const int4*)(ws + L.rect);
     d.count = (const int32_t*)(ws + L.count);
-    d.dkey = (const uint32_t*)(ws + L.dkey);
-    d.loc = (const int64_t*)(ws + L.loc_off);
-    d.blk = (const int64_t*)(ws + L.blk_sum);
+    d.order = order;
+    d.loc = loc;
+    d.blk = blk;
     d.BN = L.BN; d.N = L.N; d.T = L.T; d.cap = L.cap;
-    d.GX = L.GX; d.alpha = c.blend == WIPES_BLEND_ALPHA;
+    d.GX = L.GX;
     d.keys = kA; d.vals = vA;
     launch_begin(K_DUPLICATE, s);
-    k_duplicate<<<(unsigned)((L.BN + 255) / 256), 256, 0, s>>>(d);
+    k_duplicate<<<gBN, 256, 0, s>>>(d);
     launch_end(K_DUPLICATE, s);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // LSD passes: depth bits (ALPHA) then the view|tile bits.
+    // stable LSD passes over the (view*T + tile) bits only
     int shifts[kMaxPasses];
-    for (int p = 0; p < L.passes; ++p)
-      shifts[p] = p < L.lo_passes ? 8 * p : 32 + 8 * (p - L.lo_passes);
-    e = launch_sort(L, ws, kA, vA, kB, vB, shifts, L.passes, s);
+    for (int p = 0; p < L.passes; ++p) shifts[p] = 8 * p;
+    e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s);
     if (e != cudaSuccess) return e;
   }
-  const uint64_t* kf = *final_in_b ? kB : kA;
+  const uint32_t* kf = *final_in_b ? kB : kA;
   launch_begin(K_TILE_RANGES, s);
   k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(kf, hdr, L.cap, L.BT,
                                                                   (int32_t*)(ws + L.toff));

@@ -54,12 +54,14 @@ static_assert(sizeof(WsHeader) <= 512, "header must fit its slot");
 struct Layout {
   int64_t N = 0, BN = 0, cap = 0, BT = 0, T = 0;
   int32_t B = 0, GX = 0, GY = 0;
-  int32_t hi_bits = 0, passes = 0, lo_passes = 0;
+  int32_t hi_bits = 0, passes = 0, pre_passes = 0;  // dup-sort / depth-presort passes
+  int32_t alpha = 0;
   int64_t nblk_scan = 0;   // blocks of the count scan
   int64_t sort_tiles = 0;  // onesweep tiles of kSortTile keys
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
-         blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, sort_hist = 0,
-         sort_status = 0, toff = 0, order = 0, rgrad = 0, total = 0;
+         blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
+         pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
+         order = 0, rgrad = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -74,9 +76,17 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   int hb = 0;
   while (((int64_t)1 << hb) < L.BT) ++hb;
   L.hi_bits = hb;
-  L.lo_passes = (c.blend == WIPES_BLEND_ALPHA) ? 4 : 0;
-  L.passes = L.lo_passes + (hb + kRadixBits - 1) / kRadixBits;
-  L.sort_tiles = (L.cap + kSortTile - 1) / kSortTile;
+  // dups are keyed by the 32-bit (view*T + tile) id alone: SUM lists are in
+  // index order by emission; ALPHA emits in (view, depth, index) order after a
+  // depth presort of the (view, primitive) records (4 depth-byte passes + the
+  // view bytes), so only the tile bits are sorted per dup.
+  L.alpha = c.blend == WIPES_BLEND_ALPHA;
+  L.passes = (hb + kRadixBits - 1) / kRadixBits;
+  int vb = 0;
+  while (((int64_t)1 << vb) < B) ++vb;
+  L.pre_passes = L.alpha ? 4 + (vb + kRadixBits - 1) / kRadixBits : 0;
+  const int64_t sort_n = L.cap > L.BN ? L.cap : L.BN;
+  L.sort_tiles = (sort_n + kSortTile - 1) / kSortTile;
   L.nblk_scan = (L.BN + kScanTile - 1) / kScanTile;
   if (L.nblk_scan < 1) L.nblk_scan = 1;
   size_t o = 0;
@@ -89,10 +99,18 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.rec = take(64 * L.BN);
   L.loc_off = take(sizeof(int64_t) * L.BN);
   L.blk_sum = take(sizeof(int64_t) * (L.nblk_scan + 1));
-  L.keysA = take(sizeof(uint64_t) * L.cap);
-  L.keysB = take(sizeof(uint64_t) * L.cap);
+  L.keysA = take(sizeof(uint32_t) * L.cap);
+  L.keysB = take(sizeof(uint32_t) * L.cap);
   L.valsA = take(sizeof(uint32_t) * L.cap);
   L.valsB = take(sizeof(uint32_t) * L.cap);
+  const int64_t pn = L.alpha ? L.BN : 0;
+  L.pkA = take(sizeof(uint64_t) * pn);
+  L.pkB = take(sizeof(uint64_t) * pn);
+  L.pvA = take(sizeof(uint32_t) * pn);
+  L.pvB = take(sizeof(uint32_t) * pn);
+  L.cnt2 = take(sizeof(int32_t) * pn);
+  L.loc2 = take(sizeof(int64_t) * pn);
+  L.blk2 = take(sizeof(int64_t) * (L.alpha ? L.nblk_scan + 1 : 0));
   L.sort_hist = take(sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses));
   L.sort_status = take(sizeof(uint32_t) * 256 * (L.sort_tiles > 0 ? L.sort_tiles : 1));
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
@@ -128,8 +146,12 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
                                 const wipes_camera* cams, char* ws, uint8_t* cull_flags,
                                 cudaStream_t s);
 cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
-cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, uint64_t* kB,
-                        uint32_t* vB, const int* shifts, int npass, cudaStream_t s);
+template <typename K>
+cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
+                        const int* shifts, int npass, int64_t n_fixed, int64_t cap,
+                        cudaStream_t s);
+cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
+                          cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);
 cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
                             int* final_in_b);

@@ -1,23 +1,23 @@
-// Onesweep LSD radix sort of (uint64 key, uint32 value) pairs over selected
-// 8-bit digits ("an efficient GPU sorting
-// algorithm"), hand-written for sm_100a (no CUB):
+// Onesweep LSD radix sort of (key, uint32 value) pairs, key = uint32 or
+// uint64, over selected 8-bit digits ("an
+// efficient GPU sorting algorithm"), hand-written for sm_100a (no CUB):
 //
 //  1. k_sort_hist  : one read of the keys builds the global 256-bin histogram
 //                    of EVERY pass at once (shared-memory atomics, then one
 //                    global atomic per (block, pass, digit)).
 //  2. k_sort_pass  : one launch per digit. Each CTA takes the next tile of
-//                    kTile keys (tile id from an atomic counter, so tiles are
-//                    assigned in launch order), ranks them stably in shared
+//                    kSortTile keys (tile id from an atomic counter, so tiles
+//                    are assigned in launch order), ranks them stably in shared
 //                    memory (warp-striped layout, __match_any_sync per step),
 //                    publishes its per-digit counts, resolves its per-digit
 //                    global offsets by DECOUPLED LOOK-BACK over the preceding
 //                    tiles, stages the pairs in shared memory in sorted order
 //                    and writes them out with coalesced runs.
 //
-// Per pass the keys/values are read once and written once (12 + 12 B per
-// pair) — the HBM floor of an LSD pass. Stability: within a tile the rank
-// follows input order (warp-major, then step, then lane); across tiles the
-// look-back prefix follows tile order.
+// Per pass the keys/values are read once and written once — the HBM floor of
+// an LSD pass. Stability: within a tile the rank follows input order
+// (warp-major, then step, then lane); across tiles the look-back prefix
+// follows tile order.
 #include "common.cuh"
 
 namespace wipes {
@@ -27,17 +27,14 @@ namespace {
 constexpr int kWarps = kSortThreads / 32;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
-__device__ __forceinline__ int64_t n_keys(const WsHeader* h, int64_t cap) {
-  int64_t t = h->total;
-  return t < cap ? t : cap;
-}
-
+template <typename K>
 struct SortArgs {
-  const uint64_t* kin;
+  const K* kin;
   const uint32_t* vin;
-  uint64_t* kout;
+  K* kout;
   uint32_t* vout;
   const WsHeader* hdr;
+  int64_t n_fixed;     // >= 0: number of keys; < 0: min(hdr->total, cap)
   int64_t cap;
   uint32_t* ghist;     // [kMaxPasses][256]
   uint32_t* counter;   // [kMaxPasses] tile counters
@@ -46,14 +43,22 @@ struct SortArgs {
   int32_t npass, pass, shift;
 };
 
-__global__ void __launch_bounds__(256) k_sort_hist(SortArgs a) {
+template <typename K>
+__device__ __forceinline__ int64_t n_keys(const SortArgs<K>& a) {
+  if (a.n_fixed >= 0) return a.n_fixed;
+  const int64_t t = a.hdr->total;
+  return t < a.cap ? t : a.cap;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) k_sort_hist(SortArgs<K> a) {
   __shared__ uint32_t h[kMaxPasses][256];
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int64_t n = n_keys(a.hdr, a.cap);
+  const int64_t n = n_keys(a);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = a.kin[i];
+    const K k = a.kin[i];
 #pragma unroll
     for (int p = 0; p < kMaxPasses; ++p)
       if (p < a.npass) atomicAdd(&h[p][(uint32_t)(k >> a.shifts[p]) & 255u], 1u);
@@ -65,8 +70,9 @@ __global__ void __launch_bounds__(256) k_sort_hist(SortArgs a) {
   }
 }
 
+template <typename K>
 struct SortSmem {
-  uint64_t keys[kSortTile];
+  K keys[kSortTile];
   uint32_t vals[kSortTile];
   uint32_t wcnt[kWarps][256];  // per-warp running counts, then warp-exclusive prefixes
   uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
@@ -74,11 +80,12 @@ struct SortSmem {
   uint32_t tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs a) {
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+  SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t n = n_keys(a.hdr, a.cap);
+  const int64_t n = n_keys(a);
   if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
   for (int i = tid; i < kWarps * 256; i += kSortThreads) (&sm.wcnt[0][0])[i] = 0;
   __syncthreads();
@@ -88,14 +95,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs a) {
   const int shift = a.shift;
   const uint32_t lt = (1u << lane) - 1u;
   // ---- load (warp-striped) and rank stably within the tile ----------------
-  uint64_t key[kSortItems];
+  K key[kSortItems];
   uint32_t val[kSortItems];
   uint32_t dig[kSortItems], rank[kSortItems];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
     const bool valid = idx < n;
-    key[i] = valid ? a.kin[idx] : 0ull;
+    key[i] = valid ? a.kin[idx] : (K)0;
     val[i] = valid ? a.vin[idx] : 0u;
     dig[i] = valid ? ((uint32_t)(key[i] >> shift) & 255u) : 256u;
   }
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs a) {
   const int64_t rem = n - base;
   const int tn = rem < kSortTile ? (int)rem : kSortTile;
   for (int j = tid; j < tn; j += kSortThreads) {
-    const uint64_t k = sm.keys[j];
+    const K k = sm.keys[j];
     const uint32_t dd = (uint32_t)(k >> shift) & 255u;
     const int64_t pos = (int64_t)sm.gofs[dd] + (j - (int64_t)sm.bexcl[dd]);
     a.kout[pos] = k;
@@ -175,20 +182,21 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs a) {
 
 }  // namespace
 
-size_t sort_smem_bytes() { return sizeof(SortSmem); }
-
-cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, uint64_t* kB,
-                        uint32_t* vB, const int* shifts, int npass, cudaStream_t s) {
-  if (npass == 0 || L.cap == 0) return cudaSuccess;
+template <typename K>
+cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
+                        const int* shifts, int npass, int64_t n_fixed, int64_t cap,
+                        cudaStream_t s) {
+  if (npass == 0 || cap == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(SortSmem));
+    cudaFuncSetAttribute(k_sort_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SortSmem<K>));
     attr = true;
   }
-  SortArgs a;
+  SortArgs<K> a;
   a.hdr = (const WsHeader*)(ws + L.hdr);
-  a.cap = L.cap;
+  a.n_fixed = n_fixed;
+  a.cap = cap;
   a.ghist = (uint32_t*)(ws + L.sort_hist);
   a.counter = a.ghist + kMaxPasses * 256;
   a.status = (uint32_t*)(ws + L.sort_status);
@@ -196,13 +204,13 @@ cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, u
   for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
   cudaError_t e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
   if (e != cudaSuccess) return e;
-  a.kin = kA; a.vin = vA; a.pass = 0;
-  const int64_t hist_blocks = (L.cap + 4095) / 4096;
+  a.kin = kA; a.vin = vA; a.pass = 0; a.shift = 0;
+  const int64_t hist_blocks = (cap + 4095) / 4096;
   launch_begin(K_RADIX_HIST, s);
-  k_sort_hist<<<(unsigned)(hist_blocks < 1184 ? (hist_blocks > 0 ? hist_blocks : 1) : 1184), 256, 0,
-                s>>>(a);
+  k_sort_hist<K><<<(unsigned)(hist_blocks < 1184 ? (hist_blocks > 0 ? hist_blocks : 1) : 1184),
+                   256, 0, s>>>(a);
   launch_end(K_RADIX_HIST, s);
-  const int64_t tiles = (L.cap + kSortTile - 1) / kSortTile;
+  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
   for (int p = 0; p < npass; ++p) {
     const bool from_a = (p & 1) == 0;
     a.kin = from_a ? kA : kB; a.vin = from_a ? vA : vB;
@@ -212,12 +220,21 @@ cudaError_t launch_sort(const Layout& L, char* ws, uint64_t* kA, uint32_t* vA, u
     e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * 256 * (size_t)tiles, s);
     if (e != cudaSuccess) return e;
     launch_begin(K_RADIX_SCATTER, s);
-    k_sort_pass<<<(unsigned)tiles, kSortThreads, sizeof(SortSmem), s>>>(a);
+    k_sort_pass<K><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
     launch_end(K_RADIX_SCATTER, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
+
+template cudaError_t launch_sort<uint32_t>(const Layout&, char*, uint32_t*, uint32_t*,
+                                           uint32_t*, uint32_t*, const int*, int, int64_t,
+                                           int64_t, cudaStream_t);
+template cudaError_t launch_sort<uint64_t>(const Layout&, char*, uint64_t*, uint32_t*,
+                                           uint64_t*, uint32_t*, const int*, int, int64_t,
+                                           int64_t, cudaStream_t);
+
+size_t sort_smem_bytes64() { return sizeof(SortSmem<uint64_t>); }
 
 }  // namespace wipes
