@@ -19,6 +19,12 @@ namespace wipes {
 namespace {
 
 constexpr double kLog2e = 1.4426950408889634;
+#ifndef WIPES_PRE3D_MINB
+#define WIPES_PRE3D_MINB 2  // min CTAs/SM, FP64 3D backward (no spills at 234 registers)
+#endif
+#ifndef WIPES_PRE3D_FWD_MINB
+#define WIPES_PRE3D_FWD_MINB 8  // min CTAs/SM, FP64 3D forward (measured faster at 64 registers)
+#endif
 
 struct PreOut {
   int4* rect;
@@ -193,7 +199,9 @@ __device__ __forceinline__ double s3at(const double* S, int i, int j) {
   return S[k];
 }
 
-// O2 steps 1-9 in the pinned order.
+// O2 steps 1-9 in the pinned order. PINNED = false (backward
+// only, where no integer decision is taken) replaces divisions by reciprocals.
+template <bool PINNED = true>
 __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_clamp,
                          const double* mu, const double* s, const double* q, const double* f,
                          Proj3& P) {
@@ -207,7 +215,12 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
   double x = P.p[0], y = P.p[1], z = P.p[2];
   double w = q[0], qx = q[1], qy = q[2], qz = q[3];
   double n = sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
-  w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+  if (PINNED) {
+    w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+  } else {
+    const double rn = 1.0 / n;
+    w *= rn; qx *= rn; qy *= rn; qz *= rn;
+  }
   P.qn[0] = w; P.qn[1] = qx; P.qn[2] = qy; P.qn[3] = qz; P.qnorm = n;
   double* R = P.Rq;
   R[0] = 1.0 - 2.0 * ((qy * qy) + (qz * qz));
@@ -225,7 +238,8 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
     for (int j = i; j < 3; ++j)
       P.S3[k++] = (((R[3 * i] * s2[0]) * R[3 * j] + (R[3 * i + 1] * s2[1]) * R[3 * j + 1]) +
                    (R[3 * i + 2] * s2[2]) * R[3 * j + 2]);
-  double tx = x / z, ty = y / z;
+  const double rz = PINNED ? 0.0 : 1.0 / z;
+  double tx = PINNED ? x / z : x * rz, ty = PINNED ? y / z : y * rz;
   P.clx = P.cly = false;
   if (ewa_clamp) {
     double limx = (1.3 * (double)W) / (2.0 * fx);
@@ -236,10 +250,17 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
     ty = fmin(fmax(ty, -limy), limy);
   }
   P.thx = tx; P.thy = ty;
-  P.j00 = fx / z;
-  P.j11 = fy / z;
-  P.j02 = -(fx * tx) / z;
-  P.j12 = -(fy * ty) / z;
+  if (PINNED) {
+    P.j00 = fx / z;
+    P.j11 = fy / z;
+    P.j02 = -(fx * tx) / z;
+    P.j12 = -(fy * ty) / z;
+  } else {
+    P.j00 = fx * rz;
+    P.j11 = fy * rz;
+    P.j02 = -(fx * tx) * rz;
+    P.j12 = -(fy * ty) * rz;
+  }
   for (int jj = 0; jj < 3; ++jj) {
     P.M[jj] = P.j00 * Rv[jj] + P.j02 * Rv[6 + jj];
     P.M[3 + jj] = P.j11 * Rv[3 + jj] + P.j12 * Rv[6 + jj];
@@ -266,7 +287,7 @@ struct Pre3DArgs {
   CamBlock cams;
 };
 
-__global__ void __launch_bounds__(128) k_pre3d(const __grid_constant__ Pre3DArgs a) {
+__global__ void __launch_bounds__(128, WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)a.cams.nv * a.N) return;
   int vl = (int)(gid / a.N);
@@ -439,7 +460,7 @@ struct Bwd3DArgs {
 // One thread per OUTPUT parameter row. With view_stride = 0 it sums the
 // contributions of the launch's views in view order (deterministic); launches
 // after the first (B > 128 views) add to the rows written before.
-__global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3DArgs a) {
+__global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __grid_constant__ Bwd3DArgs a) {
   int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= a.nrows) return;
   int v_lo, v_hi;
@@ -461,27 +482,29 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
     if (a.flag[o] != 0) continue;
     const float* cam = a.cams.v[v - a.cams.v0];
     Proj3 P;
-    project3(cam, a.c.W, a.c.H, a.ewa_clamp, mu, s, q, f, P);
+    project3<false>(cam, a.c.W, a.c.H, a.ewa_clamp, mu, s, q, f, P);
     double x = P.p[0], y = P.p[1], z = P.p[2];
     double fx = cam[12], fy = cam[13];
+    const double rz = 1.0 / z, rz2 = rz * rz, rfx = 1.0 / fx, rfy = 1.0 / fy;
     double Rv[9];
     for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
     // conic of the (diag-offset) Sigma' and the record gradients from moments
     double sxx = P.Sp[0] + a.c.diag, sxy = P.Sp[1], syy = P.Sp[2] + a.c.diag;
     double det = sxx * syy - sxy * sxy;
-    double A[3] = {syy / det, -sxy / det, sxx / det};
+    const double rdet = 1.0 / det;
+    double A[3] = {syy * rdet, -sxy * rdet, sxx * rdet};
     double g[kRecGrads];
-    moments_to_grads(a.mom + kMoments * o, A, (z * P.g[0]) / fx, (z * P.g[1]) / fy, 0.5,
+    moments_to_grads(a.mom + kMoments * o, A, (z * P.g[0]) * rfx, (z * P.g[1]) * rfy, 0.5,
                      a.opacity[pi], g);
     gphi += g[RG_PHI];
     gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
     gal += g[RG_ALPHA];
     double dp[3] = {0, 0, 0};
-    dp[0] += g[RG_MUX] * fx / z;
-    dp[1] += g[RG_MUY] * fy / z;
-    dp[2] += -g[RG_MUX] * fx * x / (z * z) - g[RG_MUY] * fy * y / (z * z);
-    dp[2] += g[RG_FX] * P.g[0] / fx + g[RG_FY] * P.g[1] / fy;
-    double dg0 = g[RG_FX] * z / fx, dg1 = g[RG_FY] * z / fy;
+    dp[0] += g[RG_MUX] * fx * rz;
+    dp[1] += g[RG_MUY] * fy * rz;
+    dp[2] += -g[RG_MUX] * fx * x * rz2 - g[RG_MUY] * fy * y * rz2;
+    dp[2] += g[RG_FX] * P.g[0] * rfx + g[RG_FY] * P.g[1] * rfy;
+    double dg0 = g[RG_FX] * z * rfx, dg1 = g[RG_FY] * z * rfy;
     for (int k = 0; k < 3; ++k) gf[k] += Rv[k] * dg0 + Rv[3 + k] * dg1;
     double gsv[3];
     conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gsv);
@@ -504,13 +527,13 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
     double dj02 = dM[0][0] * Rv[6] + dM[0][1] * Rv[7] + dM[0][2] * Rv[8];
     double dj11 = dM[1][0] * Rv[3] + dM[1][1] * Rv[4] + dM[1][2] * Rv[5];
     double dj12 = dM[1][0] * Rv[6] + dM[1][1] * Rv[7] + dM[1][2] * Rv[8];
-    dp[2] += dj00 * (-fx / (z * z)) + dj11 * (-fy / (z * z));
-    double dtx_dx = P.clx ? 0.0 : 1.0 / z, dtx_dz = P.clx ? 0.0 : -x / (z * z);
-    double dty_dy = P.cly ? 0.0 : 1.0 / z, dty_dz = P.cly ? 0.0 : -y / (z * z);
-    dp[0] += dj02 * (-(fx / z) * dtx_dx);
-    dp[2] += dj02 * (fx * P.thx / (z * z) - (fx / z) * dtx_dz);
-    dp[1] += dj12 * (-(fy / z) * dty_dy);
-    dp[2] += dj12 * (fy * P.thy / (z * z) - (fy / z) * dty_dz);
+    dp[2] += dj00 * (-fx * rz2) + dj11 * (-fy * rz2);
+    double dtx_dx = P.clx ? 0.0 : rz, dtx_dz = P.clx ? 0.0 : -x * rz2;
+    double dty_dy = P.cly ? 0.0 : rz, dty_dz = P.cly ? 0.0 : -y * rz2;
+    dp[0] += dj02 * (-(fx * rz) * dtx_dx);
+    dp[2] += dj02 * (fx * P.thx * rz2 - (fx * rz) * dtx_dz);
+    dp[1] += dj12 * (-(fy * rz) * dty_dy);
+    dp[2] += dj12 * (fy * P.thy * rz2 - (fy * rz) * dty_dz);
     for (int k = 0; k < 3; ++k) gmu[k] += Rv[k] * dp[0] + Rv[3 + k] * dp[1] + Rv[6 + k] * dp[2];
     const double* R = P.Rq;
     double dRq[9];
@@ -537,7 +560,8 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd(const __grid_constant__ Bwd3D
     dqn[3] = dRq[0] * (-4 * qz) + dRq[1] * (-2 * w) + dRq[2] * (2 * qx) + dRq[3] * (2 * w) +
              dRq[4] * (-4 * qz) + dRq[5] * (2 * qy) + dRq[6] * (2 * qx) + dRq[7] * (2 * qy);
     double dot = dqn[0] * P.qn[0] + dqn[1] * P.qn[1] + dqn[2] * P.qn[2] + dqn[3] * P.qn[3];
-    for (int k = 0; k < 4; ++k) gq[k] += (dqn[k] - P.qn[k] * dot) / P.qnorm;
+    const double rq = 1.0 / P.qnorm;
+    for (int k = 0; k < 4; ++k) gq[k] += (dqn[k] - P.qn[k] * dot) * rq;
   }
   auto put = [&](float* dst, double v) { *dst = a.accumulate ? *dst + (float)v : (float)v; };
   if (a.g.mean) for (int k = 0; k < 3; ++k) put(&a.g.mean[3 * pi + k], gmu[k]);
