@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j0 >= a.BN) return;
   const int64_t o = a.order ? (int64_t)a.order[j0] : j0;
+  WCHECK(o >= 0 && o < a.BN);
   const int32_t n = a.count[o];
   if (n == 0) return;
   int64_t j = a.loc[j0] + a.blk[j0 / kScanTile];
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
     const uint32_t rowt = vt + (uint32_t)ty * (uint32_t)a.GX;
     for (int tx = r.x; tx < r.z; ++tx, ++j) {
       if (j >= a.cap) return;
+      WCHECK(j >= 0 && rowt + (uint32_t)tx < (uint32_t)((v + 1) * a.T));
       a.keys[j] = rowt + (uint32_t)tx;
       a.vals[j] = (uint32_t)i;
     }
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, const
   int64_t tp = i == 0 ? -1 : (int64_t)keys[i - 1];
   int64_t tc = i == n ? BT : (int64_t)keys[i];
   if (tc > BT) tc = BT;
+  WCHECK(tp >= -1 && tc <= BT && tp <= tc);
   for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
 }
 

@@ -4,9 +4,18 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cassert>
 #include <cuda_runtime.h>
 
 #include "../../include/wipes.h"
+
+// Debug builds (-DWIPES_CHECKS, see tools/sanitize_run.py) assert every index
+// the kernels derive from data before using it.
+#ifdef WIPES_CHECKS
+#define WCHECK(c) assert(c)
+#else
+#define WCHECK(c) ((void)0)
+#endif
 
 namespace wipes {
 

@@ -172,6 +172,7 @@ __device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chu
   const int chunk = item % chunks;
   const int sub = (item / chunks) % Gm::S;
   it.tile = a.order[item / (chunks * Gm::S)];
+  WCHECK(it.tile >= 0 && it.tile < a.BT);
   it.v = it.tile / a.T;
   const int64_t t_in_v = it.tile - it.v * a.T;
   const int ty = (int)(t_in_v / a.GX), tx = (int)(t_in_v - (int64_t)ty * a.GX);
@@ -217,6 +218,7 @@ __device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* re
   bool hit = false;
   if (valid) {
     pid = (int32_t)a.vals[idx];
+    WCHECK(pid >= 0 && pid < a.N);
     const float4* r = recv + 4 * (int64_t)pid;
     r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
     hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G);

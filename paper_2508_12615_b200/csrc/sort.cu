@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
     const uint32_t dd = dig[i];
     if (dd < 256u) {
       const uint32_t loc = sm.bexcl[dd] + sm.wcnt[wid][dd] + rank[i];
+      WCHECK(loc < (uint32_t)kSortTile);
       sm.keys[loc] = key[i];
       sm.vals[loc] = val[i];
     }
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
     const K k = sm.keys[j];
     const uint32_t dd = (uint32_t)(k >> shift) & 255u;
     const int64_t pos = (int64_t)sm.gofs[dd] + (j - (int64_t)sm.bexcl[dd]);
+    WCHECK(pos >= 0 && pos < n);
     a.kout[pos] = k;
     a.vout[pos] = sm.vals[j];
   }
