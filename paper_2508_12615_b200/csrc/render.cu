@@ -105,6 +105,33 @@ struct Geo {
 
 // Conservative test: can the record's opacity-extent AABB (padded) touch the
 // footprint whose pixel centres span [sx0 + 0.5, sx0 + 7.5] x [sy0 + 0.5, sy0 + h - 0.5]?
+// Exact (up to a small margin) test of the record's ellipse {e >= thr} against
+// the footprint's pixel-centre rectangle: the exponent e = A dx^2 + B dx dy +
+// C dy^2 + log2(alpha) is concave (A, C < 0); if its maximiser (the centre) is
+// outside the rectangle, the constrained maximum lies on an edge facing the
+// centre (KKT: the active constraint's normal has a positive product with
+// centre - argmax), where e is a 1-D concave quadratic maximised in closed form.
+__device__ __forceinline__ bool ellipse_hits_rect(const float4& r0, const float4& r1, float sx0,
+                                                  float sy0, float h, float thr) {
+  const float x0 = (sx0 + 0.5f - r0.x) - r0.z, x1 = x0 + 7.f;
+  const float y0 = (sy0 + 0.5f - r0.y) - r0.w, y1 = y0 + (h - 1.f);
+  const bool inx = x0 <= 0.f && 0.f <= x1, iny = y0 <= 0.f && 0.f <= y1;
+  if (inx && iny) return true;
+  const float A = r1.x, B = r1.y, C = r1.z, L = r1.w;
+  float best = -INFINITY;
+  if (!inx) {  // facing vertical edge x = xe, maximise over y
+    const float xe = x0 > 0.f ? x0 : x1;
+    const float y = fminf(fmaxf(-B * xe / (2.f * C), y0), y1);
+    best = fmaxf(best, fmaf(fmaf(A, xe, B * y), xe, fmaf(C * y, y, L)));
+  }
+  if (!iny) {  // facing horizontal edge y = ye, maximise over x
+    const float ye = y0 > 0.f ? y0 : y1;
+    const float x = fminf(fmaxf(-B * ye / (2.f * A), x0), x1);
+    best = fmaxf(best, fmaf(fmaf(A, x, B * ye), x, fmaf(C * ye, ye, L)));
+  }
+  return best >= thr;
+}
+
 __device__ __forceinline__ bool hits_footprint(const float4& r0, const float4& r3, float sx0,
                                                float sy0, float h) {
   __half2 e2 = *reinterpret_cast<const __half2*>(&r3.w);
@@ -222,7 +249,11 @@ __device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* re
     const float4* r = recv + 4 * (int64_t)pid;
     r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
     hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G);
-    if (hit) { r1 = ldg_nc(r + 1); r2 = ldg_nc(r + 2); }
+    if (hit) {
+      r1 = ldg_nc(r + 1);
+      hit = ellipse_hits_rect(r0, r1, it.sx0, it.sy0, 8.f * G, a.skip_e - 0.01f);
+      if (hit) r2 = ldg_nc(r + 2);
+    }
   }
   const uint32_t bal = __ballot_sync(kFull, hit);
   if (hit) {
