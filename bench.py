@@ -189,7 +189,8 @@ def main():
 
     name = args.config
     base = gen.CONFIGS[name]
-    shared = base["kind"] == "3d"
+    rows = base.get("shard") == "rows"           # one image, tile rows sharded
+    shared = base["kind"] == "3d" or rows          # one problem shared by all ranks
     # weak scaling: every rank its own independent problem (different seed);
     # 3D batch: one scene, views sharded across ranks + gradient all_reduce.
     c = gen.make_config(name, seed=args.seed + (0 if shared else rank))
@@ -197,11 +198,12 @@ def main():
     blend = c["blend"]
     cams = c["cams"]
     vs = c["view_stride"]
-    my_views = list(range(rank, B, world)) if shared else None
-    if shared:
+    my_views = list(range(rank, B, world)) if (shared and not rows) else None
+    if my_views is not None:
         cams = [cams[v] for v in my_views]
     Bl = len(cams) if cams is not None else 1
-    r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev)
+    r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev,
+                   row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0)
     params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
     if c["kind"] == "6d":
         pass
@@ -290,6 +292,8 @@ def main():
     units = world * args.steps if not shared else args.steps   # iterations (problems) processed
     value = units / (total_ms / 1e3)
     render_fps = (world * args.steps * Bl if not shared else args.steps * B) / (total_fwd_ms / 1e3)
+    if rows:
+        render_fps = args.steps / (total_fwd_ms / 1e3)
 
     # ---- e2e: same metric through the public API with HOST buffers --------
     host_params = {k: torch.from_numpy(v).pin_memory() for k, v in c["params"].items()}
@@ -354,7 +358,9 @@ def main():
             "config": {"workload": f"{name}: {c['desc']}", "H": H, "W": W, "N": N, "views": B,
                        "blend": blend, "dup": int(n_tot2),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
-                       "parallelism": (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
+                       "parallelism": (f"tile rows r = rank (mod {world}) of one image per GPU + "
+                                       "NCCL all_reduce of per-primitive gradients") if rows else
+                                      (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
                                        "per-primitive gradients") if shared else
                                       f"replicas: {world} independent image(s), one per GPU"},
             "render_fps": render_fps,

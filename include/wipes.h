@@ -89,6 +89,12 @@ typedef struct {
   int32_t ewa_clamp;      /* 1: clamp x/z, y/z at 1.3 x half-FOV inside J      */
   float background[3];    /* ALPHA only                                        */
   int32_t deterministic;  /* reserved (must be 0 in ABI v1)                    */
+  /* Image-space sharding: when row_mod > 1 only tile rows ty
+   * with ty % row_mod == row_rem are binned and rendered (the rest of the image
+   * is left unbinned: zero in SUM mode, background in ALPHA mode, no gradient).
+   * Each rank of a row_mod-way split renders its rows; summing the ranks'
+   * gradients gives the full-image gradient. 0 / 0 = all rows. */
+  int32_t row_mod, row_rem;
 } wipes_config;
 
 /* Primitive parameters (device). Shapes, with N primitives:

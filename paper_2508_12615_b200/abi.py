@@ -37,7 +37,7 @@ class wipes_config(C.Structure):
                 ("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float),
                 ("dilation", C.c_float), ("cov_eps", C.c_float), ("det_min", C.c_float),
                 ("ewa_clamp", C.c_int32), ("background", C.c_float * 3),
-                ("deterministic", C.c_int32)]
+                ("deterministic", C.c_int32), ("row_mod", C.c_int32), ("row_rem", C.c_int32)]
 
 
 class wipes_params(C.Structure):
@@ -123,13 +123,14 @@ def check(status: int, where: str):
 def make_config(width, height, tile=16, prim="2d", blend="sum", cov2="sigma", proj="paper",
                 extent="opacity", alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4,
                 dilation=None, cov_eps=0.0, det_min=1e-12, ewa_clamp=True,
-                background=(0.0, 0.0, 0.0), deterministic=0) -> wipes_config:
+                background=(0.0, 0.0, 0.0), deterministic=0, row_mod=0,
+                row_rem=0) -> wipes_config:
     if dilation is None:
         dilation = 0.3 if prim == "3d" else 0.0
     return wipes_config(int(width), int(height), int(tile), PRIM[prim], BLEND[blend], COV2[cov2],
                         PROJ[proj], EXTENT[extent], alpha_min, alpha_max, T_min, dilation,
                         cov_eps, det_min, int(bool(ewa_clamp)), (C.c_float * 3)(*background),
-                        int(deterministic))
+                        int(deterministic), int(row_mod), int(row_rem))
 
 
 def cameras(cams) -> "C.Array":

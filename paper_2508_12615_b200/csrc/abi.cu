@@ -76,6 +76,8 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
   if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
     return fail(WIPES_EINVAL, "need 0 <= alpha_min < alpha_max <= 1");
   if (!(c->T_min >= 0.f) || !(c->T_min < 1.f)) return fail(WIPES_EINVAL, "T_min");
+  if (c->row_mod < 0 || (c->row_mod > 1 && (c->row_rem < 0 || c->row_rem >= c->row_mod)))
+    return fail(WIPES_EINVAL, "row_mod / row_rem");
   if (N < 0 || N > ((int64_t)1 << 31) - 1) return fail(WIPES_EINVAL, "N out of range");
   if (B < 1) return fail(WIPES_EINVAL, "B must be >= 1");
   if (c->prim == WIPES_PRIM_2D && B != 1) return fail(WIPES_EINVAL, "2D primitives need B == 1");

@@ -120,7 +120,7 @@ struct DupArgs {
   const int64_t* loc;
   const int64_t* blk;
   int64_t BN, N, T, cap;
-  int32_t GX;
+  int32_t GX, row_mod, row_rem;
   uint32_t* keys;
   uint32_t* vals;
 };
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   const int64_t v = o / a.N, i = o - v * a.N;
   const int4 r = a.rect[o];
   const uint32_t vt = (uint32_t)(v * a.T);
-  for (int ty = r.y; ty < r.w; ++ty) {
+  const int ty0 = a.row_mod > 1 ? band_first_row(r.y, a.row_mod, a.row_rem) : r.y;
+  const int dty = a.row_mod > 1 ? a.row_mod : 1;
+  for (int ty = ty0; ty < r.w; ty += dty) {
     const uint32_t rowt = vt + (uint32_t)ty * (uint32_t)a.GX;
     for (int tx = r.x; tx < r.z; ++tx, ++j) {
       if (j >= a.cap) return;
@@ -320,6 +322,7 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     d.blk = blk;
     d.BN = L.BN; d.N = L.N; d.T = L.T; d.cap = L.cap;
     d.GX = L.GX;
+    d.row_mod = c.row_mod; d.row_rem = c.row_rem;
     d.keys = kA; d.vals = vA;
     launch_begin(K_DUPLICATE, s);
     k_duplicate<<<gBN, 256, 0, s>>>(d);

@@ -75,6 +75,16 @@ struct Layout {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Image-space sharding: first tile row >= y0 with ty % mod == rem, and the
+// number of such rows in [y0, y1).
+__host__ __device__ inline int band_first_row(int y0, int mod, int rem) {
+  return y0 + (((rem - y0) % mod) + mod) % mod;
+}
+__host__ __device__ inline int rows_in_band(int y0, int y1, int mod, int rem) {
+  const int f = band_first_row(y0, mod, rem);
+  return f < y1 ? (y1 - 1 - f) / mod + 1 : 0;
+}
+
 inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t cap) {
   Layout L;
   L.N = N; L.B = B; L.BN = N * (int64_t)B; L.cap = cap < 0 ? 0 : cap;

@@ -43,7 +43,7 @@ __device__ __forceinline__ uint32_t orderable(float v) {
 }
 
 struct Cfg2 {
-  int32_t W, H, tile, GX, GY, extent, alpha_blend;
+  int32_t W, H, tile, GX, GY, extent, alpha_blend, row_mod, row_rem;
   double alpha_min, det_min, diag;  // diag = cov_eps + dilation
 };
 
@@ -82,7 +82,9 @@ __device__ int finish2d(const Cfg2& c, double mux, double muy, double sxx, doubl
   fy0 = fmin(fmax(fy0, 0.0), (double)c.GY);
   fy1 = fmin(fmax(fy1, 0.0), (double)c.GY);
   int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-  int n = max(0, x1 - x0) * max(0, y1 - y0);
+  int ny = max(0, y1 - y0);
+  if (c.row_mod > 1) ny = rows_in_band(y0, y1, c.row_mod, c.row_rem);
+  int n = max(0, x1 - x0) * ny;
   *rect = make_int4(x0, y0, x1, y1);
   *count = n;
   return n == 0 ? 4 : 0;
@@ -577,6 +579,7 @@ Cfg2 make_cfg2(const wipes_config& c, const Layout& L) {
   Cfg2 r;
   r.W = c.width; r.H = c.height; r.tile = c.tile; r.GX = L.GX; r.GY = L.GY;
   r.extent = c.extent; r.alpha_blend = c.blend == WIPES_BLEND_ALPHA;
+  r.row_mod = c.row_mod; r.row_rem = c.row_rem;
   r.alpha_min = (double)c.alpha_min;
   r.det_min = (double)c.det_min;
   r.diag = (double)c.cov_eps + (double)c.dilation;

@@ -183,8 +183,8 @@ CONFIGS = {
                desc="3D static NVS: 1M 3D wavelet primitives, 8 x 1080p views, alpha blending"),
     "c4": dict(kind="6d", H=1014, W=1352, N=300000, B=100, blend="alpha",
                desc="6D dynamic NVS: per-frame params, 100 frames at 1352x1014"),
-    "c5": dict(kind="2d", H=2160, W=3840, N=3000000, blend="sum",
-               desc="Scale sweep: 4K image, 3M 2D primitives, weighted sum"),
+    "c5": dict(kind="2d", H=2160, W=3840, N=3000000, blend="sum", shard="rows",
+               desc="Scale sweep: 4K image, 3M 2D primitives, weighted sum, tile-row sharded"),
     "p3d": dict(kind="3d", H=256, W=256, N=20000, B=2, blend="alpha", scale_mult=4.0,
                 desc="parity-only mini 3D"),
     "p6d": dict(kind="6d", H=96, W=128, N=5000, B=3, blend="alpha", scale_mult=4.0,

@@ -83,3 +83,49 @@ def test_view_sharded_gradients_equal_single_process(ora):
     ref = ora.forward_backward(cfg, c["params"], dL, cams=c["cams"])["grads"]
     for k, v in ref.items():
         np.testing.assert_allclose(got[k], v.astype(np.float32), rtol=1e-5, atol=1e-6)
+
+
+def _worker_rows(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    H, W = 48, 64
+    p = gen.gen2d(H, W, 200, seed=9, freq_std=0.5)
+    cfg = oracle.Cfg(width=W, height=H)
+    dL = gen.gen_dLdC(1, H, W, seed=9)[0].transpose(1, 2, 0).copy()
+    # this rank owns tile rows ty = rank (mod world): only its pixels carry dL/dC
+    rows = wdist.tile_rows(-(-H // 16), rank, world)
+    mask = np.isin(np.arange(H) // 16, rows)
+    dL[~mask] = 0.0
+    out = oracle.forward_backward(cfg, p, dL.reshape(-1, 3))
+    grads = {k: torch.from_numpy(v.astype(np.float32)) for k, v in out["grads"].items()}
+    wdist.GradBucket(grads).all_reduce()
+    if rank == 0:
+        q.put({k: v.numpy().copy() for k, v in grads.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_tile_row_sharded_gradients_equal_single_process(ora):
+    """Image-space sharding: ranks own tile rows ty = r (mod
+    world); the all_reduce of their gradients equals the full-image gradient."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_rows, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    H, W = 48, 64
+    p = gen.gen2d(H, W, 200, seed=9, freq_std=0.5)
+    dL = gen.gen_dLdC(1, H, W, seed=9)[0].transpose(1, 2, 0).reshape(-1, 3)
+    ref = ora.forward_backward(ora.Cfg(width=W, height=H), p, dL)["grads"]
+    for k, v in ref.items():
+        np.testing.assert_allclose(got[k], v.astype(np.float32), rtol=1e-5, atol=1e-6)

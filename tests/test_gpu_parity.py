@@ -259,3 +259,43 @@ def test_full_size_sampled_parity(ora, name):
     if c["blend"] == "alpha":
         nbad, _ = pixel_violations(_np(out["T_final"]).reshape(-1)[pix], ro["T"], ro["margin"])
         assert nbad == 0
+
+
+# ------------------------------------------------------ image-space sharding --
+@pytest.mark.parametrize("blend", ["sum", "alpha"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharding_equals_full(ora, blend, world):
+    """SURVEY §8(e) tile-row sharding of one image: rank r bins and renders the
+    tile rows ty = r (mod world). Its rows are bit-identical to the unsharded
+    render (same per-tile lists, same order), its counts are the oracle's rects
+    restricted to its rows, and the ranks' gradients sum to the full gradient."""
+    H, W, N = 160, 144, 3000
+    p = gen.gen2d(H, W, N, seed=5, freq_std=0.4, phase=True, alpha=(0.3, 1.0),
+                  depth=(blend == "alpha"))
+    dp = to_dev(p)
+    dL = torch.from_numpy(gen.gen_dLdC(1, H, W, seed=5)).cuda()
+    full = gpu_rasterizer("2d", H, W, blend)
+    img = full.forward(dp)["image"].clone()
+    gfull = {k: v.clone() for k, v in full.backward(dL).items()}
+    cfg_o = oracle_cfg(ora, "2d", H, W, blend)
+    pr = ora.project2d(cfg_o, p)
+    gsum = None
+    rows = (np.arange(H) // 16)
+    for r in range(world):
+        rs = gpu_rasterizer("2d", H, W, blend, row_mod=world, row_rem=r)
+        out = rs.forward(dp)
+        torch.cuda.synchronize()
+        mask = torch.from_numpy(rows % world == r).cuda()
+        assert torch.equal(out["image"][..., mask, :], img[..., mask, :])
+        cnt = _np(rs.get_preprocess()["count"])
+        nx = np.maximum(pr.rect[:, 2] - pr.rect[:, 0], 0)
+        ny = np.array([sum(1 for ty in range(y0, y1) if ty % world == r)
+                       for (_, y0, _, y1) in pr.rect])
+        assert np.array_equal(cnt, nx * ny * (pr.flag == 0))
+        g = rs.backward(dL)
+        torch.cuda.synchronize()
+        gsum = {k: v.clone() for k, v in g.items()} if gsum is None else \
+            {k: gsum[k] + g[k] for k in g}
+    for k in gfull:
+        a, b = _np(gsum[k]), _np(gfull[k])
+        assert np.allclose(a, b, rtol=1e-4, atol=1e-6), (k, np.abs(a - b).max())
