@@ -255,12 +255,15 @@ def chain2d(cfg: Cfg, p: dict, pr: Projected, rgrad):
 
 
 def chain3d(cfg: Cfg, p: dict, cams, pr: Projected, rgrad, view_stride: int = 0):
+    """3D chain rule. Paper mode: analytic (oracle.cpp ora_chain3d); exact mode:
+    J^T g with J the central-difference Jacobian of the exact projection."""
     N, B = pr.N, pr.B
     NP = N if view_stride == 0 else B * N
     out = {k: np.zeros(s, np.float64) for k, s in
            [("mean", (NP, 3)), ("scale", (NP, 3)), ("quat", (NP, 4)), ("freq", (NP, 3)),
             ("phase", (NP,)), ("color", (NP, 3)), ("opacity", (NP,))]}
-    lib().ora_chain3d(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), cams_c(cams),
+    fn = lib().ora_chain3d_exact if cfg.exact_proj else lib().ora_chain3d
+    fn(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), cams_c(cams),
                       _p(_d(p["mean"])), _p(_d(p["scale"])), _p(_d(p["quat"])),
                       _p(_d(p["freq"])), _p(pr.flag), _p(np.ascontiguousarray(pr.rec)),
                       _p(_d(rgrad)), C.c_int64(view_stride), _p(out["mean"]),

@@ -828,4 +828,89 @@ void ora_chain3d(const ora_cfg* cfg, int64_t N, int32_t B, const ora_cam* cams,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact-mode (NEXT-1) record quantities of one (view, primitive)
+// as a plain function of its 13 parameters (mu 3, scale 3, quat 4, freq 3):
+// out = (mu'x, mu'y, conic a, b, c, f'x, f'y, beta). Same formulas as
+// ora_project3d's exact branch. Returns false if culled.
+// ---------------------------------------------------------------------------
+static bool exact_record(const ora_cfg& c, const ora_cam& cam, const double* prm, double* out) {
+  proj3 P;
+  project3_core(c, cam, prm, prm + 3, prm + 6, prm + 10, P);
+  double x = P.p[0], y = P.p[1], z = P.p[2];
+  if (!(z >= cam.near_z && z <= cam.far_z)) return false;
+  out[0] = (cam.fx * (x / z)) + cam.cx;
+  out[1] = (cam.fy * (y / z)) + cam.cy;
+  double dd = c.cov_eps + c.dilation;
+  double sxx = P.Sp[0] + dd, sxy = P.Sp[1], syy = P.Sp[2] + dd;
+  double det = sxx * syy - sxy * sxy;
+  out[2] = syy / det; out[3] = -sxy / det; out[4] = sxx / det;
+  double a = P.Shat[0], b = P.Shat[1], d = P.Shat[3];
+  double det2 = a * d - b * b;
+  double sx = P.Shat[2], sy = P.Shat[4];
+  double ux = (d * sx - b * sy) / det2, uy = (-b * sx + a * sy) / det2;
+  double vv = P.Shat[5] - (sx * ux + sy * uy);
+  out[5] = P.fhat[0] + P.fhat[2] * ux;
+  out[6] = P.fhat[1] + P.fhat[2] * uy;
+  out[7] = std::exp(-0.5 * P.fhat[2] * P.fhat[2] * vv);
+  return true;
+}
+
+// 3D chain for EXACT projection: parameter gradients = J^T g_rec with the
+// Jacobian J of exact_record taken by central differences in double (h = 1e-6
+// relative). view_stride 0 => sum over views. (Pinned by whole-pipeline FD in
+// tests/test_oracle_grad.py.)
+void ora_chain3d_exact(const ora_cfg* cfg, int64_t N, int32_t B, const ora_cam* cams,
+                       const double* mean, const double* scale, const double* quat,
+                       const double* freq, const int32_t* flag, const double* rec,
+                       const double* rgrad, int64_t view_stride, double* g_mean,
+                       double* g_scale, double* g_quat,
+                       double* g_freq, double* g_phase, double* g_color, double* g_opacity) {
+  const ora_cfg& c = *cfg;
+  (void)rec;  // same signature as ora_chain3d
+  int64_t NP = view_stride == 0 ? N : (int64_t)B * N;
+  std::memset(g_mean, 0, sizeof(double) * 3 * NP);
+  std::memset(g_scale, 0, sizeof(double) * 3 * NP);
+  std::memset(g_quat, 0, sizeof(double) * 4 * NP);
+  std::memset(g_freq, 0, sizeof(double) * 3 * NP);
+  std::memset(g_phase, 0, sizeof(double) * NP);
+  std::memset(g_color, 0, sizeof(double) * 3 * NP);
+  std::memset(g_opacity, 0, sizeof(double) * NP);
+  static const int gi[8] = {G_MUX, G_MUY, G_A, G_B, G_C, G_FX, G_FY, G_BETA};
+  for (int32_t v = 0; v < B; ++v) {
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t o = (int64_t)v * N + i;
+      if (flag[o] != 0) continue;
+      const int64_t pi = (int64_t)v * view_stride + i;
+      const double* g = rgrad + o * ORA_G;
+      g_phase[pi] += g[G_PHI];
+      for (int k = 0; k < 3; ++k) g_color[3 * pi + k] += g[G_CR + k];
+      g_opacity[pi] += g[G_ALPHA];
+      double prm[13];
+      for (int k = 0; k < 3; ++k) prm[k] = mean[3 * pi + k];
+      for (int k = 0; k < 3; ++k) prm[3 + k] = scale[3 * pi + k];
+      for (int k = 0; k < 4; ++k) prm[6 + k] = quat[4 * pi + k];
+      for (int k = 0; k < 3; ++k) prm[10 + k] = freq[3 * pi + k];
+      double gp[13];
+      for (int k = 0; k < 13; ++k) {
+        const double h = 1e-6 * std::max(1.0, std::fabs(prm[k]));
+        double pp[13], pm[13], rp[8], rm[8];
+        std::memcpy(pp, prm, sizeof(prm));
+        std::memcpy(pm, prm, sizeof(prm));
+        pp[k] += h;
+        pm[k] -= h;
+        bool okp = exact_record(c, cams[v], pp, rp), okm = exact_record(c, cams[v], pm, rm);
+        double acc = 0.0;
+        if (okp && okm)
+          for (int r = 0; r < 8; ++r) acc += g[gi[r]] * (rp[r] - rm[r]) / (2.0 * h);
+        gp[k] = acc;
+      }
+      for (int k = 0; k < 3; ++k) g_mean[3 * pi + k] += gp[k];
+      for (int k = 0; k < 3; ++k) g_scale[3 * pi + k] += gp[3 + k];
+      for (int k = 0; k < 4; ++k) g_quat[4 * pi + k] += gp[6 + k];
+      for (int k = 0; k < 3; ++k) g_freq[3 * pi + k] += gp[10 + k];
+    }
+  }
+}
+
 }  // extern "C"

@@ -178,3 +178,35 @@ def test_occluded_primitive_small_gradient(ora):
     g2 = ora.forward_backward(cfg, both, dL)["grads"]
     for k in ("mean", "cov", "freq", "color", "opacity"):
         assert np.max(np.abs(g2[k][0])) <= 1.5e-2 * np.max(np.abs(g1[k][0])) + 1e-12, k
+
+
+@pytest.mark.parametrize("blend", [False, True])
+def test_fd_3d_exact_projection(ora, blend):
+    """NEXT-1 exact z-integration (beta = exp(-1/2 f_z^2 v)): the
+    oracle's exact-mode gradients (Jacobian of its pinned exact projection)
+    agree with central FD of the whole exact-mode pipeline."""
+    p = _scene3d(5, seed=8)
+    p["freq"] = p["freq"] * 2.0   # make f_hat_z (and beta < 1) matter
+    cams = _cams(2, seed=2)
+    cfg = ora.Cfg(width=W, height=H, prim3d=True, alpha_blend=blend, alpha_min=0.0,
+                  dilation=0.3, exact_proj=True, T_min=1e-4 if blend else 0.0)
+    pr = ora.project3d(cfg, p, cams)
+    beta = pr.field("beta")[pr.flag == 0]
+    assert beta.min() < 0.9  # the exact mode differs from the paper mode here
+    _fd_check(ora, cfg, p, cams=cams, min_margin=1e-3 if blend else 0.0, h=1e-6)
+
+
+def test_exact_chain_matches_paper_chain_when_fz_zero(ora):
+    """With f = 0, exact and paper modes coincide (beta = 1, f' = 0): the
+    FD-Jacobian exact chain must reproduce the hand-derived paper chain."""
+    p = _scene3d(5, seed=9)
+    p["freq"] = np.zeros_like(p["freq"])
+    cams = _cams(2, seed=3)
+    rng = np.random.default_rng(0)
+    dL = rng.uniform(-1, 1, (2 * H * W, 3))
+    ce = ora.Cfg(width=W, height=H, prim3d=True, alpha_min=0.0, dilation=0.3, exact_proj=True)
+    cp = ora.Cfg(width=W, height=H, prim3d=True, alpha_min=0.0, dilation=0.3)
+    ge = ora.forward_backward(ce, p, dL, cams=cams)["grads"]
+    gpp = ora.forward_backward(cp, p, dL, cams=cams)["grads"]
+    for k in ("mean", "scale", "quat", "opacity", "color"):
+        np.testing.assert_allclose(ge[k], gpp[k], rtol=1e-6, atol=1e-8)
