@@ -57,7 +57,12 @@ enum { WIPES_PRIM_2D = 0, WIPES_PRIM_3D = 1 };
 enum { WIPES_BLEND_SUM = 0, WIPES_BLEND_ALPHA = 1 };
 /* 2D covariance parameterisations ("Cholesky and RS") */
 enum { WIPES_COV2_SIGMA = 0, WIPES_COV2_CHOLESKY = 1, WIPES_COV2_RS = 2 };
-/* Eq. 7 as written (beta = 1) / exact z-marginal (NEXT-1) */
+/* Eq. 7 as written (beta = 1) / exact z-marginal (NEXT-1,
+ * SPEC S:193, R4): with the full ray-space covariance Sigma_hat,
+ * S2 its undilated 2x2 block, sigma = Sigma_hat[0:2, 2], v = Sigma_hat_zz -
+ * sigma^T S2^-1 sigma, f_hat = (J3 R)^-T f:  f' = f_hat_xy + f_hat_z S2^-1 sigma,
+ * beta = exp(-1/2 f_hat_z^2 v). Tile rects, counts and depth keys are the same
+ * in both modes; EXACT adds 4 bytes per (view, primitive) to the workspace. */
 enum { WIPES_PROJ_PAPER = 0, WIPES_PROJ_EXACT = 1 };
 /* tile extent: opacity-aware AABB (R7, default) / SPEC's 3-sigma square */
 enum { WIPES_EXTENT_OPACITY = 0, WIPES_EXTENT_SIGMA3 = 1 };

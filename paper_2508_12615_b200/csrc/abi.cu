@@ -69,8 +69,6 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
   if (c->proj != WIPES_PROJ_PAPER && c->proj != WIPES_PROJ_EXACT) return fail(WIPES_EINVAL, "proj");
   if (c->extent != WIPES_EXTENT_OPACITY && c->extent != WIPES_EXTENT_SIGMA3)
     return fail(WIPES_EINVAL, "extent");
-  if (c->proj == WIPES_PROJ_EXACT)
-    return fail(WIPES_EUNSUPPORTED, "exact z-integration projection is not built (NEXT-1)");
   if (c->deterministic != 0)
     return fail(WIPES_EUNSUPPORTED, "deterministic reduction is not built in ABI v1");
   if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
@@ -284,6 +282,7 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
   if (L.BN > 0) {
     launch_begin(K_MEMSET, s);
     e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kMoments * L.BN, s);
+    if (e == cudaSuccess && L.exact) e = cudaMemsetAsync(w + L.rbeta, 0, sizeof(float) * L.BN, s);
     launch_end(K_MEMSET, s);
     if (e != cudaSuccess) return cuda_fail(e, "rgrad memset");
   }

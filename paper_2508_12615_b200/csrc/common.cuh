@@ -65,12 +65,13 @@ struct Layout {
   int32_t B = 0, GX = 0, GY = 0;
   int32_t hi_bits = 0, passes = 0, pre_passes = 0;  // dup-sort / depth-presort passes
   int32_t alpha = 0;
+  int32_t exact = 0;       // 3D exact z-integration: extra beta moment per record
   int64_t nblk_scan = 0;   // blocks of the count scan
   int64_t sort_tiles = 0;  // onesweep tiles of kSortTile keys
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
          pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
-         order = 0, rgrad = 0, total = 0;
+         order = 0, rgrad = 0, rbeta = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -135,6 +136,8 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
   L.order = take(sizeof(int32_t) * (L.BT + 1));
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
+  L.exact = c.prim == WIPES_PRIM_3D && c.proj == WIPES_PROJ_EXACT;
+  L.rbeta = take(sizeof(float) * (L.exact ? L.BN : 0));
   L.total = o;
   return L;
 }

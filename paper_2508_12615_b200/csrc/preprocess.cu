@@ -280,16 +280,146 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
   P.g[2] = ((Rv[6] * f[0] + Rv[7] * f[1]) + Rv[8] * f[2]);
 }
 
+// ------------------------------------------------ exact projection (NEXT-1) --
+// Exact z-marginal of the modulated ray-space Gaussian (DESIGN.md
+// R4): with the full ray-space covariance Sigma_hat (J3 row 3 = [0 0 1]),
+// S2 its undilated upper-left 2x2, sigma = (Sigma_hat_xz, Sigma_hat_yz),
+// v = Sigma_hat_zz - sigma^T S2^-1 sigma and f_hat = (J3 R)^-T f:
+//   f' = f_hat_xy + f_hat_z S2^-1 sigma,  beta = exp(-1/2 f_hat_z^2 v).
+// Written once, generic over the scalar (double in the forward, a forward-mode
+// dual number in the backward, where it yields the exact Jacobian).
+struct Dual {
+  double v, d;
+};
+__device__ __forceinline__ Dual mk(double v) { return {v, 0.0}; }
+__device__ __forceinline__ Dual operator+(Dual a, Dual b) { return {a.v + b.v, a.d + b.d}; }
+__device__ __forceinline__ Dual operator-(Dual a, Dual b) { return {a.v - b.v, a.d - b.d}; }
+__device__ __forceinline__ Dual operator-(Dual a) { return {-a.v, -a.d}; }
+__device__ __forceinline__ Dual operator*(Dual a, Dual b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__device__ __forceinline__ Dual operator*(double a, Dual b) { return {a * b.v, a * b.d}; }
+__device__ __forceinline__ Dual operator*(Dual a, double b) { return {a.v * b, a.d * b}; }
+__device__ __forceinline__ Dual operator+(Dual a, double b) { return {a.v + b, a.d}; }
+__device__ __forceinline__ Dual operator-(double a, Dual b) { return {a - b.v, -b.d}; }
+__device__ __forceinline__ Dual operator/(Dual a, Dual b) {
+  const double r = 1.0 / b.v;
+  return {a.v * r, (a.d - a.v * r * b.d) * r};
+}
+__device__ __forceinline__ Dual operator/(Dual a, double b) { return {a.v / b, a.d / b}; }
+__device__ __forceinline__ Dual operator/(double a, Dual b) {
+  const double r = 1.0 / b.v;
+  return {a * r, -a * r * r * b.d};
+}
+__device__ __forceinline__ Dual sqrtT(Dual a) {
+  const double s = sqrt(a.v);
+  return {s, a.d / (2.0 * s)};
+}
+__device__ __forceinline__ Dual expT(Dual a) {
+  const double e = exp(a.v);
+  return {e, e * a.d};
+}
+__device__ __forceinline__ double sqrtT(double a) { return sqrt(a); }
+__device__ __forceinline__ double expT(double a) { return exp(a); }
+__device__ __forceinline__ double val(double a) { return a; }
+__device__ __forceinline__ double val(Dual a) { return a.v; }
+template <typename T>
+__device__ __forceinline__ T cst(double a);
+template <>
+__device__ __forceinline__ double cst<double>(double a) { return a; }
+template <>
+__device__ __forceinline__ Dual cst<Dual>(double a) { return mk(a); }
+template <typename T>
+__device__ __forceinline__ T clampT(T a, double lo, double hi) {  // zero partial when clamped
+  if (val(a) < lo) return cst<T>(lo);
+  if (val(a) > hi) return cst<T>(hi);
+  return a;
+}
+
+// out = (mu'x, mu'y, conic a, b, c, f'x, f'y, beta); false if behind near/far.
+template <typename T>
+__device__ bool exact_rec(const float* cam, int32_t W, int32_t H, int32_t ewa_clamp,
+                          double diag, const T* mu, const T* s, const T* q, const T* f,
+                          T* out) {
+  double Rv[9];
+  for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
+  const double fx = cam[12], fy = cam[13], cx = cam[14], cy = cam[15];
+  T p[3];
+  for (int r = 0; r < 3; ++r)
+    p[r] = Rv[3 * r] * mu[0] + Rv[3 * r + 1] * mu[1] + Rv[3 * r + 2] * mu[2] + (double)cam[9 + r];
+  const T x = p[0], y = p[1], z = p[2];
+  if (!(val(z) >= (double)cam[16] && val(z) <= (double)cam[17])) return false;
+  const T n = sqrtT(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const T w = q[0] / n, qx = q[1] / n, qy = q[2] / n, qz = q[3] / n;
+  T R[9];
+  R[0] = 1.0 - 2.0 * (qy * qy + qz * qz);
+  R[1] = 2.0 * (qx * qy - w * qz);
+  R[2] = 2.0 * (qx * qz + w * qy);
+  R[3] = 2.0 * (qx * qy + w * qz);
+  R[4] = 1.0 - 2.0 * (qx * qx + qz * qz);
+  R[5] = 2.0 * (qy * qz - w * qx);
+  R[6] = 2.0 * (qx * qz - w * qy);
+  R[7] = 2.0 * (qy * qz + w * qx);
+  R[8] = 1.0 - 2.0 * (qx * qx + qy * qy);
+  const T s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+  T S3[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      S3[i][j] = R[3 * i] * s2[0] * R[3 * j] + R[3 * i + 1] * s2[1] * R[3 * j + 1] +
+                 R[3 * i + 2] * s2[2] * R[3 * j + 2];
+  T tx = x / z, ty = y / z;
+  if (ewa_clamp) {
+    const double limx = (1.3 * (double)W) / (2.0 * fx), limy = (1.3 * (double)H) / (2.0 * fy);
+    tx = clampT(tx, -limx, limx);
+    ty = clampT(ty, -limy, limy);
+  }
+  const T j00 = fx / z, j11 = fy / z, j02 = -(fx * tx) / z, j12 = -(fy * ty) / z;
+  T M3[3][3];
+  for (int c = 0; c < 3; ++c) {
+    M3[0][c] = j00 * Rv[c] + j02 * Rv[6 + c];
+    M3[1][c] = j11 * Rv[3 + c] + j12 * Rv[6 + c];
+    M3[2][c] = cst<T>(Rv[6 + c]);
+  }
+  T Sh[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = i; j < 3; ++j) {
+      T acc = cst<T>(0.0);
+      for (int a = 0; a < 3; ++a) {
+        const T ta = M3[i][0] * S3[0][a] + M3[i][1] * S3[1][a] + M3[i][2] * S3[2][a];
+        acc = acc + ta * M3[j][a];
+      }
+      Sh[i][j] = acc;
+    }
+  T g[3];
+  for (int r = 0; r < 3; ++r) g[r] = Rv[3 * r] * f[0] + Rv[3 * r + 1] * f[1] + Rv[3 * r + 2] * f[2];
+  const T fhx = (z * g[0]) / fx, fhy = (z * g[1]) / fy;
+  const T fhz = g[2] - j02 * fhx - j12 * fhy;
+  const T a2 = Sh[0][0], b2 = Sh[0][1], d2 = Sh[1][1], sx = Sh[0][2], sy = Sh[1][2];
+  const T det2 = a2 * d2 - b2 * b2;
+  const T ux = (d2 * sx - b2 * sy) / det2, uy = (a2 * sy - b2 * sx) / det2;
+  const T vv = Sh[2][2] - (sx * ux + sy * uy);
+  out[0] = fx * (x / z) + cx;
+  out[1] = fy * (y / z) + cy;
+  const T sxx = a2 + diag, sxy = b2, syy = d2 + diag;
+  const T det = sxx * syy - sxy * sxy;
+  out[2] = syy / det;
+  out[3] = -sxy / det;
+  out[4] = sxx / det;
+  out[5] = fhx + fhz * ux;
+  out[6] = fhy + fhz * uy;
+  out[7] = expT(-0.5 * (fhz * fhz * vv));
+  return true;
+}
+
 struct Pre3DArgs {
   Cfg2 c;
-  int32_t ewa_clamp;
+  int32_t ewa_clamp, exact;
   int64_t N, view_stride;
   const float *mean, *scale, *quat, *freq, *phase, *color, *opacity;
   PreOut o;
   CamBlock cams;
 };
 
-__global__ void __launch_bounds__(128, WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
+template <bool EXACT>
+__global__ void __launch_bounds__(128, EXACT ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)a.cams.nv * a.N) return;
   int vl = (int)(gid / a.N);
@@ -311,7 +441,7 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_FWD_MINB) k_pre3d(const __gri
   int flag = 0;
   uint32_t dk = 0;
   double conic[3] = {0, 0, 0}, ext[2] = {0, 0};
-  double mux = 0, muy = 0, fpx = 0, fpy = 0;
+  double mux = 0, muy = 0, fpx = 0, fpy = 0, beta = 1.0;
   double qq = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
   bool ok = fin(mu[0]) && fin(mu[1]) && fin(mu[2]) && fin(s[0]) && fin(s[1]) && fin(s[2]) &&
             fin(q[0]) && fin(q[1]) && fin(q[2]) && fin(q[3]) && fin(f[0]) && fin(f[1]) &&
@@ -331,6 +461,14 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_FWD_MINB) k_pre3d(const __gri
       muy = (fy * (y / z)) + cy;
       fpx = (z * P.g[0]) / fx;
       fpy = (z * P.g[1]) / fy;
+      if (EXACT) {  // f' and beta of the exact z-marginal (no integer decision uses them)
+        double rec8[8];
+        if (exact_rec<double>(cam, c.W, c.H, a.ewa_clamp, c.diag, mu, s, q, f, rec8)) {
+          fpx = rec8[5];
+          fpy = rec8[6];
+          beta = rec8[7];
+        }
+      }
       float dz = (float)z;
       dk = orderable(dz);
       flag = finish2d(c, mux, muy, P.Sp[0] + c.diag, P.Sp[1], P.Sp[2] + c.diag, al, &rect,
@@ -343,7 +481,7 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_FWD_MINB) k_pre3d(const __gri
   a.o.dkey[o] = dk;
   if (a.o.cull_flags) a.o.cull_flags[o] = (uint8_t)flag;
   if (flag == 0)
-    write_record(a.o.rec + 4 * o, mux, muy, conic, al, fpx, fpy, phi, 1.0, cr, cg, cb, ext);
+    write_record(a.o.rec + 4 * o, mux, muy, conic, al, fpx, fpy, phi, beta, cr, cg, cb, ext);
   else
     zero_record(a.o.rec + 4 * o);
 }
@@ -455,6 +593,7 @@ struct Bwd3DArgs {
   const float* opacity;
   const uint8_t* flag;
   const float* mom;
+  const float* mom_beta;  // exact mode only
   wipes_grads g;
   CamBlock cams;  // views [v0, v0 + nv) of this launch
 };
@@ -575,6 +714,64 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
   if (a.g.opacity) put(&a.g.opacity[pi], gal);
 }
 
+// Exact-mode (NEXT-1) backward: the record gradients (from the 12 moments and
+// the beta moment) are pulled back through the exact projection by forward-mode
+// differentiation of exact_rec: one dual-number pass per parameter direction
+// (mu, s, q, f: 13), each giving the column J[:, k] of the 8-output Jacobian;
+// phase, colour and opacity pass straight through the record.
+__global__ void __launch_bounds__(128) k_pre3d_bwd_exact(const __grid_constant__ Bwd3DArgs a) {
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= a.nrows) return;
+  int v_lo, v_hi;
+  int64_t i, pi;
+  if (a.view_stride == 0) { v_lo = a.cams.v0; v_hi = a.cams.v0 + a.cams.nv; i = row; pi = row; }
+  else {
+    int vl = (int)(row / a.N);
+    v_lo = a.cams.v0 + vl; v_hi = v_lo + 1; i = row - (int64_t)vl * a.N;
+    pi = (int64_t)v_lo * a.view_stride + i;
+  }
+  double x0[13] = {a.mean[3 * pi], a.mean[3 * pi + 1], a.mean[3 * pi + 2],
+                   a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2],
+                   a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3],
+                   a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
+  double gx[13];
+  for (int k = 0; k < 13; ++k) gx[k] = 0.0;
+  double gphi = 0, gcol[3] = {0, 0, 0}, gal = 0;
+  for (int v = v_lo; v < v_hi; ++v) {
+    const int64_t o = (int64_t)v * a.N + i;
+    if (a.flag[o] != 0) continue;
+    const float* cam = a.cams.v[v - a.cams.v0];
+    double r8[8];
+    exact_rec<double>(cam, a.c.W, a.c.H, a.ewa_clamp, a.c.diag, x0, x0 + 3, x0 + 6, x0 + 10, r8);
+    const double A[3] = {r8[2], r8[3], r8[4]};
+    double g[kRecGrads];
+    moments_to_grads(a.mom + kMoments * o, A, r8[5], r8[6], 0.5 * r8[7], a.opacity[pi], g);
+    gphi += g[RG_PHI];
+    gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
+    gal += g[RG_ALPHA];
+    const double gr[8] = {g[RG_MUX], g[RG_MUY], g[RG_A], g[RG_B], g[RG_C],
+                          g[RG_FX],  g[RG_FY],  0.5 * (double)a.mom_beta[o]};
+#pragma unroll 1
+    for (int k = 0; k < 13; ++k) {
+      Dual xd[13];
+      for (int j = 0; j < 13; ++j) xd[j] = {x0[j], j == k ? 1.0 : 0.0};
+      Dual out[8];
+      exact_rec<Dual>(cam, a.c.W, a.c.H, a.ewa_clamp, a.c.diag, xd, xd + 3, xd + 6, xd + 10, out);
+      double acc = 0.0;
+      for (int r = 0; r < 8; ++r) acc += gr[r] * out[r].d;
+      gx[k] += acc;
+    }
+  }
+  auto put = [&](float* dst, double v) { *dst = a.accumulate ? *dst + (float)v : (float)v; };
+  if (a.g.mean) for (int k = 0; k < 3; ++k) put(&a.g.mean[3 * pi + k], gx[k]);
+  if (a.g.scale) for (int k = 0; k < 3; ++k) put(&a.g.scale[3 * pi + k], gx[3 + k]);
+  if (a.g.quat) for (int k = 0; k < 4; ++k) put(&a.g.quat[4 * pi + k], gx[6 + k]);
+  if (a.g.freq) for (int k = 0; k < 3; ++k) put(&a.g.freq[3 * pi + k], gx[10 + k]);
+  if (a.g.phase) put(&a.g.phase[pi], gphi);
+  if (a.g.color) for (int k = 0; k < 3; ++k) put(&a.g.color[3 * pi + k], gcol[k]);
+  if (a.g.opacity) put(&a.g.opacity[pi], gal);
+}
+
 Cfg2 make_cfg2(const wipes_config& c, const Layout& L) {
   Cfg2 r;
   r.W = c.width; r.H = c.height; r.tile = c.tile; r.GX = L.GX; r.GY = L.GY;
@@ -633,6 +830,7 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
   static thread_local Pre3DArgs a;  // ~9 KB: keep off the host stack
   a.c = make_cfg2(c, L);
   a.ewa_clamp = c.ewa_clamp;
+  a.exact = L.exact;
   a.N = L.N;
   a.view_stride = p.view_stride;
   a.mean = p.mean; a.scale = p.scale; a.quat = p.quat; a.freq = p.freq; a.phase = p.phase;
@@ -643,7 +841,10 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
     fill_cams(a.cams, cams, v0, nv);
     int64_t n = (int64_t)nv * L.N;
     launch_begin(K_PRE3D, s);
-    k_pre3d<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+    if (a.exact)
+      k_pre3d<true><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+    else
+      k_pre3d<false><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
     launch_end(K_PRE3D, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -684,6 +885,7 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
   a.opacity = p.opacity;
   a.flag = (const uint8_t*)(ws + L.flag);
   a.mom = (const float*)(ws + L.rgrad);
+  a.mom_beta = L.exact ? (const float*)(ws + L.rbeta) : nullptr;
   a.g = g;
   for (int v0 = 0; v0 < L.B; v0 += WIPES_MAX_CAMERAS_PER_LAUNCH) {
     int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;
@@ -691,7 +893,10 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
     a.accumulate = (p.view_stride == 0 && v0 > 0) ? 1 : 0;
     a.nrows = p.view_stride == 0 ? L.N : (int64_t)nv * L.N;
     launch_begin(K_PRE3D_BWD, s);
-    k_pre3d_bwd<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+    if (L.exact)
+      k_pre3d_bwd_exact<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+    else
+      k_pre3d_bwd<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
     launch_end(K_PRE3D_BWD, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -91,6 +91,7 @@ struct RenderArgs {
   const float* T_in;
   const int32_t* nc_in;
   float* mom;            // [B*N, 12] gradient moments
+  float* mom_beta;       // [B*N] exact mode: M12 = sum gw alpha G cos(theta) (dbeta = M12/2)
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
@@ -464,11 +465,11 @@ __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w,
 }
 
 // Backward of one pixel for one record (predicated on `h`).
-template <bool ALPHA>
+template <bool ALPHA, bool EXACT>
 __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, const float4& r2,
                                           const float4& r3, const float (&g)[3], float amin,
                                           float amax, float& T, float (&S)[3], float (&m)[kMom],
-                                          bool& any) {
+                                          float& mb, bool& any) {
   const float ag = ex2(e);
   const float th = pair_theta(r2, dx, dy);
   const float cs = cos_a(th), sn = sin_a(th);
@@ -479,6 +480,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
     add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g[0], we * g[1], we * g[2]);
+    if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
     const float al = fminf(amax, w);
     const float ri = rcp_a(1.f - al);
@@ -492,10 +494,11 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
     T = ok ? Tk : T;
     add_moments(m, (ok && w < amax) ? dLda : 0.f, ok ? w : 0.f, ag, sn, dx, dy, aT * g[0],
                 aT * g[1], aT * g[2]);
+    if (EXACT) mb = __fmaf_rn((ok && w < amax) ? dLda * ag : 0.f, cs, mb);
   }
 }
 
-template <int TS, bool ALPHA>
+template <int TS, bool ALPHA, bool EXACT>
 __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs a) {
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
@@ -574,14 +577,20 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
 #pragma unroll
         for (int k = 0; k < kMom; ++k) m[k] = 0.f;
         bool any = false;
+        float mb = 0.f;
 #pragma unroll
         for (int p = 0; p < P; ++p)
           if (bm[p])
-            bwd_pixel<ALPHA>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min, a.alpha_max,
-                             T[p], S[p], m, any);
+            bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min,
+                                    a.alpha_max, T[p], S[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
         const float red = transpose_reduce12(m, lane);
         if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
+        if (EXACT) {
+#pragma unroll
+          for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
+          if (lane == 0) atomicAdd(a.mom_beta + vN + ws.pid[i], mb);
+        }
       }
       __syncwarp();
     }
@@ -636,7 +645,11 @@ template <int TS>
 cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   ra.queue = Q_BWD;
-  void (*k)(RenderArgs) = alpha ? k_render_bwd<TS, true> : k_render_bwd<TS, false>;
+  void (*k)(RenderArgs);
+  if (ra.mom_beta)
+    k = alpha ? k_render_bwd<TS, true, true> : k_render_bwd<TS, false, true>;
+  else
+    k = alpha ? k_render_bwd<TS, true, false> : k_render_bwd<TS, false, false>;
   launch_begin(K_RENDER_BWD, s);
   k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
   launch_end(K_RENDER_BWD, s);
@@ -666,6 +679,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.image = nullptr; ra.T_final = nullptr; ra.n_contrib = nullptr;
   ra.dLdC = nullptr; ra.T_in = nullptr; ra.nc_in = nullptr;
   ra.mom = (float*)(ws + L.rgrad);
+  ra.mom_beta = L.exact ? (float*)(ws + L.rbeta) : nullptr;
   ra.stats = nullptr;
   return ra;
 }

@@ -95,9 +95,18 @@ def test_einval_null_and_alignment(L):
 
 
 def test_unsupported_modes(L):
-    cfg = abi.make_config(64, 64, prim="3d", proj="exact")
+    cfg = abi.make_config(64, 64, prim="2d", deterministic=1)
     st, _ = abi.wipes_preprocess(cfg, _pp(), 10, None, 1, 0x100000, 1 << 30, 100, False, None, None)
     assert st == abi.WIPES_EUNSUPPORTED
+
+
+def test_exact_projection_workspace_has_beta_moments(L):
+    """NEXT-1: the exact mode adds one float per (view, primitive) record."""
+    c0 = abi.make_config(64, 64, prim="3d")
+    c1 = abi.make_config(64, 64, prim="3d", proj="exact")
+    n0 = abi.wipes_workspace_bytes(c0, 100000, 2, 0)
+    n1 = abi.wipes_workspace_bytes(c1, 100000, 2, 0)
+    assert n1 - n0 >= 4 * 200000
 
 
 def test_product_package_never_imports_oracle():

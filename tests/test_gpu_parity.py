@@ -178,6 +178,40 @@ def test_mini_3d_6d_parity(ora, name):
         assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
 
 
+@pytest.mark.parametrize("name,blend", [("p3d", "alpha"), ("p3d", "sum"), ("p6d", "alpha")])
+def test_exact_projection_parity(ora, name, blend):
+    """NEXT-1 exact z-integration (R4): f' and
+    beta = exp(-1/2 f_hat_z^2 v) from the full ray-space covariance in the
+    forward, the beta moment and the dual-number Jacobian of the exact
+    projection in the backward, against the oracle's exact mode (whose chain is
+    pinned by whole-pipeline finite differences, test_oracle_grad.py)."""
+    c = gen.make_config(name, seed=0)
+    H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+    p, cams, vs = c["params"], c["cams"], c["view_stride"]
+    cfg_o = oracle_cfg(ora, "3d", H, W, blend, use_rect=True, exact_proj=True)
+    pr = ora.project3d(cfg_o, p, cams, view_stride=vs)
+    beta = pr.field("beta")[pr.flag == 0]
+    assert np.median(beta) < 0.95  # the exact mode is exercised
+    r = gpu_rasterizer("3d", H, W, blend, proj="exact")
+    r.preprocess(to_dev(p), cams, view_stride=vs)
+    r.bin_sort()
+    img, T, nc = r.render()
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    dL = gen.gen_dLdC(B, H, W, seed=2)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    nbad, namb = pixel_violations(_pixels(_np(img)), ro["color"], ro["margin"])
+    assert nbad == 0, (nbad, namb)
+    assert namb <= 0.002 * B * H * W
+    grads = r.backward(torch.from_numpy(dL).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain3d(cfg_o, p, cams, pr, ro["rgrad"], view_stride=vs)
+    for k in ("mean", "scale", "quat", "freq", "color", "opacity"):
+        nbad, worst = grad_violations(_np(grads[k]), og[k])
+        frac = nbad / og[k].size
+        assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
+
+
 # --------------------------------------------------------------- contract --
 def test_capacity_protocol_overflow_then_retry():
     H = W = 64
