@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
+                    help="3D projection: Eq. 7 as written (default) or NEXT-1 exact z-marginal")
     return ap.parse_args()
 
 
@@ -203,6 +205,7 @@ def main():
         cams = [cams[v] for v in my_views]
     Bl = len(cams) if cams is not None else 1
     r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev,
+                   proj=args.proj if c["kind"] != "2d" else "paper",
                    row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0)
     params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
     if c["kind"] == "6d":
@@ -355,7 +358,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if shared else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{name}: {c['desc']}", "H": H, "W": W, "N": N, "views": B,
+            "config": {"workload": f"{name}: {c['desc']}"
+                       + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else ""),
+                       "H": H, "W": W, "N": N, "views": B,
                        "blend": blend, "dup": int(n_tot2),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "parallelism": (f"tile rows r = rank (mod {world}) of one image per GPU + "

@@ -10,6 +10,7 @@
 //                 for all parameters"), in FP64.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -601,6 +602,11 @@ struct Bwd3DArgs {
 // One thread per OUTPUT parameter row. With view_stride = 0 it sums the
 // contributions of the launch's views in view order (deterministic); launches
 // after the first (B > 128 views) add to the rows written before.
+// EXACT adds the adjoint of the exact z-marginal (NEXT-1; R4):
+// f' = f_hat_xy + f_hat_z u, u = S2^-1 sigma, beta = exp(-1/2 f_hat_z^2 v),
+// v = Sigma_hat_zz - sigma.u, pulled back by hand onto f_hat, J (j02, j12)
+// and the full 3x3 ray-space covariance Sigma_hat = M3 S3 M3^T.
+template <bool EXACT>
 __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __grid_constant__ Bwd3DArgs a) {
   int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= a.nrows) return;
@@ -634,26 +640,77 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
     double det = sxx * syy - sxy * sxy;
     const double rdet = 1.0 / det;
     double A[3] = {syy * rdet, -sxy * rdet, sxx * rdet};
+    const double fhx = (z * P.g[0]) * rfx, fhy = (z * P.g[1]) * rfy;
+    double fpx = fhx, fpy = fhy, hb = 0.5;
+    // exact mode: sigma = (Sigma_hat_02, Sigma_hat_12), s22 = Sigma_hat_22
+    double sg[2] = {0, 0}, s22 = 0, u[2] = {0, 0}, vv = 0, fhz = 0, beta = 1.0;
+    double i00 = 0, i01 = 0, i11 = 0;
+    if (EXACT) {
+      double t2[3];
+      for (int k = 0; k < 3; ++k)
+        t2[k] = s3at(P.S3, k, 0) * Rv[6] + s3at(P.S3, k, 1) * Rv[7] + s3at(P.S3, k, 2) * Rv[8];
+      sg[0] = P.M[0] * t2[0] + P.M[1] * t2[1] + P.M[2] * t2[2];
+      sg[1] = P.M[3] * t2[0] + P.M[4] * t2[1] + P.M[5] * t2[2];
+      s22 = Rv[6] * t2[0] + Rv[7] * t2[1] + Rv[8] * t2[2];
+      const double rd2 = 1.0 / (P.Sp[0] * P.Sp[2] - P.Sp[1] * P.Sp[1]);  // undilated S2
+      i00 = P.Sp[2] * rd2; i01 = -P.Sp[1] * rd2; i11 = P.Sp[0] * rd2;
+      u[0] = i00 * sg[0] + i01 * sg[1];
+      u[1] = i01 * sg[0] + i11 * sg[1];
+      vv = s22 - (sg[0] * u[0] + sg[1] * u[1]);
+      fhz = P.g[2] - P.j02 * fhx - P.j12 * fhy;
+      fpx = fhx + fhz * u[0];
+      fpy = fhy + fhz * u[1];
+      beta = exp(-0.5 * fhz * fhz * vv);
+      hb = 0.5 * beta;
+    }
     double g[kRecGrads];
-    moments_to_grads(a.mom + kMoments * o, A, (z * P.g[0]) * rfx, (z * P.g[1]) * rfy, 0.5,
-                     a.opacity[pi], g);
+    moments_to_grads(a.mom + kMoments * o, A, fpx, fpy, hb, a.opacity[pi], g);
     gphi += g[RG_PHI];
     gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
     gal += g[RG_ALPHA];
+    double gFX = g[RG_FX], gFY = g[RG_FY];  // -> dL/df_hat_x, dL/df_hat_y
+    double E[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // exact adjoint on Sigma_hat
+    double dj02x = 0, dj12x = 0;
+    if (EXACT) {
+      const double gq = 0.5 * (double)a.mom_beta[o] * beta;  // dL/d(exponent of beta)
+      const double g_fhz = gq * (-fhz * vv) + g[RG_FX] * u[0] + g[RG_FY] * u[1];
+      const double g_v = gq * (-0.5 * fhz * fhz);
+      const double gu0 = fhz * g[RG_FX] - g_v * sg[0], gu1 = fhz * g[RG_FY] - g_v * sg[1];
+      const double w0 = i00 * gu0 + i01 * gu1, w1 = i01 * gu0 + i11 * gu1;
+      E[0][0] = -w0 * u[0];
+      E[0][1] = E[1][0] = -0.5 * (w0 * u[1] + w1 * u[0]);
+      E[1][1] = -w1 * u[1];
+      E[0][2] = E[2][0] = 0.5 * (w0 - g_v * u[0]);
+      E[1][2] = E[2][1] = 0.5 * (w1 - g_v * u[1]);
+      E[2][2] = g_v;
+      gFX -= g_fhz * P.j02;
+      gFY -= g_fhz * P.j12;
+      dj02x = -g_fhz * fhx;
+      dj12x = -g_fhz * fhy;
+      for (int k = 0; k < 3; ++k) gf[k] += Rv[6 + k] * g_fhz;
+    }
     double dp[3] = {0, 0, 0};
     dp[0] += g[RG_MUX] * fx * rz;
     dp[1] += g[RG_MUY] * fy * rz;
     dp[2] += -g[RG_MUX] * fx * x * rz2 - g[RG_MUY] * fy * y * rz2;
-    dp[2] += g[RG_FX] * P.g[0] * rfx + g[RG_FY] * P.g[1] * rfy;
-    double dg0 = g[RG_FX] * z * rfx, dg1 = g[RG_FY] * z * rfy;
+    dp[2] += gFX * P.g[0] * rfx + gFY * P.g[1] * rfy;
+    double dg0 = gFX * z * rfx, dg1 = gFY * z * rfy;
     for (int k = 0; k < 3; ++k) gf[k] += Rv[k] * dg0 + Rv[3 + k] * dg1;
     double gsv[3];
     conic_grad_to_cov(A, g[RG_A], g[RG_B], g[RG_C], gsv);
-    double GS[2][2] = {{gsv[0], 0.5 * gsv[1]}, {0.5 * gsv[1], gsv[2]}};
-    double M[2][3] = {{P.M[0], P.M[1], P.M[2]}, {P.M[3], P.M[4], P.M[5]}};
-    double GM[2][3];
-    for (int r = 0; r < 2; ++r)
-      for (int cc = 0; cc < 3; ++cc) GM[r][cc] = GS[r][0] * M[0][cc] + GS[r][1] * M[1][cc];
+    constexpr int NR = EXACT ? 3 : 2;  // rows of M3 = [M; Rv row 2] that carry gradient
+    const double GS[3][3] = {{gsv[0] + E[0][0], 0.5 * gsv[1] + E[0][1], E[0][2]},
+                             {0.5 * gsv[1] + E[1][0], gsv[2] + E[1][1], E[1][2]},
+                             {E[2][0], E[2][1], E[2][2]}};
+    const double M[3][3] = {{P.M[0], P.M[1], P.M[2]}, {P.M[3], P.M[4], P.M[5]},
+                            {Rv[6], Rv[7], Rv[8]}};
+    double GM[3][3];
+    for (int r = 0; r < NR; ++r)
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int k = 0; k < NR; ++k) acc += GS[r][k] * M[k][cc];
+        GM[r][cc] = acc;
+      }
     double dM[2][3];
     for (int r = 0; r < 2; ++r)
       for (int cc = 0; cc < 3; ++cc) {
@@ -663,11 +720,15 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
       }
     double dS3[3][3];
     for (int r = 0; r < 3; ++r)
-      for (int cc = 0; cc < 3; ++cc) dS3[r][cc] = M[0][r] * GM[0][cc] + M[1][r] * GM[1][cc];
+      for (int cc = 0; cc < 3; ++cc) {
+        double acc = 0.0;
+        for (int k = 0; k < NR; ++k) acc += M[k][r] * GM[k][cc];
+        dS3[r][cc] = acc;
+      }
     double dj00 = dM[0][0] * Rv[0] + dM[0][1] * Rv[1] + dM[0][2] * Rv[2];
-    double dj02 = dM[0][0] * Rv[6] + dM[0][1] * Rv[7] + dM[0][2] * Rv[8];
+    double dj02 = dM[0][0] * Rv[6] + dM[0][1] * Rv[7] + dM[0][2] * Rv[8] + dj02x;
     double dj11 = dM[1][0] * Rv[3] + dM[1][1] * Rv[4] + dM[1][2] * Rv[5];
-    double dj12 = dM[1][0] * Rv[6] + dM[1][1] * Rv[7] + dM[1][2] * Rv[8];
+    double dj12 = dM[1][0] * Rv[6] + dM[1][1] * Rv[7] + dM[1][2] * Rv[8] + dj12x;
     dp[2] += dj00 * (-fx * rz2) + dj11 * (-fy * rz2);
     double dtx_dx = P.clx ? 0.0 : rz, dtx_dz = P.clx ? 0.0 : -x * rz2;
     double dty_dy = P.cly ? 0.0 : rz, dty_dz = P.cly ? 0.0 : -y * rz2;
@@ -893,10 +954,13 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
     a.accumulate = (p.view_stride == 0 && v0 > 0) ? 1 : 0;
     a.nrows = p.view_stride == 0 ? L.N : (int64_t)nv * L.N;
     launch_begin(K_PRE3D_BWD, s);
-    if (L.exact)
+    static const bool dual = getenv("WIPES_EXACT_DUAL") != nullptr;
+    if (L.exact && dual)  // forward-mode (dual number) cross-check of the hand adjoint
       k_pre3d_bwd_exact<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+    else if (L.exact)
+      k_pre3d_bwd<true><<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
     else
-      k_pre3d_bwd<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+      k_pre3d_bwd<false><<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
     launch_end(K_PRE3D_BWD, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

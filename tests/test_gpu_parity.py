@@ -212,6 +212,43 @@ def test_exact_projection_parity(ora, name, blend):
         assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
 
 
+_EXACT_GRADS = """
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+from paper_2508_12615_b200 import gen
+from parity_util import gpu_rasterizer, to_dev
+c = gen.make_config('p3d', seed=0)
+r = gpu_rasterizer('3d', c['H'], c['W'], 'alpha', proj='exact')
+r.forward(to_dev(c['params']), c['cams'])
+g = r.backward(torch.from_numpy(gen.gen_dLdC(c['B'], c['H'], c['W'], seed=2)).cuda())
+np.savez(sys.argv[2], **{k: v.cpu().numpy() for k, v in g.items()})
+"""
+
+
+def test_exact_adjoint_matches_forward_mode(tmp_path):
+    """The hand-written adjoint of the exact projection (k_pre3d_bwd<EXACT>)
+    against forward-mode dual-number differentiation of the same exact
+    projection code (k_pre3d_bwd_exact, selected by WIPES_EXACT_DUAL)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag in ("adj", "dual"):
+        f = str(tmp_path / f"{tag}.npz")
+        e = {k: v for k, v in os.environ.items() if k != "WIPES_EXACT_DUAL"}
+        if tag == "dual":
+            e["WIPES_EXACT_DUAL"] = "1"
+        subprocess.run([sys.executable, "-c", _EXACT_GRADS, root, f], check=True, env=e,
+                       timeout=600)
+        out[tag] = np.load(f)
+    for k in out["adj"].files:
+        a, d = out["adj"][k].astype(np.float64), out["dual"][k].astype(np.float64)
+        # the two runs differ only by float atomic ordering in the render backward
+        tol = 1e-5 + 1e-4 * np.abs(d)
+        assert np.all(np.abs(a - d) <= tol), (k, np.max(np.abs(a - d) - tol))
+
+
 # --------------------------------------------------------------- contract --
 def test_capacity_protocol_overflow_then_retry():
     H = W = 64
