@@ -207,6 +207,71 @@ wipes_status wipes_render_stats(const wipes_config* cfg, int64_t N, int32_t B, v
                                 size_t ws_bytes, int64_t dup_capacity, uint64_t* stats3,
                                 void* stream);
 
+/* ---- NEXT-2: the image-fitting step around the rasterizer --
+ * One fitting iteration (Eq. 4 objective,
+ * PAPER.md:299 "all hyperparameters were kept consistent with GSImage") is
+ *   preprocess -> bin_sort -> render_fwd -> wipes_loss_l2 -> render_bwd ->
+ *   wipes_adam_step,
+ * all on one stream and graph-capturable (no host synchronisation: the Adam
+ * step counter lives in device memory, and an optional device guard word
+ * (wipes_overflow_flag) turns the update into a no-op for a step whose
+ * intersections overflowed the capacity). */
+
+/* Bytes of scratch (device) shared by wipes_loss_l2 and wipes_adam_step; zero
+ * it once before first use (the calls leave their counters at zero). */
+size_t wipes_train_scratch_bytes(void);
+
+/* L2 objective, mean over the n floats (B*3*H*W) of image vs target (SPEC
+ * S:336 "returns pre-update L2 loss (mean over pixels and channels)"):
+ *   loss = (1/n) sum (image - target)^2   (device double, written once),
+ *   dL_dimage = (2/n) (image - target)    (device float [n]).
+ * The sum is reduced in FP64 in a fixed order (run-to-run deterministic).
+ * image/target/dL_dimage: device [n] float32, 4-byte aligned; dL_dimage may
+ * alias neither input. */
+wipes_status wipes_loss_l2(const float* image, const float* target, int64_t n,
+                           float* dL_dimage, double* loss, void* scratch, void* stream);
+
+/* Parameter activations ("opacity_raw = 0 (opacity 0.5)"). */
+enum { WIPES_ACT_NONE = 0, WIPES_ACT_SIGMOID = 1 };
+#define WIPES_MAX_ADAM_GROUPS 8
+
+/* One parameter group (all pointers device float32 [n]):
+ * param   raw parameter theta (in/out),
+ * grad    dL/d(act(theta)) as produced by wipes_render_bwd (in),
+ * m, v    Adam moments (in/out; zero-initialised by the caller),
+ * act     act(theta) written after the update (the rasterizer's input for the
+ *         next step); NULL when activation == WIPES_ACT_NONE (the rasterizer
+ *         reads param directly). */
+typedef struct {
+  float* param;
+  const float* grad;
+  float* m;
+  float* v;
+  float* act;
+  int64_t n;
+  float lr;
+  int32_t activation;
+} wipes_adam_group;
+
+/* Adam (Kingma & Ba; SPEC S:321-324 AdamState, beta1 0.9, beta2 0.999,
+ * eps 1e-15), one launch for all groups. With t = *step + 1:
+ *   g  = grad * act'(theta)          (chain through the activation),
+ *   m  = b1 m + (1 - b1) g,  v = b2 v + (1 - b2) g^2,
+ *   theta -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps),
+ *   act = act(theta),  *step = t.
+ * step: device int64 (in/out). guard: device int32 or NULL — when *guard != 0
+ * nothing is modified (used with wipes_overflow_flag). */
+wipes_status wipes_adam_step(const wipes_adam_group* groups, int32_t n_groups, float beta1,
+                             float beta2, float eps, int64_t* step, const int32_t* guard,
+                             void* scratch, void* stream);
+
+/* act = act(param) for every group with an activation (initialisation). */
+wipes_status wipes_activate(const wipes_adam_group* groups, int32_t n_groups, void* stream);
+
+/* Device address of the workspace's capacity-overflow word (int32, set by
+ * wipes_preprocess when the intersections exceed dup_capacity). */
+const int32_t* wipes_overflow_flag(const void* ws);
+
 /* Instrumentation: per-kernel CUDA-event timing (process-global, not for use
  * during graph capture) and a launch counter. */
 int          wipes_num_kernels(void);

@@ -12,8 +12,11 @@ passages each function follows); this module only builds it with gcc
 
 Parity status: pinned by ``tests/test_oracle_*.py`` (closed forms, invariants,
 finite differences, DFT, brute-force compositing). The exact z-integration
-mode (``exact_proj=1``) is pinned only by 1-D quadrature of its kernel value;
-its chain rule is not implemented ("parity unpinned" for exact-mode gradients).
+mode (``exact_proj=1``) is pinned by 1-D quadrature of its kernel value, its
+chain rule by whole-pipeline finite differences and by agreement with the
+paper-mode chain at f = 0. The NEXT-2 fitting step (``loss_l2``,
+``adam_step``, ``sigmoid``) is written out below in numpy FP64 from its
+textbook definitions and pinned by closed forms in tests/test_oracle_train.py.
 """
 from __future__ import annotations
 
@@ -322,3 +325,37 @@ def forward_backward(cfg: Cfg, p: dict, dLdC, cams=None, view_stride=0, pix=None
     else:
         out["grads"] = chain2d(cfg, p, pr, out["rgrad"])
     return out
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: the fitting step around the rasterizer. Plain
+# numpy FP64, definitions written out.
+# ---------------------------------------------------------------------------
+def loss_l2(image, target):
+    """L2 loss, mean over pixels and channels, and its gradient
+    dL/dimage = 2 (image - target) / n."""
+    d = np.asarray(image, np.float64) - np.asarray(target, np.float64)
+    n = d.size
+    return float(np.sum(d * d) / n), 2.0 * d / n
+
+
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-np.asarray(x, np.float64)))
+
+
+def adam_step(param, grad, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-15, activation="none"):
+    """Adam (Kingma & Ba 2015, Alg. 1; SPEC S:321-324 AdamState defaults) at
+    step t >= 1 on the raw parameter; ``grad`` is dL/d(act(param)) and is
+    chained through the activation first. Returns (param, m, v, act)."""
+    p = np.asarray(param, np.float64)
+    g = np.asarray(grad, np.float64)
+    if activation == "sigmoid":
+        s = sigmoid(p)
+        g = g * s * (1.0 - s)
+    m = b1 * np.asarray(m, np.float64) + (1.0 - b1) * g
+    v = b2 * np.asarray(v, np.float64) + (1.0 - b2) * g * g
+    mh = m / (1.0 - b1 ** t)
+    vh = v / (1.0 - b2 ** t)
+    p = p - lr * mh / (np.sqrt(vh) + eps)
+    act = sigmoid(p) if activation == "sigmoid" else p
+    return p, m, v, act

@@ -51,6 +51,16 @@ class wipes_grads(C.Structure):
                                           "color", "opacity")]
 
 
+class wipes_adam_group(C.Structure):
+    _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p),
+                ("v", C.c_void_p), ("act", C.c_void_p), ("n", C.c_int64), ("lr", C.c_float),
+                ("activation", C.c_int32)]
+
+
+ACT = {"none": 0, "sigmoid": 1}
+MAX_ADAM_GROUPS = 8
+
+
 class WipesError(RuntimeError):
     def __init__(self, status, where, detail):
         super().__init__(f"{where}: {status_name(status)}: {detail}")
@@ -84,6 +94,13 @@ def lib():
                                    vp, sz, i64, vp, vp, vp, P(wipes_grads), vp]
     L.wipes_get_grad_moments.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
     L.wipes_render_stats.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
+    L.wipes_train_scratch_bytes.restype = sz
+    L.wipes_loss_l2.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    L.wipes_adam_step.argtypes = [P(wipes_adam_group), i32, C.c_float, C.c_float, C.c_float, vp,
+                                  vp, vp, vp]
+    L.wipes_activate.argtypes = [P(wipes_adam_group), i32, vp]
+    L.wipes_overflow_flag.argtypes = [vp]
+    L.wipes_overflow_flag.restype = vp
     L.wipes_num_kernels.restype = C.c_int
     L.wipes_kernel_name.argtypes = [C.c_int]
     L.wipes_kernel_name.restype = C.c_char_p
@@ -96,7 +113,8 @@ def lib():
     L.wipes_abi_version.restype = C.c_int
     for fn in ("wipes_preprocess", "wipes_bin_sort", "wipes_check_overflow",
                "wipes_get_preprocess", "wipes_render_fwd", "wipes_render_bwd",
-               "wipes_get_grad_moments", "wipes_timing_collect", "wipes_render_stats"):
+               "wipes_get_grad_moments", "wipes_timing_collect", "wipes_render_stats",
+               "wipes_loss_l2", "wipes_adam_step", "wipes_activate"):
         getattr(L, fn).restype = C.c_int
     _lib = L
     return L
@@ -105,7 +123,8 @@ def lib():
 EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
             "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
             "wipes_render_bwd", "wipes_get_grad_moments", "wipes_render_stats",
-            "wipes_num_kernels",
+            "wipes_train_scratch_bytes", "wipes_loss_l2", "wipes_adam_step", "wipes_activate",
+            "wipes_overflow_flag", "wipes_num_kernels",
             "wipes_kernel_name", "wipes_timing_enable", "wipes_timing_collect",
             "wipes_launch_count", "wipes_status_string", "wipes_last_error",
             "wipes_abi_version"]
@@ -210,6 +229,36 @@ def wipes_get_grad_moments(cfg, N, B, ws, ws_bytes, cap, out, stream):
 
 def wipes_render_stats(cfg, N, B, ws, ws_bytes, cap, stats3, stream):
     return lib().wipes_render_stats(C.byref(cfg), N, B, ws, ws_bytes, cap, stats3, stream)
+
+
+def wipes_train_scratch_bytes() -> int:
+    return int(lib().wipes_train_scratch_bytes())
+
+
+def wipes_loss_l2(image, target, n, dL_dimage, loss, scratch, stream):
+    return lib().wipes_loss_l2(image, target, n, dL_dimage, loss, scratch, stream)
+
+
+def adam_groups(groups):
+    """list of dicts (param, grad, m, v, act, n, lr, activation) -> ctypes array."""
+    arr = (wipes_adam_group * max(len(groups), 1))()
+    for k, g in enumerate(groups):
+        arr[k] = wipes_adam_group(g["param"], g["grad"], g["m"], g["v"], g.get("act"), g["n"],
+                                  float(g["lr"]), ACT[g.get("activation", "none")])
+    return arr
+
+
+def wipes_adam_step(groups, n_groups, beta1, beta2, eps, step, guard, scratch, stream):
+    return lib().wipes_adam_step(groups, n_groups, beta1, beta2, eps, step, guard, scratch,
+                                 stream)
+
+
+def wipes_activate(groups, n_groups, stream):
+    return lib().wipes_activate(groups, n_groups, stream)
+
+
+def wipes_overflow_flag(ws) -> int:
+    return int(lib().wipes_overflow_flag(ws) or 0)
 
 
 def kernel_names():

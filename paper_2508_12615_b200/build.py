@@ -25,6 +25,7 @@ SOURCES = {
     "binning.cu": [],
     "sort.cu": [],
     "render.cu": [],
+    "train.cu": [],
     "abi.cu": [],
 }
 

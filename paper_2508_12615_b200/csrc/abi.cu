@@ -42,7 +42,8 @@ cudaEvent_t take_event() {
 const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
-    "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order"};
+    "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order", "loss_l2",
+    "adam"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -326,6 +327,65 @@ wipes_status wipes_render_stats(const wipes_config* cfg, int64_t N, int32_t B, v
                           (unsigned long long*)stats3);
   if (e != cudaSuccess) return cuda_fail(e, "render_stats");
   return WIPES_OK;
+}
+
+size_t wipes_train_scratch_bytes(void) { return train_scratch_bytes(); }
+
+wipes_status wipes_loss_l2(const float* image, const float* target, int64_t n, float* dL_dimage,
+                           double* loss, void* scratch, void* stream) {
+  if (n < 0) return fail(WIPES_EINVAL, "n < 0");
+  if (!image || !target || !dL_dimage || !loss || !scratch)
+    return fail(WIPES_EINVAL, "image, target, dL_dimage, loss and scratch must be non-NULL");
+  if (!aligned(image, 4) || !aligned(target, 4) || !aligned(dL_dimage, 4) || !aligned(loss, 8) ||
+      !aligned(scratch, 16))
+    return fail(WIPES_EINVAL, "misaligned pointer");
+  if (dL_dimage == image || dL_dimage == target)
+    return fail(WIPES_EINVAL, "dL_dimage aliases an input");
+  cudaError_t e = launch_loss_l2(image, target, n, dL_dimage, loss, scratch, (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "loss_l2 launch");
+}
+
+static wipes_status check_groups(const wipes_adam_group* g, int32_t ng, bool need_grad) {
+  if (!g || ng < 1 || ng > WIPES_MAX_ADAM_GROUPS)
+    return fail(WIPES_EINVAL, "need 1 <= n_groups <= WIPES_MAX_ADAM_GROUPS");
+  for (int k = 0; k < ng; ++k) {
+    if (g[k].n < 0) return fail(WIPES_EINVAL, "group n < 0");
+    if (g[k].activation != WIPES_ACT_NONE && g[k].activation != WIPES_ACT_SIGMOID)
+      return fail(WIPES_EINVAL, "group activation");
+    if (g[k].n == 0) continue;
+    if (!g[k].param || (need_grad && (!g[k].grad || !g[k].m || !g[k].v)))
+      return fail(WIPES_EINVAL, "group param/grad/m/v is NULL");
+    if (g[k].activation != WIPES_ACT_NONE && !g[k].act)
+      return fail(WIPES_EINVAL, "group with an activation needs act");
+    if (!(g[k].lr >= 0.f)) return fail(WIPES_EINVAL, "group lr must be >= 0");
+  }
+  return WIPES_OK;
+}
+
+wipes_status wipes_adam_step(const wipes_adam_group* groups, int32_t n_groups, float beta1,
+                             float beta2, float eps, int64_t* step, const int32_t* guard,
+                             void* scratch, void* stream) {
+  wipes_status st = check_groups(groups, n_groups, true);
+  if (st != WIPES_OK) return st;
+  if (!(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f))
+    return fail(WIPES_EINVAL, "need 0 <= beta1, beta2 < 1 and eps >= 0");
+  if (!step || !aligned(step, 8) || !scratch || !aligned(scratch, 16))
+    return fail(WIPES_EINVAL, "step/scratch NULL or misaligned");
+  cudaError_t e = launch_adam(groups, n_groups, beta1, beta2, eps, step, guard, scratch, 0,
+                              (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "adam launch");
+}
+
+wipes_status wipes_activate(const wipes_adam_group* groups, int32_t n_groups, void* stream) {
+  wipes_status st = check_groups(groups, n_groups, false);
+  if (st != WIPES_OK) return st;
+  cudaError_t e = launch_adam(groups, n_groups, 0.f, 0.f, 0.f, nullptr, nullptr, nullptr, 1,
+                              (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "activate launch");
+}
+
+const int32_t* wipes_overflow_flag(const void* ws) {
+  return ws ? &((const WsHeader*)ws)->overflow : nullptr;
 }
 
 int wipes_num_kernels(void) { return K_NUM; }

@@ -146,7 +146,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
 enum KernelId {
   K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
   K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
-  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_NUM
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_NUM
 };
 
 // Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph
@@ -162,6 +162,12 @@ void launch_begin(int kid, cudaStream_t s);
 void launch_end(int kid, cudaStream_t s);
 
 // ---- launchers (defined in the .cu files) ----------------------------------
+size_t train_scratch_bytes();
+cudaError_t launch_loss_l2(const float* img, const float* tgt, int64_t n, float* grad,
+                           double* loss, void* scratch, cudaStream_t s);
+cudaError_t launch_adam(const wipes_adam_group* groups, int ng, float b1, float b2, float eps,
+                        int64_t* step, const int32_t* guard, void* scratch, int activate_only,
+                        cudaStream_t s);
 cudaError_t launch_preprocess2d(const wipes_config& c, const wipes_params& p, const Layout& L,
                                 char* ws, uint8_t* cull_flags, cudaStream_t s);
 cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, const Layout& L,

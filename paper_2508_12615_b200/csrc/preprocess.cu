@@ -463,12 +463,21 @@ __global__ void __launch_bounds__(128, EXACT ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d
       fpx = (z * P.g[0]) / fx;
       fpy = (z * P.g[1]) / fy;
       if (EXACT) {  // f' and beta of the exact z-marginal (no integer decision uses them)
-        double rec8[8];
-        if (exact_rec<double>(cam, c.W, c.H, a.ewa_clamp, c.diag, mu, s, q, f, rec8)) {
-          fpx = rec8[5];
-          fpy = rec8[6];
-          beta = rec8[7];
-        }
+        // sigma = M S3 Rv2^T, s22 = Rv2 S3 Rv2^T (Rv2 = third row of the view rotation)
+        double t2[3];
+        for (int k = 0; k < 3; ++k)
+          t2[k] = s3at(P.S3, k, 0) * cam[6] + s3at(P.S3, k, 1) * cam[7] + s3at(P.S3, k, 2) * cam[8];
+        const double sgx = P.M[0] * t2[0] + P.M[1] * t2[1] + P.M[2] * t2[2];
+        const double sgy = P.M[3] * t2[0] + P.M[4] * t2[1] + P.M[5] * t2[2];
+        const double s22 = cam[6] * t2[0] + cam[7] * t2[1] + cam[8] * t2[2];
+        const double det2 = P.Sp[0] * P.Sp[2] - P.Sp[1] * P.Sp[1];  // undilated S2
+        const double ux = (P.Sp[2] * sgx - P.Sp[1] * sgy) / det2;
+        const double uy = (P.Sp[0] * sgy - P.Sp[1] * sgx) / det2;
+        const double vv = s22 - (sgx * ux + sgy * uy);
+        const double fhz = P.g[2] - P.j02 * fpx - P.j12 * fpy;
+        fpx = fpx + fhz * ux;
+        fpy = fpy + fhz * uy;
+        beta = exp(-0.5 * fhz * fhz * vv);
       }
       float dz = (float)z;
       dk = orderable(dz);

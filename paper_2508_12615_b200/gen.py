@@ -172,6 +172,74 @@ def gen_dLdC(B: int, H: int, W: int, seed: int = 0) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
+# NEXT-2 fitting inputs: a synthetic target and the SPEC's initialisation
+# --------------------------------------------------------------------------
+def zone_plate(H: int, W: int, k: float = 60.0) -> np.ndarray:
+    """SPEC S:422-427 gen_zone_plate: I = 1/2 + 1/2 sin(k (u^2 + v^2)) with
+    u, v in [-1, 1] at pixel centres, replicated to 3 channels -> [3, H, W]."""
+    u = (np.arange(W) + 0.5) / W * 2.0 - 1.0
+    v = (np.arange(H) + 0.5) / H * 2.0 - 1.0
+    img = 0.5 + 0.5 * np.sin(k * (u[None, :] ** 2 + v[:, None] ** 2))
+    return np.ascontiguousarray(np.broadcast_to(img, (3, H, W)).astype(F32))
+
+
+def smooth_target(H: int, W: int, seed: int = 0, octaves: int = 5) -> np.ndarray:
+    """A natural-image-like [3, H, W] target in [0, 1]: a sum of random
+    sinusoidal gratings with 1/f amplitudes (no dataset is available)."""
+    g = _rng(seed)
+    y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+    img = np.zeros((3, H, W))
+    for o in range(octaves):
+        for _ in range(4):
+            f = (2.0 ** o) * 2 * math.pi / max(H, W) * g.uniform(0.5, 1.5)
+            th = g.uniform(0, math.pi)
+            ph = g.uniform(0, 2 * math.pi)
+            wave = np.sin(f * (x * math.cos(th) + y * math.sin(th)) + ph)
+            img += (0.5 ** o) * g.uniform(0.2, 1.0, 3)[:, None, None] * wave
+    img -= img.min()
+    img /= max(img.max(), 1e-12)
+    return np.ascontiguousarray(img.astype(F32))
+
+
+def init2d_from_target(target: np.ndarray, N: int, seed: int = 0, cov_mode: str = "cholesky",
+                       freq_std: float = 0.05, phase: bool = False) -> dict:
+    """SPEC S:328-331 init_primitives: positions uniform over the image; colours
+    bilinearly sampled from the target at each position; opacity_raw = 0;
+    covariance parameters giving Sigma = diag(s^2, s^2), s = sqrt(W H / N);
+    freq ~ N(0, freq_std^2) per axis (rad/px). Returns raw float32 params."""
+    C_, H, W = target.shape
+    if N > H * W:
+        raise ValueError("ImageTooSmall: N exceeds the pixel count")
+    g = _rng(seed)
+    mean = np.stack([g.uniform(0, W, N), g.uniform(0, H, N)], 1)
+    # bilinear sample at the position (pixel centres at integer + 0.5)
+    xs = np.clip(mean[:, 0] - 0.5, 0, W - 1)
+    ys = np.clip(mean[:, 1] - 0.5, 0, H - 1)
+    x0 = np.floor(xs).astype(np.int64)
+    y0 = np.floor(ys).astype(np.int64)
+    x1 = np.minimum(x0 + 1, W - 1)
+    y1 = np.minimum(y0 + 1, H - 1)
+    fx, fy = xs - x0, ys - y0
+    t = target.astype(np.float64)
+    color = ((1 - fx) * (1 - fy) * t[:, y0, x0] + fx * (1 - fy) * t[:, y0, x1]
+             + (1 - fx) * fy * t[:, y1, x0] + fx * fy * t[:, y1, x1]).T
+    s = math.sqrt(W * H / N)
+    if cov_mode == "sigma":
+        cov = np.tile([s * s, 0.0, s * s], (N, 1))
+    elif cov_mode == "cholesky":
+        cov = np.tile([s, 0.0, s], (N, 1))
+    elif cov_mode == "rs":
+        cov = np.tile([0.0, s, s], (N, 1))
+    else:
+        raise ValueError(cov_mode)
+    out = dict(mean=mean, cov=cov, freq=g.normal(0, freq_std, (N, 2)), color=color,
+               opacity=np.zeros(N))
+    if phase:
+        out["phase"] = np.zeros(N)
+    return {k: np.ascontiguousarray(v.astype(F32)) for k, v in out.items()}
+
+
+# --------------------------------------------------------------------------
 # Named configurations (BASELINE.json configs; SURVEY §8(d))
 # --------------------------------------------------------------------------
 CONFIGS = {

@@ -21,7 +21,7 @@ def L():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "wipes.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(wipes_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(wipes_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(L):
@@ -118,3 +118,22 @@ def test_product_package_never_imports_oracle():
                 s = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"\bimport\s+oracle\b|from\s+oracle\b|oracle\.cpp|liboracle",
                                      s), f
+
+
+def test_train_entry_points_validate(L):
+    """NEXT-2 entry points reject bad arguments before any launch."""
+    assert abi.wipes_train_scratch_bytes() >= 8 * 1184
+    st = abi.wipes_loss_l2(0x1000, 0x2000, 10, None, 0x3000, 0x4000, None)
+    assert st == abi.WIPES_EINVAL
+    st = abi.wipes_loss_l2(0x1000, 0x2000, 10, 0x1000, 0x3000, 0x4000, None)
+    assert st == abi.WIPES_EINVAL and b"alias" in L.wipes_last_error()
+    g = abi.adam_groups([dict(param=0x1000, grad=0x2000, m=0x3000, v=0x4000, n=4, lr=0.1,
+                              activation="sigmoid")])
+    st = abi.wipes_adam_step(g, 1, 0.9, 0.999, 1e-15, 0x5000, None, 0x6000, None)
+    assert st == abi.WIPES_EINVAL and b"act" in L.wipes_last_error()
+    g = abi.adam_groups([dict(param=0x1000, grad=0x2000, m=0x3000, v=0x4000, n=4, lr=0.1)])
+    st = abi.wipes_adam_step(g, 1, 1.0, 0.999, 1e-15, 0x5000, None, 0x6000, None)
+    assert st == abi.WIPES_EINVAL and b"beta" in L.wipes_last_error()
+    st = abi.wipes_adam_step(g, 9, 0.9, 0.999, 1e-15, 0x5000, None, 0x6000, None)
+    assert st == abi.WIPES_EINVAL
+    assert abi.wipes_overflow_flag(0x100000) == 0x100000 + 8
