@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-fit", action="store_true",
+                    help="skip the NEXT-2 fitting-step measurement (2D configs)")
     ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
                     help="3D projection: Eq. 7 as written (default) or NEXT-1 exact z-marginal")
     return ap.parse_args()
@@ -112,6 +114,39 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU ---
+def fit_rate(H, W, N, args, flush, dev):
+    """NEXT-2: full fitting iterations (render -> L2 loss -> backward -> Adam,
+    one CUDA graph per iteration, raster.Fitter2D) on this frame size, timed
+    with CUDA events over args.steps replays (L2 flushed between)."""
+    import torch
+    from paper_2508_12615_b200 import gen
+    from paper_2508_12615_b200.train import Fitter2D
+    tgt = gen.smooth_target(H, W, seed=args.seed)
+    p = gen.init2d_from_target(tgt, N, seed=args.seed, freq_std=0.05)
+    fit = Fitter2D(torch.from_numpy(tgt).to(dev), {k: torch.from_numpy(v) for k, v in p.items()},
+                   cov2="cholesky")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush.zero_()
+        fit.step()
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fit.step()
+        b.record(stream)
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    loss, over = fit.poll()
+    return {"value": args.steps / (ms / 1e3), "unit": "fitting iters/s",
+            "ms_per_step": ms / args.steps, "loss": loss, "overflowed": over,
+            "steps_applied": fit.steps_taken(),
+            "workload": f"NEXT-2 image fit {W}x{H}, {N} Cholesky primitives, L2 + Adam "
+                        "(preprocess, bin/sort, render, loss, backward, Adam: one CUDA graph)"}
+
+
 def cpu_oracle_sample(c, npix, seed):
     """The oracle as it stands (double-precision brute force over ALL primitives
     per pixel, no tiling) on a bounded random pixel sample of the workload;
@@ -377,6 +412,8 @@ def main():
             "roofline": roof,
             "paper_context": "render FPS on one A6000: Kodak 1708-1779 (Table 1, PAPER.md:148-149); "
                              "Mip-NeRF360 95.7 (Table 2, PAPER.md:239)"}
+    if c["kind"] == "2d" and not rows and not args.no_fit:
+        line["fit"] = fit_rate(H, W, N, args, flush, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fac, cores = cpu_oracle_sample(c, args.cpu_pixels, seed=123)
         line["cpu_baseline"] = {"value": 1.0 / (dt * fac), "unit": "iters/s", "cores": cores,
