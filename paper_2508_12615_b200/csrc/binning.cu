@@ -149,12 +149,13 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   }
 }
 
-// ALPHA depth presort inputs: key = (view << 32) | orderable depth bits.
-__global__ void __launch_bounds__(256) k_presort_keys(const uint32_t* dkey, int64_t BN, int64_t N,
-                                                      uint64_t* pk, uint32_t* pv) {
+// ALPHA depth presort inputs: key = orderable depth bits, value = o = view*N +
+// primitive (the view digits of the last passes are taken from value / N).
+__global__ void __launch_bounds__(256) k_presort_keys(const uint32_t* dkey, int64_t BN,
+                                                      uint32_t* pk, uint32_t* pv) {
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= BN) return;
-  pk[o] = ((uint64_t)(o / N) << 32) | (uint64_t)dkey[o];
+  pk[o] = dkey[o];
   pv[o] = (uint32_t)o;
 }
 
@@ -288,16 +289,22 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     cudaError_t e;
     if (L.alpha) {
       // depth presort of the (view, primitive) records, then offsets in that order
-      uint64_t* pkA = (uint64_t*)(ws + L.pkA);
-      uint64_t* pkB = (uint64_t*)(ws + L.pkB);
+      uint32_t* pkA = (uint32_t*)(ws + L.pkA);
+      uint32_t* pkB = (uint32_t*)(ws + L.pkB);
       uint32_t* pvA = (uint32_t*)(ws + L.pvA);
       uint32_t* pvB = (uint32_t*)(ws + L.pvB);
       launch_begin(K_DUPLICATE, s);
-      k_presort_keys<<<gBN, 256, 0, s>>>((const uint32_t*)(ws + L.dkey), L.BN, L.N, pkA, pvA);
+      k_presort_keys<<<gBN, 256, 0, s>>>((const uint32_t*)(ws + L.dkey), L.BN, pkA, pvA);
       launch_end(K_DUPLICATE, s);
+      // 4 depth-byte passes on the key, then the view bytes of value / N
       int shifts[kMaxPasses];
-      for (int p = 0; p < L.pre_passes; ++p) shifts[p] = 8 * p;  // depth bytes, then view bytes
-      e = launch_sort<uint64_t>(L, ws, pkA, pvA, pkB, pvB, shifts, L.pre_passes, L.BN, L.BN, s);
+      uint32_t vmask = 0;
+      for (int p = 0; p < L.pre_passes; ++p) {
+        shifts[p] = p < 4 ? 8 * p : 8 * (p - 4);
+        if (p >= 4) vmask |= 1u << p;
+      }
+      e = launch_sort<uint32_t>(L, ws, pkA, pvA, pkB, pvB, shifts, L.pre_passes, L.BN, L.BN, s,
+                                (uint32_t)L.N, vmask);
       if (e != cudaSuccess) return e;
       order = (L.pre_passes & 1) ? pvB : pvA;
       launch_begin(K_DUPLICATE, s);

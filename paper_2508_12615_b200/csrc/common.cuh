@@ -124,8 +124,8 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.valsA = take(sizeof(uint32_t) * L.cap);
   L.valsB = take(sizeof(uint32_t) * L.cap);
   const int64_t pn = L.alpha ? L.BN : 0;
-  L.pkA = take(sizeof(uint64_t) * pn);
-  L.pkB = take(sizeof(uint64_t) * pn);
+  L.pkA = take(sizeof(uint32_t) * pn);
+  L.pkB = take(sizeof(uint32_t) * pn);
   L.pvA = take(sizeof(uint32_t) * pn);
   L.pvB = take(sizeof(uint32_t) * pn);
   L.cnt2 = take(sizeof(int32_t) * pn);
@@ -177,7 +177,7 @@ cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
-                        cudaStream_t s);
+                        cudaStream_t s, uint32_t vdiv = 1, uint32_t vmask = 0);
 cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
                           cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);

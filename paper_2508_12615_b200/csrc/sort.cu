@@ -25,6 +25,10 @@ namespace wipes {
 namespace {
 
 constexpr int kWarps = kSortThreads / 32;
+#ifndef WIPES_SORT_LOOKBACK
+#define WIPES_SORT_LOOKBACK 4
+#endif
+constexpr int kLookBack = WIPES_SORT_LOOKBACK;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
 template <typename K>
@@ -41,6 +45,7 @@ struct SortArgs {
   uint32_t* status;    // [tiles][256] look-back words of this pass
   int32_t shifts[kMaxPasses];
   int32_t npass, pass, shift;
+  uint32_t vdiv, vmask;  // pass p with bit p of vmask: digit of (value / vdiv), not of key
 };
 
 template <typename K>
@@ -59,9 +64,13 @@ __global__ void __launch_bounds__(256) k_sort_hist(SortArgs<K> a) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const K k = a.kin[i];
+    const uint32_t vq = a.vmask ? a.vin[i] / a.vdiv : 0u;
 #pragma unroll
     for (int p = 0; p < kMaxPasses; ++p)
-      if (p < a.npass) atomicAdd(&h[p][(uint32_t)(k >> a.shifts[p]) & 255u], 1u);
+      if (p < a.npass) {
+        const uint32_t src = ((a.vmask >> p) & 1u) ? (vq >> a.shifts[p]) : (uint32_t)(k >> a.shifts[p]);
+        atomicAdd(&h[p][src & 255u], 1u);
+      }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < a.npass * 256; i += blockDim.x) {
@@ -80,8 +89,12 @@ struct SortSmem {
   uint32_t tile;
 };
 
+#ifndef WIPES_SORT_MINB
+#define WIPES_SORT_MINB 4
+#endif
+
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
+__global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(SortArgs<K> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -93,6 +106,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
   const int64_t base = (int64_t)tile * kSortTile;
   if (base >= n) return;  // beyond the data: nobody waits on this tile
   const int shift = a.shift;
+  const bool vp = (a.vmask >> a.pass) & 1u;
   const uint32_t lt = (1u << lane) - 1u;
   // ---- load (warp-striped) and rank stably within the tile ----------------
   K key[kSortItems];
@@ -104,7 +118,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
     const bool valid = idx < n;
     key[i] = valid ? a.kin[idx] : (K)0;
     val[i] = valid ? a.vin[idx] : 0u;
-    dig[i] = valid ? ((uint32_t)(key[i] >> shift) & 255u) : 256u;
+    const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
+    dig[i] = valid ? (src & 255u) : 256u;
   }
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -130,6 +145,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
   volatile uint32_t* st = a.status;
   st[(int64_t)tile * 256 + d] = kFlagAgg | cnt;
   uint32_t prefix = 0;
+#ifdef WIPES_SORT_LB1
   for (int64_t t = (int64_t)tile - 1; t >= 0;) {
     const uint32_t s = st[t * 256 + d];
     const uint32_t f = s & ~kValMask;
@@ -138,6 +154,28 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
     if (f == kFlagInc) break;
     --t;
   }
+#else
+  // look back kLookBack predecessors per round: their status words are loaded
+  // together (independent loads), then consumed in tile order
+  for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+    uint32_t s[kLookBack];
+#pragma unroll
+    for (int j = 0; j < kLookBack; ++j)
+      s[j] = t - j >= 0 ? st[(t - j) * 256 + d] : (2u << 30);  // before tile 0: inclusive 0
+    int used = 0;
+    bool stop = false;
+#pragma unroll
+    for (int j = 0; j < kLookBack; ++j) {
+      const uint32_t f = s[j] & ~kValMask;
+      if (stop || used < j || f == 0u) continue;  // unpublished: re-read from here
+      prefix += s[j] & kValMask;
+      ++used;
+      stop = f == kFlagInc;
+    }
+    if (stop) break;
+    t -= used;
+  }
+#endif
   __threadfence();
   st[(int64_t)tile * 256 + d] = kFlagInc | (prefix + cnt);
   // global digit base = exclusive scan of the pass histogram (block scan)
@@ -174,11 +212,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
   const int tn = rem < kSortTile ? (int)rem : kSortTile;
   for (int j = tid; j < tn; j += kSortThreads) {
     const K k = sm.keys[j];
-    const uint32_t dd = (uint32_t)(k >> shift) & 255u;
+    const uint32_t v = sm.vals[j];
+    const uint32_t dd = (vp ? (v / a.vdiv) >> shift : (uint32_t)(k >> shift)) & 255u;
     const int64_t pos = (int64_t)sm.gofs[dd] + (j - (int64_t)sm.bexcl[dd]);
     WCHECK(pos >= 0 && pos < n);
     a.kout[pos] = k;
-    a.vout[pos] = sm.vals[j];
+    a.vout[pos] = v;
   }
 }
 
@@ -187,7 +226,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(SortArgs<K> a) {
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
-                        cudaStream_t s) {
+                        cudaStream_t s, uint32_t vdiv, uint32_t vmask) {
   if (npass == 0 || cap == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -203,6 +242,8 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   a.counter = a.ghist + kMaxPasses * 256;
   a.status = (uint32_t*)(ws + L.sort_status);
   a.npass = npass;
+  a.vdiv = vdiv ? vdiv : 1u;
+  a.vmask = vmask;
   for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
   cudaError_t e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
   if (e != cudaSuccess) return e;
@@ -232,10 +273,10 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
 
 template cudaError_t launch_sort<uint32_t>(const Layout&, char*, uint32_t*, uint32_t*,
                                            uint32_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t);
 template cudaError_t launch_sort<uint64_t>(const Layout&, char*, uint64_t*, uint32_t*,
                                            uint64_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t);
 
 size_t sort_smem_bytes64() { return sizeof(SortSmem<uint64_t>); }
 
