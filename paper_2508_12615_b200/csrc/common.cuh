@@ -26,7 +26,10 @@ constexpr int kScanItems = 8;                  // items per thread
 constexpr int kScanTile = kScanBlock * kScanItems;
 constexpr int kRadixBits = 8;
 constexpr int kSortThreads = 256;              // onesweep CTA (one digit per thread)
-constexpr int kSortItems = 8;                  // keys per thread per tile
+#ifndef WIPES_SORT_ITEMS
+#define WIPES_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = WIPES_SORT_ITEMS;   // keys per thread per tile
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 8;
 constexpr int32_t kWsMagic = 0x57495053;       // "WIPS"

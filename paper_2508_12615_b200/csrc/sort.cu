@@ -84,6 +84,7 @@ struct SortSmem {
   K keys[kSortTile];
   uint32_t vals[kSortTile];
   uint32_t wcnt[kWarps][256];  // per-warp running counts, then warp-exclusive prefixes
+  uint32_t thist[256];         // tile digit histogram (published before the ranking)
   uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
   uint32_t gofs[256];          // global output offset of the tile's first key per digit
   uint32_t tile;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   const int64_t n = n_keys(a);
   if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
   for (int i = tid; i < kWarps * 256; i += kSortThreads) (&sm.wcnt[0][0])[i] = 0;
+  sm.thist[tid] = 0;  // kSortThreads == 256
   __syncthreads();
   const uint32_t tile = sm.tile;
   const int64_t base = (int64_t)tile * kSortTile;
@@ -121,6 +123,14 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
     dig[i] = valid ? (src & 255u) : 256u;
   }
+  // tile histogram first, so the aggregate is published before the ranking
+  // and the successors' look-back rarely has to wait for it
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i)
+    if (dig[i] < 256u) atomicAdd(&sm.thist[dig[i]], 1u);
+  __syncthreads();
+  volatile uint32_t* st = a.status;
+  st[(int64_t)tile * 256 + tid] = kFlagAgg | sm.thist[tid];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = dig[i];
@@ -141,9 +151,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     sm.wcnt[w][d] = cnt;
     cnt += c;
   }
-  // publish the tile aggregate, then look back for the exclusive prefix
-  volatile uint32_t* st = a.status;
-  st[(int64_t)tile * 256 + d] = kFlagAgg | cnt;
+  // look back for the exclusive prefix (the aggregate was published above)
   uint32_t prefix = 0;
 #ifdef WIPES_SORT_LB1
   for (int64_t t = (int64_t)tile - 1; t >= 0;) {
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     t -= used;
   }
 #endif
-  __threadfence();
+  // flag and value share one 32-bit word: no fence needed between publishes
   st[(int64_t)tile * 256 + d] = kFlagInc | (prefix + cnt);
   // global digit base = exclusive scan of the pass histogram (block scan)
   const uint32_t gh = a.ghist[a.pass * 256 + d];
