@@ -125,26 +125,65 @@ struct DupArgs {
   uint32_t* vals;
 };
 
+// Warp-cooperative emission: the 32 records of a warp own one contiguous
+// output range (their offsets are consecutive in the scan), so the warp
+// writes it lane-strided — every store instruction covers 32 consecutive
+// pairs — finding each pair's record by a binary search over the lanes'
+// start offsets and its tile from the record's rect.
 __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j0 >= a.BN) return;
-  const int64_t o = a.order ? (int64_t)a.order[j0] : j0;
-  WCHECK(o >= 0 && o < a.BN);
-  const int32_t n = a.count[o];
-  if (n == 0) return;
-  int64_t j = a.loc[j0] + a.blk[j0 / kScanTile];
-  const int64_t v = o / a.N, i = o - v * a.N;
-  const int4 r = a.rect[o];
-  const uint32_t vt = (uint32_t)(v * a.T);
-  const int ty0 = a.row_mod > 1 ? band_first_row(r.y, a.row_mod, a.row_rem) : r.y;
+  const int lane = threadIdx.x & 31;
+  constexpr unsigned kFullMask = 0xffffffffu;
+  int32_t n = 0;
+  int64_t start = INT64_MAX;  // beyond BN: never owns a pair
+  int4 r = make_int4(0, 0, 0, 0);
+  uint32_t vt = 0, ival = 0;
+  int ty0 = 0, wdt = 1;
+  if (j0 < a.BN) {
+    const int64_t o = a.order ? (int64_t)a.order[j0] : j0;
+    WCHECK(o >= 0 && o < a.BN);
+    n = a.count[o];
+    start = a.loc[j0] + a.blk[j0 / kScanTile];
+    const int64_t v = o / a.N;
+    ival = (uint32_t)(o - v * a.N);
+    vt = (uint32_t)(v * a.T);
+    if (n > 0) {
+      r = a.rect[o];
+      ty0 = a.row_mod > 1 ? band_first_row(r.y, a.row_mod, a.row_rem) : r.y;
+      wdt = r.z - r.x;
+    }
+  }
+  // the warp's output range [S, E) (lane 0 is always a valid record)
+  if (j0 - lane >= a.BN) return;  // whole warp beyond the records
+  const int64_t S = __shfl_sync(kFullMask, start, 0);
+  int64_t E = j0 < a.BN ? start + n : 0;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const int64_t t = __shfl_xor_sync(kFullMask, E, off);
+    E = t > E ? t : E;
+  }
   const int dty = a.row_mod > 1 ? a.row_mod : 1;
-  for (int ty = ty0; ty < r.w; ty += dty) {
-    const uint32_t rowt = vt + (uint32_t)ty * (uint32_t)a.GX;
-    for (int tx = r.x; tx < r.z; ++tx, ++j) {
-      if (j >= a.cap) return;
-      WCHECK(j >= 0 && rowt + (uint32_t)tx < (uint32_t)((v + 1) * a.T));
-      a.keys[j] = rowt + (uint32_t)tx;
-      a.vals[j] = (uint32_t)i;
+  for (int64_t j = S + lane; j - lane < E; j += 32) {
+    const bool live = j < E;
+    // owner = the last lane with start <= j (starts are non-decreasing; a
+    // zero-count lane shares its start with the next lane, which owns it)
+    int owner = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const int64_t sv = __shfl_sync(kFullMask, start, owner + step);
+      if (sv <= j) owner += step;
+    }
+    const int64_t so = __shfl_sync(kFullMask, start, owner);
+    const int ox = __shfl_sync(kFullMask, r.x, owner);
+    const int ow = __shfl_sync(kFullMask, wdt, owner);
+    const int oty = __shfl_sync(kFullMask, ty0, owner);
+    const uint32_t ovt = __shfl_sync(kFullMask, vt, owner);
+    const uint32_t oi = __shfl_sync(kFullMask, ival, owner);
+    if (live && j < a.cap) {
+      const int t = (int)(j - so);
+      const int row = t / ow, col = t - row * ow;
+      a.keys[j] = ovt + (uint32_t)(oty + row * dty) * (uint32_t)a.GX + (uint32_t)(ox + col);
+      a.vals[j] = oi;
     }
   }
 }
