@@ -8,7 +8,8 @@
 //  2. k_sort_pass  : one launch per digit. Each CTA takes the next tile of
 //                    kSortTile keys (tile id from an atomic counter, so tiles
 //                    are assigned in launch order), ranks them stably in shared
-//                    memory (warp-striped layout, __match_any_sync per step),
+//                    memory (warp-striped layout, lanes with equal digits found
+//                    by 9 ballots per step),
 //                    publishes its per-digit counts, resolves its per-digit
 //                    global offsets by DECOUPLED LOOK-BACK over the preceding
 //                    tiles, stages the pairs in shared memory in sorted order
@@ -134,7 +135,18 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = dig[i];
+#ifdef WIPES_SORT_MATCH
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#else
+    // lanes with the same digit: AND over the 9 digit bits (bit 8 marks an
+    // invalid slot) of the matching ballots — cheaper than MATCH.ANY
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+#endif
     const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;
     rank[i] = before + __popc(peers & lt);
     __syncwarp();

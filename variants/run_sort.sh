@@ -8,7 +8,7 @@ for v in "$@"; do
 import json,sys
 try:
   d=json.loads(sys.stdin.read()); k=d['kernel_ms_per_step']
-  print('$v $c', round(d['ms_per_step'],4), 'scatter', round(k['radix_scatter'],4), 'hist', round(k['radix_hist'],4), 'dup', round(k['duplicate'],4))
+  print('$v $c', round(d['ms_per_step'],4), 'scatter', round(k['radix_scatter'],4), 'hist', round(k.get('radix_hist',0),4), 'dup', round(k['duplicate'],4))
 except Exception as e: print('$v $c FAILED', e)"
   done
 done
