@@ -30,6 +30,9 @@ constexpr int kWarps = kSortThreads / 32;
 #define WIPES_SORT_LOOKBACK 4
 #endif
 constexpr int kLookBack = WIPES_SORT_LOOKBACK;
+#ifndef WIPES_SORT_BACKOFF
+#define WIPES_SORT_BACKOFF 64  // ns: keeps spinning warps off the issue slots
+#endif
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
 template <typename K>
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
       stop = f == kFlagInc;
     }
     if (stop) break;
+    if (used == 0) __nanosleep(WIPES_SORT_BACKOFF);  // predecessor unpublished: back off
     t -= used;
   }
 #endif
