@@ -52,7 +52,7 @@ class ora_cfg(C.Structure):
                 ("use_rect", C.c_int32),
                 ("alpha_min", C.c_double), ("alpha_max", C.c_double), ("T_min", C.c_double),
                 ("dilation", C.c_double), ("cov_eps", C.c_double), ("det_min", C.c_double),
-                ("bg", C.c_double * 3)]
+                ("bg", C.c_double * 3), ("color_per_view", C.c_int32)]
 
 
 class ora_cam(C.Structure):
@@ -85,14 +85,16 @@ class Cfg:
     cov_eps: float = 0.0
     det_min: float = float(np.float32(1e-12))
     bg: tuple = (0.0, 0.0, 0.0)
+    sh_degree: Optional[int] = None  # NEXT-3: None = flat RGB `color`; 0..3 = SH `sh`
 
-    def c(self) -> ora_cfg:
+    def c(self, color_per_view: bool = False) -> ora_cfg:
         return ora_cfg(self.width, self.height, self.tile, int(self.prim3d),
                        int(self.alpha_blend), COV_MODES[self.cov2],
                        0 if self.extent == "opacity" else 1, int(self.ewa_clamp),
                        int(self.exact_proj), int(self.use_rect),
                        self.alpha_min, self.alpha_max, self.T_min, self.dilation,
-                       self.cov_eps, self.det_min, (C.c_double * 3)(*self.bg))
+                       self.cov_eps, self.det_min, (C.c_double * 3)(*self.bg),
+                       int(color_per_view))
 
 
 P_FIELDS = ["mux", "muy", "a", "b", "c", "fx", "fy", "phi", "beta", "cr", "cg", "cb",
@@ -175,14 +177,18 @@ def project3d(cfg: Cfg, p: dict, cams, view_stride: int = 0) -> Projected:
     mean = _d(p["mean"]).reshape(-1, 3)
     N = mean.shape[0] if view_stride == 0 else int(view_stride)
     scale, quat, freq = _d(p["scale"]), _d(p["quat"]), _d(p["freq"])
-    phase, color, op = _d(p.get("phase")), _d(p["color"]), _d(p["opacity"])
+    phase, op = _d(p.get("phase")), _d(p["opacity"])
+    cc = cams_c(cams)
+    if cfg.sh_degree is not None:  # NEXT-3: per (view, primitive) SH colours
+        color = sh_colors(cfg.sh_degree, mean, p["sh"], cams, N, view_stride)
+    else:
+        color = _d(p["color"])
     flag = np.zeros(B * N, np.int32)
     rect = np.zeros((B * N, 4), np.int32)
     count = np.zeros(B * N, np.int32)
     keylo = np.zeros(B * N, np.uint32)
     rec = np.zeros((B * N, NP_), np.float64)
-    cf = cfg.c()
-    cc = cams_c(cams)
+    cf = cfg.c(color_per_view=cfg.sh_degree is not None)
     lib().ora_project3d(C.byref(cf), C.c_int64(N), C.c_int32(B), cc, _p(mean), _p(scale),
                         _p(quat), _p(freq), _p(phase), _p(color), _p(op),
                         C.c_int64(view_stride), _p(flag), _p(rect), _p(count), _p(keylo),
@@ -272,6 +278,31 @@ def chain3d(cfg: Cfg, p: dict, cams, pr: Projected, rgrad, view_stride: int = 0)
                       _p(_d(rgrad)), C.c_int64(view_stride), _p(out["mean"]),
                       _p(out["scale"]), _p(out["quat"]), _p(out["freq"]), _p(out["phase"]),
                       _p(out["color"]), _p(out["opacity"]))
+    if cfg.sh_degree is not None:  # colour comes from SH: dL/dsh + view-direction term
+        K = (cfg.sh_degree + 1) ** 2
+        del out["color"]
+        out["sh"] = np.zeros((NP, K, 3), np.float64)
+        lib().ora_sh_chain(C.c_int32(cfg.sh_degree), C.c_int64(N), C.c_int32(B), cams_c(cams),
+                           _p(_d(p["mean"])), _p(_d(p["sh"])), C.c_int64(view_stride),
+                           _p(pr.flag), _p(_d(rgrad)), _p(out["sh"]), _p(out["mean"]))
+    return out
+
+
+def sh_basis(deg: int, dirs) -> np.ndarray:
+    """O9: real SH basis values [n, (deg+1)^2] at unit directions [n, 3]."""
+    d = _d(dirs).reshape(-1, 3)
+    K = (deg + 1) ** 2
+    out = np.zeros((d.shape[0], K), np.float64)
+    lib().ora_sh_basis(C.c_int32(deg), C.c_int64(d.shape[0]), _p(d), _p(out))
+    return out
+
+
+def sh_colors(deg: int, mean, sh, cams, N: int, view_stride: int = 0) -> np.ndarray:
+    """O9: SH colour of every (view, primitive) [B*N, 3] (clamped at 0)."""
+    B = len(cams)
+    out = np.zeros((B * N, 3), np.float64)
+    lib().ora_sh_colors(C.c_int32(deg), C.c_int64(N), C.c_int32(B), cams_c(cams),
+                        _p(_d(mean)), _p(_d(sh)), C.c_int64(view_stride), _p(out))
     return out
 
 

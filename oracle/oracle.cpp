@@ -57,6 +57,7 @@ struct ora_cfg {
   double alpha_min, alpha_max, T_min;
   double dilation, cov_eps, det_min;
   double bg[3];
+  int32_t color_per_view;  // 1: color is [B*N,3] per (view, primitive) (SH colours)
 };
 
 struct ora_cam {
@@ -362,10 +363,11 @@ void ora_project3d(const ora_cfg* cfg, int64_t N, int32_t B, const ora_cam* cams
                        phase ? phase[pi] : 0.0,
                        opacity[pi], 0.0, 0.0};
       r[P_PHI] = in[13];
-      r[P_CR] = color[3 * pi]; r[P_CG] = color[3 * pi + 1]; r[P_CB] = color[3 * pi + 2];
+      const double* col = c.color_per_view ? color + 3 * o : color + 3 * pi;
+      r[P_CR] = col[0]; r[P_CG] = col[1]; r[P_CB] = col[2];
       r[P_ALPHA] = in[14];
       in[15] = ((in[6] * in[6] + in[7] * in[7]) + in[8] * in[8]) + in[9] * in[9];
-      if (!finite_all(in, 15) || !finite_all(color + 3 * pi, 3) || !(in[15] > 0.0)) {
+      if (!finite_all(in, 15) || !finite_all(col, 3) || !(in[15] > 0.0)) {
         flag[o] = 5;
         continue;
       }
@@ -911,6 +913,136 @@ void ora_chain3d_exact(const ora_cfg* cfg, int64_t N, int32_t B, const ora_cam* 
       for (int k = 0; k < 3; ++k) g_freq[3 * pi + k] += gp[10 + k];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// O9 (NEXT-3): spherical-harmonic colour, PAPER.md:106 ("color attributes
+// encoded by spherical harmonic coefficients c") with the 3DGS settings the
+// paper keeps: real SH up to degree 3 in the 3DGS sign convention,
+// colour = max(0, sum_k Y_k(d) sh_k + 1/2), d = (mu - C)/|mu - C|, C = -R^T t.
+// Constants are written from their closed forms (normalisation of the real
+// SH, e.g. Y_00 = 1/(2 sqrt(pi))); pinned by orthonormality on the sphere
+// (tests/test_oracle_sh.py).
+// ---------------------------------------------------------------------------
+static void sh_basis(int deg, const double* d, double* Y) {
+  const double pi = 3.14159265358979323846;
+  const double x = d[0], y = d[1], z = d[2];
+  const double c0 = 0.5 / std::sqrt(pi);
+  const double c1 = std::sqrt(3.0 / (4.0 * pi));
+  const double c2a = 0.5 * std::sqrt(15.0 / pi), c2b = 0.25 * std::sqrt(5.0 / pi),
+               c2c = 0.25 * std::sqrt(15.0 / pi);
+  const double c3a = 0.25 * std::sqrt(35.0 / (2.0 * pi)), c3b = 0.5 * std::sqrt(105.0 / pi),
+               c3c = 0.25 * std::sqrt(21.0 / (2.0 * pi)), c3d = 0.25 * std::sqrt(7.0 / pi),
+               c3e = 0.25 * std::sqrt(105.0 / pi);
+  Y[0] = c0;
+  if (deg < 1) return;
+  Y[1] = -c1 * y;
+  Y[2] = c1 * z;
+  Y[3] = -c1 * x;
+  if (deg < 2) return;
+  Y[4] = c2a * x * y;
+  Y[5] = -c2a * y * z;
+  Y[6] = c2b * (2.0 * z * z - x * x - y * y);
+  Y[7] = -c2a * x * z;
+  Y[8] = c2c * (x * x - y * y);
+  if (deg < 3) return;
+  Y[9] = -c3a * y * (3.0 * x * x - y * y);
+  Y[10] = c3b * x * y * z;
+  Y[11] = -c3c * y * (4.0 * z * z - x * x - y * y);
+  Y[12] = c3d * z * (2.0 * z * z - 3.0 * x * x - 3.0 * y * y);
+  Y[13] = -c3c * x * (4.0 * z * z - x * x - y * y);
+  Y[14] = c3e * z * (x * x - y * y);
+  Y[15] = -c3a * x * (x * x - 3.0 * y * y);
+}
+
+void ora_sh_basis(int32_t deg, int64_t n, const double* dirs, double* out) {
+  const int K = (deg + 1) * (deg + 1);
+  for (int64_t i = 0; i < n; ++i) {
+    double Y[16];
+    sh_basis(deg, dirs + 3 * i, Y);
+    for (int k = 0; k < K; ++k) out[i * K + k] = Y[k];
+  }
+}
+
+static void sh_color(int deg, const ora_cam& cam, const double* mu, const double* sh,
+                     double* rgb, bool* clamped) {
+  double C[3], v[3];
+  for (int j = 0; j < 3; ++j)
+    C[j] = -(cam.R[j] * cam.t[0] + cam.R[3 + j] * cam.t[1] + cam.R[6 + j] * cam.t[2]);
+  for (int j = 0; j < 3; ++j) v[j] = mu[j] - C[j];
+  const double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  const double d[3] = {v[0] / n, v[1] / n, v[2] / n};
+  double Y[16];
+  sh_basis(deg, d, Y);
+  const int K = (deg + 1) * (deg + 1);
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) acc += Y[k] * sh[3 * k + ch];
+    acc += 0.5;
+    clamped[ch] = acc < 0.0;
+    rgb[ch] = clamped[ch] ? 0.0 : acc;
+  }
+}
+
+// Per (view, primitive) SH colours [B*N, 3] (the records' colour input).
+void ora_sh_colors(int32_t deg, int64_t N, int32_t B, const ora_cam* cams, const double* mean,
+                   const double* sh, int64_t view_stride, double* rgb) {
+  const int K = (deg + 1) * (deg + 1);
+  for (int32_t v = 0; v < B; ++v)
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t o = (int64_t)v * N + i, pi = (int64_t)v * view_stride + i;
+      bool cl[3];
+      sh_color(deg, cams[v], mean + 3 * pi, sh + 3 * K * pi, rgb + 3 * o, cl);
+    }
+}
+
+// SH part of the chain: record colour gradients (rgrad G_CR..G_CB) ->
+// dL/dsh (linear: Y_k dc where unclamped) and the view-direction term of
+// dL/dmu, taken by central differences of sh_color in mu (h = 1e-6 |.|),
+// ADDED to g_mean. Rows of g_sh / g_mean: param rows (view_stride 0 => summed
+// over views).
+void ora_sh_chain(int32_t deg, int64_t N, int32_t B, const ora_cam* cams, const double* mean,
+                  const double* sh, int64_t view_stride, const int32_t* flag,
+                  const double* rgrad, double* g_sh, double* g_mean) {
+  const int K = (deg + 1) * (deg + 1);
+  const int64_t NP = view_stride == 0 ? N : (int64_t)B * N;
+  std::memset(g_sh, 0, sizeof(double) * 3 * K * NP);
+  for (int32_t v = 0; v < B; ++v)
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t o = (int64_t)v * N + i, pi = (int64_t)v * view_stride + i;
+      if (flag[o] != 0) continue;
+      const double* g = rgrad + o * ORA_G;
+      const double* mu = mean + 3 * pi;
+      const double* shp = sh + 3 * K * pi;
+      double rgb[3], C[3], v3[3];
+      bool cl[3];
+      sh_color(deg, cams[v], mu, shp, rgb, cl);
+      for (int j = 0; j < 3; ++j)
+        C[j] = -(cams[v].R[j] * cams[v].t[0] + cams[v].R[3 + j] * cams[v].t[1] +
+                 cams[v].R[6 + j] * cams[v].t[2]);
+      for (int j = 0; j < 3; ++j) v3[j] = mu[j] - C[j];
+      const double nn = std::sqrt(v3[0] * v3[0] + v3[1] * v3[1] + v3[2] * v3[2]);
+      const double d[3] = {v3[0] / nn, v3[1] / nn, v3[2] / nn};
+      double Y[16];
+      sh_basis(deg, d, Y);
+      for (int ch = 0; ch < 3; ++ch) {
+        if (cl[ch]) continue;
+        for (int k = 0; k < K; ++k) g_sh[(3 * K) * pi + 3 * k + ch] += Y[k] * g[G_CR + ch];
+      }
+      for (int j = 0; j < 3; ++j) {
+        double mp[3] = {mu[0], mu[1], mu[2]}, mm[3] = {mu[0], mu[1], mu[2]};
+        const double h = 1e-6 * std::max(1.0, std::fabs(mu[j]));
+        mp[j] += h;
+        mm[j] -= h;
+        double cp[3], cm[3];
+        bool t1[3], t2[3];
+        sh_color(deg, cams[v], mp, shp, cp, t1);
+        sh_color(deg, cams[v], mm, shp, cm, t2);
+        double acc = 0.0;
+        for (int ch = 0; ch < 3; ++ch) acc += (cp[ch] - cm[ch]) / (2.0 * h) * g[G_CR + ch];
+        g_mean[3 * pi + j] += acc;
+      }
+    }
 }
 
 }  // extern "C"

@@ -210,3 +210,20 @@ def test_exact_chain_matches_paper_chain_when_fz_zero(ora):
     gpp = ora.forward_backward(cp, p, dL, cams=cams)["grads"]
     for k in ("mean", "scale", "quat", "opacity", "color"):
         np.testing.assert_allclose(ge[k], gpp[k], rtol=1e-6, atol=1e-8)
+
+
+@pytest.mark.parametrize("blend", [False, True])
+def test_fd_3d_sh(ora, blend):
+    """NEXT-3 SH colour: dL/dsh and the view-direction term of
+    dL/dmu against central FD of the whole pipeline (degree 3, two views)."""
+    p = _scene3d(5, seed=11)
+    del p["color"]
+    rng = np.random.default_rng(12)
+    p["sh"] = rng.normal(0, 0.3, (5, 16, 3))
+    p["sh"][:, 0, :] = rng.uniform(0.5, 1.5, (5, 3))  # colours well above the clamp
+    cams = _cams(2, seed=4)
+    cfg = ora.Cfg(width=W, height=H, prim3d=True, alpha_blend=blend, alpha_min=0.0,
+                  dilation=0.3, T_min=1e-4 if blend else 0.0, sh_degree=3)
+    n = _fd_check(ora, cfg, p, cams=cams, groups=["sh", "mean"],
+                  min_margin=1e-3 if blend else 0.0)
+    assert n == 5 * 48 + 15
