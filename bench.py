@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-fit", action="store_true",
                     help="skip the NEXT-2 fitting-step measurement (2D configs)")
+    ap.add_argument("--sh", type=int, default=None,
+                    help="3D configs: SH colour of this degree (NEXT-3) instead of flat RGB")
     ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
                     help="3D projection: Eq. 7 as written (default) or NEXT-1 exact z-marginal")
     return ap.parse_args()
@@ -230,7 +232,8 @@ def main():
     shared = base["kind"] == "3d" or rows          # one problem shared by all ranks
     # weak scaling: every rank its own independent problem (different seed);
     # 3D batch: one scene, views sharded across ranks + gradient all_reduce.
-    c = gen.make_config(name, seed=args.seed + (0 if shared else rank))
+    over = {"sh_degree": args.sh} if (args.sh is not None and gen.CONFIGS[name]["kind"] != "2d") else {}
+    c = gen.make_config(name, seed=args.seed + (0 if shared else rank), **over)
     H, W, N, B = c["H"], c["W"], c["N"], c["B"]
     blend = c["blend"]
     cams = c["cams"]
@@ -241,6 +244,7 @@ def main():
     Bl = len(cams) if cams is not None else 1
     r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev,
                    proj=args.proj if c["kind"] != "2d" else "paper",
+                   sh_degree=c.get("sh_degree"),
                    row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0)
     params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
     if c["kind"] == "6d":
@@ -394,7 +398,8 @@ def main():
             "higher_is_better": True, "scaling": "strong" if shared else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{name}: {c['desc']}"
-                       + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else ""),
+                       + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else "")
+                       + (f" (SH degree {c['sh_degree']} colour)" if c.get("sh_degree") is not None else ""),
                        "H": H, "W": W, "N": N, "views": B,
                        "blend": blend, "dup": int(n_tot2),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",

@@ -1,5 +1,5 @@
 /* ==========================================================================
- * include/wipes.h — C ABI of the B200-native WIPES rasterizer (ABI version 1)
+ * include/wipes.h — C ABI of the B200-native WIPES rasterizer (ABI version 2)
  * ==========================================================================
  * WIPES: Wavelet-based vIsual PrimitivES, arXiv 2508.12615 (/root/reference/
  * PAPER.md). This library implements the paper's one data-parallel hot path,
@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define WIPES_ABI_VERSION 1
+#define WIPES_ABI_VERSION 2
 #define WIPES_MAX_CAMERAS_PER_LAUNCH 128 /* more views are processed in chunks */
 #define WIPES_GRAD_MOMENTS 12            /* see wipes_get_grad_moments */
 
@@ -64,6 +64,7 @@ enum { WIPES_COV2_SIGMA = 0, WIPES_COV2_CHOLESKY = 1, WIPES_COV2_RS = 2 };
  * beta = exp(-1/2 f_hat_z^2 v). Tile rects, counts and depth keys are the same
  * in both modes; EXACT adds 4 bytes per (view, primitive) to the workspace. */
 enum { WIPES_PROJ_PAPER = 0, WIPES_PROJ_EXACT = 1 };
+enum { WIPES_COLOR_RGB = 0, WIPES_COLOR_SH = 1 };
 /* tile extent: opacity-aware AABB (R7, default) / SPEC's 3-sigma square */
 enum { WIPES_EXTENT_OPACITY = 0, WIPES_EXTENT_SIGMA3 = 1 };
 
@@ -93,13 +94,22 @@ typedef struct {
   float det_min;          /* cull if det(Sigma') < det_min (1e-12)             */
   int32_t ewa_clamp;      /* 1: clamp x/z, y/z at 1.3 x half-FOV inside J      */
   float background[3];    /* ALPHA only                                        */
-  int32_t deterministic;  /* reserved (must be 0 in ABI v1)                    */
+  int32_t deterministic;  /* reserved (must be 0 in ABI v2)                    */
   /* Image-space sharding: when row_mod > 1 only tile rows ty
    * with ty % row_mod == row_rem are binned and rendered (the rest of the image
    * is left unbinned: zero in SUM mode, background in ALPHA mode, no gradient).
    * Each rank of a row_mod-way split renders its rows; summing the ranks'
    * gradients gives the full-image gradient. 0 / 0 = all rows. */
   int32_t row_mod, row_rem;
+  /* Colour (NEXT-3; "color attributes encoded by spherical
+   * harmonic coefficients", P:380 settings "aligned with 3DGS"):
+   * WIPES_COLOR_RGB reads `color` [N,3]; WIPES_COLOR_SH (3D only) evaluates
+   * c = max(0, sum_k Y_k(d) sh[k] + 0.5) per (view, primitive) with
+   * d = (mu - C_v) / |mu - C_v|, C_v = -R^T t the camera centre, real SH of
+   * degree sh_degree in 0..3 (K = (sh_degree + 1)^2 coefficients, DESIGN.md
+   * R33 for the basis and its sign convention). */
+  int32_t color_mode;     /* WIPES_COLOR_*                                     */
+  int32_t sh_degree;      /* 0..3 (WIPES_COLOR_SH)                             */
 } wipes_config;
 
 /* Primitive parameters (device). Shapes, with N primitives:
@@ -109,6 +119,8 @@ typedef struct {
  *   3D: mean [N,3], scale [N,3] (activated), quat [N,4] (w,x,y,z; normalised
  *       inside), freq [N,3] rad/world-unit.
  *   both: phase [N] rad (NULL = 0), color [N,3], opacity [N] (activated).
+ *   3D with WIPES_COLOR_SH: sh [N, K, 3] (coefficient-major, then RGB) instead
+ *       of color.
  * view_stride (3D, counted in PRIMITIVES): view v reads row v*view_stride + i;
  * 0 = one shared set for all B views (static scene), N = per-view sets
  * (6D per-frame parameters, Eq. 8). Gradients are w.r.t. these
@@ -116,12 +128,13 @@ typedef struct {
 typedef struct {
   const float *mean, *cov, *scale, *quat, *freq, *phase, *color, *opacity, *depth;
   int64_t view_stride;
+  const float* sh;
 } wipes_params;
 
 /* Gradient outputs, same shapes as wipes_params (rows [B*N] when view_stride
  * = N). Overwritten (never accumulated into). NULL = group not written. */
 typedef struct {
-  float *mean, *cov, *scale, *quat, *freq, *phase, *color, *opacity;
+  float *mean, *cov, *scale, *quat, *freq, *phase, *color, *opacity, *sh;
 } wipes_grads;
 
 /* Bytes of opaque workspace for N primitives, B views and room for

@@ -20,6 +20,7 @@ BLEND = {"sum": 0, "alpha": 1}
 COV2 = {"sigma": 0, "cholesky": 1, "rs": 2}
 PROJ = {"paper": 0, "exact": 1}
 EXTENT = {"opacity": 0, "sigma3": 1}
+COLOR = {"rgb": 0, "sh": 1}
 GRAD_MOMENTS = 12
 MAX_CAMS_PER_LAUNCH = 128
 
@@ -37,18 +38,19 @@ class wipes_config(C.Structure):
                 ("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float),
                 ("dilation", C.c_float), ("cov_eps", C.c_float), ("det_min", C.c_float),
                 ("ewa_clamp", C.c_int32), ("background", C.c_float * 3),
-                ("deterministic", C.c_int32), ("row_mod", C.c_int32), ("row_rem", C.c_int32)]
+                ("deterministic", C.c_int32), ("row_mod", C.c_int32), ("row_rem", C.c_int32),
+                ("color_mode", C.c_int32), ("sh_degree", C.c_int32)]
 
 
 class wipes_params(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("mean", "cov", "scale", "quat", "freq", "phase",
                                           "color", "opacity", "depth")] + \
-               [("view_stride", C.c_int64)]
+               [("view_stride", C.c_int64), ("sh", C.c_void_p)]
 
 
 class wipes_grads(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("mean", "cov", "scale", "quat", "freq", "phase",
-                                          "color", "opacity")]
+                                          "color", "opacity", "sh")]
 
 
 class wipes_adam_group(C.Structure):
@@ -143,13 +145,16 @@ def make_config(width, height, tile=16, prim="2d", blend="sum", cov2="sigma", pr
                 extent="opacity", alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4,
                 dilation=None, cov_eps=0.0, det_min=1e-12, ewa_clamp=True,
                 background=(0.0, 0.0, 0.0), deterministic=0, row_mod=0,
-                row_rem=0) -> wipes_config:
+                row_rem=0, sh_degree=None) -> wipes_config:
+    """sh_degree None: flat RGB `color`; 0..3: SH colour from `sh` (3D, NEXT-3)."""
     if dilation is None:
         dilation = 0.3 if prim == "3d" else 0.0
     return wipes_config(int(width), int(height), int(tile), PRIM[prim], BLEND[blend], COV2[cov2],
                         PROJ[proj], EXTENT[extent], alpha_min, alpha_max, T_min, dilation,
                         cov_eps, det_min, int(bool(ewa_clamp)), (C.c_float * 3)(*background),
-                        int(deterministic), int(row_mod), int(row_rem))
+                        int(deterministic), int(row_mod), int(row_rem),
+                        COLOR["rgb"] if sh_degree is None else COLOR["sh"],
+                        0 if sh_degree is None else int(sh_degree))
 
 
 def cameras(cams) -> "C.Array":

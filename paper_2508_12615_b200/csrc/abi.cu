@@ -43,7 +43,7 @@ const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
     "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order", "loss_l2",
-    "adam"};
+    "adam", "sh_bwd"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -70,8 +70,14 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
   if (c->proj != WIPES_PROJ_PAPER && c->proj != WIPES_PROJ_EXACT) return fail(WIPES_EINVAL, "proj");
   if (c->extent != WIPES_EXTENT_OPACITY && c->extent != WIPES_EXTENT_SIGMA3)
     return fail(WIPES_EINVAL, "extent");
+  if (c->color_mode != WIPES_COLOR_RGB && c->color_mode != WIPES_COLOR_SH)
+    return fail(WIPES_EINVAL, "color_mode");
+  if (c->color_mode == WIPES_COLOR_SH && c->prim != WIPES_PRIM_3D)
+    return fail(WIPES_EINVAL, "color_mode SH needs 3D primitives");
+  if (c->color_mode == WIPES_COLOR_SH && (c->sh_degree < 0 || c->sh_degree > 3))
+    return fail(WIPES_EINVAL, "sh_degree must be in 0..3");
   if (c->deterministic != 0)
-    return fail(WIPES_EUNSUPPORTED, "deterministic reduction is not built in ABI v1");
+    return fail(WIPES_EUNSUPPORTED, "deterministic reduction is not built in ABI v2");
   if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
     return fail(WIPES_EINVAL, "need 0 <= alpha_min < alpha_max <= 1");
   if (!(c->T_min >= 0.f) || !(c->T_min < 1.f)) return fail(WIPES_EINVAL, "T_min");
@@ -104,7 +110,8 @@ wipes_status check_params(const wipes_config* c, const wipes_params* p, int64_t 
   if (N == 0) return WIPES_OK;
   REQ(p->mean, "mean");
   REQ(p->freq, "freq");
-  REQ(p->color, "color");
+  if (c->color_mode == WIPES_COLOR_SH) REQ(p->sh, "sh");
+  else REQ(p->color, "color");
   REQ(p->opacity, "opacity");
   if (p->phase && !aligned(p->phase, 4)) return fail(WIPES_EINVAL, "phase misaligned");
   if (c->prim == WIPES_PRIM_2D) {

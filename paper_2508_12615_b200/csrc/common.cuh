@@ -74,7 +74,7 @@ struct Layout {
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
          pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
-         order = 0, rgrad = 0, rbeta = 0, total = 0;
+         order = 0, rgrad = 0, rbeta = 0, rdc = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -141,6 +141,9 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
   L.exact = c.prim == WIPES_PRIM_3D && c.proj == WIPES_PROJ_EXACT;
   L.rbeta = take(sizeof(float) * (L.exact ? L.BN : 0));
+  // SH colour: the records' colour gradients, compacted for the SH backward
+  const bool sh = c.prim == WIPES_PRIM_3D && c.color_mode == WIPES_COLOR_SH;
+  L.rdc = take(sizeof(float) * 3 * (sh ? L.BN : 0));
   L.total = o;
   return L;
 }
@@ -149,7 +152,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
 enum KernelId {
   K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
   K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
-  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_NUM
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_SH_BWD, K_NUM
 };
 
 // Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph

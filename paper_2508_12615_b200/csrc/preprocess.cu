@@ -410,21 +410,127 @@ __device__ bool exact_rec(const float* cam, int32_t W, int32_t H, int32_t ewa_cl
   return true;
 }
 
+// ------------------------------------------------- SH colour (NEXT-3) ----
+// Real SH basis up to degree 3 in the 3DGS sign convention (R33),
+// with its gradient in d (the polynomial extension; the caller projects it
+// through the normalisation d = v / |v|).
+__device__ __forceinline__ void sh_basis(int deg, double x, double y, double z, double* Y,
+                                         double (*dY)[3]) {
+  const double c0 = 0.28209479177387814, c1 = 0.4886025119029199;
+  const double c2a = 1.0925484305920792, c2b = 0.31539156525252005, c2c = 0.5462742152960396;
+  const double c3a = 0.5900435899266435, c3b = 2.890611442640554, c3c = 0.4570457994644658,
+               c3d = 0.3731763325901154, c3e = 1.445305721320277;
+  Y[0] = c0;
+  if (dY) dY[0][0] = dY[0][1] = dY[0][2] = 0.0;
+  if (deg < 1) return;
+  Y[1] = -c1 * y; Y[2] = c1 * z; Y[3] = -c1 * x;
+  if (dY) {
+    dY[1][0] = 0; dY[1][1] = -c1; dY[1][2] = 0;
+    dY[2][0] = 0; dY[2][1] = 0; dY[2][2] = c1;
+    dY[3][0] = -c1; dY[3][1] = 0; dY[3][2] = 0;
+  }
+  if (deg < 2) return;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  Y[4] = c2a * x * y;
+  Y[5] = -c2a * y * z;
+  Y[6] = c2b * (2.0 * zz - xx - yy);
+  Y[7] = -c2a * x * z;
+  Y[8] = c2c * (xx - yy);
+  if (dY) {
+    dY[4][0] = c2a * y; dY[4][1] = c2a * x; dY[4][2] = 0;
+    dY[5][0] = 0; dY[5][1] = -c2a * z; dY[5][2] = -c2a * y;
+    dY[6][0] = -2.0 * c2b * x; dY[6][1] = -2.0 * c2b * y; dY[6][2] = 4.0 * c2b * z;
+    dY[7][0] = -c2a * z; dY[7][1] = 0; dY[7][2] = -c2a * x;
+    dY[8][0] = 2.0 * c2c * x; dY[8][1] = -2.0 * c2c * y; dY[8][2] = 0;
+  }
+  if (deg < 3) return;
+  Y[9] = -c3a * y * (3.0 * xx - yy);
+  Y[10] = c3b * x * y * z;
+  Y[11] = -c3c * y * (4.0 * zz - xx - yy);
+  Y[12] = c3d * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+  Y[13] = -c3c * x * (4.0 * zz - xx - yy);
+  Y[14] = c3e * z * (xx - yy);
+  Y[15] = -c3a * x * (xx - 3.0 * yy);
+  if (dY) {
+    dY[9][0] = -6.0 * c3a * x * y; dY[9][1] = -c3a * (3.0 * xx - 3.0 * yy); dY[9][2] = 0;
+    dY[10][0] = c3b * y * z; dY[10][1] = c3b * x * z; dY[10][2] = c3b * x * y;
+    dY[11][0] = 2.0 * c3c * x * y; dY[11][1] = -c3c * (4.0 * zz - xx - 3.0 * yy);
+    dY[11][2] = -8.0 * c3c * y * z;
+    dY[12][0] = -6.0 * c3d * x * z; dY[12][1] = -6.0 * c3d * y * z;
+    dY[12][2] = c3d * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    dY[13][0] = -c3c * (4.0 * zz - 3.0 * xx - yy); dY[13][1] = 2.0 * c3c * x * y;
+    dY[13][2] = -8.0 * c3c * x * z;
+    dY[14][0] = 2.0 * c3e * x * z; dY[14][1] = -2.0 * c3e * y * z; dY[14][2] = c3e * (xx - yy);
+    dY[15][0] = -c3a * (3.0 * xx - 3.0 * yy); dY[15][1] = 6.0 * c3a * x * y; dY[15][2] = 0;
+  }
+}
+
+// sum_k w_k grad Y_k(d) without materialising the 16 x 3 Jacobian.
+template <typename T>
+__device__ __forceinline__ void sh_grad_dir(int deg, T x, T y, T z, const T* w, T* gd) {
+  const T c1 = (T) 0.4886025119029199;
+  const T c2a = (T)1.0925484305920792, c2b = (T)0.31539156525252005, c2c = (T)0.5462742152960396;
+  const T c3a = (T)0.5900435899266435, c3b = (T)2.890611442640554, c3c = (T)0.4570457994644658,
+          c3d = (T)0.3731763325901154, c3e = (T)1.445305721320277;
+  T gx = 0, gy = 0, gz = 0;
+  if (deg >= 1) {
+    gy -= c1 * w[1]; gz += c1 * w[2]; gx -= c1 * w[3];
+  }
+  if (deg >= 2) {
+    gx += c2a * y * w[4]; gy += c2a * x * w[4];
+    gy -= c2a * z * w[5]; gz -= c2a * y * w[5];
+    gx -= (T)2 * c2b * x * w[6]; gy -= (T)2 * c2b * y * w[6]; gz += (T)4 * c2b * z * w[6];
+    gx -= c2a * z * w[7]; gz -= c2a * x * w[7];
+    gx += (T)2 * c2c * x * w[8]; gy -= (T)2 * c2c * y * w[8];
+  }
+  if (deg >= 3) {
+    const T xx = x * x, yy = y * y, zz = z * z;
+    gx -= (T)6 * c3a * x * y * w[9]; gy -= c3a * ((T)3 * xx - (T)3 * yy) * w[9];
+    gx += c3b * y * z * w[10]; gy += c3b * x * z * w[10]; gz += c3b * x * y * w[10];
+    gx += (T)2 * c3c * x * y * w[11]; gy -= c3c * ((T)4 * zz - xx - (T)3 * yy) * w[11];
+    gz -= (T)8 * c3c * y * z * w[11];
+    gx -= (T)6 * c3d * x * z * w[12]; gy -= (T)6 * c3d * y * z * w[12];
+    gz += c3d * ((T)6 * zz - (T)3 * xx - (T)3 * yy) * w[12];
+    gx -= c3c * ((T)4 * zz - (T)3 * xx - yy) * w[13]; gy += (T)2 * c3c * x * y * w[13];
+    gz -= (T)8 * c3c * x * z * w[13];
+    gx += (T)2 * c3e * x * z * w[14]; gy -= (T)2 * c3e * y * z * w[14]; gz += c3e * (xx - yy) * w[14];
+    gx -= c3a * ((T)3 * xx - (T)3 * yy) * w[15]; gy += (T)6 * c3a * x * y * w[15];
+  }
+  gd[0] = gx; gd[1] = gy; gd[2] = gz;
+}
+
+// Unit view direction d = (mu - C) / |mu - C|, C = -R^T t; returns |mu - C|.
+__device__ __forceinline__ double view_dir(const float* cam, const double* mu, double* d) {
+  double v[3];
+  for (int j = 0; j < 3; ++j) {
+    const double Cj = -((double)cam[j] * cam[9] + (double)cam[3 + j] * cam[10] +
+                        (double)cam[6 + j] * cam[11]);
+    v[j] = mu[j] - Cj;
+  }
+  const double n = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  for (int j = 0; j < 3; ++j) d[j] = v[j] / n;
+  return n;
+}
+
 struct Pre3DArgs {
   Cfg2 c;
   int32_t ewa_clamp, exact;
+  int32_t sh_deg;   // -1: flat RGB `color`; 0..3: SH colour from `sh`
   int64_t N, view_stride;
-  const float *mean, *scale, *quat, *freq, *phase, *color, *opacity;
+  const float *mean, *scale, *quat, *freq, *phase, *color, *opacity, *sh;
   PreOut o;
   CamBlock cams;
 };
 
-template <bool EXACT>
-__global__ void __launch_bounds__(128, EXACT ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
+template <bool EXACT, bool SH>
+__global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)a.cams.nv * a.N) return;
-  int vl = (int)(gid / a.N);
-  int64_t i = gid - (int64_t)vl * a.N;
+  // SH with shared parameters: view-minor order, so a primitive's
+  // coefficients (48 floats) are read once from HBM for all its views
+  const bool vminor = SH && a.view_stride == 0;
+  int vl = vminor ? (int)(gid % a.cams.nv) : (int)(gid / a.N);
+  int64_t i = vminor ? gid / a.cams.nv : gid - (int64_t)vl * a.N;
   int v = a.cams.v0 + vl;
   int64_t o = (int64_t)v * a.N + i;
   int64_t pi = (int64_t)v * a.view_stride + i;
@@ -435,7 +541,8 @@ __global__ void __launch_bounds__(128, EXACT ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d
   double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
   double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
   double phi = a.phase ? (double)a.phase[pi] : 0.0;
-  double cr = a.color[3 * pi], cg = a.color[3 * pi + 1], cb = a.color[3 * pi + 2];
+  double cr = 0.0, cg = 0.0, cb = 0.0;
+  if (!SH) { cr = a.color[3 * pi]; cg = a.color[3 * pi + 1]; cb = a.color[3 * pi + 2]; }
   double al = a.opacity[pi];
   int4 rect = make_int4(0, 0, 0, 0);
   int32_t cnt = 0;
@@ -447,6 +554,18 @@ __global__ void __launch_bounds__(128, EXACT ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d
   bool ok = fin(mu[0]) && fin(mu[1]) && fin(mu[2]) && fin(s[0]) && fin(s[1]) && fin(s[2]) &&
             fin(q[0]) && fin(q[1]) && fin(q[2]) && fin(q[3]) && fin(f[0]) && fin(f[1]) &&
             fin(f[2]) && fin(phi) && fin(al) && fin(cr) && fin(cg) && fin(cb) && (qq > 0.0);
+  if (SH && ok) {  // NEXT-3: view-dependent colour from SH
+    double d[3], Y[16];
+    view_dir(cam, mu, d);
+    sh_basis(a.sh_deg, d[0], d[1], d[2], Y, nullptr);
+    const int K = (a.sh_deg + 1) * (a.sh_deg + 1);
+    const float* shp = a.sh + (int64_t)3 * K * pi;
+    double rgb[3] = {0.5, 0.5, 0.5};
+    for (int k = 0; k < K; ++k)
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * (double)shp[3 * k + ch];
+    cr = fmax(rgb[0], 0.0); cg = fmax(rgb[1], 0.0); cb = fmax(rgb[2], 0.0);
+    ok = fin(rgb[0]) && fin(rgb[1]) && fin(rgb[2]);
+  }
   if (!ok) {
     flag = 5;
   } else {
@@ -604,6 +723,8 @@ struct Bwd3DArgs {
   const uint8_t* flag;
   const float* mom;
   const float* mom_beta;  // exact mode only
+  const float* sh;        // SH colour mode only
+  float* dc;              // SH: [B*N, 3] record colour gradients (k_pre3d_bwd -> k_sh_bwd)
   wipes_grads g;
   CamBlock cams;  // views [v0, v0 + nv) of this launch
 };
@@ -674,6 +795,10 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
     }
     double g[kRecGrads];
     moments_to_grads(a.mom + kMoments * o, A, fpx, fpy, hb, a.opacity[pi], g);
+    if (a.dc) {
+      a.dc[3 * o] = (float)g[RG_CR]; a.dc[3 * o + 1] = (float)g[RG_CG];
+      a.dc[3 * o + 2] = (float)g[RG_CB];
+    }
     gphi += g[RG_PHI];
     gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
     gal += g[RG_ALPHA];
@@ -816,6 +941,10 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd_exact(const __grid_constant__
     const double A[3] = {r8[2], r8[3], r8[4]};
     double g[kRecGrads];
     moments_to_grads(a.mom + kMoments * o, A, r8[5], r8[6], 0.5 * r8[7], a.opacity[pi], g);
+    if (a.dc) {
+      a.dc[3 * o] = (float)g[RG_CR]; a.dc[3 * o + 1] = (float)g[RG_CG];
+      a.dc[3 * o + 2] = (float)g[RG_CB];
+    }
     gphi += g[RG_PHI];
     gcol[0] += g[RG_CR]; gcol[1] += g[RG_CG]; gcol[2] += g[RG_CB];
     gal += g[RG_ALPHA];
@@ -840,6 +969,104 @@ __global__ void __launch_bounds__(128) k_pre3d_bwd_exact(const __grid_constant__
   if (a.g.phase) put(&a.g.phase[pi], gphi);
   if (a.g.color) for (int k = 0; k < 3; ++k) put(&a.g.color[3 * pi + k], gcol[k]);
   if (a.g.opacity) put(&a.g.opacity[pi], gal);
+}
+
+// NEXT-3 backward of the SH colour: the record colour gradient dc = (M9, M10,
+// M11) of each (view, primitive) gives dL/dsh_k = Y_k(d) dc (zero for a
+// clamped channel) and, through the view direction d = (mu - C)/|mu - C|,
+// dL/dmu += (I - d d^T)/|mu - C| sum_k (sh_k . dc) grad Y_k(d), ADDED to the
+// mean gradient written by k_pre3d_bwd just before on the same stream.
+#ifndef WIPES_SH_MINB
+#define WIPES_SH_MINB 4
+#endif
+// GV lanes share one parameter row (lane l takes views l, l + GV, ...) and
+// their partial sums are combined with xor shuffles in a fixed order.
+template <int DEG, int GV>
+__global__ void __launch_bounds__(128, WIPES_SH_MINB) k_sh_bwd(const __grid_constant__ Bwd3DArgs a) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / GV;
+  const int gl = (int)(gid % GV);
+  const bool active = row < a.nrows;  // whole groups only: no early return (shuffles)
+  int v_lo = 0, v_hi = 0;
+  int64_t i = 0, pi = 0;
+  if (active) {
+    if (a.view_stride == 0) { v_lo = a.cams.v0; v_hi = a.cams.v0 + a.cams.nv; i = row; pi = row; }
+    else {
+      int vl = (int)(row / a.N);
+      v_lo = a.cams.v0 + vl; v_hi = v_lo + 1; i = row - (int64_t)vl * a.N;
+      pi = (int64_t)v_lo * a.view_stride + i;
+    }
+  }
+  double mu[3] = {0, 0, 0};
+  if (active) { mu[0] = a.mean[3 * pi]; mu[1] = a.mean[3 * pi + 1]; mu[2] = a.mean[3 * pi + 2]; }
+  const float* sh = a.sh + (int64_t)3 * K * pi;  // re-read per view (L1-resident)
+  float gsh[3 * K];
+#pragma unroll
+  for (int k = 0; k < 3 * K; ++k) gsh[k] = 0.f;
+  double gmu[3] = {0, 0, 0};
+  for (int v = v_lo + gl; v < v_hi; v += GV) {
+    const int64_t o = (int64_t)v * a.N + i;
+    if (a.flag[o] != 0) continue;
+    const float* cam = a.cams.v[v - a.cams.v0];
+    double d[3], Y[16];
+    const double n = view_dir(cam, mu, d);
+    sh_basis(DEG, d[0], d[1], d[2], Y, nullptr);
+    double dc[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      double c = 0.5;
+#pragma unroll
+      for (int k = 0; k < K; ++k) c += Y[k] * (double)sh[3 * k + ch];
+      dc[ch] = c < 0.0 ? 0.0 : (double)a.dc[3 * o + ch];
+    }
+    // gradient path in FP32 (the clamp decision above is the forward's FP64 one)
+    const float dcf[3] = {(float)dc[0], (float)dc[1], (float)dc[2]};
+    float w[16];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k] = sh[3 * k] * dcf[0] + sh[3 * k + 1] * dcf[1] + sh[3 * k + 2] * dcf[2];
+      const float yk = (float)Y[k];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) gsh[3 * k + ch] += yk * dcf[ch];
+    }
+    float gdf[3];
+    sh_grad_dir<float>(DEG, (float)d[0], (float)d[1], (float)d[2], w, gdf);
+    const double gd[3] = {gdf[0], gdf[1], gdf[2]};
+    const double dd = d[0] * gd[0] + d[1] * gd[1] + d[2] * gd[2];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) gmu[j] += (gd[j] - d[j] * dd) / n;
+  }
+  if (GV > 1) {
+#pragma unroll
+    for (int off = 1; off < GV; off <<= 1) {
+#pragma unroll
+      for (int k = 0; k < 3 * K; ++k) gsh[k] += __shfl_xor_sync(0xffffffffu, gsh[k], off);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) gmu[j] += __shfl_xor_sync(0xffffffffu, gmu[j], off);
+    }
+  }
+  if (!active || gl != 0) return;
+  if (a.g.sh) {
+    float* dst = a.g.sh + (int64_t)3 * K * pi;
+#pragma unroll
+    for (int k = 0; k < 3 * K; ++k) dst[k] = a.accumulate ? dst[k] + gsh[k] : gsh[k];
+  }
+  if (a.g.mean)
+    for (int j = 0; j < 3; ++j) a.g.mean[3 * pi + j] += (float)gmu[j];
+}
+
+template <int DEG>
+void launch_sh_bwd(const Bwd3DArgs& a, int views_per_row, cudaStream_t s) {
+  auto go = [&](auto k, int gv) {
+    const int64_t threads = a.nrows * gv;
+    k<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(a);
+  };
+  if (views_per_row >= 16) go(k_sh_bwd<DEG, 16>, 16);
+  else if (views_per_row >= 8) go(k_sh_bwd<DEG, 8>, 8);
+  else if (views_per_row >= 4) go(k_sh_bwd<DEG, 4>, 4);
+  else if (views_per_row >= 2) go(k_sh_bwd<DEG, 2>, 2);
+  else go(k_sh_bwd<DEG, 1>, 1);
 }
 
 Cfg2 make_cfg2(const wipes_config& c, const Layout& L) {
@@ -901,6 +1128,8 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
   a.c = make_cfg2(c, L);
   a.ewa_clamp = c.ewa_clamp;
   a.exact = L.exact;
+  a.sh_deg = c.color_mode == WIPES_COLOR_SH ? c.sh_degree : -1;
+  a.sh = p.sh;
   a.N = L.N;
   a.view_stride = p.view_stride;
   a.mean = p.mean; a.scale = p.scale; a.quat = p.quat; a.freq = p.freq; a.phase = p.phase;
@@ -911,10 +1140,11 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
     fill_cams(a.cams, cams, v0, nv);
     int64_t n = (int64_t)nv * L.N;
     launch_begin(K_PRE3D, s);
-    if (a.exact)
-      k_pre3d<true><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+    const unsigned gr = (unsigned)((n + 127) / 128);
+    if (a.sh_deg >= 0)
+      (a.exact ? k_pre3d<true, true> : k_pre3d<false, true>)<<<gr, 128, 0, s>>>(a);
     else
-      k_pre3d<false><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a);
+      (a.exact ? k_pre3d<true, false> : k_pre3d<false, false>)<<<gr, 128, 0, s>>>(a);
     launch_end(K_PRE3D, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -956,7 +1186,11 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
   a.flag = (const uint8_t*)(ws + L.flag);
   a.mom = (const float*)(ws + L.rgrad);
   a.mom_beta = L.exact ? (const float*)(ws + L.rbeta) : nullptr;
+  a.sh = p.sh;
   a.g = g;
+  const bool use_sh = c.color_mode == WIPES_COLOR_SH;
+  a.dc = use_sh ? (float*)(ws + L.rdc) : nullptr;
+  if (use_sh) a.g.color = nullptr;  // the record colour is not a parameter in SH mode
   for (int v0 = 0; v0 < L.B; v0 += WIPES_MAX_CAMERAS_PER_LAUNCH) {
     int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;
     fill_cams(a.cams, cams, v0, nv);
@@ -971,6 +1205,17 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
     else
       k_pre3d_bwd<false><<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
     launch_end(K_PRE3D_BWD, s);
+    if (use_sh) {
+      launch_begin(K_SH_BWD, s);
+      const int vpr = p.view_stride == 0 ? nv : 1;  // views summed per parameter row
+      switch (c.sh_degree) {
+        case 0: launch_sh_bwd<0>(a, vpr, s); break;
+        case 1: launch_sh_bwd<1>(a, vpr, s); break;
+        case 2: launch_sh_bwd<2>(a, vpr, s); break;
+        default: launch_sh_bwd<3>(a, vpr, s); break;
+      }
+      launch_end(K_SH_BWD, s);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -107,7 +107,7 @@ def ring_cameras(B, W, H, radius=3.0, height=0.5, focal_frac=0.9, phase0=0.0):
 
 
 def gen3d(N: int, seed: int = 0, scale_med: float = 0.004, scale_mult: float = 1.0,
-          inner_frac: float = 0.7, phase: bool = False) -> dict:
+          inner_frac: float = 0.7, phase: bool = False, sh_degree=None) -> dict:
     """Mip-NeRF360-like synthetic scene: 70% of centres
     volume-uniform in a ball r in [0.2, 1], 30% on a shell r in [8, 20];
     per-axis scale scale_med*exp(N(0, 0.7^2)) (shell scaled by r/3);
@@ -132,16 +132,26 @@ def gen3d(N: int, seed: int = 0, scale_med: float = 0.004, scale_mult: float = 1
     out = dict(mean=mean, scale=scale, quat=quat, freq=freq, color=color, opacity=op)
     if phase:
         out["phase"] = g.uniform(-math.pi, math.pi, N)
+    if sh_degree is not None:
+        # NEXT-3 colour coefficients [N, (deg+1)^2, 3]: DC term U(-1.5, 1.5),
+        # band l >= 1 ~ N(0, (0.25 / l)^2) (a 3DGS-like spectrum; no SH arithmetic here)
+        K = (sh_degree + 1) ** 2
+        sh = np.empty((N, K, 3))
+        sh[:, 0, :] = g.uniform(-1.5, 1.5, (N, 3))
+        for l in range(1, sh_degree + 1):
+            sh[:, l * l:(l + 1) * (l + 1), :] = g.normal(0, 0.25 / l, (N, 2 * l + 1, 3))
+        out["sh"] = sh
+        del out["color"]
     return {k: np.ascontiguousarray(v.astype(F32)) for k, v in out.items()}
 
 
 def gen6d(N: int, frames: int, seed: int = 0, scale_med: float = 0.006,
-          scale_mult: float = 1.0) -> dict:
+          scale_mult: float = 1.0, sh_degree=None) -> dict:
     """Per-frame ('time-conditioned') parameters: a stand-in for the deformation
     field F_theta of Eq. 8 — the MLP itself is out of scope:
     mu_t = mu + 0.02 sin(2 pi t/T + psi) v, f_t = f (1 + 0.1 sin(.)),
     s_t = s exp(0.05 sin(.)). Returned arrays are [frames*N, k] (view_stride = N)."""
-    base = gen3d(N, seed, scale_med=scale_med, scale_mult=scale_mult)
+    base = gen3d(N, seed, scale_med=scale_med, scale_mult=scale_mult, sh_degree=sh_degree)
     g = _rng(seed + 7919)
     psi = g.uniform(0, 2 * math.pi, N)
     vdir = g.normal(size=(N, 3))
@@ -151,8 +161,9 @@ def gen6d(N: int, frames: int, seed: int = 0, scale_med: float = 0.006,
         out["mean"].append(base["mean"].astype(np.float64) + 0.02 * s[:, None] * vdir)
         out["freq"].append(base["freq"].astype(np.float64) * (1 + 0.1 * s)[:, None])
         out["scale"].append(base["scale"].astype(np.float64) * np.exp(0.05 * s)[:, None])
-        for k in ("quat", "color", "opacity"):
-            out[k].append(base[k])
+        for k in ("quat", "color", "opacity", "sh"):
+            if k in base:
+                out[k].append(base[k])
     return {k: np.ascontiguousarray(np.concatenate(v, 0).astype(F32)) for k, v in out.items()}
 
 
@@ -273,9 +284,9 @@ def make_config(name: str, seed: int = 0, **over) -> dict:
         return dict(c, B=1, params=p, cams=None, view_stride=0)
     B = c["B"]
     if kind == "3d":
-        p = gen3d(N, seed, scale_mult=c.get("scale_mult", 1.0))
+        p = gen3d(N, seed, scale_mult=c.get("scale_mult", 1.0), sh_degree=c.get("sh_degree"))
         cams = ring_cameras(B, W, H)
         return dict(c, params=p, cams=cams, view_stride=0)
-    p = gen6d(N, B, seed, scale_mult=c.get("scale_mult", 1.0))
+    p = gen6d(N, B, seed, scale_mult=c.get("scale_mult", 1.0), sh_degree=c.get("sh_degree"))
     cams = arc_cameras(B, W, H)
     return dict(c, params=p, cams=cams, view_stride=N)

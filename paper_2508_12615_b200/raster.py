@@ -23,8 +23,8 @@ import torch
 from . import abi
 
 PARAM_KEYS_2D = ("mean", "cov", "freq", "phase", "color", "opacity", "depth")
-PARAM_KEYS_3D = ("mean", "scale", "quat", "freq", "phase", "color", "opacity")
-GRAD_KEYS = ("mean", "cov", "scale", "quat", "freq", "phase", "color", "opacity")
+PARAM_KEYS_3D = ("mean", "scale", "quat", "freq", "phase", "color", "opacity", "sh")
+GRAD_KEYS = ("mean", "cov", "scale", "quat", "freq", "phase", "color", "opacity", "sh")
 
 
 def _stream() -> int:

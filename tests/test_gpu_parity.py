@@ -212,6 +212,43 @@ def test_exact_projection_parity(ora, name, blend):
         assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
 
 
+@pytest.mark.parametrize("name,blend,deg", [("p3d", "alpha", 3), ("p3d", "sum", 2),
+                                             ("p6d", "alpha", 3), ("p3d", "alpha", 0)])
+def test_sh_colour_parity(ora, name, blend, deg):
+    """NEXT-3 SH colour: per-(view, primitive) colour from
+    degree-`deg` SH in the FP64 preprocess; dL/dsh and the view-direction term
+    of dL/dmu in k_sh_bwd, against the oracle (pinned by orthonormality and
+    whole-pipeline FD, tests/test_oracle_sh.py)."""
+    c = gen.make_config(name, seed=0, sh_degree=deg)
+    H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+    p, cams, vs = c["params"], c["cams"], c["view_stride"]
+    assert "sh" in p and "color" not in p
+    cfg_o = oracle_cfg(ora, "3d", H, W, blend, use_rect=True, sh_degree=deg)
+    pr = ora.project3d(cfg_o, p, cams, view_stride=vs)
+    r = gpu_rasterizer("3d", H, W, blend, sh_degree=deg)
+    r.preprocess(to_dev(p), cams, view_stride=vs)
+    r.bin_sort()
+    img, T, nc = r.render()
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    rec = _np(r.get_preprocess()["records"]).reshape(B * N, 16)
+    live = pr.flag == 0
+    col_o = np.stack([pr.field("cr"), pr.field("cg"), pr.field("cb")], 1)
+    np.testing.assert_allclose(rec[live, 12:15], col_o[live], rtol=1e-6, atol=1e-7)
+    dL = gen.gen_dLdC(B, H, W, seed=4)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    nbad, namb = pixel_violations(_pixels(_np(img)), ro["color"], ro["margin"])
+    assert nbad == 0, (nbad, namb)
+    grads = r.backward(torch.from_numpy(dL).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain3d(cfg_o, p, cams, pr, ro["rgrad"], view_stride=vs)
+    assert "color" not in og and og["sh"].shape == p["sh"].shape
+    for k in ("mean", "scale", "quat", "freq", "opacity", "sh"):
+        nbad, worst = grad_violations(_np(grads[k]), og[k])
+        frac = nbad / og[k].size
+        assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
+
+
 _EXACT_GRADS = """
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
