@@ -285,6 +285,33 @@ wipes_status wipes_activate(const wipes_adam_group* groups, int32_t n_groups, vo
  * wipes_preprocess when the intersections exceed dup_capacity). */
 const int32_t* wipes_overflow_flag(const void* ws);
 
+/* ---- NEXT-4: tcgen05 bf16 GEMM (building block of the deformation MLP) ----
+ * D[M x N] = sum_k A(m, k) B(n, k) with bf16 operands and fp32 accumulation on
+ * the 5th-generation tensor cores (tcgen05.mma, accumulator in TMEM), followed
+ * by a fused epilogue. Operand layouts (device, bf16): A K-major: (m, k) at
+ * A[m * lda + k]; A MN-major: (m, k) at A[k * lda + m]; B likewise with n.
+ * Requirements: K, lda, ldb multiples of 8; pointers 16-byte aligned; N <= 256
+ * per launch tile (larger N is tiled). split_k > 1 splits K over CTAs (only
+ * with WIPES_GEMM_EPI_ATOMIC_F32). */
+enum {
+  WIPES_GEMM_EPI_STORE_F32 = 0,      /* C (f32) = D                           */
+  WIPES_GEMM_EPI_BIAS_F32 = 1,       /* C (f32) = D + bias[n]                 */
+  WIPES_GEMM_EPI_BIAS_RELU_BF16 = 2, /* C (bf16) = relu(D + bias[n])          */
+  WIPES_GEMM_EPI_MASK_BF16 = 3,      /* C (bf16) = D * (mask(m, n) > 0)       */
+  WIPES_GEMM_EPI_ATOMIC_F32 = 4      /* C (f32) += D (atomic)                 */
+};
+typedef struct {
+  const void* A;
+  const void* B;
+  void* C;
+  const float* bias;  /* [N] f32 (BIAS epilogues)                              */
+  const void* mask;   /* bf16, (m, n) at mask[m * ldm + n] (MASK epilogue)      */
+  int64_t M, N, K;
+  int64_t lda, ldb, ldc, ldm;
+  int32_t a_mn_major, b_mn_major, epilogue, split_k;
+} wipes_gemm_args;
+wipes_status wipes_gemm_bf16(const wipes_gemm_args* args, void* stream);
+
 /* Instrumentation: per-kernel CUDA-event timing (process-global, not for use
  * during graph capture) and a launch counter. */
 int          wipes_num_kernels(void);

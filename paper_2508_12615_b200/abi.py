@@ -59,6 +59,17 @@ class wipes_adam_group(C.Structure):
                 ("activation", C.c_int32)]
 
 
+class wipes_gemm_args(C.Structure):
+    _fields_ = [("A", C.c_void_p), ("B", C.c_void_p), ("C", C.c_void_p), ("bias", C.c_void_p),
+                ("mask", C.c_void_p), ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+                ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64), ("ldm", C.c_int64),
+                ("a_mn_major", C.c_int32), ("b_mn_major", C.c_int32), ("epilogue", C.c_int32),
+                ("split_k", C.c_int32)]
+
+
+GEMM_EPI = {"store_f32": 0, "bias_f32": 1, "bias_relu_bf16": 2, "mask_bf16": 3,
+            "atomic_f32": 4}
+
 ACT = {"none": 0, "sigmoid": 1}
 MAX_ADAM_GROUPS = 8
 
@@ -103,6 +114,8 @@ def lib():
     L.wipes_activate.argtypes = [P(wipes_adam_group), i32, vp]
     L.wipes_overflow_flag.argtypes = [vp]
     L.wipes_overflow_flag.restype = vp
+    L.wipes_gemm_bf16.argtypes = [P(wipes_gemm_args), vp]
+    L.wipes_gemm_bf16.restype = C.c_int
     L.wipes_num_kernels.restype = C.c_int
     L.wipes_kernel_name.argtypes = [C.c_int]
     L.wipes_kernel_name.restype = C.c_char_p
@@ -126,7 +139,7 @@ EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
             "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
             "wipes_render_bwd", "wipes_get_grad_moments", "wipes_render_stats",
             "wipes_train_scratch_bytes", "wipes_loss_l2", "wipes_adam_step", "wipes_activate",
-            "wipes_overflow_flag", "wipes_num_kernels",
+            "wipes_overflow_flag", "wipes_gemm_bf16", "wipes_num_kernels",
             "wipes_kernel_name", "wipes_timing_enable", "wipes_timing_collect",
             "wipes_launch_count", "wipes_status_string", "wipes_last_error",
             "wipes_abi_version"]
@@ -264,6 +277,18 @@ def wipes_activate(groups, n_groups, stream):
 
 def wipes_overflow_flag(ws) -> int:
     return int(lib().wipes_overflow_flag(ws) or 0)
+
+
+def wipes_gemm_bf16(args, stream):
+    return lib().wipes_gemm_bf16(C.byref(args), stream)
+
+
+def gemm(A, B, C, M, N, K, lda, ldb, ldc, epilogue="store_f32", a_mn=False, b_mn=False,
+         bias=None, mask=None, ldm=0, split_k=1, stream=None):
+    """Marshal a wipes_gemm_args from torch tensors / ints and launch."""
+    g = wipes_gemm_args(ptr(A), ptr(B), ptr(C), ptr(bias), ptr(mask), M, N, K, lda, ldb, ldc,
+                        ldm, int(a_mn), int(b_mn), GEMM_EPI[epilogue], split_k)
+    check(wipes_gemm_bf16(g, stream), "wipes_gemm_bf16")
 
 
 def kernel_names():

@@ -26,6 +26,7 @@ SOURCES = {
     "sort.cu": [],
     "render.cu": [],
     "train.cu": [],
+    "gemm.cu": [],
     "abi.cu": [],
 }
 

@@ -43,7 +43,7 @@ const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
     "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order", "loss_l2",
-    "adam", "sh_bwd"};
+    "adam", "sh_bwd", "gemm_tc"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -393,6 +393,25 @@ wipes_status wipes_activate(const wipes_adam_group* groups, int32_t n_groups, vo
 
 const int32_t* wipes_overflow_flag(const void* ws) {
   return ws ? &((const WsHeader*)ws)->overflow : nullptr;
+}
+
+wipes_status wipes_gemm_bf16(const wipes_gemm_args* g, void* stream) {
+  if (!g) return fail(WIPES_EINVAL, "args is NULL");
+  if (g->M < 0 || g->N < 0 || g->K < 0) return fail(WIPES_EINVAL, "negative size");
+  if (g->M == 0 || g->N == 0) return WIPES_OK;
+  if (!g->A || !g->B || !g->C) return fail(WIPES_EINVAL, "A, B and C must be non-NULL");
+  if (!aligned(g->A, 16) || !aligned(g->B, 16)) return fail(WIPES_EINVAL, "A/B not 16-byte aligned");
+  if (g->K % 8 || g->lda % 8 || g->ldb % 8) return fail(WIPES_EINVAL, "K, lda, ldb must be multiples of 8");
+  if (g->epilogue < WIPES_GEMM_EPI_STORE_F32 || g->epilogue > WIPES_GEMM_EPI_ATOMIC_F32)
+    return fail(WIPES_EINVAL, "epilogue");
+  if ((g->epilogue == WIPES_GEMM_EPI_BIAS_F32 || g->epilogue == WIPES_GEMM_EPI_BIAS_RELU_BF16) &&
+      !g->bias)
+    return fail(WIPES_EINVAL, "bias is NULL");
+  if (g->epilogue == WIPES_GEMM_EPI_MASK_BF16 && !g->mask) return fail(WIPES_EINVAL, "mask is NULL");
+  if (g->split_k > 1 && g->epilogue != WIPES_GEMM_EPI_ATOMIC_F32)
+    return fail(WIPES_EINVAL, "split_k > 1 needs the atomic epilogue");
+  cudaError_t e = launch_gemm(*g, (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "gemm launch");
 }
 
 int wipes_num_kernels(void) { return K_NUM; }
