@@ -312,6 +312,46 @@ typedef struct {
 } wipes_gemm_args;
 wipes_status wipes_gemm_bf16(const wipes_gemm_args* args, void* stream);
 
+/* ---- NEXT-4: the time-conditioned deformation field (Eq. 8;
+ * network of D-3DGS, Eq. 5; R34-R36) ----------------------
+ * (dx, dq, ds, df) = F_theta(gamma(x), gamma(t)): positional encoding
+ * gamma_L(p) = [p, sin(2^k p), cos(2^k p)]_(k<L) of the canonical centre x (Lx)
+ * and the frame time t (Lt); `depth` ReLU layers of `width`, the input
+ * re-concatenated after layer `skip` ([gamma, h]); a 13-output linear head.
+ * Per-frame parameters: mu_t = mu + dx, q_t = q + dq, s_t = s exp(ds),
+ * f_t = f + df (x enters through a stop-gradient). Every layer is a tcgen05
+ * GEMM (bf16 operands rounded to nearest even, fp32 accumulation) with a fused
+ * bias + ReLU epilogue; theta stays fp32 (flat layout: W_l [width, K_l]
+ * row-major then b_l [width] for each layer, then W_h [13, width], b_h [13];
+ * K_0 = E = 3(1+2Lx) + 1+2Lt, K_(skip+1) = E + width, else width). */
+typedef struct {
+  int32_t width;   /* multiple of 16, 16..256 (D-3DGS: 256) */
+  int32_t depth;   /* >= 1 (D-3DGS: 8)                      */
+  int32_t skip;    /* -1 (none) or 0..depth-2 (D-3DGS: 4)    */
+  int32_t Lx, Lt;  /* encoding frequencies (D-3DGS: 10, 6)   */
+} wipes_mlp_config;
+
+size_t wipes_mlp_param_count(const wipes_mlp_config* cfg);
+/* Workspace for F*N rows; the forward keeps its activations there for the
+ * backward of the same rows. */
+size_t wipes_mlp_workspace_bytes(const wipes_mlp_config* cfg, int64_t rows);
+/* Frame f, primitive i -> row f*N + i. times: (host) [F]. canon: mean, quat,
+ * scale, freq [N] (+ phase, color, opacity, sh copied to the frame rows when
+ * both canon and frame pointers are non-NULL); frame: the same groups, [F*N]
+ * rows (device, caller-owned), ready for the rasterizer with view_stride = N. */
+wipes_status wipes_mlp_forward(const wipes_mlp_config* cfg, const float* theta, int64_t N,
+                               int32_t F, const float* times, const wipes_params* canon,
+                               const wipes_params* frame, int32_t sh_coeffs, void* ws,
+                               size_t ws_bytes, void* stream);
+/* From g_frame (gradients w.r.t. the frame rows' mean, quat, scale, freq) of
+ * the last wipes_mlp_forward on this workspace: g_theta [param_count] (fp32,
+ * overwritten) and g_canon mean/quat/scale/freq [N] (overwritten; mean is the
+ * frame sum: stop-gradient into the network). */
+wipes_status wipes_mlp_backward(const wipes_mlp_config* cfg, const float* theta, int64_t N,
+                                int32_t F, const wipes_params* canon, const wipes_grads* g_frame,
+                                float* g_theta, const wipes_grads* g_canon, void* ws,
+                                size_t ws_bytes, void* stream);
+
 /* Instrumentation: per-kernel CUDA-event timing (process-global, not for use
  * during graph capture) and a launch counter. */
 int          wipes_num_kernels(void);

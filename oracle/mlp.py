@@ -38,7 +38,7 @@ def layer_in(c, l) -> int:
     E, W = embed_dim(c), c["width"]
     if l == 0:
         return E
-    return E + W if l == c["skip"] + 1 else W
+    return E + W if (c["skip"] >= 0 and l == c["skip"] + 1) else W
 
 
 def layout(c):
@@ -79,16 +79,28 @@ def embed(c, x, t):
     return np.concatenate([posenc(x, c["Lx"]), posenc(t, c["Lt"])], 1)
 
 
-def forward(c, theta, x, t):
-    """Network outputs [M, 13] and the cache for backward."""
+def round_bf16(x):
+    """Round to the nearest bfloat16 (ties to even), returned as float64: the
+    operand precision of the tensor-core kernel (R36)."""
+    b = np.ascontiguousarray(np.asarray(x, np.float64).astype(np.float32)).view(np.uint32)
+    b = (b + np.uint32(0x7FFF) + ((b >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return b.view(np.float32).astype(np.float64)
+
+
+def forward(c, theta, x, t, quantize=False):
+    """Network outputs [M, 13] and the cache for backward. quantize=True takes
+    the kernel's precision decisions (R36): the encoding and every layer's
+    activations are rounded to bf16 (so the ReLU masks are decided on the same
+    bf16 operands as on the GPU); arithmetic stays FP64."""
     P = unpack(c, theta)
-    e = embed(c, x, t)
+    q = round_bf16 if quantize else (lambda a: a)
+    e = q(embed(c, x, t))
     h = e
     ins, hs = [], []
     for l in range(c["depth"]):
-        inp = h if l != c["skip"] + 1 else np.concatenate([e, h], 1)
+        inp = np.concatenate([e, h], 1) if (c["skip"] >= 0 and l == c["skip"] + 1) else h
         ins.append(inp)
-        h = np.maximum(inp @ P[f"W{l}"].T + P[f"b{l}"], 0.0)
+        h = q(np.maximum(inp @ P[f"W{l}"].T + P[f"b{l}"], 0.0))
         hs.append(h)
     out = h @ P["Wh"].T + P["bh"]
     return out, dict(e=e, ins=ins, hs=hs)
@@ -110,7 +122,7 @@ def backward(c, theta, cache, dout):
         if l == 0:
             break
         din = dz @ P[f"W{l}"]
-        dh = din[:, embed_dim(c):] if l == c["skip"] + 1 else din
+        dh = din[:, embed_dim(c):] if (c["skip"] >= 0 and l == c["skip"] + 1) else din
     flat = np.zeros(param_count(c))
     for n, s, o in layout(c):
         flat[o:o + int(np.prod(s))] = g[n].reshape(-1)
@@ -126,13 +138,13 @@ def apply(mean, quat, scale, freq, out):
                 freq=np.asarray(freq, np.float64) + out[:, 10:13])
 
 
-def deform(c, theta, canon, times):
+def deform(c, theta, canon, times, quantize=False):
     """F frames x N primitives: rows f*N + i. Returns (per-frame params, cache)."""
     N = canon["mean"].shape[0]
     F = len(times)
     x = np.tile(np.asarray(canon["mean"], np.float64), (F, 1))
     t = np.repeat(np.asarray(times, np.float64), N)
-    out, cache = forward(c, theta, x, t)
+    out, cache = forward(c, theta, x, t, quantize=quantize)
     rep = {k: np.tile(np.asarray(canon[k], np.float64), (F, 1) if np.ndim(canon[k]) > 1 else F)
            for k in ("mean", "quat", "scale", "freq")}
     pf = apply(rep["mean"], rep["quat"], rep["scale"], rep["freq"], out)

@@ -67,6 +67,11 @@ class wipes_gemm_args(C.Structure):
                 ("split_k", C.c_int32)]
 
 
+class wipes_mlp_config(C.Structure):
+    _fields_ = [("width", C.c_int32), ("depth", C.c_int32), ("skip", C.c_int32),
+                ("Lx", C.c_int32), ("Lt", C.c_int32)]
+
+
 GEMM_EPI = {"store_f32": 0, "bias_f32": 1, "bias_relu_bf16": 2, "mask_bf16": 3,
             "atomic_f32": 4}
 
@@ -114,6 +119,16 @@ def lib():
     L.wipes_activate.argtypes = [P(wipes_adam_group), i32, vp]
     L.wipes_overflow_flag.argtypes = [vp]
     L.wipes_overflow_flag.restype = vp
+    L.wipes_mlp_param_count.argtypes = [P(wipes_mlp_config)]
+    L.wipes_mlp_param_count.restype = sz
+    L.wipes_mlp_workspace_bytes.argtypes = [P(wipes_mlp_config), i64]
+    L.wipes_mlp_workspace_bytes.restype = sz
+    L.wipes_mlp_forward.argtypes = [P(wipes_mlp_config), vp, i64, i32, P(C.c_float),
+                                    P(wipes_params), P(wipes_params), i32, vp, sz, vp]
+    L.wipes_mlp_forward.restype = C.c_int
+    L.wipes_mlp_backward.argtypes = [P(wipes_mlp_config), vp, i64, i32, P(wipes_params),
+                                     P(wipes_grads), vp, P(wipes_grads), vp, sz, vp]
+    L.wipes_mlp_backward.restype = C.c_int
     L.wipes_gemm_bf16.argtypes = [P(wipes_gemm_args), vp]
     L.wipes_gemm_bf16.restype = C.c_int
     L.wipes_num_kernels.restype = C.c_int
@@ -139,7 +154,9 @@ EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
             "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
             "wipes_render_bwd", "wipes_get_grad_moments", "wipes_render_stats",
             "wipes_train_scratch_bytes", "wipes_loss_l2", "wipes_adam_step", "wipes_activate",
-            "wipes_overflow_flag", "wipes_gemm_bf16", "wipes_num_kernels",
+            "wipes_overflow_flag", "wipes_gemm_bf16", "wipes_mlp_param_count",
+            "wipes_mlp_workspace_bytes", "wipes_mlp_forward", "wipes_mlp_backward",
+            "wipes_num_kernels",
             "wipes_kernel_name", "wipes_timing_enable", "wipes_timing_collect",
             "wipes_launch_count", "wipes_status_string", "wipes_last_error",
             "wipes_abi_version"]
@@ -289,6 +306,25 @@ def gemm(A, B, C, M, N, K, lda, ldb, ldc, epilogue="store_f32", a_mn=False, b_mn
     g = wipes_gemm_args(ptr(A), ptr(B), ptr(C), ptr(bias), ptr(mask), M, N, K, lda, ldb, ldc,
                         ldm, int(a_mn), int(b_mn), GEMM_EPI[epilogue], split_k)
     check(wipes_gemm_bf16(g, stream), "wipes_gemm_bf16")
+
+
+def wipes_mlp_param_count(cfg) -> int:
+    return int(lib().wipes_mlp_param_count(C.byref(cfg)))
+
+
+def wipes_mlp_workspace_bytes(cfg, rows) -> int:
+    return int(lib().wipes_mlp_workspace_bytes(C.byref(cfg), rows))
+
+
+def wipes_mlp_forward(cfg, theta, N, F, times, canon, frame, sh_coeffs, ws, ws_bytes, stream):
+    t = (C.c_float * max(F, 1))(*[float(x) for x in times])
+    return lib().wipes_mlp_forward(C.byref(cfg), theta, N, F, t, C.byref(canon), C.byref(frame),
+                                   sh_coeffs, ws, ws_bytes, stream)
+
+
+def wipes_mlp_backward(cfg, theta, N, F, canon, g_frame, g_theta, g_canon, ws, ws_bytes, stream):
+    return lib().wipes_mlp_backward(C.byref(cfg), theta, N, F, C.byref(canon), C.byref(g_frame),
+                                    g_theta, C.byref(g_canon), ws, ws_bytes, stream)
 
 
 def kernel_names():

@@ -27,6 +27,7 @@ SOURCES = {
     "render.cu": [],
     "train.cu": [],
     "gemm.cu": [],
+    "mlp.cu": [],
     "abi.cu": [],
 }
 

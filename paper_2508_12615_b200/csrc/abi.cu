@@ -43,7 +43,7 @@ const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
     "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order", "loss_l2",
-    "adam", "sh_bwd", "gemm_tc"};
+    "adam", "sh_bwd", "gemm_tc", "mlp_misc"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -412,6 +412,57 @@ wipes_status wipes_gemm_bf16(const wipes_gemm_args* g, void* stream) {
     return fail(WIPES_EINVAL, "split_k > 1 needs the atomic epilogue");
   cudaError_t e = launch_gemm(*g, (cudaStream_t)stream);
   return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "gemm launch");
+}
+
+size_t wipes_mlp_param_count(const wipes_mlp_config* c) {
+  if (!c || !mlp_config_valid(*c)) { fail(WIPES_EINVAL, "mlp config"); return 0; }
+  return (size_t)mlp_param_count(*c);
+}
+
+size_t wipes_mlp_workspace_bytes(const wipes_mlp_config* c, int64_t rows) {
+  if (!c || !mlp_config_valid(*c) || rows < 0) { fail(WIPES_EINVAL, "mlp config/rows"); return 0; }
+  return mlp_workspace_bytes(*c, rows);
+}
+
+static wipes_status check_mlp(const wipes_mlp_config* c, const float* theta, int64_t N, int32_t F,
+                              void* ws, size_t ws_bytes) {
+  if (!c || !mlp_config_valid(*c)) return fail(WIPES_EINVAL, "mlp config");
+  if (N < 0 || F < 1) return fail(WIPES_EINVAL, "need N >= 0 and F >= 1");
+  if (!theta) return fail(WIPES_EINVAL, "theta is NULL");
+  if (!ws || !aligned(ws, 256)) return fail(WIPES_EINVAL, "ws NULL or not 256-byte aligned");
+  if (ws_bytes < mlp_workspace_bytes(*c, N * (int64_t)F))
+    return fail(WIPES_EINVAL, "ws_bytes < wipes_mlp_workspace_bytes");
+  return WIPES_OK;
+}
+
+wipes_status wipes_mlp_forward(const wipes_mlp_config* c, const float* theta, int64_t N, int32_t F,
+                               const float* times, const wipes_params* canon,
+                               const wipes_params* frame, int32_t sh_coeffs, void* ws,
+                               size_t ws_bytes, void* stream) {
+  wipes_status st = check_mlp(c, theta, N, F, ws, ws_bytes);
+  if (st != WIPES_OK) return st;
+  if (!times || !canon || !frame) return fail(WIPES_EINVAL, "times/canon/frame NULL");
+  if (!canon->mean || !canon->quat || !canon->scale || !canon->freq || !frame->mean ||
+      !frame->quat || !frame->scale || !frame->freq)
+    return fail(WIPES_EINVAL, "mean/quat/scale/freq (canon and frame) must be non-NULL");
+  if (sh_coeffs < 0 || sh_coeffs > 16) return fail(WIPES_EINVAL, "sh_coeffs");
+  cudaError_t e = launch_mlp_forward(*c, theta, N, F, times, *canon, *frame, sh_coeffs,
+                                     (char*)ws, (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "mlp forward");
+}
+
+wipes_status wipes_mlp_backward(const wipes_mlp_config* c, const float* theta, int64_t N,
+                                int32_t F, const wipes_params* canon, const wipes_grads* gf,
+                                float* g_theta, const wipes_grads* gc, void* ws, size_t ws_bytes,
+                                void* stream) {
+  wipes_status st = check_mlp(c, theta, N, F, ws, ws_bytes);
+  if (st != WIPES_OK) return st;
+  if (!canon || !canon->scale || !gf || !gf->mean || !gf->quat || !gf->scale || !gf->freq ||
+      !g_theta || !gc)
+    return fail(WIPES_EINVAL, "canon.scale, g_frame groups, g_theta and g_canon are required");
+  cudaError_t e = launch_mlp_backward(*c, theta, N, F, *canon, *gf, g_theta, *gc, (char*)ws,
+                                      (cudaStream_t)stream);
+  return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "mlp backward");
 }
 
 int wipes_num_kernels(void) { return K_NUM; }

@@ -152,7 +152,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
 enum KernelId {
   K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
   K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
-  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_SH_BWD, K_GEMM, K_NUM
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_SH_BWD, K_GEMM, K_MLP_MISC, K_NUM
 };
 
 // Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph
@@ -170,6 +170,17 @@ void launch_end(int kid, cudaStream_t s);
 // ---- launchers (defined in the .cu files) ----------------------------------
 size_t train_scratch_bytes();
 cudaError_t launch_gemm(const wipes_gemm_args& g, cudaStream_t s);
+bool mlp_config_valid(const wipes_mlp_config& c);
+int64_t mlp_param_count(const wipes_mlp_config& c);
+size_t mlp_workspace_bytes(const wipes_mlp_config& c, int64_t rows);
+cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, int64_t N,
+                               int32_t F, const float* times, const wipes_params& canon,
+                               const wipes_params& frame, int32_t sh_coeffs, char* ws,
+                               cudaStream_t s);
+cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, int64_t N,
+                                int32_t F, const wipes_params& canon, const wipes_grads& gfr,
+                                float* g_theta, const wipes_grads& gcan, char* ws,
+                                cudaStream_t s);
 cudaError_t launch_loss_l2(const float* img, const float* tgt, int64_t n, float* grad,
                            double* loss, void* scratch, cudaStream_t s);
 cudaError_t launch_adam(const wipes_adam_group* groups, int ng, float b1, float b2, float eps,

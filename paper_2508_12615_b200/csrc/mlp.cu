@@ -1,0 +1,392 @@
+// NEXT-4: the time-conditioned deformation field of PAPER.md Eq. 8,
+// the D-3DGS network of Eq. 5, on the tcgen05 GEMM of gemm.cu
+// (include/wipes.h "NEXT-4"; R34-R36).
+//
+// Forward (rows m = f*N + i): k_mlp_embed writes the positional encoding
+// [gamma(x_i), gamma(t_f)] (bf16, zero-padded to E8) into the first E8 columns
+// of the concat buffer `cat` [M, E8 + W]; layer l is one GEMM with a fused
+// bias + ReLU + bf16 epilogue (layer `skip` writes its output into cat's last
+// W columns, so the skip layer reads [gamma, h] as one K = E8 + W operand);
+// the head GEMM adds its bias in fp32; k_mlp_apply forms the frame rows.
+// Backward: k_mlp_dout builds dL/dout (13 columns, bf16 for the GEMMs, fp32
+// for the head bias); per layer one split-K GEMM dW = dZ^T In (both operands
+// MN-major straight from the row-major activations, atomic fp32 epilogue),
+// a column sum for db, and one GEMM dIn = dZ W (W read MN-major) whose
+// epilogue applies the ReLU mask of the layer below.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace wipes {
+
+namespace {
+
+constexpr int kMlpMaxDepth = 32;
+constexpr int kMlpMaxFrames = 128;
+constexpr int kOutCols = 16;  // 13 outputs padded to one MMA N step
+
+struct MlpLayout {
+  int W, D, skip, Lx, Lt, E, E8, catw;
+  int64_t M;
+  int K[kMlpMaxDepth], Kp[kMlpMaxDepth];
+  int64_t thW[kMlpMaxDepth], thb[kMlpMaxDepth], thWh, thbh, P;
+  size_t wbf[kMlpMaxDepth], whbf, cat, h[kMlpMaxDepth], out, dout_bf, dout_f, dz[2], dws, total;
+};
+
+bool mlp_cfg_ok(const wipes_mlp_config& c) {
+  return c.width >= 16 && c.width <= 256 && c.width % 16 == 0 && c.depth >= 1 &&
+         c.depth <= kMlpMaxDepth && c.skip >= -1 && c.skip <= c.depth - 2 && c.Lx >= 0 &&
+         c.Lx <= 16 && c.Lt >= 0 && c.Lt <= 16;
+}
+
+MlpLayout mlp_layout(const wipes_mlp_config& c, int64_t M) {
+  MlpLayout L;
+  L.W = c.width; L.D = c.depth; L.skip = c.skip; L.Lx = c.Lx; L.Lt = c.Lt;
+  L.E = 3 * (1 + 2 * c.Lx) + (1 + 2 * c.Lt);
+  L.E8 = (L.E + 7) / 8 * 8;
+  L.catw = L.E8 + L.W;
+  L.M = M;
+  int64_t o = 0;
+  for (int l = 0; l < L.D; ++l) {
+    L.K[l] = l == 0 ? L.E : (l == L.skip + 1 ? L.E + L.W : L.W);
+    L.Kp[l] = l == 0 ? L.E8 : (l == L.skip + 1 ? L.E8 + L.W : L.W);
+    L.thW[l] = o; o += (int64_t)L.W * L.K[l];
+    L.thb[l] = o; o += L.W;
+  }
+  L.thWh = o; o += 13 * (int64_t)L.W;
+  L.thbh = o; o += 13;
+  L.P = o;
+  size_t b = 0;
+  auto take = [&](size_t bytes) { size_t r = b; b = align_up(b + bytes, 256); return r; };
+  int kmax = 0;
+  for (int l = 0; l < L.D; ++l) {
+    L.wbf[l] = take(2 * (size_t)L.W * L.Kp[l]);
+    kmax = L.Kp[l] > kmax ? L.Kp[l] : kmax;
+  }
+  L.whbf = take(2 * (size_t)kOutCols * L.W);
+  L.cat = take(2 * (size_t)M * L.catw);
+  for (int l = 0; l < L.D; ++l) L.h[l] = l == L.skip ? 0 : take(2 * (size_t)M * L.W);
+  L.out = take(4 * (size_t)M * kOutCols);
+  L.dout_bf = take(2 * (size_t)M * kOutCols);
+  L.dout_f = take(4 * (size_t)M * kOutCols);
+  L.dz[0] = take(2 * (size_t)M * L.W);
+  L.dz[1] = take(2 * (size_t)M * L.W);
+  L.dws = take(4 * (size_t)L.W * kmax);
+  L.total = b;
+  return L;
+}
+
+// theta (fp32, true widths) -> padded bf16 weights of one layer (l < D) or the head.
+__global__ void k_mlp_weights(const float* theta, int64_t thW, int rows, int rows_valid, int Kp,
+                              int E, int E8, int K, bool has_cat, __nv_bfloat16* dst) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * Kp) return;
+  const int j = (int)(idx / Kp), c = (int)(idx - (int64_t)j * Kp);
+  float v = 0.f;
+  if (j < rows_valid) {
+    int src = -1;
+    if (!has_cat) src = c < K ? c : -1;            // plain layer / layer 0 (K = E)
+    else src = c < E ? c : (c < E8 ? -1 : c - E8 + E);  // [gamma | pad | h]
+    if (src >= 0) v = theta[thW + (int64_t)j * K + src];
+  }
+  dst[idx] = __float2bfloat16_rn(v);
+}
+
+struct EmbedArgs {
+  const float* mean;
+  int64_t N, row0, rows;
+  int32_t f0, Lx, Lt, E8, catw;
+  float t[kMlpMaxFrames];
+  __nv_bfloat16* cat;
+};
+
+__global__ void __launch_bounds__(128) k_mlp_embed(const __grid_constant__ EmbedArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.rows) return;
+  const int64_t m = a.row0 + r;
+  const int64_t f = m / a.N, i = m - f * a.N;
+  const float x[3] = {a.mean[3 * i], a.mean[3 * i + 1], a.mean[3 * i + 2]};
+  const float t = a.t[f - a.f0];
+  __nv_bfloat16* row = a.cat + m * a.catw;
+  int c = 0;
+  for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(x[d]);
+  for (int k = 0; k < a.Lx; ++k) {
+    const float s = (float)(1 << k);
+    float sn[3], cs[3];
+    for (int d = 0; d < 3; ++d) sincosf(s * x[d], &sn[d], &cs[d]);
+    for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(sn[d]);
+    for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(cs[d]);
+  }
+  row[c++] = __float2bfloat16_rn(t);
+  for (int k = 0; k < a.Lt; ++k) {
+    float sn, cs;
+    sincosf((float)(1 << k) * t, &sn, &cs);
+    row[c++] = __float2bfloat16_rn(sn);
+    row[c++] = __float2bfloat16_rn(cs);
+  }
+  for (; c < a.E8; ++c) row[c] = __float2bfloat16_rn(0.f);
+}
+
+struct ApplyArgs {
+  int64_t N, M;
+  const float* out;  // [M, 16]
+  wipes_params canon, frame;
+  int32_t sh_coeffs;
+};
+
+__global__ void __launch_bounds__(128) k_mlp_apply(const __grid_constant__ ApplyArgs a) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= a.M) return;
+  const int64_t i = m % a.N;
+  const float* o = a.out + m * kOutCols;
+  float* fm = const_cast<float*>(a.frame.mean);
+  float* fq = const_cast<float*>(a.frame.quat);
+  float* fs = const_cast<float*>(a.frame.scale);
+  float* ff = const_cast<float*>(a.frame.freq);
+  for (int d = 0; d < 3; ++d) fm[3 * m + d] = a.canon.mean[3 * i + d] + o[d];
+  for (int d = 0; d < 4; ++d) fq[4 * m + d] = a.canon.quat[4 * i + d] + o[3 + d];
+  for (int d = 0; d < 3; ++d) fs[3 * m + d] = a.canon.scale[3 * i + d] * expf(o[7 + d]);
+  for (int d = 0; d < 3; ++d) ff[3 * m + d] = a.canon.freq[3 * i + d] + o[10 + d];
+  if (a.canon.phase && a.frame.phase) const_cast<float*>(a.frame.phase)[m] = a.canon.phase[i];
+  if (a.canon.opacity && a.frame.opacity)
+    const_cast<float*>(a.frame.opacity)[m] = a.canon.opacity[i];
+  if (a.canon.color && a.frame.color)
+    for (int d = 0; d < 3; ++d) const_cast<float*>(a.frame.color)[3 * m + d] = a.canon.color[3 * i + d];
+  if (a.canon.sh && a.frame.sh)
+    for (int d = 0; d < 3 * a.sh_coeffs; ++d)
+      const_cast<float*>(a.frame.sh)[3 * a.sh_coeffs * m + d] = a.canon.sh[3 * a.sh_coeffs * i + d];
+}
+
+// dL/dout = (g_mu_t, g_q_t, g_s_t * s_t, g_f_t) (s_t = s exp(ds)), bf16 + fp32.
+__global__ void __launch_bounds__(128) k_mlp_dout(int64_t N, int64_t M, const float* out,
+                                                  const float* scale, wipes_grads g,
+                                                  __nv_bfloat16* dbf, float* df) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int64_t i = m % N;
+  float v[kOutCols];
+  for (int d = 0; d < 3; ++d) v[d] = g.mean[3 * m + d];
+  for (int d = 0; d < 4; ++d) v[3 + d] = g.quat[4 * m + d];
+  for (int d = 0; d < 3; ++d)
+    v[7 + d] = g.scale[3 * m + d] * (scale[3 * i + d] * expf(out[m * kOutCols + 7 + d]));
+  for (int d = 0; d < 3; ++d) v[10 + d] = g.freq[3 * m + d];
+  for (int d = 13; d < kOutCols; ++d) v[d] = 0.f;
+  for (int d = 0; d < kOutCols; ++d) {
+    dbf[m * kOutCols + d] = __float2bfloat16_rn(v[d]);
+    df[m * kOutCols + d] = v[d];
+  }
+}
+
+// Canonical gradients: sums over the F frames (fixed order: deterministic).
+__global__ void __launch_bounds__(128) k_mlp_canon(int64_t N, int32_t F, const float* out,
+                                                   wipes_grads gf, wipes_grads gc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float gm[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gs[3] = {0, 0, 0}, gfr[3] = {0, 0, 0};
+  for (int f = 0; f < F; ++f) {
+    const int64_t m = (int64_t)f * N + i;
+    for (int d = 0; d < 3; ++d) gm[d] += gf.mean[3 * m + d];
+    for (int d = 0; d < 4; ++d) gq[d] += gf.quat[4 * m + d];
+    for (int d = 0; d < 3; ++d) gs[d] += gf.scale[3 * m + d] * expf(out[m * kOutCols + 7 + d]);
+    for (int d = 0; d < 3; ++d) gfr[d] += gf.freq[3 * m + d];
+  }
+  if (gc.mean) for (int d = 0; d < 3; ++d) gc.mean[3 * i + d] = gm[d];
+  if (gc.quat) for (int d = 0; d < 4; ++d) gc.quat[4 * i + d] = gq[d];
+  if (gc.scale) for (int d = 0; d < 3; ++d) gc.scale[3 * i + d] = gs[d];
+  if (gc.freq) for (int d = 0; d < 3; ++d) gc.freq[3 * i + d] = gfr[d];
+}
+
+// Column sums of a [M, ncols] matrix (row stride ld) into dst[ncols] (atomic).
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum(const T* src, int64_t ld, int64_t M, int ncols,
+                                                float* dst) {
+  const int c = threadIdx.x;
+  if (c >= ncols) return;
+  const int64_t per = (M + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = per * blockIdx.x, r1 = r0 + per < M ? r0 + per : M;
+  float acc = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    if constexpr (sizeof(T) == 2) acc += __bfloat162float(src[r * ld + c]);
+    else acc += (float)src[r * ld + c];
+  }
+  if (r1 > r0) atomicAdd(dst + c, acc);
+}
+
+// Padded dW scratch [rows, Kp] -> theta-gradient layout (true widths).
+__global__ void k_mlp_unpad(const float* dws, int rows, int Kp, int E, int E8, int K,
+                            bool has_cat, float* g) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * K) return;
+  const int j = (int)(idx / K), k = (int)(idx - (int64_t)j * K);
+  const int c = !has_cat ? k : (k < E ? k : k - E + E8);
+  g[idx] = dws[(int64_t)j * Kp + c];
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t gemm(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                 int64_t lda, int64_t ldb, int64_t ldc, int epi, bool amn, bool bmn,
+                 const float* bias, const void* mask, int64_t ldm, int split, cudaStream_t s) {
+  wipes_gemm_args g;
+  g.A = A; g.B = B; g.C = C; g.bias = bias; g.mask = mask;
+  g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.ldm = ldm;
+  g.a_mn_major = amn; g.b_mn_major = bmn; g.epilogue = epi; g.split_k = split;
+  return launch_gemm(g, s);
+}
+
+}  // namespace
+
+bool mlp_config_valid(const wipes_mlp_config& c) { return mlp_cfg_ok(c); }
+int64_t mlp_param_count(const wipes_mlp_config& c) { return mlp_layout(c, 0).P; }
+size_t mlp_workspace_bytes(const wipes_mlp_config& c, int64_t rows) {
+  return mlp_layout(c, rows).total;
+}
+
+cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, int64_t N,
+                               int32_t F, const float* times, const wipes_params& canon,
+                               const wipes_params& frame, int32_t sh_coeffs, char* ws,
+                               cudaStream_t s) {
+  const int64_t M = N * (int64_t)F;
+  const MlpLayout L = mlp_layout(c, M);
+  if (M == 0) return cudaSuccess;
+  // bf16 weights (rounded to nearest even)
+  for (int l = 0; l < L.D; ++l) {
+    const bool cat = l == L.skip + 1;
+    launch_begin(K_MLP_MISC, s);
+    k_mlp_weights<<<nblk((int64_t)L.W * L.Kp[l], 256), 256, 0, s>>>(
+        theta, L.thW[l], L.W, L.W, L.Kp[l], L.E, L.E8, L.K[l], cat,
+        (__nv_bfloat16*)(ws + L.wbf[l]));
+    launch_end(K_MLP_MISC, s);
+  }
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_weights<<<nblk((int64_t)kOutCols * L.W, 256), 256, 0, s>>>(
+      theta, L.thWh, kOutCols, 13, L.W, L.E, L.E8, L.W, false, (__nv_bfloat16*)(ws + L.whbf));
+  launch_end(K_MLP_MISC, s);
+  // positional encoding
+  __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
+  static thread_local EmbedArgs ea;
+  for (int f0 = 0; f0 < F; f0 += kMlpMaxFrames) {
+    const int nf = F - f0 < kMlpMaxFrames ? F - f0 : kMlpMaxFrames;
+    ea.mean = canon.mean; ea.N = N; ea.row0 = (int64_t)f0 * N; ea.rows = (int64_t)nf * N;
+    ea.f0 = f0; ea.Lx = L.Lx; ea.Lt = L.Lt; ea.E8 = L.E8; ea.catw = L.catw; ea.cat = cat;
+    for (int k = 0; k < nf; ++k) ea.t[k] = times[f0 + k];
+    launch_begin(K_MLP_MISC, s);
+    k_mlp_embed<<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
+    launch_end(K_MLP_MISC, s);
+  }
+  // layers
+  cudaError_t e = cudaSuccess;
+  for (int l = 0; l < L.D && e == cudaSuccess; ++l) {
+    const void* in;
+    int64_t ldin;
+    if (l == 0 || l == L.skip + 1) { in = cat; ldin = L.catw; }
+    else if (l - 1 == L.skip) { in = cat + L.E8; ldin = L.catw; }
+    else { in = ws + L.h[l - 1]; ldin = L.W; }
+    void* outp = l == L.skip ? (void*)(cat + L.E8) : (void*)(ws + L.h[l]);
+    const int64_t ldo = l == L.skip ? L.catw : L.W;
+    e = gemm(in, ws + L.wbf[l], outp, M, L.W, L.Kp[l], ldin, L.Kp[l], ldo,
+             WIPES_GEMM_EPI_BIAS_RELU_BF16, false, false, theta + L.thb[l], nullptr, 0, 1, s);
+  }
+  if (e != cudaSuccess) return e;
+  const int last = L.D - 1;
+  const void* hl = last == L.skip ? (const void*)(cat + L.E8) : (const void*)(ws + L.h[last]);
+  const int64_t ldh = last == L.skip ? L.catw : L.W;
+  e = gemm(hl, ws + L.whbf, ws + L.out, M, 13, L.W, ldh, L.W, kOutCols, WIPES_GEMM_EPI_BIAS_F32,
+           false, false, theta + L.thbh, nullptr, 0, 1, s);
+  if (e != cudaSuccess) return e;
+  ApplyArgs aa;
+  aa.N = N; aa.M = M; aa.out = (const float*)(ws + L.out); aa.canon = canon; aa.frame = frame;
+  aa.sh_coeffs = sh_coeffs;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_apply<<<nblk(M, 128), 128, 0, s>>>(aa);
+  launch_end(K_MLP_MISC, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, int64_t N,
+                                int32_t F, const wipes_params& canon, const wipes_grads& gfr,
+                                float* g_theta, const wipes_grads& gcan, char* ws,
+                                cudaStream_t s) {
+  const int64_t M = N * (int64_t)F;
+  const MlpLayout L = mlp_layout(c, M);
+  cudaError_t e = cudaMemsetAsync(g_theta, 0, sizeof(float) * L.P, s);
+  if (e != cudaSuccess || M == 0) return e;
+  __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
+  const float* out = (const float*)(ws + L.out);
+  __nv_bfloat16* dbf = (__nv_bfloat16*)(ws + L.dout_bf);
+  float* dfp = (float*)(ws + L.dout_f);
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_dout<<<nblk(M, 128), 128, 0, s>>>(N, M, out, canon.scale, gfr, dbf, dfp);
+  launch_end(K_MLP_MISC, s);
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_canon<<<nblk(N, 128), 128, 0, s>>>(N, F, out, gfr, gcan);
+  launch_end(K_MLP_MISC, s);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const unsigned cs_grid = (unsigned)(M < 4 * sms * 64 ? (M + 63) / 64 : 4 * sms);
+  auto split_for = [&](int64_t tiles) {  // split-K so that ~2 CTAs per SM run
+    int64_t sp = (2 * sms + tiles - 1) / tiles;
+    const int64_t chunks = (M + 63) / 64;
+    return (int)(sp < 1 ? 1 : (sp > chunks ? chunks : sp));
+  };
+  // head: dWh = dout^T h_last, dbh = colsum(dout), dh_last = dout Wh (masked)
+  const int last = L.D - 1;
+  const __nv_bfloat16* hl = last == L.skip ? cat + L.E8 : (const __nv_bfloat16*)(ws + L.h[last]);
+  const int64_t ldh = last == L.skip ? L.catw : L.W;
+  float* dws = (float*)(ws + L.dws);
+  e = cudaMemsetAsync(dws, 0, sizeof(float) * 13 * L.W, s);
+  if (e != cudaSuccess) return e;
+  e = gemm(dbf, hl, dws, 13, L.W, M, kOutCols, ldh, L.W, WIPES_GEMM_EPI_ATOMIC_F32, true, true,
+           nullptr, nullptr, 0, split_for(1 * ((L.W + 255) / 256)), s);
+  if (e != cudaSuccess) return e;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_unpad<<<nblk(13 * (int64_t)L.W, 256), 256, 0, s>>>(dws, 13, L.W, L.E, L.E8, L.W, false,
+                                                           g_theta + L.thWh);
+  launch_end(K_MLP_MISC, s);
+  launch_begin(K_MLP_MISC, s);
+  k_colsum<float><<<cs_grid, 256, 0, s>>>(dfp, kOutCols, M, 13, g_theta + L.thbh);
+  launch_end(K_MLP_MISC, s);
+  __nv_bfloat16* dz = (__nv_bfloat16*)(ws + L.dz[0]);
+  __nv_bfloat16* dz2 = (__nv_bfloat16*)(ws + L.dz[1]);
+  e = gemm(dbf, ws + L.whbf, dz, M, L.W, kOutCols, kOutCols, L.W, L.W, WIPES_GEMM_EPI_MASK_BF16,
+           false, true, nullptr, hl, ldh, 1, s);
+  if (e != cudaSuccess) return e;
+  for (int l = last; l >= 0; --l) {
+    // dz = dL/dz_l [M, W]; input of layer l:
+    const void* in;
+    int64_t ldin;
+    if (l == 0 || l == L.skip + 1) { in = cat; ldin = L.catw; }
+    else if (l - 1 == L.skip) { in = cat + L.E8; ldin = L.catw; }
+    else { in = ws + L.h[l - 1]; ldin = L.W; }
+    const bool has_cat = l == L.skip + 1;
+    e = cudaMemsetAsync(dws, 0, sizeof(float) * (size_t)L.W * L.Kp[l], s);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles = ((L.W + 127) / 128) * ((L.Kp[l] + 255) / 256);
+    e = gemm(dz, in, dws, L.W, L.Kp[l], M, L.W, ldin, L.Kp[l], WIPES_GEMM_EPI_ATOMIC_F32, true,
+             true, nullptr, nullptr, 0, split_for(tiles), s);
+    if (e != cudaSuccess) return e;
+    launch_begin(K_MLP_MISC, s);
+    k_mlp_unpad<<<nblk((int64_t)L.W * L.K[l], 256), 256, 0, s>>>(
+        dws, L.W, L.Kp[l], L.E, L.E8, L.K[l], has_cat, g_theta + L.thW[l]);
+    launch_end(K_MLP_MISC, s);
+    launch_begin(K_MLP_MISC, s);
+    k_colsum<__nv_bfloat16><<<cs_grid, 256, 0, s>>>(dz, L.W, M, L.W, g_theta + L.thb[l]);
+    launch_end(K_MLP_MISC, s);
+    if (l == 0) break;
+    // dz_(l-1) = (dz W_l)[:, h part] * (h_(l-1) > 0)
+    const __nv_bfloat16* wl = (const __nv_bfloat16*)(ws + L.wbf[l]) + (has_cat ? L.E8 : 0);
+    const void* mask = (l - 1 == L.skip) ? (const void*)(cat + L.E8) : (const void*)(ws + L.h[l - 1]);
+    const int64_t ldm = (l - 1 == L.skip) ? L.catw : L.W;
+    e = gemm(dz, wl, dz2, M, L.W, L.W, L.W, L.Kp[l], L.W, WIPES_GEMM_EPI_MASK_BF16, false, true,
+             nullptr, mask, ldm, 1, s);
+    if (e != cudaSuccess) return e;
+    __nv_bfloat16* t = dz; dz = dz2; dz2 = t;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace wipes

@@ -1,0 +1,119 @@
+"""NEXT-4: the time-conditioned deformation field F_theta (PAPER.md:272-274
+Eq. 8; D-3DGS network, Eq. 5) on the tcgen05 tensor cores.
+
+    d = Deformation(N=300_000)                   # D-3DGS shape: 8 x 256, skip 4
+    theta = d.init_theta(seed=0)                 # fp32 [param_count]
+    frame = d.forward(theta, canon, times)       # per-frame params, rows f*N + i
+    ...rasterize(frame, cams, view_stride=N)...
+    g_theta, g_canon = d.backward(theta, canon, g_frame)
+
+Every layer runs in libwipes.so (wipes_mlp_forward / wipes_mlp_backward); this
+class only owns the buffers. No CPU fallback.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import abi
+
+DEFORMED = ("mean", "quat", "scale", "freq")
+COPIED = ("phase", "color", "opacity", "sh")
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Deformation:
+    def __init__(self, N: int, width: int = 256, depth: int = 8, skip: int = 4, Lx: int = 10,
+                 Lt: int = 6, device="cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("Deformation needs a CUDA device (no CPU fallback)")
+        abi.lib()
+        self.cfg = abi.wipes_mlp_config(width, depth, skip, Lx, Lt)
+        self.P = abi.wipes_mlp_param_count(self.cfg)
+        if self.P == 0:
+            raise abi.WipesError(abi.WIPES_EINVAL, "wipes_mlp_param_count",
+                                 abi.lib().wipes_last_error().decode())
+        self.N, self.device = N, torch.device(device)
+        self.width, self.depth, self.skip, self.Lx, self.Lt = width, depth, skip, Lx, Lt
+        self.ws = None
+        self.rows = 0
+        self._last = None
+
+    @property
+    def embed_dim(self):
+        return 3 * (1 + 2 * self.Lx) + 1 + 2 * self.Lt
+
+    def layer_in(self, l):
+        if l == 0:
+            return self.embed_dim
+        return self.embed_dim + self.width if l == self.skip + 1 else self.width
+
+    def init_theta(self, seed: int = 0, head_scale: float = 1.0) -> torch.Tensor:
+        """nn.Linear-style init U(-1/sqrt(K), 1/sqrt(K)) for weights and biases
+        (host RNG, synthetic: no trained weights exist)."""
+        g = np.random.default_rng(seed)
+        parts = []
+        for l in range(self.depth):
+            K = self.layer_in(l)
+            b = 1.0 / math.sqrt(K)
+            parts += [g.uniform(-b, b, self.width * K), g.uniform(-b, b, self.width)]
+        b = head_scale / math.sqrt(self.width)
+        parts += [g.uniform(-b, b, 13 * self.width), g.uniform(-b, b, 13)]
+        th = np.concatenate(parts).astype(np.float32)
+        assert th.size == self.P
+        return torch.from_numpy(th).to(self.device)
+
+    def _ensure(self, rows):
+        nb = abi.wipes_mlp_workspace_bytes(self.cfg, rows)
+        if self.ws is None or self.ws.numel() < nb + 256:
+            self.ws = torch.empty(nb + 256, dtype=torch.uint8, device=self.device)
+        self.rows, self.ws_bytes = rows, nb
+
+    def _ws_ptr(self):
+        p = self.ws.data_ptr()
+        return (p + 255) // 256 * 256
+
+    @staticmethod
+    def _params(d):
+        p = abi.wipes_params()
+        for k in DEFORMED + COPIED:
+            setattr(p, k, abi.ptr(d.get(k)))
+        return p
+
+    def forward(self, theta: torch.Tensor, canon: dict, times, frame: dict = None) -> dict:
+        F = len(times)
+        rows = self.N * F
+        self._ensure(rows)
+        if frame is None:
+            frame = {k: torch.empty((rows,) + tuple(canon[k].shape[1:]), dtype=torch.float32,
+                                    device=self.device)
+                     for k in DEFORMED + COPIED if k in canon}
+        shc = int(canon["sh"].shape[1]) if "sh" in canon else 0
+        cp, fp = self._params(canon), self._params(frame)
+        abi.check(abi.wipes_mlp_forward(self.cfg, abi.ptr(theta), self.N, F, list(times), cp, fp,
+                                        shc, self._ws_ptr(), self.ws_bytes, _stream()),
+                  "wipes_mlp_forward")
+        self._last = (F, cp, fp, canon, frame)
+        return frame
+
+    def backward(self, theta: torch.Tensor, canon: dict, g_frame: dict, g_theta=None,
+                 g_canon=None):
+        F = self._last[0]
+        if g_theta is None:
+            g_theta = torch.empty(self.P, dtype=torch.float32, device=self.device)
+        if g_canon is None:
+            g_canon = {k: torch.empty_like(canon[k]) for k in DEFORMED}
+        gf, gc = abi.wipes_grads(), abi.wipes_grads()
+        for k in DEFORMED:
+            setattr(gf, k, abi.ptr(g_frame[k]))
+            setattr(gc, k, abi.ptr(g_canon.get(k)))
+        abi.check(abi.wipes_mlp_backward(self.cfg, abi.ptr(theta), self.N, F,
+                                         self._params(canon), gf, abi.ptr(g_theta), gc,
+                                         self._ws_ptr(), self.ws_bytes, _stream()),
+                  "wipes_mlp_backward")
+        return g_theta, g_canon

@@ -1,0 +1,138 @@
+"""GPU parity of the NEXT-4 deformation field (tcgen05 MLP) against the FP64
+oracle (oracle/mlp.py, pinned by torch autograd and FD in
+tests/test_oracle_mlp.py).
+
+Both sides use the same bf16-rounded weights, encoding and layer activations
+(the kernel's operand precision; the oracle's quantize=True rounds at the same
+points, so the ReLU masks are decided on the same operands, R36) and
+the oracle accumulates in FP64. What remains on the GPU side is fp32
+accumulation and, in the backward, bf16 rounding of dL/dout and of each dL/dz
+(relative 2^-9 per layer): forward deltas within 2e-2 of their rms, gradients
+within a norm-wise 2 (D + 1) 2^-9 (see _grad_ok).
+"""
+import numpy as np
+import pytest
+
+from oracle import mlp as omlp
+from paper_2508_12615_b200 import gen
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2508_12615_b200 import build
+    build.build()
+
+
+def _bf16_round(x):
+    t = torch.from_numpy(np.asarray(x, np.float32)).to(torch.bfloat16).float()
+    return t.numpy().astype(np.float64)
+
+
+def _theta_as_kernel_sees_it(d, theta):
+    """Weights rounded to bf16 (operands), biases kept fp32."""
+    c = omlp.config(d.width, d.depth, d.skip, d.Lx, d.Lt)
+    th = theta.cpu().numpy().astype(np.float64)
+    out = th.copy()
+    for name, shape, o in omlp.layout(c):
+        if name.startswith("W"):
+            n = int(np.prod(shape))
+            out[o:o + n] = _bf16_round(th[o:o + n])
+    return c, out
+
+
+def _rel_ok(got, ref, frac=2e-2):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    rms = np.sqrt(np.mean(ref ** 2)) + 1e-30
+    err = np.abs(got - ref)
+    return float(np.max(err) / rms), bool(np.all(err <= frac * rms))
+
+
+def _grad_ok(got, ref, depth):
+    """Backward: dL/dz is rounded to bf16 at every layer on the GPU, a relative
+    2^-9 per layer, so the gradient of layer l carries up to ~(D - l) 2^-9;
+    bound: norm-wise 2 D 2^-9 (x2 margin), element-wise 8x that of the rms."""
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    nrm = np.linalg.norm(ref) + 1e-30
+    rel = float(np.linalg.norm(got - ref) / nrm)
+    tol = 2 * (depth + 1) * 2.0 ** -9
+    rms = nrm / np.sqrt(ref.size)
+    return rel, rel <= tol and bool(np.all(np.abs(got - ref) <= 8 * tol * rms))
+
+
+@pytest.mark.parametrize("shape", [dict(width=256, depth=8, skip=4, Lx=10, Lt=6),
+                                   dict(width=64, depth=3, skip=0, Lx=4, Lt=2),
+                                   dict(width=128, depth=2, skip=-1, Lx=10, Lt=6)])
+def test_mlp_forward_backward_parity(shape):
+    from paper_2508_12615_b200.deform import Deformation
+    N, times = 1000, [0.0, 0.37, 1.0]
+    d = Deformation(N, **shape)
+    theta = d.init_theta(seed=1)
+    p = gen.gen3d(N, seed=3, scale_mult=4.0)
+    canon = {k: torch.from_numpy(p[k]).cuda() for k in ("mean", "quat", "scale", "freq",
+                                                         "color", "opacity")}
+    frame = d.forward(theta, canon, times)
+    torch.cuda.synchronize()
+    c, th = _theta_as_kernel_sees_it(d, theta)
+    ref, cache = omlp.deform(c, th, {k: p[k] for k in ("mean", "quat", "scale", "freq")}, times,
+                             quantize=True)
+    for k in ("mean", "quat", "freq"):  # additive deltas: dx, dq, df
+        delta_g = frame[k].cpu().numpy() - np.tile(p[k], (len(times), 1))
+        delta_o = ref[k] - np.tile(p[k].astype(np.float64), (len(times), 1))
+        worst, ok = _rel_ok(delta_g, delta_o)
+        assert ok, (k, worst)
+    # scale: compare the network output ds = log(s_t / s)
+    ds_g = np.log(frame["scale"].cpu().numpy().astype(np.float64) / np.tile(p["scale"], (3, 1)))
+    worst, ok = _rel_ok(ds_g, cache["out"][:, 7:10])
+    assert ok, ("scale", worst)
+    np.testing.assert_array_equal(frame["color"].cpu().numpy(), np.tile(p["color"], (3, 1)))
+    # backward from a random upstream gradient of the frame rows
+    rng = np.random.default_rng(5)
+    gfr = {k: rng.normal(size=frame[k].shape).astype(np.float32)
+           for k in ("mean", "quat", "scale", "freq")}
+    g_theta, g_canon = d.backward(theta, canon, {k: torch.from_numpy(v).cuda()
+                                                 for k, v in gfr.items()})
+    torch.cuda.synchronize()
+    gth_o, gcn_o = omlp.deform_backward(c, th, p, cache, gfr)
+    gth = g_theta.cpu().numpy()
+    bad = []
+    for name, shp, o in omlp.layout(c):
+        n = int(np.prod(shp))
+        worst, ok = _grad_ok(gth[o:o + n], gth_o[o:o + n], d.depth)
+        if not ok:
+            bad.append((name, round(worst, 4)))
+    assert not bad, bad
+    np.testing.assert_allclose(g_canon["mean"].cpu().numpy(), gcn_o["mean"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(g_canon["quat"].cpu().numpy(), gcn_o["quat"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(g_canon["freq"].cpu().numpy(), gcn_o["freq"], rtol=1e-5, atol=1e-5)
+    worst, ok = _grad_ok(g_canon["scale"].cpu().numpy(), gcn_o["scale"], d.depth)
+    assert ok, ("scale", worst)
+
+
+def test_mlp_feeds_the_rasterizer():
+    """6D end to end: deformation -> rasterizer (view_stride = N) -> backward
+    through both, finite gradients everywhere (NEXT-4 'feeding K2 through
+    view_stride')."""
+    from paper_2508_12615_b200.deform import Deformation
+    from paper_2508_12615_b200.raster import Rasterizer
+    N, H, W = 2000, 96, 128
+    p = gen.gen3d(N, seed=0, scale_mult=4.0)
+    cams = gen.arc_cameras(3, W, H)
+    canon = {k: torch.from_numpy(v).cuda() for k, v in p.items()}
+    d = Deformation(N)
+    theta = d.init_theta(seed=0, head_scale=0.1)
+    frame = d.forward(theta, canon, [0.0, 0.5, 1.0])
+    r = Rasterizer(W, H, prim="3d", blend="alpha")
+    out = r.forward(frame, cams, view_stride=N)
+    dL = torch.from_numpy(gen.gen_dLdC(3, H, W, seed=0)).cuda()
+    gfr = r.backward(dL)
+    g_theta, g_canon = d.backward(theta, canon, gfr)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out["image"]).all()
+    assert torch.isfinite(g_theta).all() and g_theta.abs().sum() > 0
+    for v in g_canon.values():
+        assert torch.isfinite(v).all()

@@ -131,3 +131,14 @@ def test_apply_closed_form():
     assert np.all(p["mean"] == 1) and np.all(p["scale"] == 2)
     z[:, 7:10] = math.log(3.0)
     np.testing.assert_allclose(mlp.apply(m, q, s, f, z)["scale"], 6.0)
+
+
+def test_round_bf16():
+    """bf16 = the top 16 bits of float32 with round-to-nearest-even."""
+    x = np.array([1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -9, -2.5, 1e-30, 3.0e38])
+    r = mlp.round_bf16(x)
+    assert r[0] == 1.0 and r[1] == 1.0  # 1 + 2^-8 is a tie: to the even neighbour 1.0
+    assert r[2] == 1.0 + 2 ** -7      # above the tie rounds up
+    assert r[3] == -2.5               # exactly representable
+    ref = torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(r, ref)
