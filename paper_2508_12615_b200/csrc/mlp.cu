@@ -24,6 +24,7 @@ namespace {
 constexpr int kMlpMaxDepth = 32;
 constexpr int kMlpMaxFrames = 128;
 constexpr int kOutCols = 16;  // 13 outputs padded to one MMA N step
+constexpr int kMaxE8 = 3 * (1 + 2 * 16) + (1 + 2 * 16) + 8;  // Lx, Lt <= 16
 
 struct MlpLayout {
   int W, D, skip, Lx, Lt, E, E8, catw;
@@ -107,24 +108,28 @@ __global__ void __launch_bounds__(128) k_mlp_embed(const __grid_constant__ Embed
   const int64_t f = m / a.N, i = m - f * a.N;
   const float x[3] = {a.mean[3 * i], a.mean[3 * i + 1], a.mean[3 * i + 2]};
   const float t = a.t[f - a.f0];
-  __nv_bfloat16* row = a.cat + m * a.catw;
+  // built in registers, written as 16-byte vectors (E8 is a multiple of 8)
+  __align__(16) __nv_bfloat16 buf[kMaxE8];
   int c = 0;
-  for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(x[d]);
+  for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(x[d]);
   for (int k = 0; k < a.Lx; ++k) {
     const float s = (float)(1 << k);
     float sn[3], cs[3];
     for (int d = 0; d < 3; ++d) sincosf(s * x[d], &sn[d], &cs[d]);
-    for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(sn[d]);
-    for (int d = 0; d < 3; ++d) row[c++] = __float2bfloat16_rn(cs[d]);
+    for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(sn[d]);
+    for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(cs[d]);
   }
-  row[c++] = __float2bfloat16_rn(t);
+  buf[c++] = __float2bfloat16_rn(t);
   for (int k = 0; k < a.Lt; ++k) {
     float sn, cs;
     sincosf((float)(1 << k) * t, &sn, &cs);
-    row[c++] = __float2bfloat16_rn(sn);
-    row[c++] = __float2bfloat16_rn(cs);
+    buf[c++] = __float2bfloat16_rn(sn);
+    buf[c++] = __float2bfloat16_rn(cs);
   }
-  for (; c < a.E8; ++c) row[c] = __float2bfloat16_rn(0.f);
+  for (; c < a.E8; ++c) buf[c] = __float2bfloat16_rn(0.f);
+  uint4* row = reinterpret_cast<uint4*>(a.cat + m * a.catw);
+  const uint4* src = reinterpret_cast<const uint4*>(buf);
+  for (int v = 0; v < a.E8 / 8; ++v) row[v] = src[v];
 }
 
 struct ApplyArgs {
