@@ -309,6 +309,8 @@ typedef struct {
   int64_t M, N, K;
   int64_t lda, ldb, ldc, ldm;
   int32_t a_mn_major, b_mn_major, epilogue, split_k;
+  float* colsum;      /* optional [N] f32: += column sums of the epilogue result
+                         over the rows (atomic; e.g. a bias gradient), or NULL */
 } wipes_gemm_args;
 wipes_status wipes_gemm_bf16(const wipes_gemm_args* args, void* stream);
 

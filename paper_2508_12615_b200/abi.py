@@ -64,7 +64,7 @@ class wipes_gemm_args(C.Structure):
                 ("mask", C.c_void_p), ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64), ("ldm", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_mn_major", C.c_int32), ("epilogue", C.c_int32),
-                ("split_k", C.c_int32)]
+                ("split_k", C.c_int32), ("colsum", C.c_void_p)]
 
 
 class wipes_mlp_config(C.Structure):
@@ -301,10 +301,10 @@ def wipes_gemm_bf16(args, stream):
 
 
 def gemm(A, B, C, M, N, K, lda, ldb, ldc, epilogue="store_f32", a_mn=False, b_mn=False,
-         bias=None, mask=None, ldm=0, split_k=1, stream=None):
+         bias=None, mask=None, ldm=0, split_k=1, colsum=None, stream=None):
     """Marshal a wipes_gemm_args from torch tensors / ints and launch."""
     g = wipes_gemm_args(ptr(A), ptr(B), ptr(C), ptr(bias), ptr(mask), M, N, K, lda, ldb, ldc,
-                        ldm, int(a_mn), int(b_mn), GEMM_EPI[epilogue], split_k)
+                        ldm, int(a_mn), int(b_mn), GEMM_EPI[epilogue], split_k, ptr(colsum))
     check(wipes_gemm_bf16(g, stream), "wipes_gemm_bf16")
 
 

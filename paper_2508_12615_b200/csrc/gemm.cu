@@ -1,4 +1,5 @@
 // tcgen05 GEMM with fused epilogues (NEXT-4 building block; see gemm_tc.cuh).
+// Persistent warp-specialised kernel; the per-chunk primitives are in gemm_tc.cuh.
 #include <cstdlib>
 
 #include "gemm_tc.cuh"
@@ -8,15 +9,6 @@ namespace wipes {
 namespace {
 
 using namespace tc;
-
-template <int NT>
-struct GemmSmem {
-  // a[] doubles as the epilogue scratch (4 warps x 32 x 33 floats = 16.5 KB)
-  __nv_bfloat16 a[2][kM * kKC];
-  __nv_bfloat16 b[2][NT * kKC];
-  uint64_t bar[2];
-  uint32_t tmem;
-};
 
 // Stage one operand tile (R rows x kKC) of chunk k0 into the canonical layout.
 template <int R, bool MN, int NTHR = kThreads>
@@ -56,176 +48,6 @@ __device__ __forceinline__ void stage(__nv_bfloat16* dst, const __nv_bfloat16* s
     }
     cp16(reinterpret_cast<char*>(dst) + off, s, ok);
   }
-}
-
-template <int NT, bool AMN, bool BMN, int EPI>
-__global__ void __launch_bounds__(kThreads) k_gemm(const wipes_gemm_args g) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  GemmSmem<NT>& sm = *reinterpret_cast<GemmSmem<NT>*>(smem_raw);
-  constexpr int kCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * kM, n0 = (int64_t)blockIdx.y * NT;
-  // this CTA's K range (split-K over gridDim.z, whole chunks)
-  const int64_t nchunk_all = (g.K + kKC - 1) / kKC;
-  const int64_t per = (nchunk_all + gridDim.z - 1) / gridDim.z;
-  const int64_t c_lo = per * blockIdx.z;
-  const int64_t c_hi = c_lo + per < nchunk_all ? c_lo + per : nchunk_all;
-  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(g.A);
-  const __nv_bfloat16* B = reinterpret_cast<const __nv_bfloat16*>(g.B);
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem)),
-                 "n"(kCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm.tmem;
-  const uint32_t idesc = instr_desc(NT, AMN, BMN);
-  uint32_t phase[2] = {0, 0};
-
-  const int64_t nch = c_hi - c_lo;
-  if (nch > 0) {
-    stage<kM, AMN>(sm.a[0], A, g.lda, m0, g.M, c_lo * kKC, g.K, tid);
-    stage<NT, BMN>(sm.b[0], B, g.ldb, n0, g.N, c_lo * kKC, g.K, tid);
-    cp_commit();
-  }
-  for (int64_t c = 0; c < nch; ++c) {
-    const int buf = (int)(c & 1);
-    if (c + 1 < nch) {
-      const int nb = buf ^ 1;
-      if (c >= 1) {  // buffer nb was read by the MMAs of chunk c - 1
-        mbar_wait(&sm.bar[nb], phase[nb]);
-        phase[nb] ^= 1;
-      }
-      const int64_t k0 = (c_lo + c + 1) * kKC;
-      stage<kM, AMN>(sm.a[nb], A, g.lda, m0, g.M, k0, g.K, tid);
-      stage<NT, BMN>(sm.b[nb], B, g.ldb, n0, g.N, k0, g.K, tid);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t a0 = smem_u32(sm.a[buf]), b0 = smem_u32(sm.b[buf]);
-#pragma unroll
-      for (int j = 0; j < kKC / 16; ++j)
-        mma_bf16(tmem, smem_desc(a0 + 256 * j, 128, 1024), smem_desc(b0 + 256 * j, 128, 1024),
-                 idesc, (c > 0 || j > 0) ? 1u : 0u);
-      mma_commit(&sm.bar[buf]);
-    }
-  }
-  // the last chunk's commit covers all earlier MMAs
-  if (nch > 0) {
-    const int lb = (int)((nch - 1) & 1);
-    mbar_wait(&sm.bar[lb], phase[lb]);
-  }
-  tc_fence_after();
-
-  // ---- epilogue: warp w owns rows 32w..32w+31 of the tile ------------------
-  // Each 32 x 32 accumulator block goes TMEM -> registers (lane = row) ->
-  // warp-private shared memory (the operand buffers are free now) and is then
-  // written with 8 lanes per row, 4 consecutive columns per lane, so every
-  // store instruction covers 4 rows x 32 contiguous columns.
-  float* scr = reinterpret_cast<float*>(&sm.a[0][0]) + warp * (32 * 33);
-  const bool cvec = ((uintptr_t)g.C % 16 == 0) && (g.ldc % 4 == 0);
-  const bool mvec = EPI != WIPES_GEMM_EPI_MASK_BF16 ||
-                    (((uintptr_t)g.mask % 8 == 0) && (g.ldm % 4 == 0));
-  const int rr = lane >> 3, c4 = (lane & 7) * 4;
-#pragma unroll 1
-  for (int cb = 0; cb < (NT + 31) / 32; ++cb) {
-    float v[32];
-    if (nch > 0) {
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * cb), v);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = v[i];
-    __syncwarp();
-#pragma unroll 1
-    for (int pass = 0; pass < 8; ++pass) {
-      const int r = pass * 4 + rr;
-      const int64_t m = m0 + 32 * warp + r;
-      const int tc = 32 * cb + c4;          // column within the tile
-      const int64_t n = n0 + tc;
-      if (m >= g.M || tc >= NT || n >= g.N) continue;
-      float x[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) x[j] = scr[r * 33 + c4 + j];
-      const bool full = tc + 4 <= NT && n + 4 <= g.N;
-      if (EPI == WIPES_GEMM_EPI_BIAS_F32 || EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (n + j < g.N) x[j] += g.bias[n + j];
-      }
-      if (EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = fmaxf(x[j], 0.f);
-      }
-      if (EPI == WIPES_GEMM_EPI_MASK_BF16) {
-        const __nv_bfloat16* mp = reinterpret_cast<const __nv_bfloat16*>(g.mask) + m * g.ldm + n;
-        if (full && mvec) {
-          const uint2 u = *reinterpret_cast<const uint2*>(mp);
-          const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
-          const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
-          x[0] = __low2float(a) > 0.f ? x[0] : 0.f;
-          x[1] = __high2float(a) > 0.f ? x[1] : 0.f;
-          x[2] = __low2float(b) > 0.f ? x[2] : 0.f;
-          x[3] = __high2float(b) > 0.f ? x[3] : 0.f;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (n + j < g.N) x[j] = __bfloat162float(mp[j]) > 0.f ? x[j] : 0.f;
-        }
-      }
-      if (EPI == WIPES_GEMM_EPI_ATOMIC_F32) {
-        float* cp = reinterpret_cast<float*>(g.C) + m * g.ldc + n;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (tc + j < NT && n + j < g.N) atomicAdd(cp + j, x[j]);
-      } else if (EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16 || EPI == WIPES_GEMM_EPI_MASK_BF16) {
-        __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(g.C) + m * g.ldc + n;
-        if (full && cvec && ((uintptr_t)cp % 8 == 0)) {
-          const __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]);
-          const __nv_bfloat162 b = __floats2bfloat162_rn(x[2], x[3]);
-          uint2 u;
-          u.x = *reinterpret_cast<const uint32_t*>(&a);
-          u.y = *reinterpret_cast<const uint32_t*>(&b);
-          *reinterpret_cast<uint2*>(cp) = u;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (tc + j < NT && n + j < g.N) cp[j] = __float2bfloat16_rn(x[j]);
-        }
-      } else {  // STORE_F32 / BIAS_F32
-        float* cp = reinterpret_cast<float*>(g.C) + m * g.ldc + n;
-        if (full && cvec) {
-          *reinterpret_cast<float4*>(cp) = make_float4(x[0], x[1], x[2], x[3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (tc + j < NT && n + j < g.N) cp[j] = x[j];
-        }
-      }
-    }
-    __syncwarp();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
 // ---------------------------------------------------------------------------
@@ -310,9 +132,13 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
     }
     const int tc = 32 * cb;
     const int64_t n = n0 + tc;
-    if (!mrow || tc >= NT || n >= g.N) continue;
+    if (tc >= NT || n >= g.N) continue;  // warp-uniform
     const bool full = tc + 32 <= NT && n + 32 <= g.N;
     const int nv = full ? 32 : (int)((g.N - n) < (NT - tc) ? (g.N - n) : (NT - tc));
+    if (!mrow) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
     if (EPI == WIPES_GEMM_EPI_BIAS_F32 || EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16) {
       if (full && ((uintptr_t)(g.bias + n) % 16 == 0)) {
         const float4* b4 = reinterpret_cast<const float4*>(g.bias + n);
@@ -331,7 +157,7 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
     }
-    if (EPI == WIPES_GEMM_EPI_MASK_BF16) {
+    if (EPI == WIPES_GEMM_EPI_MASK_BF16 && mrow) {
       const __nv_bfloat16* mp = reinterpret_cast<const __nv_bfloat16*>(g.mask) + m * g.ldm + n;
       if (full && mvec) {
 #pragma unroll
@@ -351,6 +177,26 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
           if (i < nv) v[i] = __bfloat162float(mp[i]) > 0.f ? v[i] : 0.f;
       }
     }
+    if (g.colsum) {
+      // column sums over the warp's 32 rows by reduce-scatter (31 shuffles):
+      // at each halving the lane with bit sz set keeps the upper half, so
+      // lane l ends with the sum of column l of this block
+      float w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) w[i] = (i < nv) ? v[i] : 0.f;
+#pragma unroll
+      for (int sz = 16; sz >= 1; sz >>= 1) {
+        const bool up = lane & sz;
+#pragma unroll
+        for (int i = 0; i < sz; ++i) {
+          const float send = up ? w[i] : w[i + sz];
+          const float keep = up ? w[i + sz] : w[i];
+          w[i] = keep + __shfl_xor_sync(0xffffffffu, send, sz);
+        }
+      }
+      if (lane < nv) atomicAdd(g.colsum + n + lane, w[0]);
+    }
+    if (!mrow) continue;
     if (EPI == WIPES_GEMM_EPI_ATOMIC_F32) {
       float* cp = reinterpret_cast<float*>(g.C) + m * g.ldc + n;
       if (full && cvec) {
@@ -567,21 +413,7 @@ cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
 
 template <int NT, bool AMN, bool BMN, int EPI>
 cudaError_t launch_nt(const wipes_gemm_args& g, cudaStream_t s) {
-  static const bool legacy = getenv("WIPES_GEMM_SIMPLE") != nullptr;
-  if (!legacy) return launch_ws<NT, AMN, BMN, EPI>(g, s);
-  auto k = k_gemm<NT, AMN, BMN, EPI>;
-  const int smem = (int)sizeof(GemmSmem<NT>) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  dim3 grid((unsigned)((g.M + kM - 1) / kM), (unsigned)((g.N + NT - 1) / NT),
-            (unsigned)(g.split_k > 0 ? g.split_k : 1));
-  launch_begin(K_GEMM, s);
-  k<<<grid, kThreads, smem, s>>>(g);
-  launch_end(K_GEMM, s);
-  return cudaGetLastError();
+  return launch_ws<NT, AMN, BMN, EPI>(g, s);
 }
 
 template <bool AMN, bool BMN, int EPI>

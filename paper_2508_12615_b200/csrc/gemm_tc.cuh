@@ -2,15 +2,14 @@
 // deformation MLP (Eq. 5
 // Eq. 8): D[M x N] = sum_k A(m, k) B(n, k), fp32 accumulation in TMEM.
 //
-// One CTA computes one 128 x NT output tile (NT <= 256, a multiple of 16).
-// Operands are staged from global memory into shared memory with cp.async in
-// the canonical no-swizzle UMMA layouts (8 x 16-byte core matrices), two
-// K-chunks of 64 in flight; one elected thread issues tcgen05.mma
-// (kind::f16, M = 128, N = NT, K = 16) and commits each chunk to an mbarrier
-// that frees its buffer; the 4 warps read the accumulator back with
-// tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = tile rows) for a fused
-// epilogue. Either operand may be K-major (element (r, k) at X[r * ld + k])
-// or MN-major (element (r, k) at X[k * ld + r]).
+// Output tiles of 128 x NT (NT <= 256, a multiple of 16). Operands are staged
+// from global memory into shared memory with cp.async in the canonical
+// no-swizzle UMMA layouts (8 x 16-byte core matrices, K chunks of 64); one
+// lane issues tcgen05.mma (kind::f16, M = 128, N = NT, K = 16) and commits
+// each chunk to an mbarrier; the accumulator is read back with tcgen05.ld
+// (warp w owns TMEM lanes 32 (w mod 4)..) for a fused epilogue. Either operand
+// may be K-major (element (r, k) at X[r * ld + k]) or MN-major (element (r, k)
+// at X[k * ld + r]). The kernel itself is in gemm.cu.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -21,7 +20,7 @@ namespace tc {
 
 constexpr int kM = 128;       // tile rows = TMEM lanes
 constexpr int kKC = 64;       // K elements per staged chunk
-constexpr int kThreads = 128; // 4 warps: loaders + epilogue; thread 0 issues MMAs
+constexpr int kThreads = 128; // default stride of the staging loop
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

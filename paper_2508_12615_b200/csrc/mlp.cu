@@ -10,9 +10,10 @@
 // the head GEMM adds its bias in fp32; k_mlp_apply forms the frame rows.
 // Backward: k_mlp_dout builds dL/dout (13 columns, bf16 for the GEMMs, fp32
 // for the head bias); per layer one split-K GEMM dW = dZ^T In (both operands
-// MN-major straight from the row-major activations, atomic fp32 epilogue),
-// a column sum for db, and one GEMM dIn = dZ W (W read MN-major) whose
-// epilogue applies the ReLU mask of the layer below.
+// MN-major straight from the row-major activations, atomic fp32 epilogue) and
+// one GEMM dIn = dZ W (W read MN-major) whose epilogue applies the ReLU mask
+// of the layer below and sums the result over the rows (that layer's bias
+// gradient).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -182,6 +183,28 @@ __global__ void __launch_bounds__(128) k_mlp_dout(int64_t N, int64_t M, const fl
   }
 }
 
+// Head-bias gradient: column sums of dL/dout (fp32) over the rows.
+__global__ void __launch_bounds__(256) k_mlp_dout_colsum(const float* df, int64_t M, float* gb) {
+  __shared__ float part[8][13];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc[13];
+  for (int d = 0; d < 13; ++d) acc[d] = 0.f;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M;
+       m += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < 13; ++d) acc[d] += df[m * kOutCols + d];
+  for (int d = 0; d < 13; ++d) {
+    float x = acc[d];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) part[w][d] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 13) {
+    float x = 0.f;
+    for (int k = 0; k < 8; ++k) x += part[k][threadIdx.x];
+    atomicAdd(gb + threadIdx.x, x);
+  }
+}
+
 // Canonical gradients: sums over the F frames (fixed order: deterministic).
 __global__ void __launch_bounds__(128) k_mlp_canon(int64_t N, int32_t F, const float* out,
                                                    wipes_grads gf, wipes_grads gc) {
@@ -201,22 +224,6 @@ __global__ void __launch_bounds__(128) k_mlp_canon(int64_t N, int32_t F, const f
   if (gc.freq) for (int d = 0; d < 3; ++d) gc.freq[3 * i + d] = gfr[d];
 }
 
-// Column sums of a [M, ncols] matrix (row stride ld) into dst[ncols] (atomic).
-template <typename T>
-__global__ void __launch_bounds__(256) k_colsum(const T* src, int64_t ld, int64_t M, int ncols,
-                                                float* dst) {
-  const int c = threadIdx.x;
-  if (c >= ncols) return;
-  const int64_t per = (M + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = per * blockIdx.x, r1 = r0 + per < M ? r0 + per : M;
-  float acc = 0.f;
-  for (int64_t r = r0; r < r1; ++r) {
-    if constexpr (sizeof(T) == 2) acc += __bfloat162float(src[r * ld + c]);
-    else acc += (float)src[r * ld + c];
-  }
-  if (r1 > r0) atomicAdd(dst + c, acc);
-}
-
 // Padded dW scratch [rows, Kp] -> theta-gradient layout (true widths).
 __global__ void k_mlp_unpad(const float* dws, int rows, int Kp, int E, int E8, int K,
                             bool has_cat, float* g) {
@@ -231,8 +238,10 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t gemm(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                  int64_t lda, int64_t ldb, int64_t ldc, int epi, bool amn, bool bmn,
-                 const float* bias, const void* mask, int64_t ldm, int split, cudaStream_t s) {
+                 const float* bias, const void* mask, int64_t ldm, int split, cudaStream_t s,
+                 float* colsum = nullptr) {
   wipes_gemm_args g;
+  g.colsum = colsum;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.mask = mask;
   g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.ldm = ldm;
   g.a_mn_major = amn; g.b_mn_major = bmn; g.epilogue = epi; g.split_k = split;
@@ -332,7 +341,6 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const unsigned cs_grid = (unsigned)(M < 4 * sms * 64 ? (M + 63) / 64 : 4 * sms);
   auto split_for = [&](int64_t tiles) {  // split-K so that ~2 CTAs per SM run
     int64_t sp = (2 * sms + tiles - 1) / tiles;
     const int64_t chunks = (M + 63) / 64;
@@ -353,12 +361,12 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
                                                            g_theta + L.thWh);
   launch_end(K_MLP_MISC, s);
   launch_begin(K_MLP_MISC, s);
-  k_colsum<float><<<cs_grid, 256, 0, s>>>(dfp, kOutCols, M, 13, g_theta + L.thbh);
+  k_mlp_dout_colsum<<<2 * sms, 256, 0, s>>>(dfp, M, g_theta + L.thbh);
   launch_end(K_MLP_MISC, s);
   __nv_bfloat16* dz = (__nv_bfloat16*)(ws + L.dz[0]);
   __nv_bfloat16* dz2 = (__nv_bfloat16*)(ws + L.dz[1]);
   e = gemm(dbf, ws + L.whbf, dz, M, L.W, kOutCols, kOutCols, L.W, L.W, WIPES_GEMM_EPI_MASK_BF16,
-           false, true, nullptr, hl, ldh, 1, s);
+           false, true, nullptr, hl, ldh, 1, s, g_theta + L.thb[last]);
   if (e != cudaSuccess) return e;
   for (int l = last; l >= 0; --l) {
     // dz = dL/dz_l [M, W]; input of layer l:
@@ -378,16 +386,14 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
     k_mlp_unpad<<<nblk((int64_t)L.W * L.K[l], 256), 256, 0, s>>>(
         dws, L.W, L.Kp[l], L.E, L.E8, L.K[l], has_cat, g_theta + L.thW[l]);
     launch_end(K_MLP_MISC, s);
-    launch_begin(K_MLP_MISC, s);
-    k_colsum<__nv_bfloat16><<<cs_grid, 256, 0, s>>>(dz, L.W, M, L.W, g_theta + L.thb[l]);
-    launch_end(K_MLP_MISC, s);
     if (l == 0) break;
     // dz_(l-1) = (dz W_l)[:, h part] * (h_(l-1) > 0)
     const __nv_bfloat16* wl = (const __nv_bfloat16*)(ws + L.wbf[l]) + (has_cat ? L.E8 : 0);
     const void* mask = (l - 1 == L.skip) ? (const void*)(cat + L.E8) : (const void*)(ws + L.h[l - 1]);
     const int64_t ldm = (l - 1 == L.skip) ? L.catw : L.W;
+    // its epilogue also sums dz_(l-1) over the rows: the bias gradient of layer l-1
     e = gemm(dz, wl, dz2, M, L.W, L.W, L.W, L.Kp[l], L.W, WIPES_GEMM_EPI_MASK_BF16, false, true,
-             nullptr, mask, ldm, 1, s);
+             nullptr, mask, ldm, 1, s, g_theta + L.thb[l - 1]);
     if (e != cudaSuccess) return e;
     __nv_bfloat16* t = dz; dz = dz2; dz2 = t;
   }
