@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-fit", action="store_true",
                     help="skip the NEXT-2 fitting-step measurement (2D configs)")
+    ap.add_argument("--no-mlp", action="store_true",
+                    help="skip the NEXT-4 deformation-MLP measurement")
+    ap.add_argument("--mlp-rows", type=int, default=300000,
+                    help="rows (primitives x frames) of the NEXT-4 MLP measurement")
     ap.add_argument("--sh", type=int, default=None,
                     help="3D configs: SH colour of this degree (NEXT-3) instead of flat RGB")
     ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
@@ -147,6 +151,54 @@ def fit_rate(H, W, N, args, flush, dev):
             "steps_applied": fit.steps_taken(),
             "workload": f"NEXT-2 image fit {W}x{H}, {N} Cholesky primitives, L2 + Adam "
                         "(preprocess, bin/sort, render, loss, backward, Adam: one CUDA graph)"}
+
+
+def mlp_rate(args, flush, dev, peaks):
+    """NEXT-4: the D-3DGS-shaped deformation field (8 x 256, skip 4, Lx 10,
+    Lt 6) forward + backward on the tcgen05 tensor cores for args.mlp_rows
+    rows (C4's 300k primitives x 1 frame, one D-3DGS training iteration),
+    CUDA-event timed over args.steps iterations (L2 flushed between)."""
+    import torch
+    from paper_2508_12615_b200 import gen
+    from paper_2508_12615_b200.deform import Deformation
+    N = args.mlp_rows
+    d = Deformation(N)
+    theta = d.init_theta(seed=args.seed, head_scale=0.1)
+    p = gen.gen3d(N, seed=args.seed)
+    canon = {k: torch.from_numpy(v).to(dev) for k, v in p.items()}
+    frame = d.forward(theta, canon, [0.5])
+    g = {k: torch.randn_like(frame[k]) for k in ("mean", "quat", "scale", "freq")}
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush.zero_()
+        d.forward(theta, canon, [0.5], frame)
+        d.backward(theta, canon, g)
+    torch.cuda.synchronize()
+    fwd = bwd = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        d.forward(theta, canon, [0.5], frame)
+        e[1].record(stream)
+        d.backward(theta, canon, g)
+        e[2].record(stream)
+        e[2].synchronize()
+        fwd += e[0].elapsed_time(e[1])
+        bwd += e[1].elapsed_time(e[2])
+    fwd /= args.steps
+    bwd /= args.steps
+    fl = sum(2 * d.width * d.layer_in(l) for l in range(d.depth)) + 2 * 13 * d.width
+    fwd_fl = N * fl
+    bwd_fl = N * (2 * fl - 2 * d.width * d.layer_in(0))
+    peak = float(peaks.get("bf16_tflops", 1695.0))
+    ach = (fwd_fl + bwd_fl) / ((fwd + bwd) / 1e3) / 1e12
+    return {"workload": f"NEXT-4 deformation MLP (D-3DGS 8x256, skip 4, PE 10/6), {N} rows, "
+                        "forward + backward, bf16 tcgen05 GEMMs with fp32 accumulation",
+            "fwd_ms": fwd, "bwd_ms": bwd, "iters_per_s": 1e3 / (fwd + bwd),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
 
 
 def cpu_oracle_sample(c, npix, seed):
@@ -419,6 +471,8 @@ def main():
                              "Mip-NeRF360 95.7 (Table 2, PAPER.md:239)"}
     if c["kind"] == "2d" and not rows and not args.no_fit:
         line["fit"] = fit_rate(H, W, N, args, flush, dev)
+    if not args.no_mlp and (c["kind"] == "6d" or name == "c2"):
+        line["mlp"] = mlp_rate(args, flush, dev, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fac, cores = cpu_oracle_sample(c, args.cpu_pixels, seed=123)
         line["cpu_baseline"] = {"value": 1.0 / (dt * fac), "unit": "iters/s", "cores": cores,
