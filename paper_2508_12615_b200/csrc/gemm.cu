@@ -1,6 +1,11 @@
 // tcgen05 GEMM with fused epilogues (NEXT-4 building block; see gemm_tc.cuh).
 // Persistent warp-specialised kernel; the per-chunk primitives are in gemm_tc.cuh.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "gemm_tc.cuh"
 
@@ -85,10 +90,17 @@ struct WsCarve {
   uint32_t a, b, bar, stages, bres, bytes;
 };
 
-template <int NT>
+// B bytes per K chunk: NT x 64 bf16; an MN-major TMA panel is whole 64-wide
+// atoms (64 x 64 bf16 = 8 KB each).
+template <int NT, bool BMN, bool TMA>
+__host__ __device__ constexpr uint32_t b_chunk_bytes() {
+  return (TMA && BMN) ? (uint32_t)((NT + 63) / 64) * 8192u : (uint32_t)NT * kKC * 2;
+}
+
+template <int NT, bool BMN = false, bool TMA = false>
 __host__ __device__ inline WsCarve ws_carve(int64_t K, int64_t split) {
   WsCarve c;
-  const uint32_t a_st = kM * kKC * 2, b_st = NT * kKC * 2;
+  const uint32_t a_st = kM * kKC * 2, b_st = b_chunk_bytes<NT, BMN, TMA>();
   const int64_t nch = (K + kKC - 1) / kKC;
   const uint32_t tail = 1024;  // barriers + tmem slot
   const uint64_t bres_bytes = (uint64_t)nch * b_st;
@@ -244,8 +256,17 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
   }
 }
 
-template <int NT, bool AMN, bool BMN, int EPI>
-__global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args g) {
+// Kernel parameters: the ABI arguments plus, for the TMA path, one tensor map
+// per operand (128-byte swizzle; K-major boxes 64 x rows, MN-major boxes
+// 64 x 64) built on the host.
+struct GemmParams {
+  wipes_gemm_args g;
+  CUtensorMap ta, tb;
+};
+
+template <int NT, bool AMN, bool BMN, int EPI, bool TMA>
+__global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant__ GemmParams P) {
+  const wipes_gemm_args& g = P.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int kCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
   constexpr int kAlloc = 2 * kCols;
@@ -258,17 +279,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args
   const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(g.A);
   const __nv_bfloat16* B = reinterpret_cast<const __nv_bfloat16*>(g.B);
   // B stays resident (loaded once per CTA) when there is one N tile and no K split
-  const WsCarve cv = ws_carve<NT>(g.K, (splits > 1 || ntiles > 1) ? 2 : 1);
+  const WsCarve cv = ws_carve<NT, BMN, TMA>(g.K, (splits > 1 || ntiles > 1) ? 2 : 1);
   const int S = (int)cv.stages;
-  __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(smem_raw + cv.a);
-  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(smem_raw + cv.b);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + cv.bar);
+  // 128-byte swizzle atoms need 1024-byte aligned buffers (the launch adds 1 KB)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(base + cv.a);
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(base + cv.b);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + cv.bar);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
-  constexpr int kAst = kM * kKC, kBst = NT * kKC;  // elements per stage / chunk
+  constexpr int kAst = kM * kKC;                                // A elements per stage
+  constexpr int kBst = b_chunk_bytes<NT, BMN, TMA>() / 2;      // B elements per chunk
 
   if (warp == kAllocWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -278,14 +302,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args
   }
   if (tid == 0) {
     for (int i = 0; i < kMaxStages; ++i) {
-      mbar_init(&full[i], kProd);
+      mbar_init(&full[i], TMA ? 1 : kProd);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * kEpiWarps);
     }
-    mbar_init(bfull, kProd);
+    mbar_init(bfull, TMA ? 1 : kProd);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -302,7 +326,44 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args
     nch = c_hi > c_lo ? c_hi - c_lo : 0;
   };
 
-  if (warp < kProdWarps) {  // ------------------------------------- producers
+  // TMA loads of one K chunk: K-major = one box (64 K x rows); MN-major = one
+  // 64 x 64 box per 64-wide M/N atom.
+  auto tma_a = [&](__nv_bfloat16* dst, int64_t m0, int64_t k0, uint64_t* bar) {
+    if (!AMN) tma_load_2d(dst, &P.ta, (int)k0, (int)m0, bar);
+    else
+      for (int q = 0; q < kM / 64; ++q) tma_load_2d(dst + q * 4096, &P.ta, (int)(m0 + 64 * q), (int)k0, bar);
+  };
+  auto tma_b = [&](__nv_bfloat16* dst, int64_t n0, int64_t k0, uint64_t* bar) {
+    if (!BMN) tma_load_2d(dst, &P.tb, (int)k0, (int)n0, bar);
+    else
+      for (int q = 0; q < (NT + 63) / 64; ++q)
+        tma_load_2d(dst + q * 4096, &P.tb, (int)(n0 + 64 * q), (int)k0, bar);
+  };
+  constexpr uint32_t kABytes = kM * kKC * 2, kBBytes = b_chunk_bytes<NT, BMN, TMA>();
+
+  if (TMA && warp == 0) {  // ------------------------------ TMA producer (1 lane)
+    if (lane == 0) {
+      int64_t it = 0, loaded_n0 = -1;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t m0, n0, c_lo, nch;
+        tile_coords(t, m0, n0, c_lo, nch);
+        if (cv.bres && n0 != loaded_n0) {
+          mbar_expect_tx(bfull, (uint32_t)(nchunk_all * kBBytes));
+          for (int64_t c = 0; c < nchunk_all; ++c) tma_b(sb + c * kBst, n0, c * kKC, bfull);
+          loaded_n0 = n0;
+        }
+        for (int64_t c = 0; c < nch; ++c, ++it) {
+          const int st = (int)(it % S);
+          const uint32_t round = (uint32_t)(it / S);
+          mbar_wait(&empty[st], (round & 1u) ^ 1u);
+          const int64_t k0 = (c_lo + c) * kKC;
+          mbar_expect_tx(&full[st], kABytes + (cv.bres ? 0u : kBBytes));
+          tma_a(sa + st * kAst, m0, k0, &full[st]);
+          if (!cv.bres) tma_b(sb + st * kBst, n0, k0, &full[st]);
+        }
+      }
+    }
+  } else if (!TMA && warp < kProdWarps) {  // --------------------- producers
     int64_t it = 0, loaded_n0 = -1;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
       int64_t m0, n0, c_lo, nch;
@@ -346,17 +407,25 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args
         const int st = (int)(it % S);
         const uint32_t round = (uint32_t)(it / S);
         mbar_wait(&full[st], round & 1u);
-        fence_proxy_async();
+        if (!TMA) fence_proxy_async();  // cp.async (generic proxy) -> tensor core reads
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(sa + st * kAst);
           const uint32_t b0 = smem_u32(sb + (cv.bres ? (c_lo + c) : st) * kBst);
-#ifndef WIPES_GEMM_DBG_NO_MMA
 #pragma unroll
-          for (int j = 0; j < kKC / 16; ++j)
-            mma_bf16(d, smem_desc(a0 + 256 * j, 128, 1024), smem_desc(b0 + 256 * j, 128, 1024),
-                     idesc, (c > 0 || j > 0) ? 1u : 0u);
-#endif
+          for (int j = 0; j < kKC / 16; ++j) {
+            uint64_t da, db;
+            if (TMA) {  // 128-byte swizzled tiles written by TMA
+              da = AMN ? smem_desc_sw128(a0 + 2048 * j, 8192, 1024)
+                       : smem_desc_sw128(a0 + 32 * j, 16, 1024);
+              db = BMN ? smem_desc_sw128(b0 + 2048 * j, 8192, 1024)
+                       : smem_desc_sw128(b0 + 32 * j, 16, 1024);
+            } else {
+              da = smem_desc(a0 + 256 * j, 128, 1024);
+              db = smem_desc(b0 + 256 * j, 128, 1024);
+            }
+            mma_bf16(d, da, db, idesc, (c > 0 || j > 0) ? 1u : 0u);
+          }
           mma_commit(&empty[st]);
         }
         __syncwarp();
@@ -390,9 +459,40 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const wipes_gemm_args
                  "n"(kAlloc));
 }
 
-template <int NT, bool AMN, bool BMN, int EPI>
-cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
-  auto k = k_gemm_ws<NT, AMN, BMN, EPI>;
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Tensor map of a bf16 operand with `rows` M/N rows and K columns.
+bool make_tmap(CUtensorMap* m, const void* ptr, bool mn, int64_t rows, int64_t K, int64_t ld,
+               int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2], strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2], es[2] = {1, 1};
+  if (!mn) { dims[0] = (cuuint64_t)K; dims[1] = (cuuint64_t)rows; box[0] = 64; box[1] = (cuuint32_t)box_rows; }
+  else { dims[0] = (cuuint64_t)rows; dims[1] = (cuuint64_t)K; box[0] = 64; box[1] = 64; }
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int NT, bool AMN, bool BMN, int EPI, bool TMA>
+cudaError_t launch_ws_t(const GemmParams& P, cudaStream_t s) {
+  const wipes_gemm_args& g = P.g;
+  auto k = k_gemm_ws<NT, AMN, BMN, EPI, TMA>;
   static int sms = 0;
   if (!sms) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
@@ -402,13 +502,28 @@ cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
   }
   const int64_t ntiles = (g.N + NT - 1) / NT;
   const int64_t splits = g.split_k > 0 ? g.split_k : 1;
-  const WsCarve cv = ws_carve<NT>(g.K, (splits > 1 || ntiles > 1) ? 2 : 1);  // as the kernel
+  const WsCarve cv = ws_carve<NT, BMN, TMA>(g.K, (splits > 1 || ntiles > 1) ? 2 : 1);
   const int64_t tiles = ((g.M + kM - 1) / kM) * ntiles * splits;
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   launch_begin(K_GEMM, s);
-  k<<<grid, kWsThreads, cv.bytes + 1024, s>>>(g);
+  k<<<grid, kWsThreads, cv.bytes + 1024, s>>>(P);
   launch_end(K_GEMM, s);
   return cudaGetLastError();
+}
+
+template <int NT, bool AMN, bool BMN, int EPI>
+cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
+  static const bool cpasync = getenv("WIPES_GEMM_CPASYNC") != nullptr;
+  GemmParams P;
+  P.g = g;
+  std::memset(&P.ta, 0, sizeof(P.ta));
+  std::memset(&P.tb, 0, sizeof(P.tb));
+  // TMA needs 16-byte aligned bases and row pitches (lda, ldb multiples of 8)
+  const bool tma = !cpasync && (uintptr_t)g.A % 16 == 0 && (uintptr_t)g.B % 16 == 0 &&
+                   make_tmap(&P.ta, g.A, AMN, g.M, g.K, g.lda, kM) &&
+                   make_tmap(&P.tb, g.B, BMN, g.N, g.K, g.ldb, NT);
+  if (tma) return launch_ws_t<NT, AMN, BMN, EPI, true>(P, s);
+  return launch_ws_t<NT, AMN, BMN, EPI, false>(P, s);
 }
 
 template <int NT, bool AMN, bool BMN, int EPI>

@@ -38,6 +38,29 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return d;  // base offset 0, legacy LBO mode, layout type 0 (no swizzle)
 }
 
+// SWIZZLE_128B variant (layout type 2 at bits [61, 64)): K-major tiles are
+// 128-byte rows (64 bf16 of K) in 8-row atoms (SBO = 1024 B, LBO unused = 16 B);
+// MN-major tiles are 128-byte rows (64 bf16 of M/N) along K in 8-row atoms
+// (SBO = 1024 B) with LBO = the distance between 64-wide M/N atoms.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return smem_desc(addr, lbo, sbo) | ((uint64_t)2 << 61);
+}
+
+// TMA: 2-D tiled tensor load into shared memory, completing on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
 // Instruction descriptor: bf16 x bf16 -> fp32, dense, M = 128, N = n.
 __device__ __forceinline__ uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
   uint32_t d = 0;
