@@ -94,7 +94,12 @@ typedef struct {
   float det_min;          /* cull if det(Sigma') < det_min (1e-12)             */
   int32_t ewa_clamp;      /* 1: clamp x/z, y/z at 1.3 x half-FOV inside J      */
   float background[3];    /* ALPHA only                                        */
-  int32_t deterministic;  /* reserved (must be 0 in ABI v2)                    */
+  int32_t deterministic;  /* 1: bitwise run-to-run deterministic backward: each
+                           * warp writes its per-record moments to a slot per
+                           * (intersection, footprint) and a gather sums a
+                           * record's slots in a fixed order (no float atomics);
+                           * the workspace grows by dup_capacity x footprints
+                           * x 48 (52 with WIPES_PROJ_EXACT) bytes. */
   /* Image-space sharding: when row_mod > 1 only tile rows ty
    * with ty % row_mod == row_rem are binned and rendered (the rest of the image
    * is left unbinned: zero in SUM mode, background in ALPHA mode, no gradient).

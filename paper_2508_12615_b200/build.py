@@ -27,6 +27,11 @@ SOURCES = {
     "render.cu": [],
     "train.cu": [],
     "gemm.cu": [],
+    "gemm_e0.cu": [],
+    "gemm_e1.cu": [],
+    "gemm_e2.cu": [],
+    "gemm_e3.cu": [],
+    "gemm_e4.cu": [],
     "mlp.cu": [],
     "abi.cu": [],
 }
@@ -48,12 +53,20 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     newest = max(os.path.getmtime(d) for d in deps)
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
         return lib
-    objs = []
-    for src, extra in SOURCES.items():
+    def compile_one(item):
+        src, extra = item
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
         cmd = [_nvcc(), *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES.items()))
+    objs = []
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed for {src}")

@@ -43,7 +43,7 @@ const char* kNames[K_NUM] = {
     "preprocess2d", "preprocess3d", "scan_blocks", "scan_sums", "duplicate", "radix_hist",
     "radix_scan_blocks", "radix_scan_sums", "radix_scatter", "tile_ranges", "render_fwd",
     "render_bwd", "preprocess2d_bwd", "preprocess3d_bwd", "memset", "tile_order", "loss_l2",
-    "adam", "sh_bwd", "gemm_tc", "mlp_misc"};
+    "adam", "sh_bwd", "gemm_tc", "mlp_misc", "det_gather"};
 
 wipes_status fail(wipes_status s, const std::string& msg) {
   g_last_error = msg;
@@ -76,8 +76,7 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
     return fail(WIPES_EINVAL, "color_mode SH needs 3D primitives");
   if (c->color_mode == WIPES_COLOR_SH && (c->sh_degree < 0 || c->sh_degree > 3))
     return fail(WIPES_EINVAL, "sh_degree must be in 0..3");
-  if (c->deterministic != 0)
-    return fail(WIPES_EUNSUPPORTED, "deterministic reduction is not built in ABI v2");
+  if (c->deterministic != 0 && c->deterministic != 1) return fail(WIPES_EINVAL, "deterministic");
   if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
     return fail(WIPES_EINVAL, "need 0 <= alpha_min < alpha_max <= 1");
   if (!(c->T_min >= 0.f) || !(c->T_min < 1.f)) return fail(WIPES_EINVAL, "T_min");
@@ -204,9 +203,7 @@ wipes_status wipes_bin_sort(const wipes_config* cfg, int64_t N, int32_t B, void*
   cudaError_t e = launch_bin_sort(*cfg, L, w, s, &fb);
   if (e != cudaSuccess) return cuda_fail(e, "bin_sort launch");
   if (keys_out && L.cap) e = launch_keys64(L, w, fb, keys_out, s);
-  if (e == cudaSuccess && vals_out && L.cap)
-    e = cudaMemcpyAsync(vals_out, w + (fb ? L.valsB : L.valsA), 4 * L.cap,
-                        cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && vals_out && L.cap) e = launch_vals_copy(L, w, fb, vals_out, s);
   if (e == cudaSuccess && tile_offsets_out)
     e = cudaMemcpyAsync(tile_offsets_out, w + L.toff, 4 * (L.BT + 1), cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "bin_sort copies");
@@ -291,11 +288,17 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
     launch_begin(K_MEMSET, s);
     e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kMoments * L.BN, s);
     if (e == cudaSuccess && L.exact) e = cudaMemsetAsync(w + L.rbeta, 0, sizeof(float) * L.BN, s);
+    if (e == cudaSuccess && L.det && L.cap)
+      e = cudaMemsetAsync(w + L.slots, 0, sizeof(float) * (size_t)L.cap * L.fps * L.slotw, s);
     launch_end(K_MEMSET, s);
     if (e != cudaSuccess) return cuda_fail(e, "rgrad memset");
   }
   e = launch_render_bwd(*cfg, L, w, final_buffer_is_b(L), dL_dimage, T_final, n_contrib, s);
   if (e != cudaSuccess) return cuda_fail(e, "render_bwd launch");
+  if (L.det) {
+    e = launch_det_gather(L, w, s);
+    if (e != cudaSuccess) return cuda_fail(e, "det_gather launch");
+  }
   e = cfg->prim == WIPES_PRIM_2D ? launch_preprocess2d_bwd(*cfg, *params, L, w, *grads, s)
                                  : launch_preprocess3d_bwd(*cfg, *params, L, cams, w, *grads, s);
   if (e != cudaSuccess) return cuda_fail(e, "preprocess_bwd launch");

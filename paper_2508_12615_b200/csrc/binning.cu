@@ -123,6 +123,7 @@ struct DupArgs {
   int32_t GX, row_mod, row_rem;
   uint32_t* keys;
   uint32_t* vals;
+  uint32_t* prevals;  // deterministic mode: vals[j] = j, prevals[j] = primitive
 };
 
 // Warp-cooperative emission: the 32 records of a warp own one contiguous
@@ -183,7 +184,12 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
       const int t = (int)(j - so);
       const int row = t / ow, col = t - row * ow;
       a.keys[j] = ovt + (uint32_t)(oty + row * dty) * (uint32_t)a.GX + (uint32_t)(ox + col);
-      a.vals[j] = oi;
+      if (a.prevals) {
+        a.vals[j] = (uint32_t)j;
+        a.prevals[j] = oi;
+      } else {
+        a.vals[j] = oi;
+      }
     }
   }
 }
@@ -219,13 +225,14 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, const
 
 // 64-bit (tile << 32 | depth bits) keys of the sorted pairs, for parity copies.
 __global__ void __launch_bounds__(256) k_keys64(const uint32_t* keys, const uint32_t* vals,
-                                                const uint32_t* dkey, const WsHeader* hdr,
-                                                int64_t cap, int64_t N, int64_t T, int32_t alpha,
-                                                uint64_t* out) {
+                                                const uint32_t* prevals, const uint32_t* dkey,
+                                                const WsHeader* hdr, int64_t cap, int64_t N,
+                                                int64_t T, int32_t alpha, uint64_t* out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= clamp_n(hdr, cap)) return;
   const uint32_t k = keys[j];
-  const uint64_t lo = alpha ? (uint64_t)dkey[(int64_t)(k / T) * N + vals[j]] : 0ull;
+  const uint32_t i = prevals ? prevals[vals[j]] : vals[j];  // primitive of entry j
+  const uint64_t lo = alpha ? (uint64_t)dkey[(int64_t)(k / T) * N + i] : 0ull;
   out[j] = ((uint64_t)k << 32) | lo;
 }
 
@@ -283,7 +290,8 @@ cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint6
   if (L.cap == 0) return cudaSuccess;
   k_keys64<<<(unsigned)((L.cap + 255) / 256), 256, 0, s>>>(
       (const uint32_t*)(ws + (final_in_b ? L.keysB : L.keysA)),
-      (const uint32_t*)(ws + (final_in_b ? L.valsB : L.valsA)), (const uint32_t*)(ws + L.dkey),
+      (const uint32_t*)(ws + (final_in_b ? L.valsB : L.valsA)),
+      L.det ? (const uint32_t*)(ws + L.prevals) : nullptr, (const uint32_t*)(ws + L.dkey),
       (const WsHeader*)(ws + L.hdr), L.cap, L.N, L.T, L.alpha, out);
   return cudaGetLastError();
 }
@@ -370,6 +378,7 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     d.GX = L.GX;
     d.row_mod = c.row_mod; d.row_rem = c.row_rem;
     d.keys = kA; d.vals = vA;
+    d.prevals = L.det ? (uint32_t*)(ws + L.prevals) : nullptr;
     launch_begin(K_DUPLICATE, s);
     k_duplicate<<<gBN, 256, 0, s>>>(d);
     launch_end(K_DUPLICATE, s);
@@ -399,6 +408,67 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
                                          (int32_t*)(ws + L.order));
     launch_end(K_TILE_ORDER, s);
   }
+  return cudaGetLastError();
+}
+
+// Sorted values as primitive ids (deterministic mode stores dup indices).
+__global__ void k_vals_copy(const uint32_t* vals, const uint32_t* prevals, const WsHeader* hdr,
+                            int64_t cap, uint32_t* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cap) return;
+  const int64_t n = hdr->total < cap ? hdr->total : cap;  // entries past the total are unset
+  out[j] = (prevals && j < n) ? prevals[vals[j]] : vals[j];
+}
+
+cudaError_t launch_vals_copy(const Layout& L, const char* ws, int final_in_b, uint32_t* out,
+                             cudaStream_t s) {
+  if (L.cap == 0) return cudaSuccess;
+  const uint32_t* v = (const uint32_t*)(ws + (final_in_b ? L.valsB : L.valsA));
+  k_vals_copy<<<(unsigned)((L.cap + 255) / 256), 256, 0, s>>>(
+      v, L.det ? (const uint32_t*)(ws + L.prevals) : nullptr, (const WsHeader*)(ws + L.hdr),
+      L.cap, out);
+  return cudaGetLastError();
+}
+
+// Deterministic backward, second half: the record at emission position j0
+// sums the moment slots of its dups [start, start + count) over the warp
+// footprints in a fixed order (dups past the capacity were never rendered).
+__global__ void __launch_bounds__(128) k_det_gather(const int32_t* count, const uint32_t* order,
+                                                    const int64_t* loc, const int64_t* blk,
+                                                    int64_t BN, int64_t cap, int fps, int slotw,
+                                                    const float* slots, float* mom,
+                                                    float* mom_beta) {
+  const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j0 >= BN) return;
+  const int64_t o = order ? (int64_t)order[j0] : j0;
+  const int32_t n = count[o];
+  const int64_t start = loc[j0] + blk[j0 / kScanTile];
+  float acc[kMoments + 1];
+  for (int k = 0; k <= kMoments; ++k) acc[k] = 0.f;
+  const int64_t end = start + n < cap ? start + n : cap;
+  for (int64_t j = start; j < end; ++j)
+    for (int f = 0; f < fps; ++f) {
+      const float* sl = slots + (j * fps + f) * slotw;
+      for (int k = 0; k < slotw; ++k) acc[k] += sl[k];
+    }
+  for (int k = 0; k < kMoments; ++k) mom[o * kMoments + k] = acc[k];
+  if (mom_beta) mom_beta[o] = acc[kMoments];
+}
+
+cudaError_t launch_det_gather(const Layout& L, char* ws, cudaStream_t s) {
+  if (L.BN == 0) return cudaSuccess;
+  const bool pre = L.alpha;  // ALPHA emits in the depth-presorted order
+  const uint32_t* order = pre ? ((L.pre_passes & 1) ? (const uint32_t*)(ws + L.pvB)
+                                                    : (const uint32_t*)(ws + L.pvA))
+                              : nullptr;
+  const int64_t* loc = (const int64_t*)(ws + (pre ? L.loc2 : L.loc_off));
+  const int64_t* blk = (const int64_t*)(ws + (pre ? L.blk2 : L.blk_sum));
+  launch_begin(K_DET_GATHER, s);
+  k_det_gather<<<(unsigned)((L.BN + 127) / 128), 128, 0, s>>>(
+      (const int32_t*)(ws + L.count), order, loc, blk, L.BN, L.cap, L.fps, L.slotw,
+      (const float*)(ws + L.slots), (float*)(ws + L.rgrad),
+      L.exact ? (float*)(ws + L.rbeta) : nullptr);
+  launch_end(K_DET_GATHER, s);
   return cudaGetLastError();
 }
 

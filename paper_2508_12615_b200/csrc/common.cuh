@@ -69,12 +69,15 @@ struct Layout {
   int32_t hi_bits = 0, passes = 0, pre_passes = 0;  // dup-sort / depth-presort passes
   int32_t alpha = 0;
   int32_t exact = 0;       // 3D exact z-integration: extra beta moment per record
+  int32_t det = 0;         // deterministic backward: per-(dup, footprint) moment slots
+  int32_t fps = 1;         // warp footprints per tile (render work items per tile)
+  int32_t slotw = 0;       // floats per slot (12 moments [+ beta])
   int64_t nblk_scan = 0;   // blocks of the count scan
   int64_t sort_tiles = 0;  // onesweep tiles of kSortTile keys
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
          pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
-         order = 0, rgrad = 0, rbeta = 0, rdc = 0, total = 0;
+         order = 0, rgrad = 0, rbeta = 0, rdc = 0, prevals = 0, slots = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -144,6 +147,15 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   // SH colour: the records' colour gradients, compacted for the SH backward
   const bool sh = c.prim == WIPES_PRIM_3D && c.color_mode == WIPES_COLOR_SH;
   L.rdc = take(sizeof(float) * 3 * (sh ? L.BN : 0));
+  // Deterministic backward (cfg.deterministic): the sorted values are dup
+  // indices j (prevals[j] = primitive), the render backward writes each
+  // warp's per-record moments to slot (j, footprint) and a gather sums a
+  // record's slots in a fixed order (no float atomics).
+  L.det = c.deterministic != 0;
+  L.fps = (c.tile / 8) * (c.tile >= 16 ? c.tile / 16 : 1);
+  L.slotw = kMoments + (L.exact ? 1 : 0);
+  L.prevals = take(sizeof(uint32_t) * (L.det ? L.cap : 0));
+  L.slots = take(sizeof(float) * (L.det ? (size_t)L.cap * L.fps * L.slotw : 0));
   L.total = o;
   return L;
 }
@@ -152,7 +164,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
 enum KernelId {
   K_PRE2D = 0, K_PRE3D, K_SCAN_BLOCKS, K_SCAN_SUMS, K_DUPLICATE, K_RADIX_HIST,
   K_RADIX_SCAN_BLOCKS, K_RADIX_SCAN_SUMS, K_RADIX_SCATTER, K_TILE_RANGES, K_RENDER_FWD,
-  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_SH_BWD, K_GEMM, K_MLP_MISC, K_NUM
+  K_RENDER_BWD, K_PRE2D_BWD, K_PRE3D_BWD, K_MEMSET, K_TILE_ORDER, K_LOSS, K_ADAM, K_SH_BWD, K_GEMM, K_MLP_MISC, K_DET_GATHER, K_NUM
 };
 
 // Camera block passed BY VALUE as a kernel parameter (no H2D copy; graph
@@ -170,6 +182,9 @@ void launch_end(int kid, cudaStream_t s);
 // ---- launchers (defined in the .cu files) ----------------------------------
 size_t train_scratch_bytes();
 cudaError_t launch_gemm(const wipes_gemm_args& g, cudaStream_t s);
+cudaError_t launch_det_gather(const Layout& L, char* ws, cudaStream_t s);
+cudaError_t launch_vals_copy(const Layout& L, const char* ws, int final_in_b, uint32_t* out,
+                             cudaStream_t s);
 bool mlp_config_valid(const wipes_mlp_config& c);
 int64_t mlp_param_count(const wipes_mlp_config& c);
 size_t mlp_workspace_bytes(const wipes_mlp_config& c, int64_t rows);

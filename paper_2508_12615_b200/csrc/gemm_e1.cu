@@ -1,0 +1,8 @@
+// tcgen05 GEMM instantiations for the bias_f32 epilogue (see gemm_impl.cuh).
+#include "gemm_impl.cuh"
+
+namespace wipes {
+cudaError_t launch_gemm_e1(const wipes_gemm_args& g, cudaStream_t s) {
+  return launch_epi<WIPES_GEMM_EPI_BIAS_F32>(g, s);
+}
+}  // namespace wipes

@@ -92,6 +92,9 @@ struct RenderArgs {
   const int32_t* nc_in;
   float* mom;            // [B*N, 12] gradient moments
   float* mom_beta;       // [B*N] exact mode: M12 = sum gw alpha G cos(theta) (dbeta = M12/2)
+  const uint32_t* prevals;  // deterministic mode: sorted vals are dup indices j -> primitive
+  float* slots;             // deterministic mode: [cap, fps, slotw] per-(dup, footprint) moments
+  int32_t fps, slotw;
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
@@ -179,6 +182,7 @@ struct WarpSmem {
   float4 rec[4][32];
   int32_t pid[32];
   int32_t pos[32];
+  int32_t dj[32];  // deterministic mode: dup index of the staged record
 };
 
 // One work item of a warp.
@@ -188,6 +192,7 @@ struct Item {
   float sx0, sy0;  // footprint origin (pixels)
   int start, end;  // record range in the tile list
   int lstart;      // start of the whole tile list (for list positions)
+  int sub;         // footprint index within the tile
 };
 
 template <int TS>
@@ -199,6 +204,7 @@ __device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chu
   if ((int64_t)item >= a.BT * Gm::S * chunks) return false;
   const int chunk = item % chunks;
   const int sub = (item / chunks) % Gm::S;
+  it.sub = sub;
   it.tile = a.order[item / (chunks * Gm::S)];
   WCHECK(it.tile >= 0 && it.tile < a.BT);
   it.v = it.tile / a.T;
@@ -242,10 +248,14 @@ __device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* re
                                            bool valid, int pos, const Item& it, WarpSmem& ws,
                                            int lane) {
   float4 r0, r1, r2, r3;
-  int32_t pid = 0;
+  int32_t pid = 0, dj = 0;
   bool hit = false;
   if (valid) {
     pid = (int32_t)a.vals[idx];
+    if (a.prevals) {  // deterministic mode: the sorted value is the dup index
+      dj = pid;
+      pid = (int32_t)a.prevals[dj];
+    }
     WCHECK(pid >= 0 && pid < a.N);
     const float4* r = recv + 4 * (int64_t)pid;
     r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
@@ -262,6 +272,7 @@ __device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* re
     ws.rec[0][k] = r0; ws.rec[1][k] = r1; ws.rec[2][k] = r2; ws.rec[3][k] = r3;
     ws.pid[k] = pid;
     ws.pos[k] = pos;
+    ws.dj[k] = dj;
   }
   __syncwarp();
   return __popc(bal);
@@ -585,11 +596,17 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
                                     a.alpha_max, T[p], S[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
         const float red = transpose_reduce12(m, lane);
-        if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
         if (EXACT) {
 #pragma unroll
           for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
-          if (lane == 0) atomicAdd(a.mom_beta + vN + ws.pid[i], mb);
+        }
+        if (a.slots) {  // deterministic: this warp's slot of (dup, footprint); no atomics
+          float* sl = a.slots + ((int64_t)ws.dj[i] * a.fps + it.sub) * a.slotw;
+          if (writer) sl[my_m] = red;
+          if (EXACT && lane == 0) sl[kMom] = mb;
+        } else {
+          if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
+          if (EXACT && lane == 0) atomicAdd(a.mom_beta + vN + ws.pid[i], mb);
         }
       }
       __syncwarp();
@@ -680,6 +697,10 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.dLdC = nullptr; ra.T_in = nullptr; ra.nc_in = nullptr;
   ra.mom = (float*)(ws + L.rgrad);
   ra.mom_beta = L.exact ? (float*)(ws + L.rbeta) : nullptr;
+  ra.prevals = L.det ? (const uint32_t*)(ws + L.prevals) : nullptr;
+  ra.slots = L.det ? (float*)(ws + L.slots) : nullptr;
+  ra.fps = L.fps;
+  ra.slotw = L.slotw;
   ra.stats = nullptr;
   return ra;
 }

@@ -94,10 +94,21 @@ def test_einval_null_and_alignment(L):
     assert st == abi.WIPES_EINVAL and b"cams" in L.wipes_last_error()
 
 
-def test_unsupported_modes(L):
-    cfg = abi.make_config(64, 64, prim="2d", deterministic=1)
+def test_bad_modes(L):
+    cfg = abi.make_config(64, 64, prim="2d", deterministic=2)
     st, _ = abi.wipes_preprocess(cfg, _pp(), 10, None, 1, 0x100000, 1 << 30, 100, False, None, None)
-    assert st == abi.WIPES_EUNSUPPORTED
+    assert st == abi.WIPES_EINVAL and b"deterministic" in L.wipes_last_error()
+    cfg = abi.make_config(64, 64, prim="2d", sh_degree=2)
+    st, _ = abi.wipes_preprocess(cfg, _pp(), 10, None, 1, 0x100000, 1 << 30, 100, False, None, None)
+    assert st == abi.WIPES_EINVAL and b"SH" in L.wipes_last_error()
+
+
+def test_deterministic_workspace_has_slots(L):
+    c0 = abi.make_config(64, 64)
+    c1 = abi.make_config(64, 64, deterministic=1)
+    n0 = abi.wipes_workspace_bytes(c0, 1000, 1, 10000)
+    n1 = abi.wipes_workspace_bytes(c1, 1000, 1, 10000)
+    assert n1 - n0 >= 10000 * (4 + 2 * 48)  # prevals + 2 footprints x 12 floats per dup
 
 
 def test_exact_projection_workspace_has_beta_moments(L):

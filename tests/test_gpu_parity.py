@@ -249,6 +249,50 @@ def test_sh_colour_parity(ora, name, blend, deg):
         assert frac <= 1e-3 + 20 * namb / og[k].size, (k, nbad, worst)
 
 
+@pytest.mark.parametrize("kind,blend,extra", [("2d", "sum", {}), ("2d", "alpha", {}),
+                                              ("3d", "alpha", {}), ("3d", "alpha",
+                                                                    {"proj": "exact"})])
+def test_deterministic_backward_bitwise_and_parity(ora, kind, blend, extra):
+    """cfg.deterministic: two backward passes are bitwise equal and
+    match the oracle like the atomic path; integer artefacts unchanged."""
+    if kind == "2d":
+        H = W = 64
+        p = gen.gen2d(H, W, 256, seed=4, freq_std=0.5, phase=True, alpha=(0.2, 1.0),
+                      color_max=1.0 if blend == "alpha" else 0.1, depth=(blend == "alpha"))
+        cams, vs, B, N = None, 0, 1, 256
+        cfg_o = oracle_cfg(ora, "2d", H, W, blend, use_rect=True)
+    else:
+        c = gen.make_config("p3d", seed=1)
+        H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+        p, cams, vs = c["params"], c["cams"], c["view_stride"]
+        cfg_o = oracle_cfg(ora, "3d", H, W, blend, use_rect=True,
+                           exact_proj=extra.get("proj") == "exact")
+    r = gpu_rasterizer(kind, H, W, blend, deterministic=1, **extra)
+    dp = to_dev(p)
+    dL = gen.gen_dLdC(B, H, W, seed=7)
+    outs = []
+    for _ in range(2):
+        out = r.forward(dp, cams, vs) if kind == "3d" else r.forward(dp)
+        g = r.backward(torch.from_numpy(dL).cuda())
+        torch.cuda.synchronize()
+        outs.append((out["image"].clone(), {k: v.clone() for k, v in g.items()}))
+    assert torch.equal(outs[0][0], outs[1][0])
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+    pr = ora.project3d(cfg_o, p, cams, view_stride=vs) if kind == "3d" else ora.project2d(cfg_o, p)
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    og = (ora.chain3d(cfg_o, p, cams, pr, ro["rgrad"], view_stride=vs) if kind == "3d"
+          else ora.chain2d(cfg_o, p, pr, ro["rgrad"]))
+    nbad_pix, namb = pixel_violations(_pixels(_np(outs[0][0])), ro["color"], ro["margin"])
+    assert nbad_pix == 0
+    for k, v in og.items():
+        if k not in outs[0][1]:
+            continue
+        nbad, worst = grad_violations(_np(outs[0][1][k]), v)
+        assert nbad <= 1e-3 * v.size + 20 * namb, (k, nbad, worst)
+
+
 _EXACT_GRADS = """
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')

@@ -164,3 +164,16 @@ def test_fit_overflow_guard_and_recovery():
     fit.fit(5, check_every=2)
     assert fit.steps_taken() == 5
     assert not torch.equal(p0, fit.raw["mean"])
+
+
+def test_fit_deterministic_loss_curve():
+    """same seed + deterministic rasterizer mode => identical loss
+    curve and parameters across runs (no float atomics anywhere in the step)."""
+    runs = []
+    for _ in range(2):
+        fit, _, _ = _fitter(64, 64, 256, seed=3, deterministic=1)
+        hist = fit.fit(40, check_every=10)
+        runs.append((hist, {k: v.clone() for k, v in fit.raw.items()}))
+    assert runs[0][0] == runs[1][0]
+    for k in runs[0][1]:
+        assert torch.equal(runs[0][1][k], runs[1][1][k]), k
