@@ -56,6 +56,8 @@ def parse():
                     help="rows (primitives x frames) of the NEXT-4 MLP measurement")
     ap.add_argument("--sh", type=int, default=None,
                     help="3D configs: SH colour of this degree (NEXT-3) instead of flat RGB")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise deterministic backward (per-intersection moment slots)")
     ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
                     help="3D projection: Eq. 7 as written (default) or NEXT-1 exact z-marginal")
     return ap.parse_args()
@@ -297,7 +299,8 @@ def main():
     r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev,
                    proj=args.proj if c["kind"] != "2d" else "paper",
                    sh_degree=c.get("sh_degree"),
-                   row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0)
+                   row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0,
+                   deterministic=int(args.deterministic))
     params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
     if c["kind"] == "6d":
         pass
@@ -451,7 +454,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{name}: {c['desc']}"
                        + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else "")
-                       + (f" (SH degree {c['sh_degree']} colour)" if c.get("sh_degree") is not None else ""),
+                       + (f" (SH degree {c['sh_degree']} colour)" if c.get("sh_degree") is not None else "")
+                       + (" (deterministic backward)" if args.deterministic else ""),
                        "H": H, "W": W, "N": N, "views": B,
                        "blend": blend, "dup": int(n_tot2),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
