@@ -195,12 +195,25 @@ def mlp_rate(args, flush, dev, peaks):
     bwd_fl = N * (2 * fl - 2 * d.width * d.layer_in(0))
     peak = float(peaks.get("bf16_tflops", 1695.0))
     ach = (fwd_fl + bwd_fl) / ((fwd + bwd) / 1e3) / 1e12
+    # algorithmic HBM bytes of the layer-by-layer schedule (each GEMM streams its
+    # bf16 operands once and writes its output once; weights are L2-resident)
+    E8 = (d.embed_dim + 7) // 8 * 8
+    kp = [E8 if l == 0 else (E8 + d.width if l == d.skip + 1 else d.width) for l in range(d.depth)]
+    fwd_b = N * (2 * E8 + sum(2 * (k + d.width) for k in kp) + 2 * d.width + 4 * 16)
+    bwd_b = N * (sum(2 * (d.width + k) for k in kp) + sum(6 * d.width for _ in kp[1:])
+                 + 2 * 16 + 2 * d.width + 4 * d.width)
+    hbm = float(peaks.get("hbm_gbs", 6464.9))
+    ach_b = (fwd_b + bwd_b) / ((fwd + bwd) / 1e3) / 1e9
     return {"workload": f"NEXT-4 deformation MLP (D-3DGS 8x256, skip 4, PE 10/6), {N} rows, "
                         "forward + backward, bf16 tcgen05 GEMMs with fp32 accumulation",
             "fwd_ms": fwd, "bwd_ms": bwd, "iters_per_s": 1e3 / (fwd + bwd),
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+            "roofline_hbm": {"bound": "hbm", "achieved": ach_b, "peak": hbm, "unit": "GB/s",
+                             "frac": ach_b / hbm,
+                             "bytes": "per layer GEMM: bf16 inputs read once + output written "
+                                      "once (forward), dW and dIn operands (backward)"}}
 
 
 def cpu_oracle_sample(c, npix, seed):
