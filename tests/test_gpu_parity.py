@@ -451,3 +451,39 @@ def test_row_sharding_equals_full(ora, blend, world):
     for k in gfull:
         a, b = _np(gsum[k]), _np(gfull[k])
         assert np.allclose(a, b, rtol=1e-4, atol=1e-6), (k, np.abs(a - b).max())
+
+
+@pytest.mark.parametrize("vs_mode,sh", [("shared", None), ("per_frame", None), ("shared", 2)])
+def test_more_than_128_views(ora, vs_mode, sh):
+    """B = 131 > WIPES_MAX_CAMERAS_PER_LAUNCH: the camera blocks are processed in
+    chunks (preprocess, preprocess backward with accumulation across chunks,
+    SH backward); results equal the oracle's."""
+    N, B, H, W = 60, 131, 32, 32
+    rng = np.random.default_rng(0)
+    base = gen.gen3d(N, seed=2, scale_mult=20.0, sh_degree=sh)
+    cams = [gen.camera((2.5 * np.cos(a), -0.3, 2.5 * np.sin(a)), W, H)
+            for a in np.linspace(0, 2 * np.pi, B, endpoint=False)]
+    if vs_mode == "per_frame":
+        p = {k: np.concatenate([v] * B, 0) for k, v in base.items()}
+        p["mean"] = (p["mean"] + rng.normal(0, 0.01, p["mean"].shape)).astype(np.float32)
+        vs = N
+    else:
+        p, vs = base, 0
+    cfg_o = oracle_cfg(ora, "3d", H, W, "alpha", use_rect=True, sh_degree=sh)
+    pr = ora.project3d(cfg_o, p, cams, view_stride=vs)
+    r = gpu_rasterizer("3d", H, W, "alpha", sh_degree=sh)
+    out = r.forward(to_dev(p), cams, vs)
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    dL = gen.gen_dLdC(B, H, W, seed=3)
+    ro = ora.render(cfg_o, pr, dLdC=_pixels(dL))
+    nbad, namb = pixel_violations(_pixels(_np(out["image"])), ro["color"], ro["margin"])
+    assert nbad == 0
+    grads = r.backward(torch.from_numpy(dL).cuda())
+    torch.cuda.synchronize()
+    og = ora.chain3d(cfg_o, p, cams, pr, ro["rgrad"], view_stride=vs)
+    for k, v in og.items():
+        if k not in grads:
+            continue
+        nbad, worst = grad_violations(_np(grads[k]), v)
+        assert nbad <= 1e-3 * v.size + 20 * namb, (k, nbad, worst)
