@@ -177,3 +177,17 @@ def test_fit_deterministic_loss_curve():
     assert runs[0][0] == runs[1][0]
     for k in runs[0][1]:
         assert torch.equal(runs[0][1][k], runs[1][1][k]), k
+
+
+def test_fit_alpha_blended_2d_with_depth():
+    """NEXT-2's optional 2D alpha-blending mode (a user depth orders
+    the primitives; Eq. 3 compositing): the fitting step runs and lowers the loss."""
+    from paper_2508_12615_b200.train import Fitter2D
+    tgt = gen.smooth_target(64, 64, seed=5)
+    p = gen.init2d_from_target(tgt, 300, seed=5, freq_std=0.05)
+    p["depth"] = np.random.default_rng(5).uniform(1, 10, 300).astype(np.float32)
+    fit = Fitter2D(torch.from_numpy(tgt).cuda(), {k: torch.from_numpy(v) for k, v in p.items()},
+                   blend="alpha")
+    l0 = fit.loss()
+    hist = fit.fit(150, check_every=50)
+    assert fit.steps_taken() == 150 and hist[-1][1] < 0.7 * l0, (l0, hist)
