@@ -89,8 +89,11 @@ constexpr int kSmemMax = 227 * 1024;
 //   B       [stages][NT x 64] (streamed) or [all K chunks][NT x 64] (resident),
 //   barriers full/empty[kMaxStages], tfull/tempty[2], bfull, TMEM address.
 struct WsCarve {
-  uint32_t a, b, bar, stages, bres, bytes;
+  uint32_t a, b, stg, bar, stages, bres, bytes;
 };
+// per epilogue warp: one 32 x 32 fp32 output block + one 32 x 32 bf16 mask block
+constexpr uint32_t kStgWarpBytes = 32 * 32 * 4 + 32 * 32 * 2;
+constexpr uint32_t kStgBytes = 8 * kStgWarpBytes;
 
 // B bytes per K chunk: NT x 64 bf16; an MN-major TMA panel is whole 64-wide
 // atoms (64 x 64 bf16 = 8 KB each).
@@ -104,19 +107,24 @@ __host__ __device__ inline WsCarve ws_carve(int64_t K, int64_t split) {
   WsCarve c;
   const uint32_t a_st = kM * kKC * 2, b_st = b_chunk_bytes<NT, BMN, TMA>();
   const int64_t nch = (K + kKC - 1) / kKC;
-  const uint32_t tail = 1024;  // barriers + tmem slot
+  const uint32_t tail = 1024 + kStgBytes;  // output staging + barriers + tmem slot
   const uint64_t bres_bytes = (uint64_t)nch * b_st;
+  const uint64_t budget = kSmemMax - 1024;  // the launch adds 1 KB for the 1024-B alignment
   c.bres = 0;
-  c.stages = kMaxStages;
-  if (split <= 1 && bres_bytes + 2ull * a_st + tail <= kSmemMax) {  // resident B
+  {  // streamed B: as many (A + B) stages as fit
+    const uint64_t st = (budget - tail) / (a_st + b_st);
+    c.stages = (uint32_t)(st < kMaxStages ? st : kMaxStages);
+  }
+  if (split <= 1 && bres_bytes + 2ull * a_st + tail <= budget) {  // resident B
     c.bres = 1;
-    const uint64_t left = kSmemMax - bres_bytes - tail;
+    const uint64_t left = budget - bres_bytes - tail;
     c.stages = (uint32_t)(left / a_st < kMaxStages ? left / a_st : kMaxStages);
   }
   c.a = 0;
   c.b = c.stages * a_st;
-  c.bar = c.b + (uint32_t)(c.bres ? bres_bytes : (uint64_t)c.stages * b_st);
-  c.bytes = c.bar + tail;
+  c.stg = c.b + (uint32_t)(c.bres ? bres_bytes : (uint64_t)c.stages * b_st);
+  c.bar = c.stg + kStgBytes;
+  c.bytes = c.bar + 1024;
   return c;
 }
 
@@ -127,7 +135,10 @@ __host__ __device__ inline WsCarve ws_carve(int64_t K, int64_t split) {
 template <int NT, int EPI>
 __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0, int cb1,
                                               uint32_t tacc, int ew, int lane, int64_t m0,
-                                              int64_t n0, bool have) {
+                                              int64_t n0, bool have, const void* tcmap,
+                                              unsigned char* stg, const void* tmmap,
+                                              uint64_t* mbar, uint32_t& mphase) {
+  unsigned char* mstg = stg + 32 * 32 * 4;  // mask block (bf16, row-major)
   const int64_t m = m0 + 32 * ew + lane;
   const bool mrow = m < g.M;
   constexpr bool kBf16Out = EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16 || EPI == WIPES_GEMM_EPI_MASK_BF16;
@@ -137,6 +148,15 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
 #pragma unroll 1
   for (int cb = cb0; cb < cb1; ++cb) {
     float v[32];
+    const bool tm = EPI == WIPES_GEMM_EPI_MASK_BF16 && tmmap != nullptr &&
+                    32 * cb < NT && n0 + 32 * cb < g.N;
+    if (tm) {  // fetch this block's ReLU mask with TMA while the accumulator is read
+      __syncwarp();
+      if (lane == 0) {
+        mbar_expect_tx(mbar, 32 * 32 * 2);
+        tma_load_2d(mstg, tmmap, (int)(n0 + 32 * cb), (int)(m0 + 32 * ew), mbar);
+      }
+    }
     if (have) {
       tmem_ld32(tacc + ((uint32_t)(32 * ew) << 16) + (uint32_t)(32 * cb), v);
     } else {
@@ -171,7 +191,22 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
     }
-    if (EPI == WIPES_GEMM_EPI_MASK_BF16 && mrow) {
+    if (tm) {
+      mbar_wait(mbar, mphase);
+      mphase ^= 1u;
+      const uint4* mr = reinterpret_cast<const uint4*>(mstg + lane * 64);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = mr[q];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const __nv_bfloat162 pr = *reinterpret_cast<const __nv_bfloat162*>(&w[h]);
+          v[8 * q + 2 * h] = __low2float(pr) > 0.f ? v[8 * q + 2 * h] : 0.f;
+          v[8 * q + 2 * h + 1] = __high2float(pr) > 0.f ? v[8 * q + 2 * h + 1] : 0.f;
+        }
+      }
+    } else if (EPI == WIPES_GEMM_EPI_MASK_BF16 && mrow) {
       const __nv_bfloat16* mp = reinterpret_cast<const __nv_bfloat16*>(g.mask) + m * g.ldm + n;
       if (full && mvec) {
 #pragma unroll
@@ -209,6 +244,38 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
         }
       }
       if (lane < nv) atomicAdd(g.colsum + n + lane, w[0]);
+    }
+    if (EPI != WIPES_GEMM_EPI_ATOMIC_F32 && tcmap) {
+      // stage the 32 x 32 block row-major in shared memory and let TMA write it
+      // (out-of-range rows/columns are clipped by the tensor map bounds)
+      if (lane == 0) bulk_wait_read();  // the previous block's store has read the buffer
+      __syncwarp();
+      if (kBf16Out) {
+        uint4* row = reinterpret_cast<uint4*>(stg + lane * 64);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const __nv_bfloat162 pr = __floats2bfloat162_rn(v[8 * q + 2 * h], v[8 * q + 2 * h + 1]);
+            w[h] = *reinterpret_cast<const uint32_t*>(&pr);
+          }
+          row[q] = u;
+        }
+      } else {
+        float4* row = reinterpret_cast<float4*>(stg + lane * 128);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          row[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tcmap, (int)n, (int)(m0 + 32 * ew), stg);
+        bulk_commit();
+      }
+      continue;
     }
     if (!mrow) continue;
     if (EPI == WIPES_GEMM_EPI_ATOMIC_F32) {
@@ -263,7 +330,9 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
 // 64 x 64) built on the host.
 struct GemmParams {
   wipes_gemm_args g;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc, tm;
+  int32_t tstore;  // 1: the epilogue writes C with TMA stores through tc
+  int32_t tmask;   // 1: the ReLU mask is fetched with TMA through tm
 };
 
 template <int NT, bool AMN, bool BMN, int EPI, bool TMA>
@@ -292,7 +361,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* mbars = bfull + 1;  // one per epilogue warp (TMA mask loads)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbars + 8);
   constexpr int kAst = kM * kKC;                                // A elements per stage
   constexpr int kBst = b_chunk_bytes<NT, BMN, TMA>() / 2;      // B elements per chunk
 
@@ -312,6 +382,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     mbar_init(bfull, TMA ? 1 : kProd);
+    for (int i = 0; i < 8; ++i) mbar_init(&mbars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -442,6 +513,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
     const int half = e >> 2, nh = kEpiWarps / 4;
     const int cb0 = kBlocks * half / nh, cb1 = kBlocks * (half + 1) / nh;
     int64_t tcount = 0;
+    uint32_t mphase = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tcount) {
       int64_t m0, n0, c_lo, nch;
       tile_coords(t, m0, n0, c_lo, nch);
@@ -449,10 +521,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_ws(const __grid_constant
       mbar_wait(&tfull[acc], (uint32_t)((tcount >> 1) & 1));
       tc_fence_after();
       epilogue_tile<NT, EPI>(g, cb0, cb1, tmem + (uint32_t)(acc * kCols), ew, lane, m0, n0,
-                             nch > 0);
+                             nch > 0, P.tstore ? (const void*)&P.tc : nullptr,
+                             base + cv.stg + e * kStgWarpBytes,
+                             P.tmask ? (const void*)&P.tm : nullptr, &mbars[e], mphase);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (P.tstore && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -491,6 +566,19 @@ bool make_tmap(CUtensorMap* m, const void* ptr, bool mn, int64_t rows, int64_t K
   return r == CUDA_SUCCESS;
 }
 
+// Output tensor map: C [M, N] (row pitch ldc), 32 x 32 boxes, no swizzle.
+bool make_out_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t M, int64_t N, int64_t ldc) {
+  auto enc = tmap_encoder();
+  const int esz = bf16 ? 2 : 4;
+  if (!enc || (uintptr_t)ptr % 16 != 0 || (ldc * esz) % 16 != 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M}, strides[1] = {(cuuint64_t)(ldc * esz)};
+  cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
+  return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+             const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NT, bool AMN, bool BMN, int EPI, bool TMA>
 cudaError_t launch_ws_t(const GemmParams& P, cudaStream_t s) {
   const wipes_gemm_args& g = P.g;
@@ -523,6 +611,13 @@ cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
   if (!make_tmap(&P.ta, g.A, AMN, g.M, g.K, g.lda, kM) ||
       !make_tmap(&P.tb, g.B, BMN, g.N, g.K, g.ldb, NT))
     return cudaErrorInvalidValue;
+  std::memset(&P.tc, 0, sizeof(P.tc));
+  std::memset(&P.tm, 0, sizeof(P.tm));
+  P.tmask = EPI == WIPES_GEMM_EPI_MASK_BF16 && make_out_tmap(&P.tm, g.mask, true, g.M, g.N, g.ldm);
+  P.tstore = EPI != WIPES_GEMM_EPI_ATOMIC_F32 &&
+             make_out_tmap(&P.tc, g.C,
+                           EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16 || EPI == WIPES_GEMM_EPI_MASK_BF16,
+                           g.M, g.N, g.ldc);
 #ifdef WIPES_GEMM_CPASYNC  // cp.async staging variant (experiments / cross-checks)
   return launch_ws_t<NT, AMN, BMN, EPI, false>(P, s);
 #else
