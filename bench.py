@@ -296,9 +296,12 @@ def main():
     name = args.config
     base = gen.CONFIGS[name]
     rows = base.get("shard") == "rows"           # one image, tile rows sharded
-    shared = base["kind"] == "3d" or rows          # one problem shared by all ranks
-    # weak scaling: every rank its own independent problem (different seed);
-    # 3D batch: one scene, views sharded across ranks + gradient all_reduce.
+    frames = base["kind"] == "6d"                 # per-frame parameter rows (view_stride = N)
+    shared = base["kind"] == "3d" or rows or frames  # one problem shared by all ranks
+    # 2D (C2): every rank its own independent image (weak scaling);
+    # 3D batch (C3): one scene, views sharded across ranks + gradient all_reduce;
+    # 6D (C4): frames sharded round-robin, per-frame parameters are disjoint so
+    # there is no exchange; C5: tile rows sharded + all_reduce.
     over = {"sh_degree": args.sh} if (args.sh is not None and gen.CONFIGS[name]["kind"] != "2d") else {}
     c = gen.make_config(name, seed=args.seed + (0 if shared else rank), **over)
     H, W, N, B = c["H"], c["W"], c["N"], c["B"]
@@ -314,9 +317,12 @@ def main():
                    sh_degree=c.get("sh_degree"),
                    row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0,
                    deterministic=int(args.deterministic))
-    params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
-    if c["kind"] == "6d":
-        pass
+    hp = c["params"]
+    if frames and world > 1:  # this rank's frames' parameter rows (view_stride = N)
+        hp = {k: np.ascontiguousarray(np.concatenate(
+            [v[f * N:(f + 1) * N] for f in my_views], 0)) for k, v in hp.items()}
+        c = dict(c, params=hp)
+    params = {k: torch.from_numpy(v).to(dev) for k, v in hp.items()}
     dL_host = gen.gen_dLdC(Bl, H, W, seed=args.seed + rank)
     dL = torch.from_numpy(dL_host).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -324,8 +330,8 @@ def main():
 
     grads = {k: torch.empty_like(v) for k, v in params.items() if k not in ("depth",)}
     flat = None
-    if shared and world > 1:
-        flat = wdist.GradBucket(grads)
+    if shared and world > 1 and not frames:
+        flat = wdist.GradBucket(grads, deterministic=args.deterministic)
 
     def step_eager(sync=False):
         r.preprocess(params, cams, vs, sync=sync)
@@ -526,6 +532,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "parallelism": (f"tile rows r = rank (mod {world}) of one image per GPU + "
                                        "NCCL all_reduce of per-primitive gradients") if rows else
+                                      (f"frames round-robin over {world} GPU(s), per-frame "
+                                       "parameters disjoint: no exchange") if frames else
                                       (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
                                        "per-primitive gradients") if shared else
                                       f"replicas: {world} independent image(s), one per GPU"},

@@ -6,6 +6,10 @@ Partitioning of the hot path:
     views; the per-primitive gradients of a SHARED parameter set are then
     summed across ranks with one all_reduce over a single flat bucket (NCCL
     over NVLink/NVSwitch on the GPU box; gloo in the CPU tests);
+  * one large image: tile rows r = rank (mod world) per GPU, gradients summed
+    the same way;
+  * 6D frames with per-frame parameter rows are disjoint across ranks: no
+    exchange;
   * independent 2D images (one primitive set each) need no exchange at all.
 """
 from __future__ import annotations
@@ -28,7 +32,7 @@ class GradBucket:
     """Rebinds the tensors of `grads` (dict name -> tensor) to views of one flat
     float32 buffer so the cross-rank gradient sum is a single collective."""
 
-    def __init__(self, grads: dict, group=None):
+    def __init__(self, grads: dict, group=None, deterministic: bool = False):
         self.keys = list(grads.keys())
         total = sum(grads[k].numel() for k in self.keys)
         dev = grads[self.keys[0]].device
@@ -41,8 +45,20 @@ class GradBucket:
             grads[k] = view
             off += n
         self.group = group
+        self.deterministic = deterministic
 
     def all_reduce(self):
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+            if self.deterministic:
+                # SURVEY §8(e) deterministic option: gather every rank's partial
+                # and sum in rank order (bitwise identical on every rank and run)
+                parts = [torch.empty_like(self.flat)
+                         for _ in range(dist.get_world_size(self.group))]
+                dist.all_gather(parts, self.flat, group=self.group)
+                acc = parts[0].clone()
+                for p in parts[1:]:
+                    acc += p
+                self.flat.copy_(acc)
+            else:
+                dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
         return self.flat

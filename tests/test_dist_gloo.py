@@ -129,3 +129,43 @@ def test_tile_row_sharded_gradients_equal_single_process(ora):
     ref = ora.forward_backward(ora.Cfg(width=W, height=H), p, dL)["grads"]
     for k, v in ref.items():
         np.testing.assert_allclose(got[k], v.astype(np.float32), rtol=1e-5, atol=1e-6)
+
+
+def _worker_det(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    rng = np.random.default_rng(100 + rank)
+    g = {"a": torch.from_numpy(rng.normal(size=(1000, 3)).astype(np.float32)),
+         "b": torch.from_numpy(rng.normal(size=500).astype(np.float32))}
+    b = wdist.GradBucket(g, deterministic=True)
+    b.all_reduce()
+    q.put((rank, {k: v.numpy().copy() for k, v in g.items()}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_deterministic_gradbucket_rank_order_sum():
+    """The deterministic all-reduce is the rank-ordered sum, identical on every rank."""
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_det, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    parts = []
+    for r in range(world):
+        rng = np.random.default_rng(100 + r)
+        parts.append({"a": rng.normal(size=(1000, 3)).astype(np.float32),
+                      "b": rng.normal(size=500).astype(np.float32)})
+    for k in ("a", "b"):
+        ref = parts[0][k].copy()
+        for r in range(1, world):
+            ref += parts[r][k]
+        for r in range(world):
+            np.testing.assert_array_equal(got[r][k], ref)
