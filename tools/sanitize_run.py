@@ -1,6 +1,8 @@
-"""Exercise every kernel path once on small inputs (for compute-sanitizer):
-2D SUM/ALPHA x {Sigma, Cholesky, RS} x tile {8, 16, 32}, 3D and 6D mini
-configs, forward + backward, stats and parity copies."""
+"""Exercise every kernel path once on small inputs (for compute-sanitizer or
+the WIPES_CHECKS device-assert build): 2D SUM/ALPHA x {Sigma, Cholesky, RS} x
+tile {8, 16, 32} x {atomic, deterministic} backward, 3D and 6D mini configs
+(paper / exact projection, RGB / SH colour), the fitting step, the tcgen05
+GEMM and the deformation MLP; forward + backward, stats and parity copies."""
 import os
 import sys
 
@@ -33,16 +35,46 @@ def run2d():
 
 def run3d():
     for name in ("p3d", "p6d"):
-        c = gen.make_config(name, seed=0, N=3000)
-        r = Rasterizer(c["W"], c["H"], prim="3d", blend="alpha")
-        r.forward(dev(c["params"]), c["cams"], c["view_stride"])
-        r.backward(torch.rand(c["B"], 3, c["H"], c["W"], device="cuda") - 0.5)
-        r.render_stats()
-        r.bin_sort_outputs()
+        for proj, sh, det in (("paper", None, 0), ("exact", None, 1), ("paper", 3, 0),
+                              ("exact", 2, 1)):
+            c = gen.make_config(name, seed=0, N=3000, sh_degree=sh)
+            r = Rasterizer(c["W"], c["H"], prim="3d", blend="alpha", proj=proj, sh_degree=sh,
+                           deterministic=det)
+            r.forward(dev(c["params"]), c["cams"], c["view_stride"])
+            r.backward(torch.rand(c["B"], 3, c["H"], c["W"], device="cuda") - 0.5)
+            r.render_stats()
+            r.bin_sort_outputs()
+
+
+def run_next():
+    from paper_2508_12615_b200 import abi
+    from paper_2508_12615_b200.deform import Deformation
+    from paper_2508_12615_b200.train import Fitter2D
+    tgt = gen.smooth_target(48, 40, seed=0)
+    p = gen.init2d_from_target(tgt, 200, seed=0)
+    for det in (0, 1):
+        f = Fitter2D(torch.from_numpy(tgt).cuda(), dev(p), deterministic=det)
+        f.fit(5, check_every=5)
+    d = Deformation(1000)
+    th = d.init_theta(0)
+    q = gen.gen3d(1000, seed=0)
+    canon = dev(q)
+    fr = d.forward(th, canon, [0.0, 0.5])
+    d.backward(th, canon, {k: torch.randn_like(fr[k]) for k in ("mean", "quat", "scale", "freq")})
+    for amn in (False, True):
+        for bmn in (False, True):
+            A = torch.randn(304, 136, device="cuda").to(torch.bfloat16)
+            B = torch.randn(72, 136, device="cuda").to(torch.bfloat16)
+            A2 = A.t().contiguous() if amn else A
+            B2 = B.t().contiguous() if bmn else B
+            C = torch.zeros(304, 72, device="cuda")
+            abi.gemm(A2, B2, C, 304, 72, 136, 304 if amn else 136, 72 if bmn else 136, 72,
+                     epilogue="atomic_f32", a_mn=amn, b_mn=bmn, split_k=3)
 
 
 if __name__ == "__main__":
     run2d()
     run3d()
+    run_next()
     torch.cuda.synchronize()
     print("sanitize_run: ok")
