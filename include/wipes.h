@@ -345,11 +345,14 @@ size_t wipes_mlp_workspace_bytes(const wipes_mlp_config* cfg, int64_t rows);
 /* Frame f, primitive i -> row f*N + i. times: (host) [F]. canon: mean, quat,
  * scale, freq [N] (+ phase, color, opacity, sh copied to the frame rows when
  * both canon and frame pointers are non-NULL); frame: the same groups, [F*N]
- * rows (device, caller-owned), ready for the rasterizer with view_stride = N. */
+ * rows (device, caller-owned), ready for the rasterizer with view_stride = N.
+ * train: 1 keeps every layer's activations in `ws` for wipes_mlp_backward;
+ * 0 (inference) writes only the frame rows. When width is a multiple of 64,
+ * depth <= 8 and F <= 128, all layers of a 128-row tile run fused on chip. */
 wipes_status wipes_mlp_forward(const wipes_mlp_config* cfg, const float* theta, int64_t N,
                                int32_t F, const float* times, const wipes_params* canon,
-                               const wipes_params* frame, int32_t sh_coeffs, void* ws,
-                               size_t ws_bytes, void* stream);
+                               const wipes_params* frame, int32_t sh_coeffs, int32_t train,
+                               void* ws, size_t ws_bytes, void* stream);
 /* From g_frame (gradients w.r.t. the frame rows' mean, quat, scale, freq) of
  * the last wipes_mlp_forward on this workspace: g_theta [param_count] (fp32,
  * overwritten) and g_canon mean/quat/scale/freq [N] (overwritten; mean is the

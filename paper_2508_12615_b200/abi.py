@@ -124,7 +124,7 @@ def lib():
     L.wipes_mlp_workspace_bytes.argtypes = [P(wipes_mlp_config), i64]
     L.wipes_mlp_workspace_bytes.restype = sz
     L.wipes_mlp_forward.argtypes = [P(wipes_mlp_config), vp, i64, i32, P(C.c_float),
-                                    P(wipes_params), P(wipes_params), i32, vp, sz, vp]
+                                    P(wipes_params), P(wipes_params), i32, i32, vp, sz, vp]
     L.wipes_mlp_forward.restype = C.c_int
     L.wipes_mlp_backward.argtypes = [P(wipes_mlp_config), vp, i64, i32, P(wipes_params),
                                      P(wipes_grads), vp, P(wipes_grads), vp, sz, vp]
@@ -316,10 +316,11 @@ def wipes_mlp_workspace_bytes(cfg, rows) -> int:
     return int(lib().wipes_mlp_workspace_bytes(C.byref(cfg), rows))
 
 
-def wipes_mlp_forward(cfg, theta, N, F, times, canon, frame, sh_coeffs, ws, ws_bytes, stream):
+def wipes_mlp_forward(cfg, theta, N, F, times, canon, frame, sh_coeffs, train, ws, ws_bytes,
+                      stream):
     t = (C.c_float * max(F, 1))(*[float(x) for x in times])
     return lib().wipes_mlp_forward(C.byref(cfg), theta, N, F, t, C.byref(canon), C.byref(frame),
-                                   sh_coeffs, ws, ws_bytes, stream)
+                                   sh_coeffs, int(train), ws, ws_bytes, stream)
 
 
 def wipes_mlp_backward(cfg, theta, N, F, canon, g_frame, g_theta, g_canon, ws, ws_bytes, stream):

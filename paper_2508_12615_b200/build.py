@@ -33,6 +33,7 @@ SOURCES = {
     "gemm_e3.cu": [],
     "gemm_e4.cu": [],
     "mlp.cu": [],
+    "mlp_fused.cu": [],
     "abi.cu": [],
 }
 

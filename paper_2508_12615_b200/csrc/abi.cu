@@ -440,8 +440,8 @@ static wipes_status check_mlp(const wipes_mlp_config* c, const float* theta, int
 
 wipes_status wipes_mlp_forward(const wipes_mlp_config* c, const float* theta, int64_t N, int32_t F,
                                const float* times, const wipes_params* canon,
-                               const wipes_params* frame, int32_t sh_coeffs, void* ws,
-                               size_t ws_bytes, void* stream) {
+                               const wipes_params* frame, int32_t sh_coeffs, int32_t train,
+                               void* ws, size_t ws_bytes, void* stream) {
   wipes_status st = check_mlp(c, theta, N, F, ws, ws_bytes);
   if (st != WIPES_OK) return st;
   if (!times || !canon || !frame) return fail(WIPES_EINVAL, "times/canon/frame NULL");
@@ -449,7 +449,7 @@ wipes_status wipes_mlp_forward(const wipes_mlp_config* c, const float* theta, in
       !frame->quat || !frame->scale || !frame->freq)
     return fail(WIPES_EINVAL, "mean/quat/scale/freq (canon and frame) must be non-NULL");
   if (sh_coeffs < 0 || sh_coeffs > 16) return fail(WIPES_EINVAL, "sh_coeffs");
-  cudaError_t e = launch_mlp_forward(*c, theta, N, F, times, *canon, *frame, sh_coeffs,
+  cudaError_t e = launch_mlp_forward(*c, theta, N, F, times, *canon, *frame, sh_coeffs, train,
                                      (char*)ws, (cudaStream_t)stream);
   return e == cudaSuccess ? WIPES_OK : cuda_fail(e, "mlp forward");
 }

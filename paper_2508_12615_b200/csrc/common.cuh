@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cassert>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 #include "../../include/wipes.h"
 
@@ -185,13 +186,29 @@ cudaError_t launch_gemm(const wipes_gemm_args& g, cudaStream_t s);
 cudaError_t launch_det_gather(const Layout& L, char* ws, cudaStream_t s);
 cudaError_t launch_vals_copy(const Layout& L, const char* ws, int final_in_b, uint32_t* out,
                              cudaStream_t s);
+// Description of one fused deformation-MLP forward (mlp_fused.cu).
+struct MlpFusedDesc {
+  int32_t W, D, skip, Lx, Lt, E8, catw, train, shc, F;
+  int64_t N, M;
+  const float* times;  // (host) [F]
+  const float* theta;
+  int64_t thb[32], thbh;
+  wipes_params canon, frame;
+  float* out;
+  const __nv_bfloat16* wbf[32];
+  int32_t Kp[32];
+  const __nv_bfloat16* whbf;
+  __nv_bfloat16* h[32];
+  __nv_bfloat16* cat;
+};
+bool launch_mlp_fused_fwd(const MlpFusedDesc& d, cudaStream_t s, cudaError_t* err);
 bool mlp_config_valid(const wipes_mlp_config& c);
 int64_t mlp_param_count(const wipes_mlp_config& c);
 size_t mlp_workspace_bytes(const wipes_mlp_config& c, int64_t rows);
 cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, int64_t N,
                                int32_t F, const float* times, const wipes_params& canon,
-                               const wipes_params& frame, int32_t sh_coeffs, char* ws,
-                               cudaStream_t s);
+                               const wipes_params& frame, int32_t sh_coeffs, int32_t train,
+                               char* ws, cudaStream_t s);
 cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, int64_t N,
                                 int32_t F, const wipes_params& canon, const wipes_grads& gfr,
                                 float* g_theta, const wipes_grads& gcan, char* ws,

@@ -1,0 +1,386 @@
+// NEXT-4 fused forward of the deformation field (DESIGN.md NEXT-4): every
+// layer of one 128-row tile runs back to back with the activations kept in
+// shared memory, so HBM sees only the canonical parameters in and the frame
+// rows out (plus, when training, one store of each layer's activations for
+// the backward).
+//
+// One CTA per SM, persistent over 128-row tiles:
+//   warp 0      TMA producer: streams every layer's bf16 weights (K chunks of
+//               64, 128-byte swizzle) through a ring (weights do not depend on
+//               the tile, so it runs a layer or more ahead);
+//   warp 1      one lane issues tcgen05.mma (M = 128, N = width or 16) per
+//               chunk: A = the activation tile in shared memory, B = the ring
+//               stage; commits each chunk to empty[s] and each layer to accf;
+//   warp 2      owns the TMEM accumulator (256 columns);
+//   warps 4-11  epilogue (two warps per TMEM lane quarter, one per column
+//               half): the positional encoding at tile start, then per layer
+//               bias + ReLU -> bf16 -> the activation tile (written in the
+//               SW128 K-major layout the next MMA reads), optional TMA stores
+//               of the activations, and the head's apply into the frame rows.
+// Activation tile X: 6 chunks of [128 rows x 64 bf16]: chunks 0-1 hold the
+// encoding (zero padded to 128 columns), chunks 2-5 hold h (width <= 256).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "gemm_tc.cuh"
+
+namespace wipes {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kFMaxD = 8;
+constexpr int kFMaxFrames = 128;
+constexpr int kFStages = 3;
+constexpr int kFEpiWarps = 8;
+constexpr int kFThreads = 32 * (4 + kFEpiWarps);
+constexpr uint32_t kXChunk = 128 * 64 * 2;  // 16 KB
+
+struct FusedArgs {
+  int32_t W, D, skip, Lx, Lt, E8, catw, train, shc;
+  int64_t N, M;
+  float t[kFMaxFrames];
+  const float* theta;
+  int64_t thb[kFMaxD], thbh;
+  wipes_params canon, frame;
+  float* out;  // [M, 16] head outputs (training)
+  CUtensorMap wl[kFMaxD + 1];  // weights per layer (the skip layer's h part in wl[kFMaxD])
+  CUtensorMap wh;              // head weights [16, W]
+  CUtensorMap hs[kFMaxD];      // activation stores (training)
+  CUtensorMap cate, cath;      // concat buffer: encoding part / h part (training)
+};
+
+// The K chunks of layer l (l == D: head) and which X chunk / weight map / k0 each uses.
+__device__ __forceinline__ int layer_chunks(const FusedArgs& a, int l) {
+  if (l == a.D) return a.W / 64;
+  if (l == 0) return 2;
+  if (l == a.skip + 1) return 2 + a.W / 64;
+  return a.W / 64;
+}
+
+__device__ __forceinline__ void chunk_info(const FusedArgs& a, int l, int c, int& xchunk,
+                                           const CUtensorMap*& map, int& k0) {
+  if (l == a.D) { xchunk = 2 + c; map = &a.wh; k0 = 64 * c; return; }
+  if (l == 0) { xchunk = c; map = &a.wl[0]; k0 = 64 * c; return; }
+  if (l == a.skip + 1) {
+    if (c < 2) { xchunk = c; map = &a.wl[l]; k0 = 64 * c; }
+    else { xchunk = c; map = &a.wl[kFMaxD]; k0 = 64 * (c - 2); }
+    return;
+  }
+  xchunk = 2 + c; map = &a.wl[l]; k0 = 64 * c;
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// store 8 bf16 (one 16-byte unit) of row r, column c0 (multiple of 8) into X
+__device__ __forceinline__ void x_store8(unsigned char* X, int r, int c0, const uint4& u) {
+  const int chunk = c0 >> 6, unit = (c0 & 63) >> 3;
+  *reinterpret_cast<uint4*>(X + chunk * kXChunk + r * 128 + ((unit ^ (r & 7)) << 4)) = u;
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  uint4 u;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+    w[h] = *reinterpret_cast<const uint32_t*>(&p);
+  }
+  return u;
+}
+
+__global__ void __launch_bounds__(kFThreads, 1) k_mlp_fused_fwd(const __grid_constant__ FusedArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* X = base;                                  // 6 x 16 KB
+  unsigned char* ring = base + 6 * kXChunk;                 // kFStages x (256 x 64 bf16)
+  constexpr uint32_t kStage = 256 * 64 * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kFStages * kStage);
+  uint64_t* empty = full + kFStages;
+  uint64_t* xready = empty + kFStages;
+  uint64_t* accf = xready + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tiles = (a.M + 127) / 128;
+
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kFStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(xready, 1);
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {  // ------------------------------------------- TMA producer
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int l = 0; l <= a.D; ++l) {
+          const int nch = layer_chunks(a, l);
+          for (int c = 0; c < nch; ++c, ++it) {
+            const int st = (int)(it % kFStages);
+            const uint32_t round = (uint32_t)(it / kFStages);
+            mbar_wait(&empty[st], (round & 1u) ^ 1u);
+            int xc, k0;
+            const CUtensorMap* map;
+            chunk_info(a, l, c, xc, map, k0);
+            mbar_expect_tx(&full[st], l == a.D ? 16 * 128 : (uint32_t)a.W * 128);
+            tma_load_2d(ring + st * kStage, map, k0, 0, &full[st]);
+          }
+        }
+    }
+  } else if (warp == 1) {  // -------------------------------------- MMA issuer
+    const uint32_t id_l = instr_desc(a.W, false, false), id_h = instr_desc(16, false, false);
+    int64_t it = 0;
+    uint32_t xph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+      for (int l = 0; l <= a.D; ++l) {
+        mbar_wait(xready, xph);
+        xph ^= 1u;
+        tc_fence_after();
+        const int nch = layer_chunks(a, l);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = (int)(it % kFStages);
+          const uint32_t round = (uint32_t)(it / kFStages);
+          mbar_wait(&full[st], round & 1u);
+          tc_fence_after();
+          if (lane == 0) {
+            int xc, k0;
+            const CUtensorMap* map;
+            chunk_info(a, l, c, xc, map, k0);
+            const uint32_t a0 = smem_u32(X + xc * kXChunk), b0 = smem_u32(ring + st * kStage);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              mma_bf16(tmem, smem_desc_sw128(a0 + 32 * j, 16, 1024),
+                       smem_desc_sw128(b0 + 32 * j, 16, 1024), l == a.D ? id_h : id_l,
+                       (c > 0 || j > 0) ? 1u : 0u);
+            mma_commit(&empty[st]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) mma_commit(accf);
+        __syncwarp();
+      }
+  } else if (warp >= 4) {  // -------------------------------------- epilogue
+    const int e = warp - 4, q = e & 3, half = e >> 2;
+    const int r = 32 * q + lane;  // tile row = TMEM lane
+    const int nb = a.W / 32, cb0 = half * nb / 2, cb1 = (half + 1) * nb / 2;
+    const bool issuer = (e == 0 && lane == 0);
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int64_t m0 = t * 128, m = m0 + r;
+      const bool mrow = m < a.M;
+      // ---- positional encoding of row r into X chunks 0-1 (zero padded) ----
+      if (issuer) bulk_wait_read();  // previous tile's stores have read X
+      named_sync(1, 32 * kFEpiWarps);
+      if (half == 0) {
+        float x[3] = {0.f, 0.f, 0.f}, tt = 0.f;
+        if (mrow) {
+          const int64_t f = m / a.N, i = m - f * a.N;
+          x[0] = a.canon.mean[3 * i]; x[1] = a.canon.mean[3 * i + 1]; x[2] = a.canon.mean[3 * i + 2];
+          tt = a.t[f];
+        }
+        float buf[8];
+        int n = 0, c0 = 0;
+        auto push = [&](float v) {
+          buf[n++] = v;
+          if (n == 8) { x_store8(X, r, c0, pack8(buf)); c0 += 8; n = 0; }
+        };
+        for (int d = 0; d < 3; ++d) push(x[d]);
+        for (int k = 0; k < a.Lx; ++k) {
+          float sn[3], cs[3];
+          for (int d = 0; d < 3; ++d) sincosf((float)(1 << k) * x[d], &sn[d], &cs[d]);
+          for (int d = 0; d < 3; ++d) push(sn[d]);
+          for (int d = 0; d < 3; ++d) push(cs[d]);
+        }
+        push(tt);
+        for (int k = 0; k < a.Lt; ++k) {
+          float sn, cs;
+          sincosf((float)(1 << k) * tt, &sn, &cs);
+          push(sn);
+          push(cs);
+        }
+        while (c0 < 128) push(0.f);
+      }
+      fence_proxy_async();
+      named_sync(1, 32 * kFEpiWarps);
+      if (issuer) {
+        if (a.train) {
+          tma_store_2d(&a.cate, 0, (int)m0, X);
+          tma_store_2d(&a.cate, 64, (int)m0, X + kXChunk);
+          bulk_commit();
+        }
+        mbar_arrive(xready);
+      }
+      // ---- layers -----------------------------------------------------------
+      for (int l = 0; l <= a.D; ++l) {
+        mbar_wait(accf, aph);
+        aph ^= 1u;
+        tc_fence_after();
+        if (l < a.D) {
+          if (issuer) bulk_wait_read();  // X chunks 2-5 free of pending stores
+          named_sync(1, 32 * kFEpiWarps);
+          const float* bias = a.theta + a.thb[l];
+          for (int cb = cb0; cb < cb1; ++cb) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * cb), v);
+            const float4* b4 = reinterpret_cast<const float4*>(bias + 32 * cb);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float4 b = __ldg(b4 + k);
+              v[4 * k] = fmaxf(v[4 * k] + b.x, 0.f);
+              v[4 * k + 1] = fmaxf(v[4 * k + 1] + b.y, 0.f);
+              v[4 * k + 2] = fmaxf(v[4 * k + 2] + b.z, 0.f);
+              v[4 * k + 3] = fmaxf(v[4 * k + 3] + b.w, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x_store8(X + 2 * kXChunk, r, 32 * cb + 8 * u, pack8(v + 8 * u));
+          }
+          tc_fence_before();
+          fence_proxy_async();
+          named_sync(1, 32 * kFEpiWarps);
+          if (issuer) {
+            if (a.train) {
+              const CUtensorMap* hm = l == a.skip ? &a.cath : &a.hs[l];
+              for (int j = 0; j < a.W / 64; ++j)
+                tma_store_2d(hm, 64 * j, (int)m0, X + (2 + j) * kXChunk);
+              bulk_commit();
+            }
+            mbar_arrive(xready);
+          }
+        } else {  // head: bias, then the frame rows (and the outputs for the backward)
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16), v);
+          tc_fence_before();
+          if (half == 0 && mrow) {
+            const int64_t i = m % a.N;
+            for (int k = 0; k < 13; ++k) v[k] += a.theta[a.thbh + k];
+            float* fm = const_cast<float*>(a.frame.mean);
+            float* fq = const_cast<float*>(a.frame.quat);
+            float* fs = const_cast<float*>(a.frame.scale);
+            float* ff = const_cast<float*>(a.frame.freq);
+            for (int d = 0; d < 3; ++d) fm[3 * m + d] = a.canon.mean[3 * i + d] + v[d];
+            for (int d = 0; d < 4; ++d) fq[4 * m + d] = a.canon.quat[4 * i + d] + v[3 + d];
+            for (int d = 0; d < 3; ++d) fs[3 * m + d] = a.canon.scale[3 * i + d] * expf(v[7 + d]);
+            for (int d = 0; d < 3; ++d) ff[3 * m + d] = a.canon.freq[3 * i + d] + v[10 + d];
+            if (a.canon.phase && a.frame.phase) const_cast<float*>(a.frame.phase)[m] = a.canon.phase[i];
+            if (a.canon.opacity && a.frame.opacity)
+              const_cast<float*>(a.frame.opacity)[m] = a.canon.opacity[i];
+            if (a.canon.color && a.frame.color)
+              for (int d = 0; d < 3; ++d)
+                const_cast<float*>(a.frame.color)[3 * m + d] = a.canon.color[3 * i + d];
+            if (a.canon.sh && a.frame.sh)
+              for (int d = 0; d < 3 * a.shc; ++d)
+                const_cast<float*>(a.frame.sh)[3 * a.shc * m + d] = a.canon.sh[3 * a.shc * i + d];
+            if (a.train) {
+              float4* o = reinterpret_cast<float4*>(a.out + m * 16);
+              o[0] = make_float4(v[0], v[1], v[2], v[3]);
+              o[1] = make_float4(v[4], v[5], v[6], v[7]);
+              o[2] = make_float4(v[8], v[9], v[10], v[11]);
+              o[3] = make_float4(v[12], 0.f, 0.f, 0.f);
+            }
+          }
+        }
+      }
+    }
+    if (issuer) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// bf16 2-D map: cols x rows (row pitch in elements), box bc x br, 128-byte swizzle
+bool map2d(CUtensorMap* m, const void* p, int64_t cols, int64_t rows, int64_t pitch, int bc,
+           int br) {
+  auto enc = encoder();
+  if (!enc || (uintptr_t)p % 16 || (pitch * 2) % 16) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows}, str[1] = {(cuuint64_t)pitch * 2};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br}, es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Host side of the fused forward; returns false when the shape is outside its
+// envelope (the caller then runs the layer-by-layer path).
+bool launch_mlp_fused_fwd(const MlpFusedDesc& d, cudaStream_t s, cudaError_t* err) {
+  if (d.W % 64 || d.W > 256 || d.D > kFMaxD || d.F > kFMaxFrames || d.E8 > 128 || d.M == 0)
+    return false;
+  static thread_local FusedArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.W = d.W; a.D = d.D; a.skip = d.skip; a.Lx = d.Lx; a.Lt = d.Lt; a.E8 = d.E8;
+  a.catw = d.catw; a.train = d.train; a.shc = d.shc; a.N = d.N; a.M = d.M;
+  for (int f = 0; f < d.F; ++f) a.t[f] = d.times[f];
+  a.theta = d.theta; a.thbh = d.thbh;
+  for (int l = 0; l < d.D; ++l) a.thb[l] = d.thb[l];
+  a.canon = d.canon; a.frame = d.frame; a.out = d.out;
+  bool ok = true;
+  for (int l = 0; l < d.D && ok; ++l) {
+    if (l == 0) ok = map2d(&a.wl[0], d.wbf[0], d.E8, d.W, d.Kp[0], 64, d.W);
+    else if (l == d.skip + 1) {
+      ok = map2d(&a.wl[l], d.wbf[l], d.E8, d.W, d.Kp[l], 64, d.W) &&
+           map2d(&a.wl[kFMaxD], d.wbf[l] + d.E8, d.W, d.W, d.Kp[l], 64, d.W);
+    } else ok = map2d(&a.wl[l], d.wbf[l], d.W, d.W, d.Kp[l], 64, d.W);
+  }
+  ok = ok && map2d(&a.wh, d.whbf, d.W, 16, d.W, 64, 16);
+  if (ok && d.train) {
+    for (int l = 0; l < d.D && ok; ++l)
+      if (l != d.skip) ok = map2d(&a.hs[l], d.h[l], d.W, d.M, d.W, 64, 128);
+    ok = ok && map2d(&a.cate, d.cat, d.E8, d.M, d.catw, 64, 128) &&
+         (d.skip < 0 || map2d(&a.cath, d.cat + d.E8, d.W, d.M, d.catw, 64, 128));
+  }
+  if (!ok) return false;
+  const int smem = 6 * (int)kXChunk + kFStages * 256 * 64 * 2 + 1024 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_fused_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (d.M + 127) / 128;
+  launch_begin(K_GEMM, s);
+  k_mlp_fused_fwd<<<(unsigned)(tiles < sms ? tiles : sms), kFThreads, smem, s>>>(a);
+  launch_end(K_GEMM, s);
+  *err = cudaGetLastError();
+  return true;
+}
+
+}  // namespace wipes

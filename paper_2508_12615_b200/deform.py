@@ -85,7 +85,9 @@ class Deformation:
             setattr(p, k, abi.ptr(d.get(k)))
         return p
 
-    def forward(self, theta: torch.Tensor, canon: dict, times, frame: dict = None) -> dict:
+    def forward(self, theta: torch.Tensor, canon: dict, times, frame: dict = None,
+                train: bool = True) -> dict:
+        """train=False skips keeping the activations (inference only)."""
         F = len(times)
         rows = self.N * F
         self._ensure(rows)
@@ -96,7 +98,7 @@ class Deformation:
         shc = int(canon["sh"].shape[1]) if "sh" in canon else 0
         cp, fp = self._params(canon), self._params(frame)
         abi.check(abi.wipes_mlp_forward(self.cfg, abi.ptr(theta), self.N, F, list(times), cp, fp,
-                                        shc, self._ws_ptr(), self.ws_bytes, _stream()),
+                                        shc, train, self._ws_ptr(), self.ws_bytes, _stream()),
                   "wipes_mlp_forward")
         self._last = (F, cp, fp, canon, frame)
         return frame

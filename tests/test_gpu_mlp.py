@@ -136,3 +136,45 @@ def test_mlp_feeds_the_rasterizer():
     assert torch.isfinite(g_theta).all() and g_theta.abs().sum() > 0
     for v in g_canon.values():
         assert torch.isfinite(v).all()
+
+
+@pytest.mark.parametrize("fused_train", [False, True])
+def test_mlp_inference_and_fused_paths_agree(fused_train, tmp_path):
+    """The fused on-chip forward (mlp_fused.cu; used for train=False, and for
+    training with WIPES_MLP_FUSED=1) gives the same frame rows as the
+    layer-by-layer schedule up to fp32 accumulation order; with training on,
+    its stored activations drive the same backward."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2508_12615_b200 import gen
+from paper_2508_12615_b200.deform import Deformation
+N = 1000
+d = Deformation(N)
+th = d.init_theta(2)
+p = gen.gen3d(N, seed=4)
+canon = {{k: torch.from_numpy(v).cuda() for k, v in p.items()}}
+f = d.forward(th, canon, [0.1, 0.9], train={fused_train})
+g = {{k: torch.ones_like(f[k]) for k in ("mean", "quat", "scale", "freq")}}
+out = {{k: v.cpu().numpy() for k, v in f.items()}}
+if {fused_train}:
+    gt, gc = d.backward(th, canon, g)
+    out["g_theta"] = gt.cpu().numpy()
+np.savez(sys.argv[1], **out)
+"""
+    res = {}
+    for tag, env in (("fused", {"WIPES_MLP_FUSED": "1"}), ("unfused", {"WIPES_MLP_UNFUSED": "1"})):
+        path = str(tmp_path / f"mlp_{tag}.npz")
+        e = {k: v for k, v in os.environ.items() if not k.startswith("WIPES_MLP_")}
+        e.update(env)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=e, timeout=300)
+        res[tag] = np.load(path)
+    for k in ("mean", "quat", "scale", "freq", "color", "opacity"):
+        a, b = res["fused"][k].astype(np.float64), res["unfused"][k].astype(np.float64)
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-5 * (np.abs(b).max() + 1e-30))
+    if fused_train:
+        a, b = res["fused"]["g_theta"], res["unfused"]["g_theta"]
+        assert np.linalg.norm(a - b) <= 1e-3 * np.linalg.norm(b)
