@@ -119,3 +119,42 @@ class Deformation:
                                          self._ws_ptr(), self.ws_bytes, _stream()),
                   "wipes_mlp_backward")
         return g_theta, g_canon
+
+
+class _DeformFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, d: "Deformation", times, keys, theta, *canon_vals):
+        canon = {k: v for k, v in zip(keys, canon_vals)}
+        frame = d.forward(theta, canon, times, train=True)
+        ctx.d, ctx.keys, ctx.canon, ctx.theta = d, keys, canon, theta
+        ctx.out_keys = tuple(k for k in DEFORMED + COPIED if k in frame)
+        return tuple(frame[k] for k in ctx.out_keys)
+
+    @staticmethod
+    def backward(ctx, *g_out):
+        g = dict(zip(ctx.out_keys, g_out))
+        g_frame = {k: (g[k] if g.get(k) is not None else torch.zeros_like(ctx.canon[k]).repeat(
+            len(g_out[0]) // ctx.canon[k].shape[0], *([1] * (ctx.canon[k].dim() - 1))))
+            for k in DEFORMED}
+        g_frame = {k: v.contiguous() for k, v in g_frame.items()}
+        g_theta, g_canon = ctx.d.backward(ctx.theta, ctx.canon, g_frame)
+        grads = []
+        F = g_out[0].shape[0] // ctx.canon["mean"].shape[0]
+        for k in ctx.keys:
+            if k in DEFORMED:
+                grads.append(g_canon[k])
+            elif g.get(k) is not None:  # copied groups: sum of the frame rows' gradients
+                grads.append(g[k].reshape(F, *ctx.canon[k].shape).sum(0))
+            else:
+                grads.append(None)
+        return (None, None, None, g_theta) + tuple(grads)
+
+
+def deform(d: Deformation, theta: torch.Tensor, canon: dict, times) -> dict:
+    """Differentiable deformation: returns the frame rows as a dict; gradients
+    flow to theta and the canonical parameters (x enters the network through a
+    stop-gradient, R35)."""
+    keys = tuple(k for k in DEFORMED + COPIED if k in canon)
+    outs = _DeformFn.apply(d, list(times), keys, theta, *[canon[k] for k in keys])
+    out_keys = tuple(k for k in DEFORMED + COPIED if k in canon)
+    return dict(zip(out_keys, outs))
