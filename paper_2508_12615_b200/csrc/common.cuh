@@ -202,6 +202,23 @@ struct MlpFusedDesc {
   __nv_bfloat16* cat;
 };
 bool launch_mlp_fused_fwd(const MlpFusedDesc& d, cudaStream_t s, cudaError_t* err);
+// One hidden layer's backward in one pass (mlp_fused.cu): dz_(l-1) = (dz W) * (act > 0)
+// and the partial sums of dW = dz^T act and db_(l-1) = colsum(dz_(l-1)) per CTA group.
+struct MlpBwdDesc {
+  int32_t W;                   // width (the fused path takes W == 256)
+  int64_t M;                   // rows
+  const __nv_bfloat16* dz;     // [M, W] dL/dz_l
+  const __nv_bfloat16* act;    // [M, W] (pitch act_ld) input of layer l = h_(l-1), also the ReLU mask
+  const __nv_bfloat16* wl;     // [W, W] (pitch w_ld) bf16 weights of layer l (out x in)
+  int64_t act_ld, w_ld;
+  __nv_bfloat16* dzo;          // [M, W] dL/dz_(l-1)
+  float* wpart;                // [groups, W, W] partial dW (rows: out, cols: in)
+  float* bpart;                // [groups * 4, W] partial colsums of dz_(l-1)
+  int32_t max_groups;
+};
+constexpr int kMlpBwdMaxGroups = 128;
+// returns the number of groups (partials) launched, or 0 when outside the envelope
+int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err);
 bool mlp_config_valid(const wipes_mlp_config& c);
 int64_t mlp_param_count(const wipes_mlp_config& c);
 size_t mlp_workspace_bytes(const wipes_mlp_config& c, int64_t rows);

@@ -36,6 +36,7 @@ struct MlpLayout {
   int K[kMlpMaxDepth], Kp[kMlpMaxDepth];
   int64_t thW[kMlpMaxDepth], thb[kMlpMaxDepth], thWh, thbh, P;
   size_t wbf[kMlpMaxDepth], whbf, cat, h[kMlpMaxDepth], out, dout_bf, dout_f, dz[2], dws, total;
+  size_t wpart, bpart;  // fused layer backward partials (width 256 only)
 };
 
 bool mlp_cfg_ok(const wipes_mlp_config& c) {
@@ -77,6 +78,11 @@ MlpLayout mlp_layout(const wipes_mlp_config& c, int64_t M) {
   L.dz[0] = take(2 * (size_t)M * L.W);
   L.dz[1] = take(2 * (size_t)M * L.W);
   L.dws = take(4 * (size_t)L.W * kmax);
+  L.wpart = L.bpart = 0;
+  if (L.W == 256) {
+    L.wpart = take(4 * (size_t)kMlpBwdMaxGroups * 256 * 256);
+    L.bpart = take(4 * (size_t)kMlpBwdMaxGroups * 4 * 256);
+  }
   L.total = b;
   return L;
 }
@@ -239,6 +245,56 @@ __global__ void k_mlp_unpad(const float* dws, int rows, int Kp, int E, int E8, i
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// dst[row * ldd + col] (+)= sum_p parts[p n + i] for i = row * cols + col
+// (deterministic: thread row y sums the parts p = y (mod blockDim.y) in order,
+// then the row sums are added in order y = 0, 1, ..). cols, ldd, n % 4 == 0.
+__global__ void k_mlp_partsum(const float* parts, int np, int64_t n, int64_t cols, int64_t ldd,
+                              float* dst, bool add) {
+  __shared__ float4 red[1024];
+  const int64_t i = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int S = blockDim.y, y = threadIdx.y;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n) {
+    int p = y;
+    for (; p + 3 * S < np; p += 4 * S) {  // four loads in flight per thread
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(parts + (int64_t)(p + u * S) * n + i));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    }
+    for (; p < np; p += S) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(parts + (int64_t)p * n + i));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  red[y * blockDim.x + threadIdx.x] = acc;
+  __syncthreads();
+  if (y == 0 && i < n) {
+    float* d = dst + (i / cols) * ldd + (i % cols);
+    float4 t = add ? *reinterpret_cast<const float4*>(d) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < S; ++k) {
+      const float4 v = red[k * blockDim.x + threadIdx.x];
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    *reinterpret_cast<float4*>(d) = t;
+  }
+}
+
+void partsum(const float* parts, int np, int64_t n, float* dst, bool add, cudaStream_t s,
+             int64_t cols = 0, int64_t ldd = 0) {
+  if (cols == 0) cols = ldd = n;
+  const int bx = n / 4 < 128 ? (int)(n / 4) : 128, by = 1024 / bx < 16 ? 1024 / bx : 16;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_partsum<<<nblk(n / 4, bx), dim3(bx, by), 0, s>>>(parts, np, n, cols, ldd, dst, add);
+  launch_end(K_MLP_MISC, s);
+}
+
+bool mlp_unfused_env() {
+  static const bool unfused = getenv("WIPES_MLP_UNFUSED") != nullptr;
+  return unfused;
+}
+
 cudaError_t gemm(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                  int64_t lda, int64_t ldb, int64_t ldc, int epi, bool amn, bool bmn,
                  const float* bias, const void* mask, int64_t ldm, int split, cudaStream_t s,
@@ -284,7 +340,7 @@ cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, in
   // faster for inference only (0.60 vs 0.66 ms at 300k rows); with train = 1
   // its activation stores make it slower (0.76 ms), so training keeps the
   // layer-by-layer schedule unless WIPES_MLP_FUSED=1.
-  static const bool unfused = getenv("WIPES_MLP_UNFUSED") != nullptr;
+  const bool unfused = mlp_unfused_env();
   static const bool fused_train = getenv("WIPES_MLP_FUSED") != nullptr;
   if (!unfused && (!train || fused_train)) {
     MlpFusedDesc d;
@@ -404,6 +460,44 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
     else if (l - 1 == L.skip) { in = cat + L.E8; ldin = L.catw; }
     else { in = ws + L.h[l - 1]; ldin = L.W; }
     const bool has_cat = l == L.skip + 1;
+    if (l >= 1 && L.W == 256 && !mlp_unfused_env()) {
+      // both GEMMs of the layer in one pass over dz and h_(l-1) (mlp_fused.cu);
+      // after the skip the input is [encoding | h]: the fused pass takes the h
+      // part, a narrow GEMM the encoding columns of dW
+      MlpBwdDesc d;
+      d.W = L.W; d.M = M;
+      d.dz = dz;
+      d.act = (const __nv_bfloat16*)in + (has_cat ? L.E8 : 0);
+      d.act_ld = ldin;
+      d.wl = (const __nv_bfloat16*)(ws + L.wbf[l]) + (has_cat ? L.E8 : 0);
+      d.w_ld = L.Kp[l];
+      d.dzo = dz2;
+      d.wpart = (float*)(ws + L.wpart); d.bpart = (float*)(ws + L.bpart);
+      d.max_groups = kMlpBwdMaxGroups;
+      cudaError_t fe = cudaSuccess;
+      const int groups = launch_mlp_bwd_layer(d, s, &fe);
+      if (fe != cudaSuccess) return fe;
+      if (groups > 0) {
+        const int64_t n = (int64_t)L.W * L.W;
+        if (!has_cat) {
+          partsum(d.wpart, groups, n, g_theta + L.thW[l], false, s);
+        } else {
+          e = cudaMemsetAsync(dws, 0, sizeof(float) * (size_t)L.W * L.Kp[l], s);
+          if (e != cudaSuccess) return e;
+          e = gemm(dz, in, dws, L.W, L.E8, M, L.W, ldin, L.Kp[l], WIPES_GEMM_EPI_ATOMIC_F32, true,
+                   true, nullptr, nullptr, 0, split_for((L.W + 127) / 128), s);
+          if (e != cudaSuccess) return e;
+          partsum(d.wpart, groups, n, dws + L.E8, false, s, L.W, L.Kp[l]);
+          launch_begin(K_MLP_MISC, s);
+          k_mlp_unpad<<<nblk((int64_t)L.W * L.K[l], 256), 256, 0, s>>>(
+              dws, L.W, L.Kp[l], L.E, L.E8, L.K[l], true, g_theta + L.thW[l]);
+          launch_end(K_MLP_MISC, s);
+        }
+        partsum(d.bpart, 2 * groups, L.W, g_theta + L.thb[l - 1], true, s);
+        __nv_bfloat16* t = dz; dz = dz2; dz2 = t;
+        continue;
+      }
+    }
     e = cudaMemsetAsync(dws, 0, sizeof(float) * (size_t)L.W * L.Kp[l], s);
     if (e != cudaSuccess) return e;
     const int64_t tiles = ((L.W + 127) / 128) * ((L.Kp[l] + 255) / 256);

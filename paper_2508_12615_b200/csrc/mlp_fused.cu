@@ -309,6 +309,215 @@ __global__ void __launch_bounds__(kFThreads, 1) k_mlp_fused_fwd(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
 }
 
+// ---------------------------------------------------------------------------
+// Fused backward of one hidden layer (width 256): the two GEMMs of a layer's
+// backward read the same operands (dz_l and the layer input h_(l-1), which is
+// also the ReLU mask), so one pass computes both:
+//   dz_(l-1) = (dz_l W_l) * (h_(l-1) > 0)      [M, 256] bf16
+//   dW_l     = dz_l^T h_(l-1)                   [256, 256] fp32 (per-group partials)
+//   db_(l-1) = colsum(dz_(l-1))                 (per-group partials)
+// CTA pairs ("groups") walk the same 128-row tiles; member m owns input
+// columns [128 m, 128 m + 128): its slice of dW (all 256 rows), the same
+// columns of dz_(l-1), and the matching half of the mask. Both members load
+// the whole dz tile (the second read hits L2), so HBM sees dz and h once and
+// dz_(l-1) once per layer, against twice and once for the two-GEMM schedule.
+// Per CTA: W slice resident (64 KB, MN-major B of the dIn MMA), dz tiles in a
+// ring of 3 x 32 KB halves (K-major A of dIn, MN-major A of dW: the same
+// SW128 bytes serve both), h tiles in a ring of 2 x 32 KB (MN-major B of dW,
+// mask of the epilogue). TMEM: dIn accumulator double-buffered (2 x 128
+// columns) + dW halves (2 x 128 columns, accumulated over all the group's tiles).
+constexpr int kBThreads = 32 * (4 + kFEpiWarps);
+constexpr uint32_t kHalf = 32768;  // 128 rows x 128 columns bf16 (two SW128 boxes)
+
+struct BwdArgs {
+  int64_t M;
+  int32_t groups;
+  float* wpart;
+  float* bpart;
+  __nv_bfloat16* dzo;
+  CUtensorMap tdz, tact, tw;
+};
+
+__global__ void __launch_bounds__(kBThreads, 1) k_mlp_bwd_layer(const __grid_constant__ BwdArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* Wsl = base;                 // 2 boxes [256 rows (out) x 64 in]
+  unsigned char* dzr = base + 2 * kHalf;     // 3 x 32 KB
+  unsigned char* actr = dzr + 3 * kHalf;     // 2 x 32 KB
+  uint64_t* fdz = reinterpret_cast<uint64_t*>(actr + 2 * kHalf);
+  uint64_t* edz = fdz + 3;
+  uint64_t* fact = edz + 3;
+  uint64_t* eact = fact + 2;
+  uint64_t* accf = eact + 2;
+  uint64_t* acce = accf + 2;
+  uint64_t* wbar = acce + 2;
+  uint64_t* dwdone = wbar + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dwdone + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int member = blockIdx.x & 1, grp = blockIdx.x >> 1;
+  const int c0 = 128 * member;
+  const int64_t tiles = (a.M + 127) / 128;
+
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) { mbar_init(&fdz[i], 1); mbar_init(&edz[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&fact[i], 1);
+      mbar_init(&eact[i], 1 + kFEpiWarps);  // the dW MMAs and the epilogue's mask reads
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], kFEpiWarps);
+    }
+    mbar_init(wbar, 1);
+    mbar_init(dwdone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {  // ------------------------------------------- TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(wbar, 2 * kHalf);
+      tma_load_2d(Wsl, &a.tw, c0, 0, wbar);
+      tma_load_2d(Wsl + kHalf, &a.tw, c0 + 64, 0, wbar);
+      int64_t k = 0;
+      for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+        const int m0 = (int)(t * 128);
+        for (int h = 0; h < 2; ++h) {
+          const int64_t q = 2 * k + h;
+          const int st = (int)(q % 3);
+          mbar_wait(&edz[st], ((uint32_t)(q / 3) & 1u) ^ 1u);
+          mbar_expect_tx(&fdz[st], kHalf);
+          tma_load_2d(dzr + st * kHalf, &a.tdz, 128 * h, m0, &fdz[st]);
+          tma_load_2d(dzr + st * kHalf + kHalf / 2, &a.tdz, 128 * h + 64, m0, &fdz[st]);
+          if (h == 0) {  // the mask/B tile between the two dz halves (MMA order)
+            const int sa = (int)(k & 1);
+            mbar_wait(&eact[sa], ((uint32_t)(k >> 1) & 1u) ^ 1u);
+            mbar_expect_tx(&fact[sa], kHalf);
+            tma_load_2d(actr + sa * kHalf, &a.tact, c0, m0, &fact[sa]);
+            tma_load_2d(actr + sa * kHalf + kHalf / 2, &a.tact, c0 + 64, m0, &fact[sa]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // -------------------------------------- MMA issuer
+    // dIn is computed transposed, D[i, r] = sum_j W[j, i] dz[r, j] (A = the W slice,
+    // MN-major; B = the dz tile, K-major), so TMEM lanes are columns and the
+    // epilogue's stores and column sums run along rows
+    const uint32_t id_in = instr_desc(128, true, false), id_w = instr_desc(128, true, true);
+    mbar_wait(wbar, 0);
+    tc_fence_after();
+    const uint32_t wb = smem_u32(Wsl);
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1), sa = (int)(k & 1);
+      const uint32_t tin = tmem + 128u * b;
+      mbar_wait(&acce[b], ((uint32_t)(k >> 1) & 1u) ^ 1u);  // epilogue drained buffer b
+      tc_fence_after();
+      for (int h = 0; h < 2; ++h) {
+        const int64_t q = 2 * k + h;
+        const int st = (int)(q % 3);
+        mbar_wait(&fdz[st], (uint32_t)(q / 3) & 1u);
+        tc_fence_after();
+        const uint32_t dzb = smem_u32(dzr + st * kHalf);
+        if (lane == 0) {
+          // dIn^T: K = dz features 128 h .. 128 h + 127 (two K-major boxes)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const int ks = 8 * h + s;  // global K16 step (out features 16 ks ..)
+            mma_bf16(tin, smem_desc_sw128(wb + 2048 * ks, kHalf, 1024),
+                     smem_desc_sw128(dzb + (s >> 2) * (kHalf / 2) + 32 * (s & 3), 16, 1024), id_in,
+                     ks > 0 ? 1u : 0u);
+          }
+          if (h == 1) mma_commit(&accf[b]);
+        }
+        __syncwarp();
+        if (h == 0) {
+          mbar_wait(&fact[sa], (uint32_t)(k >> 1) & 1u);
+          tc_fence_after();
+        }
+        const uint32_t acb = smem_u32(actr + sa * kHalf);
+        if (lane == 0) {
+          // dW half h: M = out features (MN-major dz), N = in columns (MN-major act), K = rows
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            mma_bf16(tmem + 256u + 128u * h, smem_desc_sw128(dzb + 2048 * s, kHalf / 2, 1024),
+                     smem_desc_sw128(acb + 2048 * s, kHalf / 2, 1024), id_w,
+                     (k > 0 || s > 0) ? 1u : 0u);
+          mma_commit(&edz[st]);
+          if (h == 1) mma_commit(&eact[sa]);
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) mma_commit(dwdone);
+    __syncwarp();
+  } else if (warp >= 4) {  // -------------------------------------- epilogue
+    const int e = warp - 4, q = e & 3, half = e >> 2;
+    const int r = 32 * q + lane;  // TMEM lane: dIn column c0 + r; dW row 128 half + r
+    const int ci = r;             // this thread's dIn column within the slice
+    // mask bytes of column ci in row ro of an h slot (SW128 box ci / 64)
+    const uint32_t mcol = (ci >> 6) * (kHalf / 2) + (((ci & 63) >> 3) << 4) + (ci & 7) * 2;
+    float cs = 0.f;  // column sum over this thread's rows (64 half .. 64 half + 63 of each tile)
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1), sa = (int)(k & 1);
+      mbar_wait(&accf[b], (uint32_t)(k >> 1) & 1u);
+      mbar_wait(&fact[sa], (uint32_t)(k >> 1) & 1u);  // mask bytes visible to this thread
+      tc_fence_after();
+      float v[64];
+      {
+        float v0[32], v1[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128u * b + 64u * half;
+        tmem_ld32(ta, v0);
+        tmem_ld32(ta + 32u, v1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { v[i] = v0[i]; v[32 + i] = v1[i]; }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      const unsigned char* slot = actr + sa * kHalf;
+      const int64_t m0 = t * 128 + 64 * half;
+      __nv_bfloat16* dst = a.dzo + m0 * 256 + c0 + ci;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int ro = 64 * half + j;  // tile row
+        const __nv_bfloat16 mv =
+            *reinterpret_cast<const __nv_bfloat16*>(slot + ro * 128 + (mcol ^ ((ro & 7) << 4)));
+        const float x = __bfloat162float(mv) > 0.f ? v[j] : 0.f;
+        cs += x;  // rows >= M hold zeros (TMA zero fill)
+        if (m0 + j < a.M) dst[(int64_t)j * 256] = __float2bfloat16_rn(x);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&eact[sa]);
+    }
+    a.bpart[((int64_t)grp * 2 + half) * 256 + c0 + ci] = cs;
+    // dW slice: TMEM lanes = out features 128 half + r, columns = in c0 ..
+    mbar_wait(dwdone, 0);
+    tc_fence_after();
+    float* wp = a.wpart + ((int64_t)grp * 256 + 128 * half + r) * 256 + c0;
+#pragma unroll 1
+    for (int cb = 0; cb < 4; ++cb) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 256u + 128u * half + 32u * cb, v);
+      float4* d4 = reinterpret_cast<float4*>(wp + 32 * cb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -381,6 +590,37 @@ bool launch_mlp_fused_fwd(const MlpFusedDesc& d, cudaStream_t s, cudaError_t* er
   launch_end(K_GEMM, s);
   *err = cudaGetLastError();
   return true;
+}
+
+int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err) {
+  if (d.W != 256 || d.M <= 0 || d.M > INT32_MAX - 128) return 0;
+  static thread_local BwdArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.M = d.M; a.wpart = d.wpart; a.bpart = d.bpart; a.dzo = d.dzo;
+  if (!map2d(&a.tdz, d.dz, 256, d.M, 256, 64, 128) ||
+      !map2d(&a.tact, d.act, 256, d.M, d.act_ld, 64, 128) ||
+      !map2d(&a.tw, d.wl, 256, 256, d.w_ld, 64, 256) || (uintptr_t)d.dzo % 16)
+    return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (d.M + 127) / 128;
+  int64_t groups = sms / 2;
+  if (groups > d.max_groups) groups = d.max_groups;
+  if (groups > tiles) groups = tiles;
+  if (groups < 1) return 0;
+  a.groups = (int32_t)groups;
+  const int smem = 7 * (int)kHalf + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_bwd_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  launch_begin(K_GEMM, s);
+  k_mlp_bwd_layer<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
+  launch_end(K_GEMM, s);
+  *err = cudaGetLastError();
+  return (int)groups;
 }
 
 }  // namespace wipes
