@@ -55,21 +55,34 @@ def _rel_ok(got, ref, frac=2e-2):
 def _grad_ok(got, ref, depth):
     """Backward: dL/dz is rounded to bf16 at every layer on the GPU, a relative
     2^-9 per layer, so the gradient of layer l carries up to ~(D - l) 2^-9;
-    bound: norm-wise 2 D 2^-9 (x2 margin), element-wise 8x that of the rms."""
+    bound (R36): norm-wise tol = 2 (D + 1) 2^-9, element-wise
+    tol |ref| + 8 tol rms. The relative term matters at many rows: an entry fed
+    by a constant-sign input column (t, the x coordinates) sums coherently over
+    the rows and outgrows the rms by ~sqrt(rows), while its rounding error stays
+    relative to itself."""
     got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
     nrm = np.linalg.norm(ref) + 1e-30
     rel = float(np.linalg.norm(got - ref) / nrm)
     tol = 2 * (depth + 1) * 2.0 ** -9
     rms = nrm / np.sqrt(ref.size)
-    return rel, rel <= tol and bool(np.all(np.abs(got - ref) <= 8 * tol * rms))
+    return rel, rel <= tol and bool(np.all(np.abs(got - ref) <= tol * np.abs(ref) + 8 * tol * rms))
 
 
 @pytest.mark.parametrize("shape", [dict(width=256, depth=8, skip=4, Lx=10, Lt=6),
                                    dict(width=64, depth=3, skip=0, Lx=4, Lt=2),
                                    dict(width=128, depth=2, skip=-1, Lx=10, Lt=6)])
 def test_mlp_forward_backward_parity(shape):
+    _mlp_parity(shape, 1000, [0.0, 0.37, 1.0])
+
+
+def test_mlp_parity_many_tiles_per_cta():
+    """40,000 rows (313 row tiles, ragged): every CTA pair of the fused layer
+    backward accumulates dW over several tiles and cycles its operand rings."""
+    _mlp_parity(dict(width=256, depth=8, skip=4, Lx=10, Lt=6), 20000, [0.25, 0.75])
+
+
+def _mlp_parity(shape, N, times):
     from paper_2508_12615_b200.deform import Deformation
-    N, times = 1000, [0.0, 0.37, 1.0]
     d = Deformation(N, **shape)
     theta = d.init_theta(seed=1)
     p = gen.gen3d(N, seed=3, scale_mult=4.0)
@@ -86,10 +99,10 @@ def test_mlp_forward_backward_parity(shape):
         worst, ok = _rel_ok(delta_g, delta_o)
         assert ok, (k, worst)
     # scale: compare the network output ds = log(s_t / s)
-    ds_g = np.log(frame["scale"].cpu().numpy().astype(np.float64) / np.tile(p["scale"], (3, 1)))
+    ds_g = np.log(frame["scale"].cpu().numpy().astype(np.float64) / np.tile(p["scale"], (len(times), 1)))
     worst, ok = _rel_ok(ds_g, cache["out"][:, 7:10])
     assert ok, ("scale", worst)
-    np.testing.assert_array_equal(frame["color"].cpu().numpy(), np.tile(p["color"], (3, 1)))
+    np.testing.assert_array_equal(frame["color"].cpu().numpy(), np.tile(p["color"], (len(times), 1)))
     # backward from a random upstream gradient of the frame rows
     rng = np.random.default_rng(5)
     gfr = {k: rng.normal(size=frame[k].shape).astype(np.float32)
