@@ -476,10 +476,15 @@ __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w,
 }
 
 // Backward of one pixel for one record (predicated on `h`).
+// ALPHA: T is the transmittance in front of the pixel's current record, sdg =
+// S.g with S the colour accumulated behind it (incl. T_final bg); since
+// S' = S + c aT, sdg is carried directly: sdg' = sdg + (c.g) aT. A
+// non-contributing pair gets al = 0, so rcp(1) = 1 leaves T, sdg unchanged and
+// aT = 0 without selects; only dL/dw needs the gate.
 template <bool ALPHA, bool EXACT>
 __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, const float4& r2,
                                           const float4& r3, const float (&g)[3], float amin,
-                                          float amax, float& T, float (&S)[3], float (&m)[kMom],
+                                          float amax, float& T, float& sdg, float (&m)[kMom],
                                           float& mb, bool& any) {
   const float ag = ex2(e);
   const float th = pair_theta(r2, dx, dy);
@@ -493,19 +498,16 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
     add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g[0], we * g[1], we * g[2]);
     if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
-    const float al = fminf(amax, w);
-    const float ri = rcp_a(1.f - al);
+    const float al = ok ? fminf(amax, w) : 0.f;
+    const float ri = rcp_a(1.f - al);  // exactly 1 when al = 0
     const float Tk = T * ri;
-    const float sdg = __fmaf_rn(S[0], g[0], __fmaf_rn(S[1], g[1], __fmul_rn(S[2], g[2])));
     const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
-    const float aT = ok ? al * Tk : 0.f;
-    S[0] = __fmaf_rn(r3.x, aT, S[0]);
-    S[1] = __fmaf_rn(r3.y, aT, S[1]);
-    S[2] = __fmaf_rn(r3.z, aT, S[2]);
-    T = ok ? Tk : T;
-    add_moments(m, (ok && w < amax) ? dLda : 0.f, ok ? w : 0.f, ag, sn, dx, dy, aT * g[0],
-                aT * g[1], aT * g[2]);
-    if (EXACT) mb = __fmaf_rn((ok && w < amax) ? dLda * ag : 0.f, cs, mb);
+    const float aT = al * Tk;
+    sdg = __fmaf_rn(gdc, aT, sdg);
+    T = Tk;
+    const float gw = (ok && w < amax) ? dLda : 0.f;
+    add_moments(m, gw, w, ag, sn, dx, dy, aT * g[0], aT * g[1], aT * g[2]);
+    if (EXACT) mb = __fmaf_rn(gw * ag, cs, mb);
   }
 }
 
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
     const int64_t HW = (int64_t)a.H * a.W;
     const float* gp = a.dLdC + it.v * 3 * HW;
     bool in[P];
-    float g[P][3], T[P], S[P][3];
+    float g[P][3], T[P], sdg[P];
     int last[P];
     int ml = 0;
 #pragma unroll
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
       in[p] = it.x < a.W && y < a.H;
       g[p][0] = g[p][1] = g[p][2] = 0.f;
       T[p] = 1.f;
-      S[p][0] = S[p][1] = S[p][2] = 0.f;
+      sdg[p] = 0.f;
       last[p] = 0;
       if (in[p]) {
         const int64_t q = (int64_t)y * a.W + it.x;
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
         if (ALPHA) {
           T[p] = a.T_in[it.v * HW + q];
           last[p] = a.nc_in[it.v * HW + q];
-          S[p][0] = T[p] * a.bg0; S[p][1] = T[p] * a.bg1; S[p][2] = T[p] * a.bg2;
+          sdg[p] = T[p] * __fmaf_rn(a.bg0, g[p][0], __fmaf_rn(a.bg1, g[p][1], a.bg2 * g[p][2]));
           ml = max(ml, last[p]);
         }
       }
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
         for (int p = 0; p < P; ++p)
           if (bm[p])
             bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min,
-                                    a.alpha_max, T[p], S[p], m, mb, any);
+                                    a.alpha_max, T[p], sdg[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
         const float red = transpose_reduce12(m, lane);
         if (EXACT) {
