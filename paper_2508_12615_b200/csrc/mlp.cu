@@ -87,20 +87,27 @@ MlpLayout mlp_layout(const wipes_mlp_config& c, int64_t M) {
   return L;
 }
 
-// theta (fp32, true widths) -> padded bf16 weights of one layer (l < D) or the head.
-__global__ void k_mlp_weights(const float* theta, int64_t thW, int rows, int rows_valid, int Kp,
-                              int E, int E8, int K, bool has_cat, __nv_bfloat16* dst) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)rows * Kp) return;
-  const int j = (int)(idx / Kp), c = (int)(idx - (int64_t)j * Kp);
-  float v = 0.f;
-  if (j < rows_valid) {
-    int src = -1;
-    if (!has_cat) src = c < K ? c : -1;            // plain layer / layer 0 (K = E)
-    else src = c < E ? c : (c < E8 ? -1 : c - E8 + E);  // [gamma | pad | h]
-    if (src >= 0) v = theta[thW + (int64_t)j * K + src];
+// theta (fp32, true widths) -> padded bf16 weights of every layer and the head.
+// All layers and the head in one launch (blockIdx.y = layer).
+struct WeightJobs {
+  int n;
+  struct Job { int64_t thW; int rows, rows_valid, Kp, K; bool has_cat; __nv_bfloat16* dst; } j[kMlpMaxDepth + 1];
+};
+__global__ void k_mlp_weights_all(const float* theta, int E, int E8, const __grid_constant__ WeightJobs w) {
+  const WeightJobs::Job& jb = w.j[blockIdx.y];
+  const int64_t n = (int64_t)jb.rows * jb.Kp;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / jb.Kp), c = (int)(idx - (int64_t)j * jb.Kp);
+    float v = 0.f;
+    if (j < jb.rows_valid) {
+      int src = -1;
+      if (!jb.has_cat) src = c < jb.K ? c : -1;
+      else src = c < E ? c : (c < E8 ? -1 : c - E8 + E);
+      if (src >= 0) v = theta[jb.thW + (int64_t)j * jb.K + src];
+    }
+    jb.dst[idx] = __float2bfloat16_rn(v);
   }
-  dst[idx] = __float2bfloat16_rn(v);
 }
 
 struct EmbedArgs {
@@ -323,18 +330,23 @@ cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, in
   const MlpLayout L = mlp_layout(c, M);
   if (M == 0) return cudaSuccess;
   // bf16 weights (rounded to nearest even)
-  for (int l = 0; l < L.D; ++l) {
-    const bool cat = l == L.skip + 1;
+  {
+    WeightJobs wj;
+    wj.n = L.D + 1;
+    for (int l = 0; l <= L.D; ++l) {
+      WeightJobs::Job& jb = wj.j[l];
+      if (l < L.D) {
+        jb.thW = L.thW[l]; jb.rows = L.W; jb.rows_valid = L.W; jb.Kp = L.Kp[l]; jb.K = L.K[l];
+        jb.has_cat = l == L.skip + 1; jb.dst = (__nv_bfloat16*)(ws + L.wbf[l]);
+      } else {
+        jb.thW = L.thWh; jb.rows = kOutCols; jb.rows_valid = 13; jb.Kp = L.W; jb.K = L.W;
+        jb.has_cat = false; jb.dst = (__nv_bfloat16*)(ws + L.whbf);
+      }
+    }
     launch_begin(K_MLP_MISC, s);
-    k_mlp_weights<<<nblk((int64_t)L.W * L.Kp[l], 256), 256, 0, s>>>(
-        theta, L.thW[l], L.W, L.W, L.Kp[l], L.E, L.E8, L.K[l], cat,
-        (__nv_bfloat16*)(ws + L.wbf[l]));
+    k_mlp_weights_all<<<dim3(64, wj.n), 256, 0, s>>>(theta, L.E, L.E8, wj);
     launch_end(K_MLP_MISC, s);
   }
-  launch_begin(K_MLP_MISC, s);
-  k_mlp_weights<<<nblk((int64_t)kOutCols * L.W, 256), 256, 0, s>>>(
-      theta, L.thWh, kOutCols, 13, L.W, L.E, L.E8, L.W, false, (__nv_bfloat16*)(ws + L.whbf));
-  launch_end(K_MLP_MISC, s);
   __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
   // fused path (mlp_fused.cu): all layers of a 128-row tile on chip. Measured
   // faster for inference only (0.60 vs 0.66 ms at 300k rows); with train = 1

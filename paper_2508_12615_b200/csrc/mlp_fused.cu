@@ -35,9 +35,14 @@ using namespace tc;
 
 constexpr int kFMaxD = 8;
 constexpr int kFMaxFrames = 128;
-constexpr int kFStages = 3;
-constexpr int kFEpiWarps = 8;
+constexpr int kFStages = 4;  // a whole 256-wide layer of weights in flight (224 KB with X)
+#ifndef WIPES_FWD_EPI_WARPS
+#define WIPES_FWD_EPI_WARPS 16
+#endif
+constexpr int kFEpiWarps = WIPES_FWD_EPI_WARPS;  // forward epilogue: 4 per TMEM lane quarter
+constexpr int kFParts = kFEpiWarps / 4;          // column parts per lane quarter
 constexpr int kFThreads = 32 * (4 + kFEpiWarps);
+constexpr int kBEpiWarps = 8;                    // layer backward epilogue
 constexpr uint32_t kXChunk = 128 * 64 * 2;  // 16 KB
 
 struct FusedArgs {
@@ -180,9 +185,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_mlp_fused_fwd(const __grid_con
         __syncwarp();
       }
   } else if (warp >= 4) {  // -------------------------------------- epilogue
-    const int e = warp - 4, q = e & 3, half = e >> 2;
+    const int e = warp - 4, q = e & 3, half = e >> 2;  // half: column part 0 .. kFParts - 1
     const int r = 32 * q + lane;  // tile row = TMEM lane
-    const int nb = a.W / 32, cb0 = half * nb / 2, cb1 = (half + 1) * nb / 2;
+    const int nb = a.W / 32, cb0 = half * nb / kFParts, cb1 = (half + 1) * nb / kFParts;
     const bool issuer = (e == 0 && lane == 0);
     uint32_t aph = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_mlp_fused_fwd(const __grid_con
 // SW128 bytes serve both), h tiles in a ring of 2 x 32 KB (MN-major B of dW,
 // mask of the epilogue). TMEM: dIn accumulator double-buffered (2 x 128
 // columns) + dW halves (2 x 128 columns, accumulated over all the group's tiles).
-constexpr int kBThreads = 32 * (4 + kFEpiWarps);
+constexpr int kBThreads = 32 * (4 + kBEpiWarps);
 constexpr uint32_t kHalf = 32768;  // 128 rows x 128 columns bf16 (two SW128 boxes)
 
 struct BwdArgs {
@@ -368,9 +373,9 @@ __global__ void __launch_bounds__(kBThreads, 1) k_mlp_bwd_layer(const __grid_con
     for (int i = 0; i < 3; ++i) { mbar_init(&fdz[i], 1); mbar_init(&edz[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&fact[i], 1);
-      mbar_init(&eact[i], 1 + kFEpiWarps);  // the dW MMAs and the epilogue's mask reads
+      mbar_init(&eact[i], 1 + kBEpiWarps);  // the dW MMAs and the epilogue's mask reads
       mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], kFEpiWarps);
+      mbar_init(&acce[i], kBEpiWarps);
     }
     mbar_init(wbar, 1);
     mbar_init(dwdone, 1);
