@@ -454,28 +454,31 @@ __device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) 
 // Moments of one pair, gw = dL/dw and w already zeroed when the
 // pair does not contribute: M0 = gw w, M1 = gw w dx, M2 = gw w dy,
 // M3 = gw w dx^2, M4 = gw w dx dy, M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx,
-// M8 = M6 dy, M9..11 = dL/dc terms.
+// M8 = M6 dy, M9..11 = dL/dc terms. A lane's pixels share dx (one column), so
+// the slots accumulate only the dx-free sums and finish_moments applies dx once
+// per record: M1 = dx M0, M3 = dx M1, M4 = dx M2, M7 = dx M6.
 __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w, float ag,
-                                            float sn, float dx, float dy, float c0, float c1,
-                                            float c2) {
+                                            float sn, float dy, float c0, float c1, float c2) {
   const float gww = gw * w;
-  const float m1 = gww * dx, m2 = gww * dy;
+  const float m2 = gww * dy;
   const float m6 = gw * ag * sn;
   m[0] += gww;
-  m[1] += m1;
   m[2] += m2;
-  m[3] = __fmaf_rn(m1, dx, m[3]);
-  m[4] = __fmaf_rn(m1, dy, m[4]);
   m[5] = __fmaf_rn(m2, dy, m[5]);
   m[6] += m6;
-  m[7] = __fmaf_rn(m6, dx, m[7]);
   m[8] = __fmaf_rn(m6, dy, m[8]);
   m[9] += c0;
   m[10] += c1;
   m[11] += c2;
 }
 
-// Backward of one pixel for one record (predicated on `h`).
+__device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx) {
+  m[1] = m[0] * dx;
+  m[3] = m[1] * dx;
+  m[4] = m[2] * dx;
+  m[7] = m[6] * dx;
+}
+
 // ALPHA: T is the transmittance in front of the pixel's current record, sdg =
 // S.g with S the colour accumulated behind it (incl. T_final bg); since
 // S' = S + c aT, sdg is carried directly: sdg' = sdg + (c.g) aT. A
@@ -495,7 +498,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
   const float gdc = __fmaf_rn(r3.x, g[0], __fmaf_rn(r3.y, g[1], __fmul_rn(r3.z, g[2])));
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
-    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dx, dy, we * g[0], we * g[1], we * g[2]);
+    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dy, we * g[0], we * g[1], we * g[2]);
     if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
     const float al = ok ? fminf(amax, w) : 0.f;
@@ -506,7 +509,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
     sdg = __fmaf_rn(gdc, aT, sdg);
     T = Tk;
     const float gw = (ok && w < amax) ? dLda : 0.f;
-    add_moments(m, gw, w, ag, sn, dx, dy, aT * g[0], aT * g[1], aT * g[2]);
+    add_moments(m, gw, w, ag, sn, dy, aT * g[0], aT * g[1], aT * g[2]);
     if (EXACT) mb = __fmaf_rn(gw * ag, cs, mb);
   }
 }
@@ -597,6 +600,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
             bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min,
                                     a.alpha_max, T[p], sdg[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
+        finish_moments(m, dx);
         const float red = transpose_reduce12(m, lane);
         if (EXACT) {
 #pragma unroll
