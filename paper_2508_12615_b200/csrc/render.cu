@@ -454,25 +454,30 @@ __device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) 
 // Moments of one pair, gw = dL/dw and w already zeroed when the
 // pair does not contribute: M0 = gw w, M1 = gw w dx, M2 = gw w dy,
 // M3 = gw w dx^2, M4 = gw w dx dy, M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx,
-// M8 = M6 dy, M9..11 = dL/dc terms. A lane's pixels share dx (one column), so
-// the slots accumulate only the dx-free sums and finish_moments applies dx once
-// per record: M1 = dx M0, M3 = dx M1, M4 = dx M2, M7 = dx M6.
+// M8 = M6 dy, M9..11 = dL/dc terms. A lane's pixels share dx (one column) and
+// have dy = dy0 + ky with the slot offset ky in {0, 4, 8, 12} a compile-time
+// constant, so the slots accumulate sums over ky only (slot 0 adds nothing to
+// them) and finish_moments applies dx and dy0 once per record.
 __device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w, float ag,
-                                            float sn, float dy, float c0, float c1, float c2) {
+                                            float sn, float ky, float c0, float c1, float c2) {
   const float gww = gw * w;
-  const float m2 = gww * dy;
   const float m6 = gw * ag * sn;
   m[0] += gww;
-  m[2] += m2;
-  m[5] = __fmaf_rn(m2, dy, m[5]);
   m[6] += m6;
-  m[8] = __fmaf_rn(m6, dy, m[8]);
+  if (ky != 0.f) {
+    m[2] = __fmaf_rn(gww, ky, m[2]);       // sum gww ky
+    m[5] = __fmaf_rn(gww, ky * ky, m[5]);  // sum gww ky^2
+    m[8] = __fmaf_rn(m6, ky, m[8]);        // sum m6 ky
+  }
   m[9] += c0;
   m[10] += c1;
   m[11] += c2;
 }
 
-__device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx) {
+__device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx, float dy0) {
+  m[5] = __fmaf_rn(dy0, __fmaf_rn(dy0, m[0], 2.f * m[2]), m[5]);
+  m[2] = __fmaf_rn(dy0, m[0], m[2]);
+  m[8] = __fmaf_rn(dy0, m[6], m[8]);
   m[1] = m[0] * dx;
   m[3] = m[1] * dx;
   m[4] = m[2] * dx;
@@ -485,7 +490,8 @@ __device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx) {
 // non-contributing pair gets al = 0, so rcp(1) = 1 leaves T, sdg unchanged and
 // aT = 0 without selects; only dL/dw needs the gate.
 template <bool ALPHA, bool EXACT>
-__device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, const float4& r2,
+__device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, float ky,
+                                          const float4& r2,
                                           const float4& r3, const float (&g)[3], float amin,
                                           float amax, float& T, float& sdg, float (&m)[kMom],
                                           float& mb, bool& any) {
@@ -498,7 +504,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
   const float gdc = __fmaf_rn(r3.x, g[0], __fmaf_rn(r3.y, g[1], __fmul_rn(r3.z, g[2])));
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
-    add_moments(m, ok ? gdc : 0.f, we, ag, sn, dy, we * g[0], we * g[1], we * g[2]);
+    add_moments(m, ok ? gdc : 0.f, we, ag, sn, ky, we * g[0], we * g[1], we * g[2]);
     if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
     const float al = ok ? fminf(amax, w) : 0.f;
@@ -509,7 +515,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, c
     sdg = __fmaf_rn(gdc, aT, sdg);
     T = Tk;
     const float gw = (ok && w < amax) ? dLda : 0.f;
-    add_moments(m, gw, w, ag, sn, dy, aT * g[0], aT * g[1], aT * g[2]);
+    add_moments(m, gw, w, ag, sn, ky, aT * g[0], aT * g[1], aT * g[2]);
     if (EXACT) mb = __fmaf_rn(gw * ag, cs, mb);
   }
 }
@@ -597,10 +603,10 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
 #pragma unroll
         for (int p = 0; p < P; ++p)
           if (bm[p])
-            bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], r2, r3, g[p], a.alpha_min,
-                                    a.alpha_max, T[p], sdg[p], m, mb, any);
+            bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], 8.f * (p >> 1) + 4.f * (p & 1), r2,
+                                    r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
-        finish_moments(m, dx);
+        finish_moments(m, dx, dy[0]);
         const float red = transpose_reduce12(m, lane);
         if (EXACT) {
 #pragma unroll
