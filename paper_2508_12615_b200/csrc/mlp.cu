@@ -193,10 +193,21 @@ __global__ void __launch_bounds__(128) k_mlp_dout(int64_t N, int64_t M, const fl
     v[7 + d] = g.scale[3 * m + d] * (scale[3 * i + d] * expf(out[m * kOutCols + 7 + d]));
   for (int d = 0; d < 3; ++d) v[10 + d] = g.freq[3 * m + d];
   for (int d = 13; d < kOutCols; ++d) v[d] = 0.f;
-  for (int d = 0; d < kOutCols; ++d) {
-    dbf[m * kOutCols + d] = __float2bfloat16_rn(v[d]);
-    df[m * kOutCols + d] = v[d];
+  // one row = 32 B of bf16 + 64 B of fp32: 16-byte vector stores
+  static_assert(kOutCols == 16, "row of 16 outputs");
+  uint4 u[2];
+  uint32_t* w = reinterpret_cast<uint32_t*>(u);
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const __nv_bfloat162 pr = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+    w[h] = *reinterpret_cast<const uint32_t*>(&pr);
   }
+  uint4* db = reinterpret_cast<uint4*>(dbf + m * kOutCols);
+  db[0] = u[0];
+  db[1] = u[1];
+  float4* d4 = reinterpret_cast<float4*>(df + m * kOutCols);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 
 // Head-bias gradient: column sums of dL/dout (fp32) over the rows.

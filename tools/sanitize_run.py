@@ -61,6 +61,14 @@ def run_next():
     canon = dev(q)
     fr = d.forward(th, canon, [0.0, 0.5])
     d.backward(th, canon, {k: torch.randn_like(fr[k]) for k in ("mean", "quat", "scale", "freq")})
+    d.forward(th, canon, [0.0, 0.5], train=False)  # the fused on-chip forward
+    # 20,000 rows (157 tiles, ragged): multi-tile rings of the fused layer backward
+    d2 = Deformation(10000)
+    th2 = d2.init_theta(1)
+    c2 = dev(gen.gen3d(10000, seed=2))
+    fr2 = d2.forward(th2, c2, [0.25, 0.75])
+    d2.backward(th2, c2, {k: torch.randn_like(fr2[k]) for k in ("mean", "quat", "scale", "freq")})
+    d2.forward(th2, c2, [0.25, 0.75], train=False)
     for amn in (False, True):
         for bmn in (False, True):
             A = torch.randn(304, 136, device="cuda").to(torch.bfloat16)
