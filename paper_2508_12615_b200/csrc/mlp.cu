@@ -266,31 +266,42 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 // dst[row * ldd + col] (+)= sum_p parts[p n + i] for i = row * cols + col
 // (deterministic: thread row y sums the parts p = y (mod blockDim.y) in order,
 // then the row sums are added in order y = 0, 1, ..). cols, ldd, n % 4 == 0.
-__global__ void k_mlp_partsum(const float* parts, int np, int64_t n, int64_t cols, int64_t ldd,
-                              float* dst, bool add) {
+// Up to two independent jobs per launch (blockIdx.y).
+struct PartJob {
+  const float* parts;
+  int np;
+  int64_t n, cols, ldd;
+  float* dst;
+  bool add;
+};
+struct PartJobs { PartJob j[2]; };
+
+__global__ void k_mlp_partsum(const __grid_constant__ PartJobs jobs) {
   __shared__ float4 red[1024];
+  const PartJob& jb = jobs.j[blockIdx.y];
   const int64_t i = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if ((int64_t)blockIdx.x * blockDim.x * 4 >= jb.n) return;  // whole block idle (uniform)
   const int S = blockDim.y, y = threadIdx.y;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (i < n) {
+  if (i < jb.n) {
     int p = y;
-    for (; p + 3 * S < np; p += 4 * S) {  // four loads in flight per thread
+    for (; p + 3 * S < jb.np; p += 4 * S) {  // four loads in flight per thread
       float4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(parts + (int64_t)(p + u * S) * n + i));
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(jb.parts + (int64_t)(p + u * S) * jb.n + i));
 #pragma unroll
       for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
     }
-    for (; p < np; p += S) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(parts + (int64_t)p * n + i));
+    for (; p < jb.np; p += S) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(jb.parts + (int64_t)p * jb.n + i));
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
   }
   red[y * blockDim.x + threadIdx.x] = acc;
   __syncthreads();
-  if (y == 0 && i < n) {
-    float* d = dst + (i / cols) * ldd + (i % cols);
-    float4 t = add ? *reinterpret_cast<const float4*>(d) : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (y == 0 && i < jb.n) {
+    float* d = jb.dst + (i / jb.cols) * jb.ldd + (i % jb.cols);
+    float4 t = jb.add ? *reinterpret_cast<const float4*>(d) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < S; ++k) {
       const float4 v = red[k * blockDim.x + threadIdx.x];
       t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
@@ -299,12 +310,23 @@ __global__ void k_mlp_partsum(const float* parts, int np, int64_t n, int64_t col
   }
 }
 
-void partsum(const float* parts, int np, int64_t n, float* dst, bool add, cudaStream_t s,
-             int64_t cols = 0, int64_t ldd = 0) {
-  if (cols == 0) cols = ldd = n;
-  const int bx = n / 4 < 128 ? (int)(n / 4) : 128, by = 1024 / bx < 16 ? 1024 / bx : 16;
+PartJob part_job(const float* parts, int np, int64_t n, float* dst, bool add, int64_t cols = 0,
+                 int64_t ldd = 0) {
+  PartJob j;
+  j.parts = parts; j.np = np; j.n = n; j.dst = dst; j.add = add;
+  j.cols = cols ? cols : n;
+  j.ldd = cols ? ldd : n;
+  return j;
+}
+
+// the weight and bias partial sums of one fused layer in one launch
+void partsum2(const PartJob& a, const PartJob& b, cudaStream_t s) {
+  PartJobs jobs;
+  jobs.j[0] = a;
+  jobs.j[1] = b;
+  const int64_t nmax = a.n > b.n ? a.n : b.n;
   launch_begin(K_MLP_MISC, s);
-  k_mlp_partsum<<<nblk(n / 4, bx), dim3(bx, by), 0, s>>>(parts, np, n, cols, ldd, dst, add);
+  k_mlp_partsum<<<dim3(nblk(nmax / 4, 128), 2), dim3(128, 8), 0, s>>>(jobs);
   launch_end(K_MLP_MISC, s);
 }
 
@@ -502,21 +524,21 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
       if (fe != cudaSuccess) return fe;
       if (groups > 0) {
         const int64_t n = (int64_t)L.W * L.W;
+        const PartJob bj = part_job(d.bpart, 2 * groups, L.W, g_theta + L.thb[l - 1], true);
         if (!has_cat) {
-          partsum(d.wpart, groups, n, g_theta + L.thW[l], false, s);
+          partsum2(part_job(d.wpart, groups, n, g_theta + L.thW[l], false), bj, s);
         } else {
           e = cudaMemsetAsync(dws, 0, sizeof(float) * (size_t)L.W * L.Kp[l], s);
           if (e != cudaSuccess) return e;
           e = gemm(dz, in, dws, L.W, L.E8, M, L.W, ldin, L.Kp[l], WIPES_GEMM_EPI_ATOMIC_F32, true,
                    true, nullptr, nullptr, 0, split_for((L.W + 127) / 128), s);
           if (e != cudaSuccess) return e;
-          partsum(d.wpart, groups, n, dws + L.E8, false, s, L.W, L.Kp[l]);
+          partsum2(part_job(d.wpart, groups, n, dws + L.E8, false, L.W, L.Kp[l]), bj, s);
           launch_begin(K_MLP_MISC, s);
           k_mlp_unpad<<<nblk((int64_t)L.W * L.K[l], 256), 256, 0, s>>>(
               dws, L.W, L.Kp[l], L.E, L.E8, L.K[l], true, g_theta + L.thW[l]);
           launch_end(K_MLP_MISC, s);
         }
-        partsum(d.bpart, 2 * groups, L.W, g_theta + L.thb[l - 1], true, s);
         __nv_bfloat16* t = dz; dz = dz2; dz2 = t;
         continue;
       }
