@@ -217,6 +217,18 @@ struct MlpBwdDesc {
   int32_t max_groups;
 };
 constexpr int kMlpBwdMaxGroups = 128;
+// One hidden layer's forward (mlp_fused.cu): out = relu(x W^T + b) in bf16, x [M, 256]
+// (pitch x_ld), W [256, 256] bf16 (out x in), b fp32 [256], out pitch out_ld.
+struct MlpFwdLayerDesc {
+  int32_t W;
+  int64_t M, x_ld, out_ld;
+  const __nv_bfloat16* x;
+  const __nv_bfloat16* w;
+  const float* bias;
+  __nv_bfloat16* out;
+};
+// returns false when outside the envelope (W != 256 or unaligned operands)
+bool launch_mlp_fwd_layer(const MlpFwdLayerDesc& d, cudaStream_t s, cudaError_t* err);
 // returns the number of groups (partials) launched, or 0 when outside the envelope
 int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err);
 bool mlp_config_valid(const wipes_mlp_config& c);

@@ -427,6 +427,18 @@ cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, in
     else { in = ws + L.h[l - 1]; ldin = L.W; }
     void* outp = l == L.skip ? (void*)(cat + L.E8) : (void*)(ws + L.h[l]);
     const int64_t ldo = l == L.skip ? L.catw : L.W;
+    if (l >= 1 && l != L.skip + 1 && L.W == 256 && !unfused) {
+      // x read once (CTA pairs split the output columns), transposed epilogue
+      MlpFwdLayerDesc d;
+      d.W = L.W; d.M = M; d.x = (const __nv_bfloat16*)in; d.x_ld = ldin;
+      d.w = (const __nv_bfloat16*)(ws + L.wbf[l]); d.bias = theta + L.thb[l];
+      d.out = (__nv_bfloat16*)outp; d.out_ld = ldo;
+      cudaError_t fe = cudaSuccess;
+      if (launch_mlp_fwd_layer(d, s, &fe)) {
+        e = fe;
+        continue;
+      }
+    }
     e = gemm(in, ws + L.wbf[l], outp, M, L.W, L.Kp[l], ldin, L.Kp[l], ldo,
              WIPES_GEMM_EPI_BIAS_RELU_BF16, false, false, theta + L.thb[l], nullptr, 0, 1, s);
   }

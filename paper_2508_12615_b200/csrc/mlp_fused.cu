@@ -523,6 +523,149 @@ __global__ void __launch_bounds__(kBThreads, 1) k_mlp_bwd_layer(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
+// ---------------------------------------------------------------------------
+// One hidden layer's forward (width 256) in the same shape as the layer
+// backward: CTA pairs walk the same 128-row tiles and member m owns output
+// columns [128 m, 128 m + 128) — its W slice (128 x 256 bf16, 64 KB) stays
+// resident as the K-major A operand, the x tiles stream through a ring of four
+// 32 KB halves as the K-major B operand, and the accumulator is transposed
+// (TMEM lanes = output columns, double-buffered 2 x 128 columns) so the
+// epilogue writes bias + ReLU + bf16 rows into a staging tile (64 B per warp
+// row, conflict-free) that one TMA store sends out. The partner's read of the
+// same x tile hits L2: HBM sees x once and h once.
+struct FwdLayerArgs {
+  int64_t M;
+  const float* bias;
+  int32_t groups;
+  CUtensorMap tx, tw, to;
+};
+
+__global__ void __launch_bounds__(kBThreads, 1) k_mlp_fwd_layer(const __grid_constant__ FwdLayerArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* Wsl = base;               // 4 boxes [128 out x 64 in] (K chunks)
+  unsigned char* ostg = base + 2 * kHalf;  // output staging [128 rows x 128 columns] bf16
+  unsigned char* xr = base + 3 * kHalf;    // 4 x 32 KB (two K boxes of one tile each)
+  constexpr int kSlots = 4;
+  uint64_t* fx = reinterpret_cast<uint64_t*>(xr + kSlots * kHalf);
+  uint64_t* ex = fx + kSlots;
+  uint64_t* accf = ex + kSlots;
+  uint64_t* acce = accf + 2;
+  uint64_t* wbar = acce + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int member = blockIdx.x & 1, grp = blockIdx.x >> 1;
+  const int c0 = 128 * member;
+  const int64_t tiles = (a.M + 127) / 128;
+
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&fx[i], 1); mbar_init(&ex[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&accf[i], 1); mbar_init(&acce[i], kBEpiWarps); }
+    mbar_init(wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {  // ------------------------------------------- TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(wbar, 2 * kHalf);
+      for (int c = 0; c < 4; ++c) tma_load_2d(Wsl + c * (kHalf / 2), &a.tw, 64 * c, c0, wbar);
+      int64_t k = 0;
+      for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+        for (int h = 0; h < 2; ++h) {
+          const int64_t q = 2 * k + h;
+          const int st = (int)(q % kSlots);
+          mbar_wait(&ex[st], ((uint32_t)(q / kSlots) & 1u) ^ 1u);
+          mbar_expect_tx(&fx[st], kHalf);
+          tma_load_2d(xr + st * kHalf, &a.tx, 128 * h, (int)(t * 128), &fx[st]);
+          tma_load_2d(xr + st * kHalf + kHalf / 2, &a.tx, 128 * h + 64, (int)(t * 128), &fx[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {  // -------------------------------------- MMA issuer
+    const uint32_t id = instr_desc(128, false, false);
+    mbar_wait(wbar, 0);
+    tc_fence_after();
+    const uint32_t wb = smem_u32(Wsl);
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1);
+      mbar_wait(&acce[b], ((uint32_t)(k >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      for (int h = 0; h < 2; ++h) {
+        const int64_t q = 2 * k + h;
+        const int st = (int)(q % kSlots);
+        mbar_wait(&fx[st], (uint32_t)(q / kSlots) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t xb = smem_u32(xr + st * kHalf);
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const int ks = 8 * h + s;  // K16 step over the input features
+            mma_bf16(tmem + 128u * b,
+                     smem_desc_sw128(wb + (ks >> 2) * (kHalf / 2) + 32 * (ks & 3), 16, 1024),
+                     smem_desc_sw128(xb + (s >> 2) * (kHalf / 2) + 32 * (s & 3), 16, 1024), id,
+                     ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&ex[st]);
+          if (h == 1) mma_commit(&accf[b]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {  // -------------------------------------- epilogue
+    const int e = warp - 4, q = e & 3, half = e >> 2;
+    const int cl = 32 * q + lane;  // TMEM lane = output column c0 + cl
+    const float bias = a.bias[c0 + cl];
+    const bool issuer = e == 0 && lane == 0;
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1);
+      mbar_wait(&accf[b], (uint32_t)(k >> 1) & 1u);
+      tc_fence_after();
+      float v[64];
+      {
+        float v0[32], v1[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128u * b + 64u * half;
+        tmem_ld32(ta, v0);
+        tmem_ld32(ta + 32u, v1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { v[i] = v0[i]; v[32 + i] = v1[i]; }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      // stage the tile row-major (lanes = 32 consecutive columns: 64 B per row,
+      // conflict-free), then one TMA store (rows >= M are clipped)
+      if (issuer) bulk_wait_read();  // the previous tile's store has read the staging
+      named_sync(1, 32 * kBEpiWarps);
+      __nv_bfloat16* sg = reinterpret_cast<__nv_bfloat16*>(ostg) + (64 * half) * 128 + cl;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) sg[j * 128] = __float2bfloat16_rn(fmaxf(v[j] + bias, 0.f));
+      fence_proxy_async();
+      named_sync(1, 32 * kBEpiWarps);
+      if (issuer) {
+        tma_store_2d(&a.to, c0, (int)(t * 128), ostg);
+        bulk_commit();
+      }
+    }
+    if (issuer) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -547,6 +690,18 @@ bool map2d(CUtensorMap* m, const void* p, int64_t cols, int64_t rows, int64_t pi
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, str, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// bf16 2-D map without swizzle (row-major staging tiles for TMA stores)
+bool map2d_plain(CUtensorMap* m, const void* p, int64_t cols, int64_t rows, int64_t pitch, int bc,
+                 int br) {
+  auto enc = encoder();
+  if (!enc || (uintptr_t)p % 16 || (pitch * 2) % 16) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows}, str[1] = {(cuuint64_t)pitch * 2};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br}, es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -626,6 +781,34 @@ int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err) 
   launch_end(K_GEMM, s);
   *err = cudaGetLastError();
   return (int)groups;
+}
+
+bool launch_mlp_fwd_layer(const MlpFwdLayerDesc& d, cudaStream_t s, cudaError_t* err) {
+  if (d.W != 256 || d.M <= 0 || d.M > INT32_MAX - 128) return false;
+  static thread_local FwdLayerArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.M = d.M; a.bias = d.bias;
+  if (!map2d(&a.tx, d.x, 256, d.M, d.x_ld, 64, 128) || !map2d(&a.tw, d.w, 256, 256, 256, 64, 128) ||
+      !map2d_plain(&a.to, d.out, 256, d.M, d.out_ld, 128, 128))
+    return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (d.M + 127) / 128;
+  int64_t groups = sms / 2;
+  if (groups > tiles) groups = tiles;
+  a.groups = (int32_t)groups;
+  const int smem = 7 * (int)kHalf + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_fwd_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  launch_begin(K_GEMM, s);
+  k_mlp_fwd_layer<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
+  launch_end(K_GEMM, s);
+  *err = cudaGetLastError();
+  return true;
 }
 
 }  // namespace wipes
