@@ -8,3 +8,8 @@ timeout 600 python bench.py --config c3 --steps 5 --warmup 3 > gpurun_out/bench_
 timeout 600 python bench.py --config c5 --steps 10 --warmup 3 --no-mlp --no-fit > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo "c5 rc=$?"
 timeout 900 python bench.py --config c4 --steps 3 --warmup 3 --no-mlp --no-fit > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "c4 rc=$?"
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+# launch lists (serialised, cold cache) and one full capture of the dominant kernel
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo "ncu c2 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline --no-mlp --no-fit > /dev/null 2>&1; echo "ncu c3 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_bwd -s 6 -c 1 -o gpurun_out/render_bwd_c2 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-mlp --no-fit > /dev/null 2>&1; echo "ncu full c2 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_bwd -s 3 -c 1 -o gpurun_out/render_bwd_c3 python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline --no-mlp --no-fit > /dev/null 2>&1; echo "ncu full c3 rc=$?"
