@@ -151,12 +151,14 @@ def test_mlp_feeds_the_rasterizer():
         assert torch.isfinite(v).all()
 
 
-@pytest.mark.parametrize("fused_train", [False, True])
-def test_mlp_inference_and_fused_paths_agree(fused_train, tmp_path):
+@pytest.mark.parametrize("fused_train,N", [(False, 1000), (True, 1000), (True, 1), (True, 65)])
+def test_mlp_inference_and_fused_paths_agree(fused_train, N, tmp_path):
     """The fused on-chip forward (mlp_fused.cu; used for train=False, and for
     training with WIPES_MLP_FUSED=1) gives the same frame rows as the
     layer-by-layer schedule up to fp32 accumulation order; with training on,
-    its stored activations drive the same backward."""
+    its stored activations drive the same backward. WIPES_MLP_UNFUSED=1 also
+    turns off the fused layer kernels (k_mlp_fwd_layer, k_mlp_bwd_layer), so
+    2 and 130 rows cover their single-tile and ragged edge cases."""
     import os
     import subprocess
     import sys
@@ -165,7 +167,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, {os.getcwd()!r})
 from paper_2508_12615_b200 import gen
 from paper_2508_12615_b200.deform import Deformation
-N = 1000
+N = {N}
 d = Deformation(N)
 th = d.init_theta(2)
 p = gen.gen3d(N, seed=4)
