@@ -348,7 +348,10 @@ size_t wipes_mlp_workspace_bytes(const wipes_mlp_config* cfg, int64_t rows);
  * rows (device, caller-owned), ready for the rasterizer with view_stride = N.
  * train: 1 keeps every layer's activations in `ws` for wipes_mlp_backward;
  * 0 (inference) writes only the frame rows. When width is a multiple of 64,
- * depth <= 8 and F <= 128, all layers of a 128-row tile run fused on chip. */
+ * depth <= 8 and F <= 128, inference runs all layers of a 128-row tile fused on
+ * chip; training runs layer by layer (width 256: the 256-input hidden layers
+ * use a kernel in which CTA pairs split the output columns). Deterministic:
+ * fixed-order fp32 accumulation, no atomics. */
 wipes_status wipes_mlp_forward(const wipes_mlp_config* cfg, const float* theta, int64_t N,
                                int32_t F, const float* times, const wipes_params* canon,
                                const wipes_params* frame, int32_t sh_coeffs, int32_t train,
@@ -356,7 +359,11 @@ wipes_status wipes_mlp_forward(const wipes_mlp_config* cfg, const float* theta, 
 /* From g_frame (gradients w.r.t. the frame rows' mean, quat, scale, freq) of
  * the last wipes_mlp_forward on this workspace: g_theta [param_count] (fp32,
  * overwritten) and g_canon mean/quat/scale/freq [N] (overwritten; mean is the
- * frame sum: stop-gradient into the network). */
+ * frame sum: stop-gradient into the network). At width 256 each hidden layer
+ * after the first computes its input gradient, weight gradient and the bias
+ * gradient below it in one pass (per-CTA-pair partial sums, reduced in a fixed
+ * order); the head, layer 0 and the encoding columns of the skip layer use
+ * split-K GEMMs with fp32 atomics (run-to-run differences at rounding level). */
 wipes_status wipes_mlp_backward(const wipes_mlp_config* cfg, const float* theta, int64_t N,
                                 int32_t F, const wipes_params* canon, const wipes_grads* g_frame,
                                 float* g_theta, const wipes_grads* g_canon, void* ws,
