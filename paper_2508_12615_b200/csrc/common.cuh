@@ -229,6 +229,20 @@ struct MlpFwdLayerDesc {
 };
 // returns false when outside the envelope (W != 256 or unaligned operands)
 bool launch_mlp_fwd_layer(const MlpFwdLayerDesc& d, cudaStream_t s, cudaError_t* err);
+// Head backward into the last hidden layer (mlp_fused.cu): dz = (dout Wh) * (h > 0),
+// dout [M, 16] bf16, Wh [16, 256] bf16, h [M, 256] (pitch h_ld); per-group partial
+// column sums of dz in bpart [groups * 2, 256]. Returns the number of groups, 0 when
+// outside the envelope.
+struct MlpHeadBwdDesc {
+  int64_t M, h_ld;
+  const __nv_bfloat16* dout;
+  const __nv_bfloat16* wh;
+  const __nv_bfloat16* h;
+  __nv_bfloat16* dz;
+  float* bpart;
+  int32_t W, max_groups;
+};
+int launch_mlp_head_bwd(const MlpHeadBwdDesc& d, cudaStream_t s, cudaError_t* err);
 // returns the number of groups (partials) launched, or 0 when outside the envelope
 int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err);
 bool mlp_config_valid(const wipes_mlp_config& c);

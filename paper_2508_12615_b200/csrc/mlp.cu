@@ -506,9 +506,25 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
   launch_end(K_MLP_MISC, s);
   __nv_bfloat16* dz = (__nv_bfloat16*)(ws + L.dz[0]);
   __nv_bfloat16* dz2 = (__nv_bfloat16*)(ws + L.dz[1]);
-  e = gemm(dbf, ws + L.whbf, dz, M, L.W, kOutCols, kOutCols, L.W, L.W, WIPES_GEMM_EPI_MASK_BF16,
-           false, true, nullptr, hl, ldh, 1, s, g_theta + L.thb[last]);
-  if (e != cudaSuccess) return e;
+  int hgroups = 0;
+  if (L.W == 256 && !mlp_unfused_env()) {  // thin-K stream: mlp_fused.cu k_mlp_head_bwd
+    MlpHeadBwdDesc hd;
+    hd.M = M; hd.h_ld = ldh; hd.dout = dbf; hd.wh = (const __nv_bfloat16*)(ws + L.whbf);
+    hd.h = hl; hd.dz = dz; hd.bpart = (float*)(ws + L.bpart); hd.W = L.W;
+    hd.max_groups = kMlpBwdMaxGroups;
+    cudaError_t he = cudaSuccess;
+    hgroups = launch_mlp_head_bwd(hd, s, &he);
+    if (he != cudaSuccess) return he;
+    if (hgroups > 0) {
+      partsum2(part_job(hd.bpart, 2 * hgroups, L.W, g_theta + L.thb[last], true),
+               part_job(nullptr, 0, 0, nullptr, false), s);  // (second job empty)
+    }
+  }
+  if (hgroups == 0) {
+    e = gemm(dbf, ws + L.whbf, dz, M, L.W, kOutCols, kOutCols, L.W, L.W, WIPES_GEMM_EPI_MASK_BF16,
+             false, true, nullptr, hl, ldh, 1, s, g_theta + L.thb[last]);
+    if (e != cudaSuccess) return e;
+  }
   for (int l = last; l >= 0; --l) {
     // dz = dL/dz_l [M, W]; input of layer l:
     const void* in;

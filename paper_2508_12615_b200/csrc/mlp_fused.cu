@@ -666,6 +666,160 @@ __global__ void __launch_bounds__(kBThreads, 1) k_mlp_fwd_layer(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
 }
 
+// ---------------------------------------------------------------------------
+// Head backward into the last hidden layer (width 256): dz = (dout Wh) * (h > 0)
+// with K = 16 (13 real outputs), i.e. a 300 MB stream with a thin contraction.
+// CTA pairs split the 256 columns; per 128-row tile one tcgen05.mma computes the
+// transposed product D[c, r] = sum_k Wh[k, c] dout[r, k] (A = the Wh slice,
+// MN-major SW128; B = the dout tile, K-major without swizzle: two 8-column TMA
+// boxes = the two K core matrices), the mask tile arrives by TMA, and the
+// epilogue (lanes = columns) masks, sums columns and stages rows for one TMA
+// store, as in the layer kernels.
+struct HeadBwdArgs {  // (mask ring of 4 x 32 KB: tiles carry no MMA work to hide loads behind)
+  int64_t M;
+  float* bpart;
+  int32_t groups;
+  CUtensorMap tdo, twh, th, tdz;
+};
+
+__global__ void __launch_bounds__(kBThreads, 1) k_mlp_head_bwd(const __grid_constant__ HeadBwdArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kB = 4;                     // dout ring slots (4 KB each)
+  constexpr int kH = 4;                     // mask ring slots (32 KB each)
+  unsigned char* hr = base;                 // mask ring: kH x 32 KB (SW128 boxes [128 x 64])
+  unsigned char* ostg = base + kH * kHalf;  // staging [128 rows x 128 columns] bf16
+  unsigned char* wa = ostg + kHalf;         // Wh slice: 2 boxes [16 k x 64 c] (2 KB each)
+  unsigned char* br = wa + 4096;            // dout ring: kB x (2 boxes [128 rows x 8 k])
+  uint64_t* fb = reinterpret_cast<uint64_t*>(br + kB * 4096);
+  uint64_t* eb = fb + kB;
+  uint64_t* fh = eb + kB;
+  uint64_t* eh = fh + kH;
+  uint64_t* accf = eh + kH;
+  uint64_t* acce = accf + 2;
+  uint64_t* wbar = acce + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int member = blockIdx.x & 1, grp = blockIdx.x >> 1;
+  const int c0 = 128 * member;
+  const int64_t tiles = (a.M + 127) / 128;
+
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kB; ++i) { mbar_init(&fb[i], 1); mbar_init(&eb[i], 1); }
+    for (int i = 0; i < kH; ++i) { mbar_init(&fh[i], 1); mbar_init(&eh[i], kBEpiWarps); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], kBEpiWarps);
+    }
+    mbar_init(wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {  // ------------------------------------------- TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(wbar, 4096);
+      tma_load_2d(wa, &a.twh, c0, 0, wbar);
+      tma_load_2d(wa + 2048, &a.twh, c0 + 64, 0, wbar);
+      int64_t k = 0;
+      for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+        const int m0 = (int)(t * 128);
+        const int st = (int)(k % kB), sa = (int)(k % kH);
+        mbar_wait(&eb[st], ((uint32_t)(k / kB) & 1u) ^ 1u);
+        mbar_expect_tx(&fb[st], 4096);
+        tma_load_2d(br + st * 4096, &a.tdo, 0, m0, &fb[st]);
+        tma_load_2d(br + st * 4096 + 2048, &a.tdo, 8, m0, &fb[st]);
+        mbar_wait(&eh[sa], ((uint32_t)(k / kH) & 1u) ^ 1u);
+        mbar_expect_tx(&fh[sa], kHalf);
+        tma_load_2d(hr + sa * kHalf, &a.th, c0, m0, &fh[sa]);
+        tma_load_2d(hr + sa * kHalf + kHalf / 2, &a.th, c0 + 64, m0, &fh[sa]);
+      }
+    }
+  } else if (warp == 1) {  // -------------------------------------- MMA issuer
+    const uint32_t id = instr_desc(128, true, false);
+    mbar_wait(wbar, 0);
+    tc_fence_after();
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1), st = (int)(k % kB);
+      mbar_wait(&acce[b], ((uint32_t)(k >> 1) & 1u) ^ 1u);
+      mbar_wait(&fb[st], (uint32_t)(k / kB) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        // A: Wh^T (M = columns, two 64-wide SW128 atoms 2 KB apart, K rows 1 KB per 8);
+        // B: dout (N = rows; no swizzle: core matrices of 8 rows x 16 B, 128 B apart
+        // along N, the second K half 2 KB further)
+        mma_bf16(tmem + 128u * b, smem_desc_sw128(smem_u32(wa), 2048, 1024),
+                 smem_desc(smem_u32(br + st * 4096), 2048, 128), id, 0u);
+        mma_commit(&eb[st]);
+        mma_commit(&accf[b]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {  // -------------------------------------- epilogue
+    const int e = warp - 4, q = e & 3, half = e >> 2;
+    const int ci = 32 * q + lane;  // TMEM lane = column c0 + ci
+    const bool issuer = e == 0 && lane == 0;
+    const uint32_t mcol = (ci >> 6) * (kHalf / 2) + (((ci & 63) >> 3) << 4) + (ci & 7) * 2;
+    float cs = 0.f;
+    int64_t k = 0;
+    for (int64_t t = grp; t < tiles; t += a.groups, ++k) {
+      const int b = (int)(k & 1), sa = (int)(k % kH);
+      mbar_wait(&accf[b], (uint32_t)(k >> 1) & 1u);
+      mbar_wait(&fh[sa], (uint32_t)(k / kH) & 1u);
+      tc_fence_after();
+      float v[64];
+      {
+        float v0[32], v1[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128u * b + 64u * half;
+        tmem_ld32(ta, v0);
+        tmem_ld32(ta + 32u, v1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { v[i] = v0[i]; v[32 + i] = v1[i]; }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      if (issuer) bulk_wait_read();  // the previous tile's store has read the staging
+      named_sync(1, 32 * kBEpiWarps);
+      const unsigned char* slot = hr + sa * kHalf;
+      __nv_bfloat16* sg = reinterpret_cast<__nv_bfloat16*>(ostg) + (64 * half) * 128 + ci;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int ro = 64 * half + j;
+        const __nv_bfloat16 mv =
+            *reinterpret_cast<const __nv_bfloat16*>(slot + ro * 128 + (mcol ^ ((ro & 7) << 4)));
+        const float x = __bfloat162float(mv) > 0.f ? v[j] : 0.f;
+        cs += x;  // rows >= M: zero-filled mask and dout
+        sg[j * 128] = __float2bfloat16_rn(x);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&eh[sa]);
+      fence_proxy_async();
+      named_sync(1, 32 * kBEpiWarps);
+      if (issuer) {
+        tma_store_2d(&a.tdz, c0, (int)(t * 128), ostg);
+        bulk_commit();
+      }
+    }
+    if (issuer) bulk_wait_all();
+    a.bpart[((int64_t)grp * 2 + half) * 256 + c0 + ci] = cs;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -809,6 +963,36 @@ bool launch_mlp_fwd_layer(const MlpFwdLayerDesc& d, cudaStream_t s, cudaError_t*
   launch_end(K_GEMM, s);
   *err = cudaGetLastError();
   return true;
+}
+
+int launch_mlp_head_bwd(const MlpHeadBwdDesc& d, cudaStream_t s, cudaError_t* err) {
+  if (d.W != 256 || d.M <= 0 || d.M > INT32_MAX - 128) return 0;
+  static thread_local HeadBwdArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.M = d.M; a.bpart = d.bpart;
+  if (!map2d_plain(&a.tdo, d.dout, 16, d.M, 16, 8, 128) ||
+      !map2d(&a.twh, d.wh, 256, 16, 256, 64, 16) || !map2d(&a.th, d.h, 256, d.M, d.h_ld, 64, 128) ||
+      !map2d_plain(&a.tdz, d.dz, 256, d.M, 256, 128, 128))
+    return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (d.M + 127) / 128;
+  int64_t groups = sms / 2;
+  if (groups > d.max_groups) groups = d.max_groups;
+  if (groups > tiles) groups = tiles;
+  a.groups = (int32_t)groups;
+  const int smem = 5 * (int)kHalf + 4096 + 4 * 4096 + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_head_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  launch_begin(K_GEMM, s);
+  k_mlp_head_bwd<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
+  launch_end(K_GEMM, s);
+  *err = cudaGetLastError();
+  return (int)groups;
 }
 
 }  // namespace wipes
