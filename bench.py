@@ -58,6 +58,8 @@ def parse():
                     help="3D configs: SH colour of this degree (NEXT-3) instead of flat RGB")
     ap.add_argument("--deterministic", action="store_true",
                     help="bitwise deterministic backward (per-intersection moment slots)")
+    ap.add_argument("--tile", type=int, default=16, choices=[8, 16, 32],
+                    help="tile size in pixels (16 is the paper's and the default)")
     ap.add_argument("--proj", default="paper", choices=["paper", "exact"],
                     help="3D projection: Eq. 7 as written (default) or NEXT-1 exact z-marginal")
     return ap.parse_args()
@@ -313,7 +315,7 @@ def main():
         cams = [cams[v] for v in my_views]
     Bl = len(cams) if cams is not None else 1
     r = Rasterizer(W, H, prim="2d" if c["kind"] == "2d" else "3d", blend=blend, device=dev,
-                   proj=args.proj if c["kind"] != "2d" else "paper",
+                   tile=args.tile, proj=args.proj if c["kind"] != "2d" else "paper",
                    sh_degree=c.get("sh_degree"),
                    row_mod=world if (rows and world > 1) else 0, row_rem=rank if rows else 0,
                    deterministic=int(args.deterministic))

@@ -98,9 +98,12 @@ struct RenderArgs {
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
-template <int TS>
+#ifndef WIPES_FWD_G
+#define WIPES_FWD_G 1  // forward footprint: 8 x 8 (the backward keeps 8 x 16 for TS >= 16)
+#endif
+template <int TS, int GG = (TS >= 16 ? 2 : 1)>
 struct Geo {
-  static constexpr int G = TS >= 16 ? 2 : 1;  // 8x8 blocks per warp footprint (stacked)
+  static constexpr int G = GG;                 // 8x8 blocks per warp footprint (stacked)
   static constexpr int P = 2 * G;             // pixels per lane
   static constexpr int FX = TS / 8;           // footprints per tile row
   static constexpr int FY = TS / (8 * G);     // footprints per tile column
@@ -195,9 +198,9 @@ struct Item {
   int sub;         // footprint index within the tile
 };
 
-template <int TS>
+template <int TS, int GG = (TS >= 16 ? 2 : 1)>
 __device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chunks, Item& it) {
-  using Gm = Geo<TS>;
+  using Gm = Geo<TS, GG>;
   int item = 0;
   if (lane == 0) item = atomicAdd(&a.hdr->work[a.queue], 1);
   item = __shfl_sync(kFull, item, 0);
@@ -299,14 +302,15 @@ __device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, i
 
 template <int TS, bool ALPHA, bool STATS>
 __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs a) {
-  using Gm = Geo<TS>;
+  constexpr int GF = (TS >= 16 ? WIPES_FWD_G : 1);
+  using Gm = Geo<TS, GF>;
   constexpr int G = Gm::G, P = Gm::P;
   __shared__ WarpSmem sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   WarpSmem& ws = sm_all[wid];
   unsigned long long st_cand = 0, st_ell = 0, st_con = 0;  // STATS only
   Item it;
-  while (next_item<TS>(a, lane, 1, it)) {
+  while (next_item<TS, GF>(a, lane, 1, it)) {
     bool in[P], done[P];
     float C[P][3], T[P];
     int last[P], stop[P];
@@ -654,7 +658,7 @@ unsigned persistent_grid(void (*kernel)(RenderArgs), int64_t items) {
 
 template <int TS>
 cudaError_t launch_fwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
-  const int64_t items = ra.BT * Geo<TS>::S;
+  const int64_t items = ra.BT * Geo<TS, (TS >= 16 ? WIPES_FWD_G : 1)>::S;
   void (*k)(RenderArgs);
   if (ra.stats) {
     ra.queue = Q_STATS;
