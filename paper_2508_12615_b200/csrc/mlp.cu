@@ -118,35 +118,53 @@ struct EmbedArgs {
   __nv_bfloat16* cat;
 };
 
+// LX, LT > 0: compile-time frequency counts (the encoding stays in registers);
+// 0: the runtime values in a (local-memory buffer).
+template <int LX, int LT>
 __global__ void __launch_bounds__(128) k_mlp_embed(const __grid_constant__ EmbedArgs a) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.rows) return;
+  const int lx = LX > 0 ? LX : a.Lx, lt = LX > 0 ? LT : a.Lt;
   const int64_t m = a.row0 + r;
   const int64_t f = m / a.N, i = m - f * a.N;
   const float x[3] = {a.mean[3 * i], a.mean[3 * i + 1], a.mean[3 * i + 2]};
   const float t = a.t[f - a.f0];
   // built in registers, written as 16-byte vectors (E8 is a multiple of 8)
-  __align__(16) __nv_bfloat16 buf[kMaxE8];
+  constexpr int kE8 = LX > 0 ? (3 * (1 + 2 * LX) + (1 + 2 * LT) + 7) / 8 * 8 : kMaxE8;
+  __align__(16) __nv_bfloat16 buf[kE8];
   int c = 0;
+#pragma unroll
   for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(x[d]);
-  for (int k = 0; k < a.Lx; ++k) {
-    const float s = (float)(1 << k);
+#pragma unroll
+  for (int k = 0; k < (LX > 0 ? LX : 16); ++k) {
+    if (LX == 0 && k >= lx) break;
+    const float sc = (float)(1 << k);
     float sn[3], cs[3];
-    for (int d = 0; d < 3; ++d) sincosf(s * x[d], &sn[d], &cs[d]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sincosf(sc * x[d], &sn[d], &cs[d]);
+#pragma unroll
     for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(sn[d]);
+#pragma unroll
     for (int d = 0; d < 3; ++d) buf[c++] = __float2bfloat16_rn(cs[d]);
   }
   buf[c++] = __float2bfloat16_rn(t);
-  for (int k = 0; k < a.Lt; ++k) {
+#pragma unroll
+  for (int k = 0; k < (LX > 0 ? LT : 16); ++k) {
+    if (LX == 0 && k >= lt) break;
     float sn, cs;
     sincosf((float)(1 << k) * t, &sn, &cs);
     buf[c++] = __float2bfloat16_rn(sn);
     buf[c++] = __float2bfloat16_rn(cs);
   }
-  for (; c < a.E8; ++c) buf[c] = __float2bfloat16_rn(0.f);
+  const int e8 = LX > 0 ? kE8 : a.E8;
+#pragma unroll
+  for (int q = 0; q < kE8; ++q)
+    if (q >= c && q < e8) buf[q] = __float2bfloat16_rn(0.f);
   uint4* row = reinterpret_cast<uint4*>(a.cat + m * a.catw);
   const uint4* src = reinterpret_cast<const uint4*>(buf);
-  for (int v = 0; v < a.E8 / 8; ++v) row[v] = src[v];
+#pragma unroll
+  for (int v = 0; v < kE8 / 8; ++v)
+    if (v < e8 / 8) row[v] = src[v];
 }
 
 struct ApplyArgs {
@@ -414,7 +432,10 @@ cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, in
     ea.f0 = f0; ea.Lx = L.Lx; ea.Lt = L.Lt; ea.E8 = L.E8; ea.catw = L.catw; ea.cat = cat;
     for (int k = 0; k < nf; ++k) ea.t[k] = times[f0 + k];
     launch_begin(K_MLP_MISC, s);
-    k_mlp_embed<<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
+    if (L.Lx == 10 && L.Lt == 6)  // the D-3DGS encoding: unrolled, in registers
+      k_mlp_embed<10, 6><<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
+    else
+      k_mlp_embed<0, 0><<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
     launch_end(K_MLP_MISC, s);
   }
   // layers
