@@ -423,17 +423,38 @@ def main():
     if flat is None:
         # Pipelined through the public API: two device buffer sets, each with its
         # captured frame; step k uploads its inputs on a copy stream while step
-        # k - 1 computes, and its gradients come back on the copy stream.
-        params2 = {k: torch.empty_like(v) for k, v in params.items()}
-        dL2 = torch.empty_like(dL)
-        grads2 = {k: torch.empty_like(v) for k, v in grads.items()}
+        # k - 1 computes, and its gradients come back on the copy stream. Each
+        # set's parameter groups (and gradient groups) are views of one flat
+        # buffer, as a training loop would keep them, so a step is one upload of
+        # the parameters, one of dL/dC and one download of the gradients.
+        def flat_views(shapes, device, pin=False):
+            sizes = {k: int(np.prod(sh)) for k, sh in shapes.items()}
+            offs, o = {}, 0
+            for k, n in sizes.items():
+                offs[k] = o
+                o += (n + 3) // 4 * 4  # 16-byte aligned groups
+            buf = torch.zeros(o, dtype=torch.float32, device=device)
+            if pin:
+                buf = buf.pin_memory()
+            return buf, {k: buf[offs[k]:offs[k] + sizes[k]].view(shapes[k]) for k in shapes}
+
+        pshapes = {k: tuple(v.shape) for k, v in host_params.items()}
+        gshapes = {k: tuple(v.shape) for k, v in grads.items()}
+        host_pflat, hp = flat_views(pshapes, "cpu", pin=True)
         for kk, v in host_params.items():
-            params2[kk].copy_(v)
-        dL2.copy_(dL)
-        fg2 = FrameGraph(r, params2, cams, vs, dL2, grads2)
-        sets = [(params, dL, fg), (params2, dL2, fg2)]
-        host_g = [host_grads, {k: torch.empty(v.shape, dtype=torch.float32).pin_memory()
-                               for k, v in grads.items()}]
+            hp[kk].copy_(v)
+        sets, gflats = [], []
+        for _ in range(2):
+            pflat, pv = flat_views(pshapes, dev)
+            pflat.copy_(host_pflat)
+            dLb = torch.empty_like(dL)
+            dLb.copy_(dL)
+            gflat, gv = flat_views(gshapes, dev)
+            sets.append((pflat, dLb, FrameGraph(r, pv, cams, vs, dLb, gv)))
+            gflats.append(gflat)
+        host_g = [flat_views(gshapes, "cpu", pin=True)[0] for _ in range(2)]
+        h2d = host_pflat.numel() * 4 + host_dL.numel() * 4
+        d2h = host_g[0].numel() * 4
         s_copy, s_comp, s_back = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         up = [torch.cuda.Event() for _ in range(2)]
         comp = [torch.cuda.Event() for _ in range(2)]
@@ -445,8 +466,7 @@ def main():
                 with torch.cuda.stream(s_copy):
                     if k >= 2:
                         s_copy.wait_event(done[b])
-                    for kk, v in host_params.items():
-                        pb[kk].copy_(v, non_blocking=True)
+                    pb.copy_(host_pflat, non_blocking=True)
                     dlb.copy_(host_dL, non_blocking=True)
                     up[b].record(s_copy)
                 with torch.cuda.stream(s_comp):
@@ -456,8 +476,7 @@ def main():
                     comp[b].record(s_comp)
                 with torch.cuda.stream(s_back):  # D2H on its own stream: uploads never queue behind it
                     s_back.wait_event(comp[b])
-                    for kk, v in fgb.grads.items():
-                        host_g[b][kk].copy_(v, non_blocking=True)
+                    host_g[b].copy_(gflats[b], non_blocking=True)
                     done[b].record(s_back)
             s_copy.wait_stream(s_back)
 
