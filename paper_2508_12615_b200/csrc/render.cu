@@ -43,6 +43,12 @@ constexpr int kMom = kMoments;  // 12
 #define WIPES_MINB_BWD 6  // ... backward
 #endif
 constexpr int kWarpsPerCta = 4;
+#ifdef WIPES_BWD_COUNT
+__device__ unsigned long long g_bwd_cnt[8];
+#define BCNT(i, v) do { if (lane == 0) atomicAdd(&g_bwd_cnt[i], (unsigned long long)(v)); } while (0)
+#else
+#define BCNT(i, v) do { } while (0)
+#endif
 constexpr int kCta = 32 * kWarpsPerCta;
 enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 
@@ -577,6 +583,8 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
       const bool valid = b0 + lane >= start && b0 + lane < end;
       const int cnt = stage_chunk<G>(a, recv, b0 + lane, valid, b0 + lane - it.lstart, it, ws,
                                      lane);
+      BCNT(0, cnt);
+      BCNT(5, 1);
       for (int ii = 0; ii < cnt; ++ii) {
         const int i = ALPHA ? cnt - 1 - ii : ii;
         const int pos = ws.pos[i];  // index within the tile list
@@ -598,6 +606,14 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
           any_h |= bm[p];
         }
         if (!any_h) continue;
+#ifdef WIPES_BWD_COUNT
+        {
+          int ns = 0, nl = 0;
+#pragma unroll
+          for (int p = 0; p < P; ++p) { ns += bm[p] != 0; nl += __popc(bm[p]); }
+          BCNT(1, 1); BCNT(2, ns); BCNT(4, nl);
+        }
+#endif
         const float4 r2 = ws.rec[2][i], r3 = ws.rec[3][i];
         float m[kMom];
 #pragma unroll
@@ -610,6 +626,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
             bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], 8.f * (p >> 1) + 4.f * (p & 1), r2,
                                     r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p], m, mb, any);
         if (!__any_sync(kFull, any)) continue;
+        BCNT(3, 1);
         finish_moments(m, dx, dy[0]);
         const float red = transpose_reduce12(m, lane);
         if (EXACT) {
@@ -751,5 +768,16 @@ cudaError_t launch_render_bwd(const wipes_config& c, const Layout& L, char* ws, 
     default: return launch_bwd_ts<32>(alpha, ra, s);
   }
 }
+
+#ifdef WIPES_BWD_COUNT
+extern "C" void wipes_debug_bwd_counters(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_bwd_cnt, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_bwd_cnt, z, sizeof(z));
+  }
+}
+#endif
 
 }  // namespace wipes
