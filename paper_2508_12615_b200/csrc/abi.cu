@@ -289,7 +289,7 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
     e = cudaMemsetAsync(w + L.rgrad, 0, sizeof(float) * kMoments * L.BN, s);
     if (e == cudaSuccess && L.exact) e = cudaMemsetAsync(w + L.rbeta, 0, sizeof(float) * L.BN, s);
     if (e == cudaSuccess && L.det && L.cap)
-      e = cudaMemsetAsync(w + L.slots, 0, sizeof(float) * (size_t)L.cap * L.fps * L.slotw, s);
+      e = cudaMemsetAsync(w + L.slotmask, 0, (size_t)L.cap * L.fps, s);
     launch_end(K_MEMSET, s);
     if (e != cudaSuccess) return cuda_fail(e, "rgrad memset");
   }

@@ -436,8 +436,8 @@ cudaError_t launch_vals_copy(const Layout& L, const char* ws, int final_in_b, ui
 __global__ void __launch_bounds__(128) k_det_gather(const int32_t* count, const uint32_t* order,
                                                     const int64_t* loc, const int64_t* blk,
                                                     int64_t BN, int64_t cap, int fps, int slotw,
-                                                    const float* slots, float* mom,
-                                                    float* mom_beta) {
+                                                    const float* slots, const uint8_t* mask,
+                                                    float* mom, float* mom_beta) {
   const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j0 >= BN) return;
   const int64_t o = order ? (int64_t)order[j0] : j0;
@@ -449,6 +449,8 @@ __global__ void __launch_bounds__(128) k_det_gather(const int32_t* count, const 
   if (slotw == kMoments) {  // 48-byte slots: 3 float4 loads each (16-byte aligned)
     const float4* sl = reinterpret_cast<const float4*>(slots) + start * fps * 3;
     for (int64_t q = 0; q < (end - start) * fps; ++q, sl += 3) {
+      const int64_t si = start * fps + q;
+      if (!mask[si]) continue;  // slot not written this frame
       const float4 a = __ldg(sl), b = __ldg(sl + 1), c = __ldg(sl + 2);
       acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
       acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
@@ -457,7 +459,9 @@ __global__ void __launch_bounds__(128) k_det_gather(const int32_t* count, const 
   } else {
     for (int64_t j = start; j < end; ++j)
       for (int f = 0; f < fps; ++f) {
-        const float* sl = slots + (j * fps + f) * slotw;
+        const int64_t si = j * fps + f;
+        if (!mask[si]) continue;  // slot not written this frame
+        const float* sl = slots + si * slotw;
         for (int k = 0; k < slotw; ++k) acc[k] += sl[k];
       }
   }
@@ -476,7 +480,7 @@ cudaError_t launch_det_gather(const Layout& L, char* ws, cudaStream_t s) {
   launch_begin(K_DET_GATHER, s);
   k_det_gather<<<(unsigned)((L.BN + 127) / 128), 128, 0, s>>>(
       (const int32_t*)(ws + L.count), order, loc, blk, L.BN, L.cap, L.fps, L.slotw,
-      (const float*)(ws + L.slots), (float*)(ws + L.rgrad),
+      (const float*)(ws + L.slots), (const uint8_t*)(ws + L.slotmask), (float*)(ws + L.rgrad),
       L.exact ? (float*)(ws + L.rbeta) : nullptr);
   launch_end(K_DET_GATHER, s);
   return cudaGetLastError();

@@ -78,7 +78,7 @@ struct Layout {
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
          pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
-         order = 0, rgrad = 0, rbeta = 0, rdc = 0, prevals = 0, slots = 0, total = 0;
+         order = 0, rgrad = 0, rbeta = 0, rdc = 0, prevals = 0, slots = 0, slotmask = 0, total = 0;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -157,6 +157,9 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.slotw = kMoments + (L.exact ? 1 : 0);
   L.prevals = take(sizeof(uint32_t) * (L.det ? L.cap : 0));
   L.slots = take(sizeof(float) * (L.det ? (size_t)L.cap * L.fps * L.slotw : 0));
+  // one byte per slot: written this frame (only the mask is cleared per frame,
+  // and the gather reads only marked slots; plain byte stores, no atomics)
+  L.slotmask = take(L.det ? (size_t)L.cap * L.fps : 0);
   L.total = o;
   return L;
 }

@@ -100,6 +100,7 @@ struct RenderArgs {
   float* mom_beta;       // [B*N] exact mode: M12 = sum gw alpha G cos(theta) (dbeta = M12/2)
   const uint32_t* prevals;  // deterministic mode: sorted vals are dup indices j -> primitive
   float* slots;             // deterministic mode: [cap, fps, slotw] per-(dup, footprint) moments
+  uint8_t* slotmask;        // deterministic mode: byte (dup * fps + footprint) = slot written
   int32_t fps, slotw;
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
@@ -634,9 +635,11 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs 
           for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
         }
         if (a.slots) {  // deterministic: this warp's slot of (dup, footprint); no atomics
-          float* sl = a.slots + ((int64_t)ws.dj[i] * a.fps + it.sub) * a.slotw;
+          const int64_t si = (int64_t)ws.dj[i] * a.fps + it.sub;
+          float* sl = a.slots + si * a.slotw;
           if (writer) sl[my_m] = red;
           if (EXACT && lane == 0) sl[kMom] = mb;
+          if (lane == 0) a.slotmask[si] = 1;
         } else {
           if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
           if (EXACT && lane == 0) atomicAdd(a.mom_beta + vN + ws.pid[i], mb);
@@ -732,6 +735,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.mom_beta = L.exact ? (float*)(ws + L.rbeta) : nullptr;
   ra.prevals = L.det ? (const uint32_t*)(ws + L.prevals) : nullptr;
   ra.slots = L.det ? (float*)(ws + L.slots) : nullptr;
+  ra.slotmask = L.det ? (uint8_t*)(ws + L.slotmask) : nullptr;
   ra.fps = L.fps;
   ra.slotw = L.slotw;
   ra.stats = nullptr;
