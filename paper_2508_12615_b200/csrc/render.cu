@@ -40,7 +40,10 @@ constexpr int kMom = kMoments;  // 12
 #define WIPES_MINB_FWD 8  // __launch_bounds__ min CTAs per SM (register cap), forward
 #endif
 #ifndef WIPES_MINB_BWD
-#define WIPES_MINB_BWD 6  // ... backward
+#define WIPES_MINB_BWD 6  // ... backward, SUM (C2 best at 80 registers)
+#endif
+#ifndef WIPES_MINB_BWD_ALPHA
+#define WIPES_MINB_BWD_ALPHA 7  // ... backward, ALPHA (72 registers: C3 -6% against 6)
 #endif
 constexpr int kWarpsPerCta = 4;
 #ifdef WIPES_BWD_COUNT
@@ -532,7 +535,8 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, f
 }
 
 template <int TS, bool ALPHA, bool EXACT>
-__global__ void __launch_bounds__(kCta, WIPES_MINB_BWD) k_render_bwd(RenderArgs a) {
+__global__ void __launch_bounds__(kCta, ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MINB_BWD)
+    k_render_bwd(RenderArgs a) {
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
   __shared__ WarpSmem sm_all[kWarpsPerCta];
