@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-sets", type=int, default=2,
+                    help="device buffer sets the pipelined e2e loop rotates through")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-fit", action="store_true",
@@ -444,7 +446,8 @@ def main():
         for kk, v in host_params.items():
             hp[kk].copy_(v)
         sets, gflats = [], []
-        for _ in range(2):
+        nsets = max(2, args.e2e_sets)
+        for _ in range(nsets):
             pflat, pv = flat_views(pshapes, dev)
             pflat.copy_(host_pflat)
             dLb = torch.empty_like(dL)
@@ -452,19 +455,19 @@ def main():
             gflat, gv = flat_views(gshapes, dev)
             sets.append((pflat, dLb, FrameGraph(r, pv, cams, vs, dLb, gv)))
             gflats.append(gflat)
-        host_g = [flat_views(gshapes, "cpu", pin=True)[0] for _ in range(2)]
+        host_g = [flat_views(gshapes, "cpu", pin=True)[0] for _ in range(nsets)]
         h2d = host_pflat.numel() * 4 + host_dL.numel() * 4
         d2h = host_g[0].numel() * 4
         s_copy, s_comp, s_back = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        up = [torch.cuda.Event() for _ in range(2)]
-        comp = [torch.cuda.Event() for _ in range(2)]
-        done = [torch.cuda.Event() for _ in range(2)]
+        up = [torch.cuda.Event() for _ in range(nsets)]
+        comp = [torch.cuda.Event() for _ in range(nsets)]
+        done = [torch.cuda.Event() for _ in range(nsets)]
         def pipeline(n):
             for k in range(n):
-                b = k & 1
+                b = k % nsets
                 pb, dlb, fgb = sets[b]
                 with torch.cuda.stream(s_copy):
-                    if k >= 2:
+                    if k >= nsets:
                         s_copy.wait_event(done[b])
                     pb.copy_(host_pflat, non_blocking=True)
                     dlb.copy_(host_dL, non_blocking=True)
@@ -486,10 +489,14 @@ def main():
         torch.cuda.synchronize()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s_copy)
+        t_host = time.perf_counter()
         pipeline(n_e2e)
+        t_host = time.perf_counter() - t_host
         b_.record(s_copy)
         b_.synchronize()
         e2e_total = a.elapsed_time(b_)
+        print(f"e2e: host enqueue {1e3 * t_host / n_e2e:.3f} ms/step, device {e2e_total / n_e2e:.3f} "
+              f"ms/step over {n_e2e} steps, {nsets} buffer sets", file=sys.stderr)
         e2e_mode = ("pipelined: step k+1's inputs uploaded (H2D stream) and step k-1's "
                     "gradients downloaded (D2H stream) while step k computes")
     else:
