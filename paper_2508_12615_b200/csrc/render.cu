@@ -55,6 +55,17 @@ __device__ unsigned long long g_bwd_cnt[8];
 constexpr int kCta = 32 * kWarpsPerCta;
 enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 
+#ifndef WIPES_FWD_UNROLL
+#define WIPES_FWD_UNROLL 1  // record-loop unroll of the SUM forward (A/B knob)
+#endif
+#ifndef WIPES_FWD_UNROLL_ALPHA
+#define WIPES_FWD_UNROLL_ALPHA 2  // ALPHA forward: C3 render_fwd 2.70 -> 2.62 ms at 2
+#endif
+#ifndef WIPES_BWD_UNROLL
+#define WIPES_BWD_UNROLL 1  // record-loop unroll of the backward (A/B knob)
+#endif
+constexpr int kBwdUnroll = WIPES_BWD_UNROLL;
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -313,6 +324,7 @@ __device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, i
 template <int TS, bool ALPHA, bool STATS>
 __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs a) {
   constexpr int GF = (TS >= 16 ? WIPES_FWD_G : 1);
+  constexpr int kFwdUnroll = ALPHA ? WIPES_FWD_UNROLL_ALPHA : WIPES_FWD_UNROLL;
   using Gm = Geo<TS, GF>;
   constexpr int G = Gm::G, P = Gm::P;
   __shared__ WarpSmem sm_all[kWarpsPerCta];
@@ -347,6 +359,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
       const bool valid = b0 + lane < it.end;
       const int cnt = stage_chunk<G>(a, recv, b0 + lane, valid, b0 - it.start + lane + 1, it, ws,
                                      lane);
+#pragma unroll kFwdUnroll
       for (int i = 0; i < cnt; ++i) {
         const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
         const float dx = pair_dx(r0, px);
@@ -590,6 +603,7 @@ __global__ void __launch_bounds__(kCta, ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MIN
                                      lane);
       BCNT(0, cnt);
       BCNT(5, 1);
+#pragma unroll kBwdUnroll
       for (int ii = 0; ii < cnt; ++ii) {
         const int i = ALPHA ? cnt - 1 - ii : ii;
         const int pos = ws.pos[i];  // index within the tile list

@@ -1,0 +1,13 @@
+#!/bin/bash
+# A/B of library variants on chosen configs (experiment helper): CFGS="c3 c4" bash variants/ab_cfg.sh base v1 ...
+for v in "$@"; do
+  if [ "$v" = "base" ]; then unset WIPES_LIB; else export WIPES_LIB=$PWD/variants/$v.so; fi
+  for c in ${CFGS:-c3}; do
+    timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-fit --no-mlp 2>/dev/null | tail -1 | python -c "
+import json,sys
+try:
+  d=json.loads(sys.stdin.read()); k=d['kernel_ms_per_step']
+  print('$v $c', round(d['ms_per_step'],4), 'fwd', round(k['render_fwd'],4), 'bwd', round(k['render_bwd'],4))
+except Exception as e: print('$v $c FAILED', e)"
+  done
+done
