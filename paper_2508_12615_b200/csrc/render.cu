@@ -65,6 +65,9 @@ enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 #define WIPES_BWD_UNROLL 1  // record-loop unroll of the backward (A/B knob)
 #endif
 constexpr int kBwdUnroll = WIPES_BWD_UNROLL;
+#ifndef WIPES_BWD_CHUNKS
+#define WIPES_BWD_CHUNKS 4  // SUM backward: record chunks per (tile, footprint) work item
+#endif
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -739,7 +742,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.BT = L.BT;
   ra.W = c.width; ra.H = c.height; ra.GX = L.GX;
   ra.queue = 0;
-  ra.chunks = 4;
+  ra.chunks = WIPES_BWD_CHUNKS;
   ra.alpha_min = c.alpha_min;
   // conservative early-out on the exponent: e < log2(alpha_min) - 1e-4 implies
   // alpha*W < alpha_min after the MUFU roundings
