@@ -65,8 +65,12 @@ enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 #define WIPES_BWD_UNROLL 1  // record-loop unroll of the backward (A/B knob)
 #endif
 constexpr int kBwdUnroll = WIPES_BWD_UNROLL;
+// SUM backward: record chunks per (tile, footprint) work item. 0 = by grid size:
+// 4 on small frames (items to fill 148 SMs), 2 from 16384 tiles up (fewer partial
+// sums / atomics per primitive). A/B on B200 (variants/ab_cfg.sh, gpurun_out/ch_ab.txt):
+// C2 bwd 0.119 ms at 4 vs 0.129 at 2; C5 bwd 2.99 ms at 4 vs 2.91 at 2; 6 and 8 slower on both.
 #ifndef WIPES_BWD_CHUNKS
-#define WIPES_BWD_CHUNKS 4  // SUM backward: record chunks per (tile, footprint) work item
+#define WIPES_BWD_CHUNKS 0
 #endif
 
 __device__ __forceinline__ float ex2(float x) {
@@ -742,7 +746,7 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.BT = L.BT;
   ra.W = c.width; ra.H = c.height; ra.GX = L.GX;
   ra.queue = 0;
-  ra.chunks = WIPES_BWD_CHUNKS;
+  ra.chunks = WIPES_BWD_CHUNKS > 0 ? WIPES_BWD_CHUNKS : (L.BT >= 16384 ? 2 : 4);
   ra.alpha_min = c.alpha_min;
   // conservative early-out on the exponent: e < log2(alpha_min) - 1e-4 implies
   // alpha*W < alpha_min after the MUFU roundings
