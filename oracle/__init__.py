@@ -240,6 +240,19 @@ def render(cfg: Cfg, pr: Projected, pix=None, dLdC=None, nthreads: int = 0):
     return dict(color=color, T=T, margin=margin, ncomp=ncomp, rgrad=rgrad)
 
 
+def render_counts(cfg: Cfg, pr: Projected, thr_ell: float):
+    """Roofline work counters per pixel over its tile list (oracle.cpp
+    ora_render_counts): dict(cand, ell, con, amb) of int64 [B*H*W]."""
+    B, N = pr.B, pr.N
+    n = B * cfg.height * cfg.width
+    out = {k: np.zeros(n, np.int64) for k in ("cand", "ell", "con", "amb")}
+    rec = np.ascontiguousarray(pr.rec)
+    lib().ora_render_counts(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), _p(rec),
+                            _p(pr.flag), _p(pr.rect), _p(pr.keylo), C.c_double(thr_ell),
+                            _p(out["cand"]), _p(out["ell"]), _p(out["con"]), _p(out["amb"]))
+    return out
+
+
 def image_pixels_to_planar(color, B, H, W):
     """[B*H*W, 3] -> [B, 3, H, W]"""
     return np.ascontiguousarray(color.reshape(B, H, W, 3).transpose(0, 3, 1, 2))

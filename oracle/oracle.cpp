@@ -1045,4 +1045,68 @@ void ora_sh_chain(int32_t deg, int64_t N, int32_t B, const ora_cam* cams, const 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Roofline work counters (SURVEY §8(d) "How n_cand and n_ell are obtained"):
+// per pixel, over the pixel's TILE LIST (the live primitives whose tile rect
+// contains the pixel's tile, in the evaluation order of O4: index for SUM,
+// (depth key, index) for ALPHA), counted up to and including the entry at
+// which ALPHA compositing stops (Q10):
+//   cand[k] : list entries processed (SUM: the whole list),
+//   ell[k]  : of those, pairs passing the skip pre-test alpha*G >= thr_ell
+//             (the envelope bound of R8: alpha*W >= alpha_min implies it),
+//   con[k]  : contributing pairs (SUM: w >= alpha_min; ALPHA: composited),
+//   amb[k]  : pairs whose log2(alpha*G) lies within 1e-5 of log2(thr_ell),
+//             i.e. whose ell decision may flip under FP32 rounding.
+// Plain counting on top of the O3/O4 predicates; no tiling of the evaluation.
+// ---------------------------------------------------------------------------
+void ora_render_counts(const ora_cfg* cfg, int64_t N, int32_t B, const double* rec,
+                       const int32_t* flag, const int32_t* rect, const uint32_t* keylo,
+                       double thr_ell, int64_t* cand, int64_t* ell, int64_t* con,
+                       int64_t* amb) {
+  const ora_cfg& c = *cfg;
+  const int64_t H = c.height, W = c.width, HW = H * W;
+  std::vector<std::vector<int64_t>> order(B);
+  for (int32_t v = 0; v < B; ++v) {
+    auto& ord = order[v];
+    for (int64_t i = 0; i < N; ++i)
+      if (flag[(int64_t)v * N + i] == 0) ord.push_back(i);
+    if (c.alpha_blend)
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+        return keylo[(int64_t)v * N + a] < keylo[(int64_t)v * N + b];
+      });
+  }
+  const double lthr = std::log2(thr_ell);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t k = 0; k < (int64_t)B * HW; ++k) {
+    const int64_t v = k / HW, rem = k % HW, yi = rem / W, xi = rem % W;
+    const double px = (double)xi + 0.5, py = (double)yi + 0.5;
+    const int64_t tx = xi / c.tile, ty = yi / c.tile;
+    int64_t nc = 0, ne = 0, nn = 0, na = 0;
+    double T = 1.0;
+    for (int64_t i : order[v]) {
+      const int64_t o = v * N + i;
+      const int32_t* rc = rect + 4 * o;
+      if (!(tx >= rc[0] && tx < rc[2] && ty >= rc[1] && ty < rc[3])) continue;
+      const double* r = rec + o * ORA_P;
+      ++nc;
+      pair_eval e;
+      eval_pair(r, px, py, e);
+      const double aG = r[P_ALPHA] * e.G;
+      if (aG >= thr_ell) ++ne;
+      if (std::fabs(std::log2(aG) - lthr) < 1e-5) ++na;
+      if (!c.alpha_blend) {
+        if (e.w >= c.alpha_min) ++nn;
+      } else {
+        const double a = std::min(c.alpha_max, e.w);
+        if (!(a >= c.alpha_min)) continue;
+        const double Tn = T * (1.0 - a);
+        if (Tn < c.T_min) break;
+        T = Tn;
+        ++nn;
+      }
+    }
+    cand[k] = nc; ell[k] = ne; con[k] = nn; amb[k] = na;
+  }
+}
+
 }  // extern "C"

@@ -524,3 +524,53 @@ def test_sigma3_extent_is_tiling_dependent(ora):
     d = ora.forward(ora.Cfg(width=W, height=H, tile=32), pd)["color"]
     assert not np.array_equal(a, b)
     assert np.array_equal(c, d)
+
+
+RECTS = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rect_examples.json")))
+
+
+@pytest.mark.parametrize("ex", RECTS["cases"])
+def test_tile_rect_hand_computed(ora, ex):
+    """O1 steps 6-7 (R7; SPEC S:248 for the 3-sigma square): the
+    oracle's tile rect equals a hand-computed one (tests/golden/rect_examples.json)
+    placed so that an extent 5-10% too large or too small moves an edge —
+    the tightness pin that the soundness lemma (every contributing pair is
+    binned) cannot give."""
+    p = dict(mean=np.array([ex["mean"]], np.float64), cov=np.array([ex["cov"]], np.float64),
+             freq=np.zeros((1, 2)), color=np.ones((1, 3)) * 0.1,
+             opacity=np.array([ex["alpha"]], np.float64))
+    cfg = ora.Cfg(width=128, height=128, extent=ex["extent"])
+    pr = ora.project2d(cfg, p)
+    assert pr.flag[0] == 0
+    assert list(pr.rect[0]) == ex["rect"], (list(pr.rect[0]), ex["derivation"])
+    x0, y0, x1, y1 = ex["rect"]
+    assert pr.count[0] == (x1 - x0) * (y1 - y0)
+
+
+@pytest.mark.parametrize("blend", [False, True])
+def test_render_counts(ora, blend):
+    """The roofline work counters (ora_render_counts) against
+    independent routes: SUM candidates = sum over tiles of list length x
+    pixels of the tile (from the CSR offsets of bin_sort); contributing pairs =
+    the forward's own per-pixel composited/contributing count (ncomp);
+    cand >= ell >= con per pixel; without truncation of the list (T_min = 0)
+    the ALPHA candidates are the whole tile lists."""
+    H, W, N = 40, 56, 300
+    p = gen.gen2d(H, W, N, seed=9, freq_std=0.2, alpha=(0.8, 1.0), color_max=1.0, depth=True,
+                  s0=4.0)
+    pd = {k: v.astype(np.float64) for k, v in p.items()}
+    GX, GY = -(-W // 16), -(-H // 16)
+    for tmin in (float(np.float32(1e-4)), 0.0):
+        cfg = ora.Cfg(width=W, height=H, alpha_blend=blend, use_rect=True, T_min=tmin)
+        pr = ora.project2d(cfg, pd)
+        oc = ora.render_counts(cfg, pr, cfg.alpha_min * 2.0 ** -1e-4)
+        ro = ora.render(cfg, pr)
+        assert np.array_equal(oc["con"], ro["ncomp"].astype(np.int64))
+        assert np.all(oc["cand"] >= oc["ell"]) and np.all(oc["ell"] >= oc["con"])
+        toff = ora.bin_sort(cfg, pr)["tile_offsets"]
+        ys, xs = np.divmod(np.arange(H * W), W)
+        listlen = (toff[1:] - toff[:-1])[(ys // 16) * GX + xs // 16]
+        if not blend or tmin == 0.0:
+            assert np.array_equal(oc["cand"], listlen)
+        else:
+            assert np.all(oc["cand"] <= listlen) and np.any(oc["cand"] < listlen)
