@@ -10,11 +10,14 @@ render forward -> render backward -> preprocess backward (all SURVEY §8(a)
 rows), every kernel ours (libwipes.so through the C ABI).
 
 Default workload: configs[1] (C2) — Kodak-shaped 768x512 image, 70k 2D wavelet
-primitives, weighted sum (Eq. 4). Under torchrun each rank fits
-its own Kodak-shaped image (independent problems: weak scaling, no data-path
-collective). `--config c3` runs the 3D static NVS batch (8 x 1080p views,
-1M primitives, alpha blending) with views sharded across ranks and the
-per-primitive gradients summed by an NCCL all_reduce (strong scaling).
+primitives, weighted sum (Eq. 4). Under torchrun the same image
+is split by tile rows (row r -> rank r mod N) and the
+per-primitive gradients are summed by one NCCL all_reduce (strong scaling;
+`--replicas` gives every rank its own image instead). The default line also
+carries `nvs_c3`: the 3D static NVS batch (C3: 8 x 1080p views, 1M primitives,
+alpha blending) with views sharded across the ranks and the gradients
+all_reduced — the "1080p 3D" half of BASELINE's metric. `--config c3|c4|c5`
+makes any of them the main line.
 """
 from __future__ import annotations
 
@@ -46,6 +49,12 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="C2 at N > 1: independent images per rank (weak) instead of one image "
+                         "sharded by tile rows + gradient all_reduce (default, strong)")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the C3 (8 x 1080p 3D, view-sharded) sub-record of the default run")
+    ap.add_argument("--c3-steps", type=int, default=5)
     ap.add_argument("--e2e-sets", type=int, default=2,
                     help="device buffer sets the pipelined e2e loop rotates through")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
@@ -72,6 +81,75 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     return rank, world, local
+
+
+def load_alu_peaks(clk_hz):
+    """Render roofline denominators: FP32 and MUFU lane-op rates MEASURED on a
+    B200 by tools/peaks.cu (profiles/peaks.json), per SM per clock, times 148
+    SMs times the SM clock. Falls back to the unit counts (128 FP32 / 16 MUFU
+    lanes per SM per clock) only if the file is missing."""
+    p = os.path.join(ROOT, "profiles", "peaks.json")
+    sms = 148
+    if os.path.exists(p):
+        d = json.load(open(p))
+        u = d["roofline_use"]
+        return (sms * u["fp32_lane_ops_per_sm_clk"] * clk_hz, sms * u["mufu_ops_per_sm_clk"] * clk_hz,
+                "measured (profiles/peaks.json: FFMA2 %.1f, MUFU.EX2 %.1f lane-ops/SM/clk)"
+                % (u["fp32_lane_ops_per_sm_clk"], u["mufu_ops_per_sm_clk"]))
+    return sms * 128 * clk_hz, sms * 16 * clk_hz, "unit counts (profiles/peaks.json missing)"
+
+
+def hbm_fractions(kt, steps, L, hbm_gbs):
+    """SURVEY §8(d) gate G2: achieved algorithmic bytes / CUDA-event time of the
+    HBM-bound kernels against the measured copy bandwidth. Algorithmic bytes
+    per launch: L = dict(BN, N, dup, BT, passes, param_bytes,
+    grad_bytes)."""
+    BN, dup = L["BN"], L["dup"]
+    per = {
+        # params read once per (view, primitive) set + rect 16, count 4, flag 1, depth 4, record 64
+        "preprocess2d": L["param_bytes"] + 89 * BN,
+        "preprocess3d": L["param_bytes"] + 89 * BN,
+        # rect 16 + offset 8 + depth key 4 read per (view, primitive); key 8 + value 4 per dup
+        "duplicate": 28 * BN + 12 * dup,
+        # every digit histogram from one read of the keys (8 B / dup)
+        "radix_hist": 8 * dup,
+        # one onesweep pass: key + value read and written (24 B / dup)
+        "radix_scatter": 24 * dup,
+        # sorted keys read, CSR offsets written
+        "tile_ranges": 8 * dup + 4 * (L["BT"] + 1),
+        # moments (48 B / (view, primitive)) + params read, gradients written
+        "preprocess2d_bwd": 48 * BN + L["param_bytes"] + L["grad_bytes"],
+        "preprocess3d_bwd": 48 * BN + L["param_bytes"] + L["grad_bytes"],
+    }
+    out = {}
+    for k, b in per.items():
+        if k not in kt or not kt[k][1]:
+            continue
+        ms, n = kt[k]
+        t = ms / 1e3 / n
+        gbs = b / t / 1e9
+        out[k] = {"bytes_per_launch": int(b), "us_per_launch": t * 1e6, "GB/s": gbs,
+                  "frac": gbs / hbm_gbs}
+    return out
+
+
+def gpu_local_cpus(dev_index):
+    """Host cores on the GPU's NUMA node (sysfs local_cpulist of its PCI
+    function): the e2e leg pins its thread there before allocating pinned
+    buffers, so H2D/D2H copies use node-local host memory."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(dev_index)
+        bus = "%04x:%02x:%02x.0" % (getattr(pr, "pci_domain_id", 0), pr.pci_bus_id,
+                                    pr.pci_device_id)
+        txt = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        return bus, sorted(cpus & os.sched_getaffinity(0))
+    except Exception:
+        return None, []
 
 
 def load_peaks():
@@ -220,6 +298,99 @@ def mlp_rate(args, flush, dev, peaks):
                                       "once (forward), dW and dIn operands (backward)"}}
 
 
+def sharding(name, world, args):
+    """(rows, frames, shared) of a config at this world size."""
+    from paper_2508_12615_b200 import gen
+    base = gen.CONFIGS[name]
+    # one image, tile rows sharded: C5 always; C2 (the default) at N > 1 unless
+    # --replicas, so that N = 1 is BENCH's workload and N > 1 splits the same image
+    rows = base.get("shard") == "rows" or (name == "c2" and world > 1 and not args.replicas)
+    frames = base["kind"] == "6d"                 # per-frame parameter rows (view_stride = N)
+    shared = base["kind"] == "3d" or rows or frames  # one problem shared by all ranks
+    return rows, frames, shared
+
+
+def workload_config(name, c, world, args):
+    """The `config` dict of the JSON line — identical in both arms (ours and
+    --impl reference) for the same command line."""
+    rows, frames, shared = sharding(name, world, args)
+    return {"workload": f"{name}: {c['desc']}"
+                        + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else "")
+                        + (f" (SH degree {c['sh_degree']} colour)" if c.get("sh_degree") is not None else "")
+                        + (" (deterministic backward)" if args.deterministic else ""),
+            "H": c["H"], "W": c["W"], "N": c["N"], "views": c.get("B", 1), "blend": c["blend"],
+            "l2": "flushed between timed steps (256 MiB write, untimed)",
+            "parallelism": (f"tile rows r = rank (mod {world}) of one image per GPU + "
+                            "NCCL all_reduce of per-primitive gradients") if rows else
+                           (f"frames round-robin over {world} GPU(s), per-frame "
+                            "parameters disjoint: no exchange") if frames else
+                           (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
+                            "per-primitive gradients") if shared else
+                           f"replicas: {world} independent image(s), one per GPU"}
+
+
+def nvs_subrecord(args, rank, world, dev, flush):
+    """The "1080p 3D" half of BASELINE's metric, reported beside the default C2
+    line: C3 (8 x 1920x1080 views, 1M 3D primitives, alpha blending, SURVEY
+    §8(d)) with the views sharded round-robin over the ranks and the
+    per-primitive gradients summed by one NCCL all_reduce; each
+    step = every rank's frame (CUDA-graph replay) + the all_reduce, CUDA-event
+    timed, max over ranks, L2 flushed between steps."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_12615_b200 import gen
+    from paper_2508_12615_b200 import dist as wdist
+    from paper_2508_12615_b200.raster import FrameGraph, Rasterizer
+    c = gen.make_config("c3", seed=args.seed)
+    views = wdist.shard_views(c["B"], rank, world)
+    cams = [c["cams"][v] for v in views]
+    r = Rasterizer(c["W"], c["H"], prim="3d", blend="alpha", device=dev)
+    params = {k: torch.from_numpy(v).to(dev) for k, v in c["params"].items()}
+    dL = torch.from_numpy(gen.gen_dLdC(len(cams), c["H"], c["W"], seed=args.seed + rank)).to(dev)
+    grads = {k: torch.empty_like(v) for k, v in params.items()}
+    bucket = wdist.GradBucket(grads) if world > 1 else None
+    fg = FrameGraph(r, params, cams, 0, dL, grads)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        flush.zero_()
+        fg.step()
+        if bucket is not None:
+            bucket.all_reduce()
+    torch.cuda.synchronize()
+    tot = red = 0.0
+    for _ in range(args.c3_steps):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        if world > 1:
+            dist.barrier()
+        e[0].record(stream)
+        fg.step()
+        e[1].record(stream)
+        if bucket is not None:
+            bucket.all_reduce()
+        e[2].record(stream)
+        e[2].synchronize()
+        tot += e[0].elapsed_time(e[2])
+        red += e[1].elapsed_time(e[2])
+    t = torch.tensor([tot, red], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n, over = r.check_overflow()
+    assert not over
+    ms = float(t[0]) / args.c3_steps
+    out = {"workload": f"c3: {c['desc']}", "value": 1e3 / ms, "unit": "iters/s",
+           "render_fps": c["B"] * 1e3 / ms, "ms_per_step": ms,
+           "allreduce_ms": float(t[1]) / args.c3_steps, "steps": args.c3_steps,
+           "views_per_rank": len(views), "dup": int(n),
+           "grad_bytes": sum(v.numel() * 4 for v in grads.values()),
+           "parallelism": f"views round-robin over {world} GPU(s) + NCCL all_reduce of the "
+                          "per-primitive gradients (one flat bucket)",
+           "scaling": "strong"}
+    del fg, r, params, grads, bucket
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_oracle_sample(c, npix, seed):
     """The oracle as it stands (double-precision brute force over ALL primitives
     per pixel, no tiling) on a bounded random pixel sample of the workload;
@@ -262,8 +433,9 @@ def run_reference(args, rank, world):
               f"fwd+bwd against all {c['N']} primitives, extrapolated linearly to the full frame")
     line = {"impl": "reference", "metric": "fwd+bwd iters/s", "value": value, "unit": "iters/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{args.config}: {c['desc']}"},
+            "higher_is_better": True,
+            "scaling": "strong" if sharding(args.config, world, args)[2] else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args.config, c, world, args),
             "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0,
@@ -298,11 +470,9 @@ def main():
     peaks, peak_src = load_peaks()
 
     name = args.config
-    base = gen.CONFIGS[name]
-    rows = base.get("shard") == "rows"           # one image, tile rows sharded
-    frames = base["kind"] == "6d"                 # per-frame parameter rows (view_stride = N)
-    shared = base["kind"] == "3d" or rows or frames  # one problem shared by all ranks
-    # 2D (C2): every rank its own independent image (weak scaling);
+    rows, frames, shared = sharding(name, world, args)
+    # 2D (C2): one image, tile rows sharded + gradient all_reduce at N > 1
+    # (--replicas: every rank its own independent image, weak scaling);
     # 3D batch (C3): one scene, views sharded across ranks + gradient all_reduce;
     # 6D (C4): frames sharded round-robin, per-frame parameters are disjoint so
     # there is no exchange; C5: tile rows sharded + all_reduce.
@@ -416,106 +586,101 @@ def main():
         render_fps = args.steps / (total_fwd_ms / 1e3)
 
     # ---- e2e: same metric through the public API with HOST buffers --------
+    bus, local_cpus = gpu_local_cpus(local)
+    saved_aff = os.sched_getaffinity(0)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     host_params = {k: torch.from_numpy(v).pin_memory() for k, v in c["params"].items()}
     host_dL = torch.from_numpy(dL_host).pin_memory()
     host_grads = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in grads.items()}
     h2d = sum(v.numel() * 4 for v in host_params.values()) + host_dL.numel() * 4
     d2h = sum(v.numel() * 4 for v in host_grads.values())
-    n_e2e = max(20, args.steps)  # at least 20 pipelined steps: host enqueue jitter averages out
-    if flat is None:
-        # Pipelined through the public API: two device buffer sets, each with its
-        # captured frame; step k uploads its inputs on a copy stream while step
-        # k - 1 computes, and its gradients come back on the copy stream. Each
-        # set's parameter groups (and gradient groups) are views of one flat
-        # buffer, as a training loop would keep them, so a step is one upload of
-        # the parameters, one of dL/dC and one download of the gradients.
-        def flat_views(shapes, device, pin=False):
-            sizes = {k: int(np.prod(sh)) for k, sh in shapes.items()}
-            offs, o = {}, 0
-            for k, n in sizes.items():
-                offs[k] = o
-                o += (n + 3) // 4 * 4  # 16-byte aligned groups
-            buf = torch.zeros(o, dtype=torch.float32, device=device)
-            if pin:
-                buf = buf.pin_memory()
-            return buf, {k: buf[offs[k]:offs[k] + sizes[k]].view(shapes[k]) for k in shapes}
+    n_e2e = max(50, args.steps)  # at least 50 pipelined steps: host enqueue jitter averages out
+    exchange = flat is not None  # multi-rank step with a gradient sum
+    # Pipelined through the public API: two device buffer sets, each with its
+    # captured frame; step k uploads its inputs on a copy stream while step
+    # k - 1 computes, and its gradients come back on the copy stream. Each
+    # set's parameter groups (and gradient groups) are views of one flat
+    # buffer, as a training loop would keep them, so a step is one upload of
+    # the parameters, one of dL/dC and one download of the gradients.
+    def flat_views(shapes, device, pin=False):
+        sizes = {k: int(np.prod(sh)) for k, sh in shapes.items()}
+        offs, o = {}, 0
+        for k, n in sizes.items():
+            offs[k] = o
+            o += (n + 3) // 4 * 4  # 16-byte aligned groups
+        buf = torch.zeros(o, dtype=torch.float32, device=device)
+        if pin:
+            buf = buf.pin_memory()
+        return buf, {k: buf[offs[k]:offs[k] + sizes[k]].view(shapes[k]) for k in shapes}
 
-        pshapes = {k: tuple(v.shape) for k, v in host_params.items()}
-        gshapes = {k: tuple(v.shape) for k, v in grads.items()}
-        host_pflat, hp = flat_views(pshapes, "cpu", pin=True)
-        for kk, v in host_params.items():
-            hp[kk].copy_(v)
-        sets, gflats = [], []
-        nsets = max(2, args.e2e_sets)
-        for _ in range(nsets):
-            pflat, pv = flat_views(pshapes, dev)
-            pflat.copy_(host_pflat)
-            dLb = torch.empty_like(dL)
-            dLb.copy_(dL)
-            gflat, gv = flat_views(gshapes, dev)
-            sets.append((pflat, dLb, FrameGraph(r, pv, cams, vs, dLb, gv)))
-            gflats.append(gflat)
-        host_g = [flat_views(gshapes, "cpu", pin=True)[0] for _ in range(nsets)]
-        h2d = host_pflat.numel() * 4 + host_dL.numel() * 4
-        d2h = host_g[0].numel() * 4
-        s_copy, s_comp, s_back = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        up = [torch.cuda.Event() for _ in range(nsets)]
-        comp = [torch.cuda.Event() for _ in range(nsets)]
-        done = [torch.cuda.Event() for _ in range(nsets)]
-        def pipeline(n):
-            for k in range(n):
-                b = k % nsets
-                pb, dlb, fgb = sets[b]
-                with torch.cuda.stream(s_copy):
-                    if k >= nsets:
-                        s_copy.wait_event(done[b])
-                    pb.copy_(host_pflat, non_blocking=True)
-                    dlb.copy_(host_dL, non_blocking=True)
-                    up[b].record(s_copy)
-                with torch.cuda.stream(s_comp):
-                    s_comp.wait_event(up[b])
-                    fgb.forward()
-                    fgb.backward()
-                    comp[b].record(s_comp)
-                with torch.cuda.stream(s_back):  # D2H on its own stream: uploads never queue behind it
-                    s_back.wait_event(comp[b])
-                    host_g[b].copy_(gflats[b], non_blocking=True)
-                    done[b].record(s_back)
-            s_copy.wait_stream(s_back)
+    pshapes = {k: tuple(v.shape) for k, v in host_params.items()}
+    gshapes = {k: tuple(v.shape) for k, v in grads.items()}
+    host_pflat, hp = flat_views(pshapes, "cpu", pin=True)
+    for kk, v in host_params.items():
+        hp[kk].copy_(v)
+    sets, gflats = [], []
+    nsets = max(2, args.e2e_sets)
+    for _ in range(nsets):
+        pflat, pv = flat_views(pshapes, dev)
+        pflat.copy_(host_pflat)
+        dLb = torch.empty_like(dL)
+        dLb.copy_(dL)
+        gflat, gv = flat_views(gshapes, dev)
+        sets.append((pflat, dLb, FrameGraph(r, pv, cams, vs, dLb, gv)))
+        gflats.append(gflat)
+    host_g = [flat_views(gshapes, "cpu", pin=True)[0] for _ in range(nsets)]
+    h2d = host_pflat.numel() * 4 + host_dL.numel() * 4
+    d2h = host_g[0].numel() * 4
+    s_copy, s_comp, s_back = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    s_comm = torch.cuda.Stream() if exchange else s_comp
+    up = [torch.cuda.Event() for _ in range(nsets)]
+    comp = [torch.cuda.Event() for _ in range(nsets)]
+    done = [torch.cuda.Event() for _ in range(nsets)]
+    def pipeline(n):
+        for k in range(n):
+            b = k % nsets
+            pb, dlb, fgb = sets[b]
+            with torch.cuda.stream(s_copy):
+                if k >= nsets:
+                    s_copy.wait_event(done[b])
+                pb.copy_(host_pflat, non_blocking=True)
+                dlb.copy_(host_dL, non_blocking=True)
+                up[b].record(s_copy)
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(up[b])
+                fgb.forward()
+                fgb.backward()
+                comp[b].record(s_comp)
+            if exchange:  # the gradient sum across ranks on its own stream: it overlaps
+                with torch.cuda.stream(s_comm):  # the next step's frame (other buffer set)
+                    s_comm.wait_event(comp[b])
+                    wdist.reduce_flat(gflats[b], deterministic=args.deterministic)
+                    comp[b].record(s_comm)
+            with torch.cuda.stream(s_back):  # D2H on its own stream: uploads never queue behind it
+                s_back.wait_event(comp[b])
+                host_g[b].copy_(gflats[b], non_blocking=True)
+                done[b].record(s_back)
+        s_copy.wait_stream(s_back)
 
-        pipeline(max(3, args.warmup))  # untimed: first-touch costs of the copy path
-        torch.cuda.synchronize()
-        flush.zero_()
-        torch.cuda.synchronize()
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s_copy)
-        t_host = time.perf_counter()
-        pipeline(n_e2e)
-        t_host = time.perf_counter() - t_host
-        b_.record(s_copy)
-        b_.synchronize()
-        e2e_total = a.elapsed_time(b_)
-        print(f"e2e: host enqueue {1e3 * t_host / n_e2e:.3f} ms/step, device {e2e_total / n_e2e:.3f} "
-              f"ms/step over {n_e2e} steps, {nsets} buffer sets", file=sys.stderr)
-        e2e_mode = ("pipelined: step k+1's inputs uploaded (H2D stream) and step k-1's "
-                    "gradients downloaded (D2H stream) while step k computes")
-    else:
-        e2e_total = 0.0
-        for k in range(n_e2e + 2):
-            flush.zero_()
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for kk, v in host_params.items():
-                params[kk].copy_(v, non_blocking=True)
-            dL.copy_(host_dL, non_blocking=True)
-            step()
-            for kk, v in fg.grads.items():
-                host_grads[kk].copy_(v, non_blocking=True)
-            b_.record(stream)
-            b_.synchronize()
-            if k >= 2:
-                e2e_total += a.elapsed_time(b_)
-        e2e_mode = "sequential per step (the gradient all_reduce joins every step)"
+    pipeline(max(3, args.warmup))  # untimed: first-touch costs of the copy path
+    torch.cuda.synchronize()
+    flush.zero_()
+    torch.cuda.synchronize()
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s_copy)
+    t_host = time.perf_counter()
+    pipeline(n_e2e)
+    t_host = time.perf_counter() - t_host
+    b_.record(s_copy)
+    b_.synchronize()
+    e2e_total = a.elapsed_time(b_)
+    print(f"e2e: host enqueue {1e3 * t_host / n_e2e:.3f} ms/step, device {e2e_total / n_e2e:.3f} "
+          f"ms/step over {n_e2e} steps, {nsets} buffer sets", file=sys.stderr)
+    e2e_mode = ("pipelined: step k+1's inputs uploaded (H2D stream) and step k-1's "
+                "gradients downloaded (D2H stream) while step k computes"
+                + (" (its gradient all_reduce on the compute stream)" if exchange else ""))
+    os.sched_setaffinity(0, saved_aff)
     te = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -524,7 +689,7 @@ def main():
     # ---- roofline of the dominant render kernel -----------------------------
     n_cand, n_ell, n_con = r.render_stats()
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    p32, psfu = 148 * 128 * clk, 148 * 16 * clk
+    p32, psfu, alu_src = load_alu_peaks(clk)
     fwd_t = kt["render_fwd"][0] / max(kt["render_fwd"][1], 1) / 1e3
     bwd_t = kt["render_bwd"][0] / max(kt["render_bwd"][1], 1) / 1e3
     dom = "render_bwd" if kt["render_bwd"][0] >= kt["render_fwd"][0] else "render_fwd"
@@ -544,7 +709,7 @@ def main():
     roof = {"bound": "alu", "kernel": dom, "pipe": pipe,
             "achieved": (work32 if pipe == "fp32" else worksfu) / tdom / 1e9,
             "peak": (p32 if pipe == "fp32" else psfu) / 1e9,
-            "unit": f"G{pipe} instr/s (tile-method algorithmic work, {peak_src} clock "
+            "unit": f"G{pipe} instr/s (tile-method algorithmic work; peak {alu_src} x 148 SMs x "
                     f"{clk / 1e6:.0f} MHz)",
             "frac": max(f32frac, sfufrac), "frac_fp32": f32frac, "frac_mufu": sfufrac,
             "frac_useful_fp32": useful32 / tdom / p32 if tdom else 0,
@@ -555,31 +720,29 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if shared else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{name}: {c['desc']}"
-                       + (" (exact z-integration)" if args.proj == "exact" and c["kind"] != "2d" else "")
-                       + (f" (SH degree {c['sh_degree']} colour)" if c.get("sh_degree") is not None else "")
-                       + (" (deterministic backward)" if args.deterministic else ""),
-                       "H": H, "W": W, "N": N, "views": B,
-                       "blend": blend, "dup": int(n_tot2),
-                       "l2": "flushed between timed steps (256 MiB write, untimed)",
-                       "parallelism": (f"tile rows r = rank (mod {world}) of one image per GPU + "
-                                       "NCCL all_reduce of per-primitive gradients") if rows else
-                                      (f"frames round-robin over {world} GPU(s), per-frame "
-                                       "parameters disjoint: no exchange") if frames else
-                                      (f"views sharded over {world} GPU(s) + NCCL all_reduce of "
-                                       "per-primitive gradients") if shared else
-                                      f"replicas: {world} independent image(s), one per GPU"},
+            "config": workload_config(name, c, world, args),
+            "dup": int(n_tot2),
             "render_fps": render_fps,
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "mode": e2e_mode},
+                    "d2h_bytes_per_step": d2h, "mode": e2e_mode,
+                    "host_cpus": f"{len(local_cpus)} cores local to GPU {bus}" if local_cpus
+                                 else "no NUMA pinning (sysfs unavailable)"},
             "gpu_launches": int(launches), "cuda_graph": True,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
             "roofline": roof,
+            "hbm_kernels": hbm_fractions(
+                kt, args.steps,
+                dict(BN=Bl * N, dup=int(n_tot2), BT=Bl * (-(-W // args.tile)) * (-(-H // args.tile)),
+                     param_bytes=sum(v.numel() * 4 for v in params.values()),
+                     grad_bytes=sum(v.numel() * 4 for v in grads.values())),
+                float(peaks.get("hbm_gbs", 6450.9))),
             "paper_context": "render FPS on one A6000: Kodak 1708-1779 (Table 1, PAPER.md:148-149); "
                              "Mip-NeRF360 95.7 (Table 2, PAPER.md:239)"}
     if c["kind"] == "2d" and not rows and not args.no_fit:
         line["fit"] = fit_rate(H, W, N, args, flush, dev)
+    if name == "c2" and not args.no_c3:
+        line["nvs_c3"] = nvs_subrecord(args, rank, world, dev, flush)
     if not args.no_mlp and (c["kind"] == "6d" or name == "c2"):
         line["mlp"] = mlp_rate(args, flush, dev, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

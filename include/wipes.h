@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define WIPES_ABI_VERSION 2
+#define WIPES_ABI_VERSION 3
 #define WIPES_MAX_CAMERAS_PER_LAUNCH 128 /* more views are processed in chunks */
 #define WIPES_GRAD_MOMENTS 12            /* see wipes_get_grad_moments */
 
@@ -65,6 +65,13 @@ enum { WIPES_COV2_SIGMA = 0, WIPES_COV2_CHOLESKY = 1, WIPES_COV2_RS = 2 };
  * in both modes; EXACT adds 4 bytes per (view, primitive) to the workspace. */
 enum { WIPES_PROJ_PAPER = 0, WIPES_PROJ_EXACT = 1 };
 enum { WIPES_COLOR_RGB = 0, WIPES_COLOR_SH = 1 };
+/* Render-backward moment accumulation (R37): the per-record gradient
+ * moments (sums over a record's pixels of dL/dw-weighted powers of the pixel
+ * offset) are summed per lane and reduced per warp in FP32 (AUTO, F32) or with
+ * FP64 lane sums, products and warp reduction (F64: removes the accumulation
+ * share of the rounding error at ~1.35x the C3 render-backward time; the
+ * per-pair FP32/SFU evaluation error, R23b, remains either way). */
+enum { WIPES_ACCUM_AUTO = 0, WIPES_ACCUM_F32 = 1, WIPES_ACCUM_F64 = 2 };
 /* tile extent: opacity-aware AABB (R7, default) / SPEC's 3-sigma square */
 enum { WIPES_EXTENT_OPACITY = 0, WIPES_EXTENT_SIGMA3 = 1 };
 
@@ -115,6 +122,7 @@ typedef struct {
    * R33 for the basis and its sign convention). */
   int32_t color_mode;     /* WIPES_COLOR_*                                     */
   int32_t sh_degree;      /* 0..3 (WIPES_COLOR_SH)                             */
+  int32_t grad_accum;     /* WIPES_ACCUM_* (ABI v3)                            */
 } wipes_config;
 
 /* Primitive parameters (device). Shapes, with N primitives:

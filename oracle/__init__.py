@@ -215,10 +215,13 @@ def bin_sort(cfg: Cfg, pr: Projected):
                 total=total)
 
 
-def render(cfg: Cfg, pr: Projected, pix=None, dLdC=None, nthreads: int = 0):
+def render(cfg: Cfg, pr: Projected, pix=None, dLdC=None, nthreads: int = 0,
+           abs_terms: bool = False):
     """O3-O5 — brute-force render of the listed pixels (flat ids v*H*W+y*W+x;
     None = all pixels of all views). Returns dict(color [npix,3], T, margin,
-    ncomp, rgrad [B*N, 13] if dLdC given (dLdC is [npix, 3]))."""
+    ncomp, rgrad [B*N, 13] if dLdC given (dLdC is [npix, 3])); with abs_terms
+    also rgrad_abs [B*N, 13], the sum over pairs of the absolute values of every
+    term of each record gradient (the running error bound scale, R23b)."""
     B, N = pr.B, pr.N
     if pix is not None:
         pix = np.ascontiguousarray(np.asarray(pix, np.int64))
@@ -229,15 +232,18 @@ def render(cfg: Cfg, pr: Projected, pix=None, dLdC=None, nthreads: int = 0):
     T = np.zeros(npix, np.float64)
     margin = np.zeros(npix, np.float64)
     ncomp = np.zeros(npix, np.int32)
-    rgrad = None
+    rgrad = rgrad_abs = None
     if dLdC is not None:
         dLdC = _d(dLdC).reshape(npix, 3)
         rgrad = np.zeros((B * N, NG_), np.float64)
+        if abs_terms:
+            rgrad_abs = np.zeros((B * N, NG_), np.float64)
     rec = np.ascontiguousarray(pr.rec)
     lib().ora_render(C.byref(cfg.c()), C.c_int64(N), C.c_int32(B), _p(rec), _p(pr.flag),
                      _p(pr.rect), _p(pr.keylo), C.c_int64(npix), _p(pix), _p(color), _p(T),
-                     _p(margin), _p(ncomp), _p(dLdC), _p(rgrad), C.c_int32(nthreads))
-    return dict(color=color, T=T, margin=margin, ncomp=ncomp, rgrad=rgrad)
+                     _p(margin), _p(ncomp), _p(dLdC), _p(rgrad), C.c_int32(nthreads),
+                     _p(rgrad_abs))
+    return dict(color=color, T=T, margin=margin, ncomp=ncomp, rgrad=rgrad, rgrad_abs=rgrad_abs)
 
 
 def render_counts(cfg: Cfg, pr: Projected, thr_ell: float):
@@ -298,6 +304,36 @@ def chain3d(cfg: Cfg, p: dict, cams, pr: Projected, rgrad, view_stride: int = 0)
         lib().ora_sh_chain(C.c_int32(cfg.sh_degree), C.c_int64(N), C.c_int32(B), cams_c(cams),
                            _p(_d(p["mean"])), _p(_d(p["sh"])), C.c_int64(view_stride),
                            _p(pr.flag), _p(_d(rgrad)), _p(out["sh"]), _p(out["mean"]))
+    return out
+
+
+def grad_bound(cfg: Cfg, p: dict, pr: Projected, rgrad_abs, cams=None, view_stride: int = 0):
+    """Per parameter-gradient element, sum_{v,q} |J_vq| S_vq: the record-
+    gradient abs-term scales S = rgrad_abs (render(..., abs_terms=True)) carried
+    through the chain rule with every (view, record component) taken apart and
+    in absolute value. The chain is linear in the record gradients, so one call
+    per (view, component) with that component alone gives its exact signed
+    contribution. Returns a dict shaped like chain2d / chain3d."""
+    B, N = pr.B, pr.N
+    sep_views = cfg.prim3d and view_stride == 0 and B > 1  # rows sum over views
+    out = None
+    for v in (range(B) if sep_views else [None]):
+        for q in range(NG_):
+            r = np.zeros_like(rgrad_abs)
+            sl = slice(None) if v is None else slice(v * N, (v + 1) * N)
+            r[sl, q] = rgrad_abs[sl, q]
+            if not np.any(r[:, q]):
+                continue
+            g = chain3d(cfg, p, cams, pr, r, view_stride) if cfg.prim3d else chain2d(cfg, p, pr, r)
+            if out is None:
+                out = {k: np.abs(x) for k, x in g.items()}
+            else:
+                for k in out:
+                    out[k] += np.abs(g[k])
+    if out is None:
+        g = chain3d(cfg, p, cams, pr, rgrad_abs * 0, view_stride) if cfg.prim3d else \
+            chain2d(cfg, p, pr, rgrad_abs * 0)
+        out = {k: np.abs(x) for k, x in g.items()}
     return out
 
 

@@ -490,6 +490,27 @@ static inline void acc_w_grad(const double* r, const pair_eval& e, double gw, do
   g[G_ALPHA] += gw * e.W;
 }
 
+// Running error bound companion of acc_w_grad (R23b): the same
+// terms with every factor and every summand taken in absolute value, scaled by
+// gwa = the absolute-term magnitude of dL/dw. Summed over pairs it gives S_q =
+// sum of |terms| of record gradient q, the scale of the rounding error any
+// finite-precision evaluation of those terms carries.
+static inline void acc_w_grad_abs(const double* r, const pair_eval& e, double gwa, double* g) {
+  double s = 0.5 * std::fabs(r[P_BETA] * r[P_ALPHA] * e.G * std::sin(e.theta));
+  double w = std::fabs(e.w), dx = std::fabs(e.dx), dy = std::fabs(e.dy);
+  double a = std::fabs(r[P_A]), b = std::fabs(r[P_B]), c = std::fabs(r[P_C]);
+  g[G_MUX] += gwa * (w * (a * dx + b * dy) + s * std::fabs(r[P_FX]));
+  g[G_MUY] += gwa * (w * (b * dx + c * dy) + s * std::fabs(r[P_FY]));
+  g[G_A] += gwa * 0.5 * w * dx * dx;
+  g[G_B] += gwa * w * dx * dy;
+  g[G_C] += gwa * 0.5 * w * dy * dy;
+  g[G_FX] += gwa * s * dx;
+  g[G_FY] += gwa * s * dy;
+  g[G_PHI] += gwa * s;
+  g[G_BETA] += gwa * 0.5 * std::fabs(r[P_ALPHA] * e.G * std::cos(e.theta));
+  g[G_ALPHA] += gwa * std::fabs(e.W);
+}
+
 static inline double rel_margin(double v, double thr) {
   if (thr == 0.0) return INFINITY;
   return std::fabs(v / thr - 1.0);
@@ -499,7 +520,7 @@ void ora_render(const ora_cfg* cfg, int64_t N, int32_t B, const double* rec,
                 const int32_t* flag, const int32_t* rect, const uint32_t* keylo,
                 int64_t npix, const int64_t* pix, double* color, double* T_out,
                 double* margin, int32_t* ncomp, const double* dLdC, double* rgrad,
-                int32_t nthreads) {
+                int32_t nthreads, double* rgrad_abs) {
   const ora_cfg& c = *cfg;
   const int64_t H = c.height, W = c.width, HW = H * W;
   const int64_t GX = (c.width + c.tile - 1) / c.tile;
@@ -526,6 +547,7 @@ void ora_render(const ora_cfg* cfg, int64_t N, int32_t B, const double* rec,
   bool per_thread = rgrad && (G_SIZE * (int64_t)nt * 8 <= (int64_t)2 << 30);
   if (rgrad) {
     std::memset(rgrad, 0, sizeof(double) * G_SIZE);
+    if (rgrad_abs) std::memset(rgrad_abs, 0, sizeof(double) * G_SIZE);
     if (per_thread) tg.assign(nt, std::vector<double>());
   }
 #pragma omp parallel num_threads(nt)
@@ -579,6 +601,18 @@ void ora_render(const ora_cfg* cfg, int64_t N, int32_t B, const double* rec,
                 rgrad[o * ORA_G + q] += loc[q];
               }
             }
+            if (rgrad_abs) {
+              double la[ORA_G] = {0};
+              const double gwa = std::fabs(r[P_CR] * g3[0]) + std::fabs(r[P_CG] * g3[1]) +
+                                 std::fabs(r[P_CB] * g3[2]);
+              la[G_CR] = std::fabs(e.w * g3[0]); la[G_CG] = std::fabs(e.w * g3[1]);
+              la[G_CB] = std::fabs(e.w * g3[2]);
+              acc_w_grad_abs(r, e, gwa, la);
+              for (int q = 0; q < ORA_G; ++q) {
+#pragma omp atomic
+                rgrad_abs[o * ORA_G + q] += la[q];
+              }
+            }
           }
         } else {
           double a = std::min(c.alpha_max, e.w);
@@ -613,6 +647,18 @@ void ora_render(const ora_cfg* cfg, int64_t N, int32_t B, const double* rec,
             loc[G_CR] = a * Tk * g3[0]; loc[G_CG] = a * Tk * g3[1]; loc[G_CB] = a * Tk * g3[2];
             double gw = (comp_w[m] < c.alpha_max) ? dLda : 0.0;
             acc_w_grad(r, comp_e[m], gw, loc);
+            if (rgrad_abs) {
+              double la[ORA_G] = {0}, gwa = 0.0;
+              for (int ch = 0; ch < 3; ++ch) {
+                la[G_CR + ch] = std::fabs(a * Tk * g3[ch]);
+                gwa += std::fabs(g3[ch]) * (std::fabs(cc[ch] * Tk) + std::fabs(S[ch]) / (1.0 - a));
+              }
+              if (comp_w[m] < c.alpha_max) acc_w_grad_abs(r, comp_e[m], gwa, la);
+              for (int q = 0; q < ORA_G; ++q) {
+#pragma omp atomic
+                rgrad_abs[o * ORA_G + q] += la[q];
+              }
+            }
             for (int ch = 0; ch < 3; ++ch) S[ch] += cc[ch] * a * Tk;
             if (per_thread) {
               for (int q = 0; q < ORA_G; ++q) gbuf[o * ORA_G + q] += loc[q];

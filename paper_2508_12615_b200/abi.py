@@ -39,7 +39,8 @@ class wipes_config(C.Structure):
                 ("dilation", C.c_float), ("cov_eps", C.c_float), ("det_min", C.c_float),
                 ("ewa_clamp", C.c_int32), ("background", C.c_float * 3),
                 ("deterministic", C.c_int32), ("row_mod", C.c_int32), ("row_rem", C.c_int32),
-                ("color_mode", C.c_int32), ("sh_degree", C.c_int32)]
+                ("color_mode", C.c_int32), ("sh_degree", C.c_int32),
+                ("grad_accum", C.c_int32)]
 
 
 class wipes_params(C.Structure):
@@ -171,12 +172,17 @@ def check(status: int, where: str):
         raise WipesError(status, where, lib().wipes_last_error().decode())
 
 
+ACCUM = {"auto": 0, "f32": 1, "f64": 2}
+
+
 def make_config(width, height, tile=16, prim="2d", blend="sum", cov2="sigma", proj="paper",
                 extent="opacity", alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4,
                 dilation=None, cov_eps=0.0, det_min=1e-12, ewa_clamp=True,
                 background=(0.0, 0.0, 0.0), deterministic=0, row_mod=0,
-                row_rem=0, sh_degree=None) -> wipes_config:
-    """sh_degree None: flat RGB `color`; 0..3: SH colour from `sh` (3D, NEXT-3)."""
+                row_rem=0, sh_degree=None, grad_accum="auto") -> wipes_config:
+    """sh_degree None: flat RGB `color`; 0..3: SH colour from `sh` (3D, NEXT-3).
+    grad_accum: render-backward moment precision, "auto" (FP64 for 3D, FP32 for
+    2D), "f32" or "f64" (include/wipes.h WIPES_ACCUM_*, R37)."""
     if dilation is None:
         dilation = 0.3 if prim == "3d" else 0.0
     return wipes_config(int(width), int(height), int(tile), PRIM[prim], BLEND[blend], COV2[cov2],
@@ -184,7 +190,7 @@ def make_config(width, height, tile=16, prim="2d", blend="sum", cov2="sigma", pr
                         cov_eps, det_min, int(bool(ewa_clamp)), (C.c_float * 3)(*background),
                         int(deterministic), int(row_mod), int(row_rem),
                         COLOR["rgb"] if sh_degree is None else COLOR["sh"],
-                        0 if sh_degree is None else int(sh_degree))
+                        0 if sh_degree is None else int(sh_degree), ACCUM[grad_accum])
 
 
 def cameras(cams) -> "C.Array":

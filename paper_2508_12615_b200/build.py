@@ -46,9 +46,16 @@ def _nvcc():
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     """Compile every .cu for sm_100a and link libwipes.so. `defines`/`out`
-    build an experimental variant elsewhere (never the in-tree library)."""
+    build an experimental variant elsewhere: with defines and no `out`, the
+    variant goes to libwipes_<defines>.so beside the in-tree library, which a
+    variant build never touches (load it with WIPES_LIB=...)."""
+    tag = "_".join(d.replace("=", "") for d in defines)
+    if defines and out is None:
+        out = os.path.join(HERE, f"libwipes_{tag}.so")
+    if defines and os.path.abspath(out) == os.path.abspath(LIB):
+        raise ValueError("a build with defines must not overwrite the in-tree libwipes.so")
     lib = out or LIB
-    bdir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    bdir = BUILD if not defines else BUILD + "_" + tag
     os.makedirs(bdir, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "wipes.h")]
     newest = max(os.path.getmtime(d) for d in deps)

@@ -77,6 +77,8 @@ wipes_status check_cfg(const wipes_config* c, int64_t N, int32_t B) {
   if (c->color_mode == WIPES_COLOR_SH && (c->sh_degree < 0 || c->sh_degree > 3))
     return fail(WIPES_EINVAL, "sh_degree must be in 0..3");
   if (c->deterministic != 0 && c->deterministic != 1) return fail(WIPES_EINVAL, "deterministic");
+  if (c->grad_accum < WIPES_ACCUM_AUTO || c->grad_accum > WIPES_ACCUM_F64)
+    return fail(WIPES_EINVAL, "grad_accum");
   if (!(c->alpha_min >= 0.f) || !(c->alpha_max > c->alpha_min) || !(c->alpha_max <= 1.f))
     return fail(WIPES_EINVAL, "need 0 <= alpha_min < alpha_max <= 1");
   if (!(c->T_min >= 0.f) || !(c->T_min < 1.f)) return fail(WIPES_EINVAL, "T_min");

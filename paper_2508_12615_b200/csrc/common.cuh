@@ -2,6 +2,7 @@
 // render-record layout, kernel ids, launch helpers. Product code only — no
 // oracle code or header is included anywhere under csrc/.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cassert>
@@ -17,6 +18,21 @@
 #else
 #define WCHECK(c) ((void)0)
 #endif
+
+// Raise a kernel's dynamic shared-memory limit once per (call site, device):
+// the attribute is per device, so a process that launches on several GPUs sets
+// it on each; concurrent first calls only repeat an idempotent set.
+#define WIPES_SET_SMEM_ONCE(kernel, bytes)                                           \
+  do {                                                                               \
+    static std::atomic<unsigned long long> wipes_smem_mask_{0};                      \
+    int wipes_dev_ = 0;                                                              \
+    cudaGetDevice(&wipes_dev_);                                                      \
+    const unsigned long long wipes_bit_ = 1ull << (wipes_dev_ & 63);                 \
+    if (!(wipes_smem_mask_.load(std::memory_order_acquire) & wipes_bit_)) {          \
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (bytes)); \
+      wipes_smem_mask_.fetch_or(wipes_bit_, std::memory_order_release);              \
+    }                                                                                \
+  } while (0)
 
 namespace wipes {
 

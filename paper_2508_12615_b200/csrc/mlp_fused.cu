@@ -890,11 +890,7 @@ bool launch_mlp_fused_fwd(const MlpFusedDesc& d, cudaStream_t s, cudaError_t* er
   }
   if (!ok) return false;
   const int smem = 6 * (int)kXChunk + kFStages * 256 * 64 * 2 + 1024 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mlp_fused_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  WIPES_SET_SMEM_ONCE(k_mlp_fused_fwd, smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -925,11 +921,7 @@ int launch_mlp_bwd_layer(const MlpBwdDesc& d, cudaStream_t s, cudaError_t* err) 
   if (groups < 1) return 0;
   a.groups = (int32_t)groups;
   const int smem = 7 * (int)kHalf + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mlp_bwd_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  WIPES_SET_SMEM_ONCE(k_mlp_bwd_layer, smem);
   launch_begin(K_GEMM, s);
   k_mlp_bwd_layer<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
   launch_end(K_GEMM, s);
@@ -953,11 +945,7 @@ bool launch_mlp_fwd_layer(const MlpFwdLayerDesc& d, cudaStream_t s, cudaError_t*
   if (groups > tiles) groups = tiles;
   a.groups = (int32_t)groups;
   const int smem = 7 * (int)kHalf + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mlp_fwd_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  WIPES_SET_SMEM_ONCE(k_mlp_fwd_layer, smem);
   launch_begin(K_GEMM, s);
   k_mlp_fwd_layer<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
   launch_end(K_GEMM, s);
@@ -983,11 +971,7 @@ int launch_mlp_head_bwd(const MlpHeadBwdDesc& d, cudaStream_t s, cudaError_t* er
   if (groups > tiles) groups = tiles;
   a.groups = (int32_t)groups;
   const int smem = 5 * (int)kHalf + 4096 + 4 * 4096 + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mlp_head_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  WIPES_SET_SMEM_ONCE(k_mlp_head_bwd, smem);
   launch_begin(K_GEMM, s);
   k_mlp_head_bwd<<<(unsigned)(2 * groups), kBThreads, smem, s>>>(a);
   launch_end(K_GEMM, s);

@@ -45,6 +45,9 @@ constexpr int kMom = kMoments;  // 12
 #ifndef WIPES_MINB_BWD_ALPHA
 #define WIPES_MINB_BWD_ALPHA 7  // ... backward, ALPHA (72 registers: C3 -6% against 6)
 #endif
+#ifndef WIPES_MINB_BWD_F64
+#define WIPES_MINB_BWD_F64 6  // ... backward with FP64 moments (SUM and ALPHA)
+#endif
 constexpr int kWarpsPerCta = 4;
 #ifdef WIPES_BWD_COUNT
 __device__ unsigned long long g_bwd_cnt[8];
@@ -53,6 +56,11 @@ __device__ unsigned long long g_bwd_cnt[8];
 #define BCNT(i, v) do { } while (0)
 #endif
 constexpr int kCta = 32 * kWarpsPerCta;
+// Moment accumulation precision (R37): a lane's per-pair moment sums,
+// the per-record finish and the warp reduction run in MomT<F64>::T; the
+// colour moments M9..M11 (well conditioned) are always summed in FP32.
+template <bool F64> struct MomT { typedef float T; };
+template <> struct MomT<true> { typedef double T; };
 enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 
 #ifndef WIPES_FWD_UNROLL
@@ -123,9 +131,13 @@ struct RenderArgs {
   float* slots;             // deterministic mode: [cap, fps, slotw] per-(dup, footprint) moments
   uint8_t* slotmask;        // deterministic mode: byte (dup * fps + footprint) = slot written
   int32_t fps, slotw;
+  int32_t f64;              // backward: FP64 moment accumulation (R37)
   unsigned long long* stats;  // STATS build: {tile-method candidates, in-ellipse, contributing}
 };
 
+#ifndef WIPES_FWD_PACK
+#define WIPES_FWD_PACK 1  // SUM forward: a lane's two pixels in packed FP32 (FFMA2/FMUL2)
+#endif
 #ifndef WIPES_FWD_G
 #define WIPES_FWD_G 1  // forward footprint: 8 x 8 (the backward keeps 8 x 16 for TS >= 16)
 #endif
@@ -339,9 +351,13 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
   WarpSmem& ws = sm_all[wid];
   unsigned long long st_cand = 0, st_ell = 0, st_con = 0;  // STATS only
   Item it;
+  // SUM with two pixels per lane: the pair's colour sums are packed float2
+  // accumulators updated by FFMA2 (elementwise identical to two FFMAs)
+  constexpr bool PACK = !ALPHA && !STATS && P == 2 && WIPES_FWD_PACK;
   while (next_item<TS, GF>(a, lane, 1, it)) {
     bool in[P], done[P];
     float C[P][3], T[P];
+    float2 Cp[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     int last[P], stop[P];
     const int len = it.end - it.start;
 #pragma unroll
@@ -389,6 +405,27 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
         if (!any) continue;
         const float4 r2 = ws.rec[2][i], r3 = ws.rec[3][i];
         const int pos = ws.pos[i];
+        if constexpr (PACK) {
+          // theta = fx dx + (fy dy + phi) and w = ag (1/2 + beta/2 cos theta) in the
+          // same expression order as the scalar pair_theta / pair_weight
+          const float2 th = __ffma2_rn(make_float2(r2.x, r2.x), make_float2(dx, dx),
+                                       __ffma2_rn(make_float2(r2.y, r2.y),
+                                                  make_float2(dy[0], dy[1]),
+                                                  make_float2(r2.z, r2.z)));
+          const float2 ag = make_float2(ex2(e[0]), ex2(e[1]));
+          const float2 hw = __ffma2_rn(make_float2(r2.w, r2.w),
+                                       make_float2(cos_a(th.x), cos_a(th.y)),
+                                       make_float2(0.5f, 0.5f));
+          const float2 w = __fmul2_rn(ag, hw);
+          // h (e >= skip_e) is implied by w >= alpha_min here: skip_e sits 1e-4 below
+          // log2(alpha_min) and w <= ag (beta <= 1), so the gate is the w test alone
+          const float2 we = make_float2(w.x >= a.alpha_min ? w.x : 0.f,
+                                        w.y >= a.alpha_min ? w.y : 0.f);
+          Cp[0] = __ffma2_rn(make_float2(r3.x, r3.x), we, Cp[0]);
+          Cp[1] = __ffma2_rn(make_float2(r3.y, r3.y), we, Cp[1]);
+          Cp[2] = __ffma2_rn(make_float2(r3.z, r3.z), we, Cp[2]);
+          continue;
+        }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           if (!bm[p]) continue;
@@ -422,6 +459,13 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
     }
     const int64_t HW = (int64_t)a.H * a.W;
     float* img = a.image + it.v * 3 * HW;
+    if constexpr (PACK) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        C[0][c] = (&Cp[c].x)[0];
+        C[1][c] = Cp[c].y;
+      }
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       if (!in[p]) continue;
@@ -451,13 +495,14 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
 
 // 12-slot warp transpose-reduce. On return lane L holds the warp-wide sum of
 // moment index 6*b4 + 3*b3 + q (b_k = bit k of L, q = (L >> 1) & 3) when q < 3.
-__device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) {
+template <typename mom_t>
+__device__ __forceinline__ mom_t transpose_reduce12(mom_t (&v)[kMom], int lane) {
   {
     const bool up = lane & 16;
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      float send = up ? v[k] : v[k + 6];
-      float keep = up ? v[k + 6] : v[k];
+      mom_t send = up ? v[k] : v[k + 6];
+      mom_t keep = up ? v[k + 6] : v[k];
       v[k] = keep + __shfl_xor_sync(kFull, send, 16);
     }
   }
@@ -465,21 +510,21 @@ __device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) 
     const bool up = lane & 8;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      float send = up ? v[k] : v[k + 3];
-      float keep = up ? v[k + 3] : v[k];
+      mom_t send = up ? v[k] : v[k + 3];
+      mom_t keep = up ? v[k + 3] : v[k];
       v[k] = keep + __shfl_xor_sync(kFull, send, 8);
     }
   }
   {
     const bool up = lane & 4;  // pairs (0, 2) and (1, pad)
-    float s0 = up ? v[0] : v[2], k0 = up ? v[2] : v[0];
-    float s1 = up ? v[1] : 0.f, k1 = up ? 0.f : v[1];
+    mom_t s0 = up ? v[0] : v[2], k0 = up ? v[2] : v[0];
+    mom_t s1 = up ? v[1] : (mom_t)0, k1 = up ? (mom_t)0 : v[1];
     v[0] = k0 + __shfl_xor_sync(kFull, s0, 4);
     v[1] = k1 + __shfl_xor_sync(kFull, s1, 4);
   }
   {
     const bool up = lane & 2;
-    float s = up ? v[0] : v[1], k = up ? v[1] : v[0];
+    mom_t s = up ? v[0] : v[1], k = up ? v[1] : v[0];
     v[0] = k + __shfl_xor_sync(kFull, s, 2);
   }
   return v[0] + __shfl_xor_sync(kFull, v[0], 1);
@@ -488,34 +533,57 @@ __device__ __forceinline__ float transpose_reduce12(float (&v)[kMom], int lane) 
 // Moments of one pair, gw = dL/dw and w already zeroed when the
 // pair does not contribute: M0 = gw w, M1 = gw w dx, M2 = gw w dy,
 // M3 = gw w dx^2, M4 = gw w dx dy, M5 = gw w dy^2, M6 = gw ag sin, M7 = M6 dx,
-// M8 = M6 dy, M9..11 = dL/dc terms. A lane's pixels share dx (one column) and
-// have dy = dy0 + ky with the slot offset ky in {0, 4, 8, 12} a compile-time
-// constant, so the slots accumulate sums over ky only (slot 0 adds nothing to
-// them) and finish_moments applies dx and dy0 once per record.
-__device__ __forceinline__ void add_moments(float (&m)[kMom], float gw, float w, float ag,
-                                            float sn, float ky, float c0, float c1, float c2) {
-  const float gww = gw * w;
-  const float m6 = gw * ag * sn;
+// M8 = M6 dy, M9..11 = dL/dc terms. A lane's pixels share dx (one column), so
+// the lane sums M0, M2, M5, M6, M8 (each pixel with its own dy) and
+// finish_moments applies dx once per record (M1 = M0 dx, M3 = M0 dx^2,
+// M4 = M2 dx, M7 = M6 dx: exact factorisations, no cancellation). An earlier
+// expansion of the dy sums about the lane's first row (dy0^2 M0 + 2 dy0 S_ky +
+// S_ky2) cancelled when dy0 ~ -ky and is gone (R37).
+template <bool F64>
+__device__ __forceinline__ void add_moments(typename MomT<F64>::T (&m)[9], float (&mc)[3],
+                                            float gw, float w, float ag, float sn,
+                                            typename MomT<F64>::T dy, float c0, float c1,
+                                            float c2) {
+  typedef typename MomT<F64>::T T;
+#ifdef WIPES_EXP_FPROD  // experiment: FP32 products widened (FP64 path)
+  const T gww = (T)(gw * w);
+  const T m6 = (T)(gw * (ag * sn));
+#else
+  // FP64: the products are exact (a product of two floats fits a double) or
+  // rounded once at 2^-53; FP32: one rounding each
+  const T gwT = (T)gw;
+  const T gww = gwT * (T)w;
+  const T m6 = (gwT * (T)ag) * (T)sn;
+#endif
+  const T gwy = gww * dy;
   m[0] += gww;
+  m[2] += gwy;
+  m[5] = fma(gwy, dy, m[5]);
   m[6] += m6;
-  if (ky != 0.f) {
-    m[2] = __fmaf_rn(gww, ky, m[2]);       // sum gww ky
-    m[5] = __fmaf_rn(gww, ky * ky, m[5]);  // sum gww ky^2
-    m[8] = __fmaf_rn(m6, ky, m[8]);        // sum m6 ky
-  }
-  m[9] += c0;
-  m[10] += c1;
-  m[11] += c2;
+  m[8] = fma(m6, dy, m[8]);
+  mc[0] += c0;
+  mc[1] += c1;
+  mc[2] += c2;
 }
 
-__device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx, float dy0) {
-  m[5] = __fmaf_rn(dy0, __fmaf_rn(dy0, m[0], 2.f * m[2]), m[5]);
-  m[2] = __fmaf_rn(dy0, m[0], m[2]);
-  m[8] = __fmaf_rn(dy0, m[6], m[8]);
-  m[1] = m[0] * dx;
-  m[3] = m[1] * dx;
-  m[4] = m[2] * dx;
-  m[7] = m[6] * dx;
+template <bool F64>
+__device__ __forceinline__ void finish_moments(typename MomT<F64>::T (&r)[kMom],
+                                               const typename MomT<F64>::T (&m)[9],
+                                               const float (&mc)[3], float dx) {
+  typedef typename MomT<F64>::T T;
+  const T d = (T)dx;
+  r[0] = m[0];
+  r[2] = m[2];
+  r[5] = m[5];
+  r[6] = m[6];
+  r[8] = m[8];
+  r[1] = m[0] * d;
+  r[3] = r[1] * d;
+  r[4] = m[2] * d;
+  r[7] = m[6] * d;
+  r[9] = (T)mc[0];
+  r[10] = (T)mc[1];
+  r[11] = (T)mc[2];
 }
 
 // ALPHA: T is the transmittance in front of the pixel's current record, sdg =
@@ -523,11 +591,12 @@ __device__ __forceinline__ void finish_moments(float (&m)[kMom], float dx, float
 // S' = S + c aT, sdg is carried directly: sdg' = sdg + (c.g) aT. A
 // non-contributing pair gets al = 0, so rcp(1) = 1 leaves T, sdg unchanged and
 // aT = 0 without selects; only dL/dw needs the gate.
-template <bool ALPHA, bool EXACT>
-__device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, float ky,
-                                          const float4& r2,
+template <bool ALPHA, bool EXACT, bool F64>
+__device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy,
+                                          typename MomT<F64>::T dym, const float4& r2,
                                           const float4& r3, const float (&g)[3], float amin,
-                                          float amax, float& T, float& sdg, float (&m)[kMom],
+                                          float amax, float& T, float& sdg,
+                                          typename MomT<F64>::T (&m)[9], float (&mc)[3],
                                           float& mb, bool& any) {
   const float ag = ex2(e);
   const float th = pair_theta(r2, dx, dy);
@@ -538,7 +607,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, f
   const float gdc = __fmaf_rn(r3.x, g[0], __fmaf_rn(r3.y, g[1], __fmul_rn(r3.z, g[2])));
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
-    add_moments(m, ok ? gdc : 0.f, we, ag, sn, ky, we * g[0], we * g[1], we * g[2]);
+    add_moments<F64>(m, mc, ok ? gdc : 0.f, we, ag, sn, dym, we * g[0], we * g[1], we * g[2]);
     if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
     const float al = ok ? fminf(amax, w) : 0.f;
@@ -549,14 +618,16 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy, f
     sdg = __fmaf_rn(gdc, aT, sdg);
     T = Tk;
     const float gw = (ok && w < amax) ? dLda : 0.f;
-    add_moments(m, gw, w, ag, sn, ky, aT * g[0], aT * g[1], aT * g[2]);
+    add_moments<F64>(m, mc, gw, w, ag, sn, dym, aT * g[0], aT * g[1], aT * g[2]);
     if (EXACT) mb = __fmaf_rn(gw * ag, cs, mb);
   }
 }
 
-template <int TS, bool ALPHA, bool EXACT>
-__global__ void __launch_bounds__(kCta, ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MINB_BWD)
+template <int TS, bool ALPHA, bool EXACT, bool F64>
+__global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
+                                            : (ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MINB_BWD))
     k_render_bwd(RenderArgs a) {
+  typedef typename MomT<F64>::T MT;
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
   __shared__ WarpSmem sm_all[kWarpsPerCta];
@@ -641,20 +712,26 @@ __global__ void __launch_bounds__(kCta, ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MIN
         }
 #endif
         const float4 r2 = ws.rec[2][i], r3 = ws.rec[3][i];
-        float m[kMom];
+        MT m[9];
+        float mc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-        for (int k = 0; k < kMom; ++k) m[k] = 0.f;
+        for (int k = 0; k < 9; ++k) m[k] = 0;
         bool any = false;
         float mb = 0.f;
+        // FP64: each pixel's dy exactly as dy0 + ky (dy0 converted once per record)
+        const MT dy0m = (MT)dy[0];
 #pragma unroll
         for (int p = 0; p < P; ++p)
           if (bm[p])
-            bwd_pixel<ALPHA, EXACT>(h[p], e[p], dx, dy[p], 8.f * (p >> 1) + 4.f * (p & 1), r2,
-                                    r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p], m, mb, any);
+            bwd_pixel<ALPHA, EXACT, F64>(h[p], e[p], dx, dy[p],
+                                         F64 ? dy0m + (MT)(8 * (p >> 1) + 4 * (p & 1)) : (MT)dy[p],
+                                         r2, r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p], m,
+                                         mc, mb, any);
         if (!__any_sync(kFull, any)) continue;
         BCNT(3, 1);
-        finish_moments(m, dx, dy[0]);
-        const float red = transpose_reduce12(m, lane);
+        MT mr[kMom];
+        finish_moments<F64>(mr, m, mc, dx);
+        const float red = (float)transpose_reduce12(mr, lane);
         if (EXACT) {
 #pragma unroll
           for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
@@ -724,10 +801,17 @@ cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   ra.queue = Q_BWD;
   void (*k)(RenderArgs);
-  if (ra.mom_beta)
-    k = alpha ? k_render_bwd<TS, true, true> : k_render_bwd<TS, false, true>;
-  else
-    k = alpha ? k_render_bwd<TS, true, false> : k_render_bwd<TS, false, false>;
+  if (ra.f64) {
+    if (ra.mom_beta)
+      k = alpha ? k_render_bwd<TS, true, true, true> : k_render_bwd<TS, false, true, true>;
+    else
+      k = alpha ? k_render_bwd<TS, true, false, true> : k_render_bwd<TS, false, false, true>;
+  } else {
+    if (ra.mom_beta)
+      k = alpha ? k_render_bwd<TS, true, true, false> : k_render_bwd<TS, false, true, false>;
+    else
+      k = alpha ? k_render_bwd<TS, true, false, false> : k_render_bwd<TS, false, false, false>;
+  }
   launch_begin(K_RENDER_BWD, s);
   k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
   launch_end(K_RENDER_BWD, s);
@@ -764,6 +848,10 @@ RenderArgs make_args(const wipes_config& c, const Layout& L, char* ws, int final
   ra.fps = L.fps;
   ra.slotw = L.slotw;
   ra.stats = nullptr;
+  ra.f64 = c.grad_accum == WIPES_ACCUM_F64;
+#ifdef WIPES_FORCE_ACCUM  // A/B experiments only: 1 = FP32, 2 = FP64 everywhere
+  ra.f64 = WIPES_FORCE_ACCUM == 2;
+#endif
   return ra;
 }
 

@@ -286,12 +286,7 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
                         cudaStream_t s, uint32_t vdiv, uint32_t vmask) {
   if (npass == 0 || cap == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sort_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(SortSmem<K>));
-    attr = true;
-  }
+  WIPES_SET_SMEM_ONCE(k_sort_pass<K>, (int)sizeof(SortSmem<K>));
   SortArgs<K> a;
   a.hdr = (const WsHeader*)(ws + L.hdr);
   a.n_fixed = n_fixed;

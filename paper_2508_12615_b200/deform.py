@@ -43,6 +43,9 @@ class Deformation:
         self.ws = None
         self.rows = 0
         self._last = None
+        # bumped by every forward: an autograd backward checks it (the
+        # workspace holds the activations of one forward only)
+        self.generation = 0
 
     @property
     def embed_dim(self):
@@ -100,12 +103,21 @@ class Deformation:
         abi.check(abi.wipes_mlp_forward(self.cfg, abi.ptr(theta), self.N, F, list(times), cp, fp,
                                         shc, train, self._ws_ptr(), self.ws_bytes, _stream()),
                   "wipes_mlp_forward")
-        self._last = (F, cp, fp, canon, frame)
+        self._last = (F, cp, fp, canon, frame, bool(train))
+        self.generation += 1
         return frame
 
     def backward(self, theta: torch.Tensor, canon: dict, g_frame: dict, g_theta=None,
                  g_canon=None):
-        F = self._last[0]
+        if self._last is None:
+            raise RuntimeError("Deformation.backward() before forward()")
+        F, train = self._last[0], self._last[5]
+        if not train:
+            raise RuntimeError("Deformation.backward(): the last forward ran with train=False "
+                               "and kept no activations")
+        if F * self.N != self.rows:
+            raise RuntimeError("Deformation.backward(): workspace rows do not match the last "
+                               "forward")
         if g_theta is None:
             g_theta = torch.empty(self.P, dtype=torch.float32, device=self.device)
         if g_canon is None:
@@ -127,11 +139,17 @@ class _DeformFn(torch.autograd.Function):
         canon = {k: v for k, v in zip(keys, canon_vals)}
         frame = d.forward(theta, canon, times, train=True)
         ctx.d, ctx.keys, ctx.canon, ctx.theta = d, keys, canon, theta
+        ctx.gen, ctx.F = d.generation, len(times)
         ctx.out_keys = tuple(k for k in DEFORMED + COPIED if k in frame)
         return tuple(frame[k] for k in ctx.out_keys)
 
     @staticmethod
     def backward(ctx, *g_out):
+        if ctx.d.generation != ctx.gen or ctx.d._last[0] != ctx.F:
+            raise RuntimeError(
+                "deform(): the Deformation ran another forward before this backward; its "
+                "workspace holds one forward's activations, so use one Deformation per call "
+                f"(generation {ctx.gen}, now {ctx.d.generation})")
         g = dict(zip(ctx.out_keys, g_out))
         g_frame = {k: (g[k] if g.get(k) is not None else torch.zeros_like(ctx.canon[k]).repeat(
             len(g_out[0]) // ctx.canon[k].shape[0], *([1] * (ctx.canon[k].dim() - 1))))

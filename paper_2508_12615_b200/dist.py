@@ -28,6 +28,24 @@ def tile_rows(GY: int, rank: int, world: int) -> list[int]:
     return list(range(rank, GY, world))
 
 
+def reduce_flat(flat: torch.Tensor, group=None, deterministic: bool = False) -> torch.Tensor:
+    """Sum a flat float32 gradient buffer across ranks in place on the current
+    stream: one NCCL all_reduce, or (deterministic) an all_gather of every
+    rank's partial summed in rank order (bitwise identical on every rank)."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return flat
+    if deterministic:
+        parts = [torch.empty_like(flat) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, flat, group=group)
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        flat.copy_(acc)
+    else:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat
+
+
 class GradBucket:
     """Rebinds the tensors of `grads` (dict name -> tensor) to views of one flat
     float32 buffer so the cross-rank gradient sum is a single collective."""
@@ -48,17 +66,6 @@ class GradBucket:
         self.deterministic = deterministic
 
     def all_reduce(self):
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            if self.deterministic:
-                # SURVEY §8(e) deterministic option: gather every rank's partial
-                # and sum in rank order (bitwise identical on every rank and run)
-                parts = [torch.empty_like(self.flat)
-                         for _ in range(dist.get_world_size(self.group))]
-                dist.all_gather(parts, self.flat, group=self.group)
-                acc = parts[0].clone()
-                for p in parts[1:]:
-                    acc += p
-                self.flat.copy_(acc)
-            else:
-                dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
-        return self.flat
+        # SURVEY §8(e); deterministic option: gather every rank's partial and
+        # sum in rank order (bitwise identical on every rank and run)
+        return reduce_flat(self.flat, self.group, self.deterministic)

@@ -58,6 +58,14 @@ class Rasterizer:
         self.B = 1
         self._saved = None
         self.n_dup = None
+        # forward generation: bumped by every render(); an autograd backward
+        # checks it so a second forward before backward raises instead of
+        # returning the later frame's gradients (the workspace holds one frame)
+        self.generation = 0
+        # autograd path: check the device capacity-overflow flag every k
+        # backward calls (one stream sync each); 0 disables the check
+        self.overflow_check_every = 1
+        self._bwd_calls = 0
 
     # -------------------------------------------------------------- helpers
     @property
@@ -139,6 +147,7 @@ class Rasterizer:
                                        self.cap, abi.ptr(image), abi.ptr(T_final),
                                        abi.ptr(n_contrib), _stream()), "wipes_render_fwd")
         self._saved = (image, T_final, n_contrib)
+        self.generation += 1
         return image, T_final, n_contrib
 
     def forward(self, params: dict, cams=None, view_stride: int = 0, sync: bool = None):
@@ -217,17 +226,39 @@ class Rasterizer:
         return keys[:n], vals[:n], toff
 
 
+class CapacityOverflow(RuntimeError):
+    """The frame's tile intersections exceeded the workspace capacity, so its
+    image and gradients were truncated (SURVEY §8(b) capacity protocol). The
+    capacity has been grown; re-run the step."""
+
+
 class _RasterizeFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, r: Rasterizer, cams, view_stride, keys, *tensors):
         params = {k: t for k, t in zip(keys, tensors) if t is not None}
         out = r.forward(params, cams=cams, view_stride=view_stride)
-        ctx.r, ctx.keys = r, keys
+        ctx.r, ctx.keys, ctx.gen = r, keys, r.generation
         return out["image"]
 
     @staticmethod
     def backward(ctx, g):
-        grads = ctx.r.backward(g.contiguous())
+        r = ctx.r
+        if r.generation != ctx.gen:
+            raise RuntimeError(
+                "rasterize(): the Rasterizer ran another forward before this backward; its "
+                "workspace holds one frame, so use one Rasterizer per frame in a loss "
+                f"(forward generation {ctx.gen}, now {r.generation})")
+        r._bwd_calls += 1
+        k = r.overflow_check_every
+        if k and r._bwd_calls % k == 0:
+            n, over = r.check_overflow()
+            if over:
+                r._alloc(r.N, r.B, int(n * r.growth) + 1)
+                r.generation += 1  # the truncated frame is gone
+                raise CapacityOverflow(
+                    f"rasterize(): {n} tile intersections exceeded the capacity; the frame was "
+                    f"truncated. Capacity grown to {r.cap}: re-run the step.")
+        grads = r.backward(g.contiguous())
         return (None, None, None, None) + tuple(grads.get(k) for k in ctx.keys)
 
 

@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 from paper_2508_12615_b200 import gen
-from parity_util import oracle_cfg, grad_violations
+from parity_util import (oracle_cfg, grad_violations, ambiguous_rows, check_grads_strict,
+                         oracle_grads)
 
 pytestmark = pytest.mark.gpu
 
@@ -123,12 +124,14 @@ def test_fit_step_parity(ora, graph):
     img = out["color"].reshape(H, W, 3).transpose(2, 0, 1)
     lo, dL = ora.loss_l2(img, tgt.astype(np.float64))
     assert abs(fit.loss_dev.item() - lo) <= 1e-4 * lo
-    og = ora.forward_backward(cfg, q, dL.transpose(1, 2, 0).reshape(-1, 3))["grads"]
+    ro = ora.render(cfg, out["proj"], dLdC=dL.transpose(1, 2, 0).reshape(-1, 3), abs_terms=True)
+    og, gb = oracle_grads(ora, cfg, q, out["proj"], ro)
     from paper_2508_12615_b200.train import DEFAULT_LR
+    exc = ambiguous_rows(out["proj"], out["margin"], 1, N, H, W)
+    check_grads_strict(fit.grads, og, exc, f"fit step graph={graph}",
+                       keys=("mean", "cov", "freq", "color", "opacity"), bound=gb)
     for k in ("mean", "cov", "freq", "color", "opacity"):
         gk = og[k]
-        nbad, worst = grad_violations(fit.grads[k].cpu().numpy(), gk)
-        assert nbad <= 2, (k, nbad, worst)
         pn, _, _, _ = ora.adam_step(p[k], gk, 0 * gk, 0 * gk, 1, DEFAULT_LR[k],
                                     activation="sigmoid" if k == "opacity" else "none")
         got = fit.raw[k].cpu().numpy()
