@@ -8,7 +8,16 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
+
+// NVTX range around each north-star ABI call (visible in nsys / ncu --nvtx;
+// header-only NVTX3: a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace wipes {
 
@@ -163,6 +172,7 @@ wipes_status wipes_preprocess(const wipes_config* cfg, const wipes_params* param
                               const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
                               int64_t dup_capacity, int64_t* n_dup, uint8_t* cull_flags,
                               void* stream) {
+  NvtxRange nvtx_range("wipes_preprocess");
   wipes_status st = check_cfg(cfg, N, B);
   if (st != WIPES_OK) return st;
   st = check_params(cfg, params, N, B);
@@ -194,6 +204,7 @@ wipes_status wipes_preprocess(const wipes_config* cfg, const wipes_params* param
 wipes_status wipes_bin_sort(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
                             size_t ws_bytes, int64_t dup_capacity, uint64_t* keys_out,
                             uint32_t* vals_out, int32_t* tile_offsets_out, void* stream) {
+  NvtxRange nvtx_range("wipes_bin_sort");
   wipes_status st = check_cfg(cfg, N, B);
   if (st != WIPES_OK) return st;
   Layout L = make_layout(*cfg, N, B, dup_capacity);
@@ -253,6 +264,7 @@ wipes_status wipes_get_preprocess(const wipes_config* cfg, int64_t N, int32_t B,
 wipes_status wipes_render_fwd(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
                               size_t ws_bytes, int64_t dup_capacity, float* image, float* T_final,
                               int32_t* n_contrib, void* stream) {
+  NvtxRange nvtx_range("wipes_render_fwd");
   wipes_status st = check_cfg(cfg, N, B);
   if (st != WIPES_OK) return st;
   Layout L = make_layout(*cfg, N, B, dup_capacity);
@@ -271,6 +283,7 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
                               const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
                               int64_t dup_capacity, const float* dL_dimage, const float* T_final,
                               const int32_t* n_contrib, wipes_grads* grads, void* stream) {
+  NvtxRange nvtx_range("wipes_render_bwd");
   wipes_status st = check_cfg(cfg, N, B);
   if (st != WIPES_OK) return st;
   st = check_params(cfg, params, N, B);

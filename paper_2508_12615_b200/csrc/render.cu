@@ -220,6 +220,8 @@ __device__ __forceinline__ float pair_weight(float ag, float cs, const float4& r
   return __fmul_rn(ag, __fmaf_rn(r2.w, cs, 0.5f));
 }
 
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
 // Warp-private staging area: the compacted hits of the current 32-record chunk.
 struct WarpSmem {
   float4 rec[4][32];
@@ -354,10 +356,14 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
   // SUM with two pixels per lane: the pair's colour sums are packed float2
   // accumulators updated by FFMA2 (elementwise identical to two FFMAs)
   constexpr bool PACK = !ALPHA && !STATS && P == 2 && WIPES_FWD_PACK;
+  // ALPHA likewise: the pair's transmittances and colour sums packed; the
+  // per-pixel decisions (skip, clamp, stop) stay scalar
+  constexpr bool PACKA = ALPHA && !STATS && P == 2 && WIPES_FWD_PACK;
   while (next_item<TS, GF>(a, lane, 1, it)) {
     bool in[P], done[P];
     float C[P][3], T[P];
     float2 Cp[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 Tp = make_float2(1.f, 1.f);
     int last[P], stop[P];
     const int len = it.end - it.start;
 #pragma unroll
@@ -426,6 +432,34 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
           Cp[2] = __ffma2_rn(make_float2(r3.z, r3.z), we, Cp[2]);
           continue;
         }
+        if constexpr (PACKA) {
+          const float2 th = __ffma2_rn(f2(r2.x), f2(dx),
+                                       __ffma2_rn(f2(r2.y), make_float2(dy[0], dy[1]), f2(r2.z)));
+          const float2 ag = make_float2(ex2(e[0]), ex2(e[1]));
+          const float2 w = __fmul2_rn(ag, __ffma2_rn(f2(r2.w), make_float2(cos_a(th.x), cos_a(th.y)),
+                                                     f2(0.5f)));
+          const bool ok0 = h[0] && w.x >= a.alpha_min, ok1 = h[1] && w.y >= a.alpha_min;
+          // alpha_step on both pixels: al = min(amax, w), T' = T (1 - al), stop if
+          // T' < T_min (not composited), else C += c al T, T = T'
+          const float2 al = make_float2(fminf(a.alpha_max, w.x), fminf(a.alpha_max, w.y));
+          const float2 Tn = __fmul2_rn(Tp, __fadd2_rn(f2(1.f), make_float2(-al.x, -al.y)));
+          const bool stp0 = ok0 && Tn.x < a.T_min, stp1 = ok1 && Tn.y < a.T_min;
+          const bool cmp0 = ok0 && !stp0, cmp1 = ok1 && !stp1;
+          const float2 aT = __fmul2_rn(al, Tp);
+          const float2 aTs = make_float2(cmp0 ? aT.x : 0.f, cmp1 ? aT.y : 0.f);
+          Cp[0] = __ffma2_rn(f2(r3.x), aTs, Cp[0]);
+          Cp[1] = __ffma2_rn(f2(r3.y), aTs, Cp[1]);
+          Cp[2] = __ffma2_rn(f2(r3.z), aTs, Cp[2]);
+          Tp = make_float2(cmp0 ? Tn.x : Tp.x, cmp1 ? Tn.y : Tp.y);
+          last[0] = cmp0 ? pos : last[0];
+          last[1] = cmp1 ? pos : last[1];
+          done[0] = done[0] || stp0;
+          done[1] = done[1] || stp1;
+          stop[0] = stp0 ? pos : stop[0];
+          stop[1] = stp1 ? pos : stop[1];
+          if (__all_sync(kFull, done[0] && done[1])) break;
+          continue;
+        }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           if (!bm[p]) continue;
@@ -459,11 +493,15 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
     }
     const int64_t HW = (int64_t)a.H * a.W;
     float* img = a.image + it.v * 3 * HW;
-    if constexpr (PACK) {
+    if constexpr (PACK || PACKA) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        C[0][c] = (&Cp[c].x)[0];
+        C[0][c] = Cp[c].x;
         C[1][c] = Cp[c].y;
+      }
+      if (PACKA) {
+        T[0] = Tp.x;
+        T[1] = Tp.y;
       }
     }
 #pragma unroll
@@ -623,6 +661,73 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy,
   }
 }
 
+#ifndef WIPES_BWD_PACK
+#define WIPES_BWD_PACK 1  // FP32 backward: a lane's pixel pairs (rows y, y + 4) in FFMA2/FMUL2
+#endif
+
+// Packed moment sums of a lane (FP32 path): .x collects the pairs' first
+// pixels (rows y0, y0 + 8), .y the second (y0 + 4, y0 + 12); the two halves
+// are added once per record. Same moments as add_moments (M0, M2, M5, M6, M8,
+// M9..11).
+struct MomPack {
+  float2 m0, m2, m5, m6, m8, c0, c1, c2;
+};
+
+// bwd_pixel for the two pixels of a lane's pair (same column, rows dy and
+// dy + 4), every FP32 operation packed where both pixels take the same one
+// (elementwise the scalar expressions, in the same order).
+template <bool ALPHA, bool EXACT>
+__device__ __forceinline__ void bwd_pair(bool h0, bool h1, float e0, float e1, float dx,
+                                         float2 dy, const float4& r2, const float4& r3,
+                                         const float2 (&g)[3], float amin, float amax,
+                                         float2& T, float2& sdg, MomPack& m, float& mb,
+                                         bool& any) {
+  const float2 ag = make_float2(ex2(e0), ex2(e1));
+  const float2 th = __ffma2_rn(f2(r2.x), f2(dx), __ffma2_rn(f2(r2.y), dy, f2(r2.z)));
+  const float2 cs = make_float2(cos_a(th.x), cos_a(th.y));
+  const float2 sn = make_float2(sin_a(th.x), sin_a(th.y));
+  const float2 w = __fmul2_rn(ag, __ffma2_rn(f2(r2.w), cs, f2(0.5f)));
+  const bool ok0 = h0 && w.x >= amin, ok1 = h1 && w.y >= amin;
+  any = any || ok0 || ok1;
+  const float2 gdc = __ffma2_rn(f2(r3.x), g[0], __ffma2_rn(f2(r3.y), g[1], __fmul2_rn(f2(r3.z), g[2])));
+  float2 gw, wm, cw;
+  if (!ALPHA) {
+    wm = make_float2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
+    gw = make_float2(ok0 ? gdc.x : 0.f, ok1 ? gdc.y : 0.f);
+    cw = wm;
+    if (EXACT) {
+      mb = __fmaf_rn(gw.x * ag.x, cs.x, mb);
+      mb = __fmaf_rn(gw.y * ag.y, cs.y, mb);
+    }
+  } else {
+    const float2 al = make_float2(ok0 ? fminf(amax, w.x) : 0.f, ok1 ? fminf(amax, w.y) : 0.f);
+    const float2 ri = make_float2(rcp_a(1.f - al.x), rcp_a(1.f - al.y));  // 1 when al = 0
+    const float2 Tk = __fmul2_rn(T, ri);
+    const float2 dLda = __ffma2_rn(Tk, gdc, __fmul2_rn(make_float2(-sdg.x, -sdg.y), ri));
+    const float2 aT = __fmul2_rn(al, Tk);
+    sdg = __ffma2_rn(gdc, aT, sdg);
+    T = Tk;
+    gw = make_float2((ok0 && w.x < amax) ? dLda.x : 0.f, (ok1 && w.y < amax) ? dLda.y : 0.f);
+    wm = w;
+    cw = aT;
+    if (EXACT) {
+      mb = __fmaf_rn(gw.x * ag.x, cs.x, mb);
+      mb = __fmaf_rn(gw.y * ag.y, cs.y, mb);
+    }
+  }
+  const float2 gww = __fmul2_rn(gw, wm);
+  const float2 m6 = __fmul2_rn(gw, __fmul2_rn(ag, sn));
+  const float2 gwy = __fmul2_rn(gww, dy);
+  m.m0 = __fadd2_rn(m.m0, gww);
+  m.m2 = __fadd2_rn(m.m2, gwy);
+  m.m5 = __ffma2_rn(gwy, dy, m.m5);
+  m.m6 = __fadd2_rn(m.m6, m6);
+  m.m8 = __ffma2_rn(m6, dy, m.m8);
+  m.c0 = __ffma2_rn(cw, g[0], m.c0);
+  m.c1 = __ffma2_rn(cw, g[1], m.c1);
+  m.c2 = __ffma2_rn(cw, g[2], m.c2);
+}
+
 template <int TS, bool ALPHA, bool EXACT, bool F64>
 __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
                                             : (ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MINB_BWD))
@@ -630,6 +735,7 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
   typedef typename MomT<F64>::T MT;
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
+  constexpr bool PACKB = !F64 && WIPES_BWD_PACK;
   __shared__ WarpSmem sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   WarpSmem& ws = sm_all[wid];
@@ -662,6 +768,15 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
           ml = max(ml, last[p]);
         }
       }
+    }
+    // packed per-pair state of the FP32 path (pair gg = pixels 2gg, 2gg + 1)
+    float2 g2[G][3], T2[G], sdg2[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) g2[gg][c] = make_float2(g[2 * gg][c], g[2 * gg + 1][c]);
+      T2[gg] = make_float2(T[2 * gg], T[2 * gg + 1]);
+      sdg2[gg] = make_float2(sdg[2 * gg], sdg[2 * gg + 1]);
     }
     int start = it.start, end = it.end;
     if (ALPHA) {  // only entries before this warp's last composited one matter
@@ -718,15 +833,35 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         for (int k = 0; k < 9; ++k) m[k] = 0;
         bool any = false;
         float mb = 0.f;
-        // FP64: each pixel's dy exactly as dy0 + ky (dy0 converted once per record)
-        const MT dy0m = (MT)dy[0];
+        if constexpr (PACKB) {
+          MomPack mp;
+          mp.m0 = mp.m2 = mp.m5 = mp.m6 = mp.m8 = mp.c0 = mp.c1 = mp.c2 = f2(0.f);
 #pragma unroll
-        for (int p = 0; p < P; ++p)
-          if (bm[p])
-            bwd_pixel<ALPHA, EXACT, F64>(h[p], e[p], dx, dy[p],
-                                         F64 ? dy0m + (MT)(8 * (p >> 1) + 4 * (p & 1)) : (MT)dy[p],
-                                         r2, r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p], m,
-                                         mc, mb, any);
+          for (int gg = 0; gg < G; ++gg)
+            if (bm[2 * gg] | bm[2 * gg + 1])
+              bwd_pair<ALPHA, EXACT>(h[2 * gg], h[2 * gg + 1], e[2 * gg], e[2 * gg + 1], dx,
+                                     make_float2(dy[2 * gg], dy[2 * gg + 1]), r2, r3, g2[gg],
+                                     a.alpha_min, a.alpha_max, T2[gg], sdg2[gg], mp, mb, any);
+          m[0] = mp.m0.x + mp.m0.y;
+          m[2] = mp.m2.x + mp.m2.y;
+          m[5] = mp.m5.x + mp.m5.y;
+          m[6] = mp.m6.x + mp.m6.y;
+          m[8] = mp.m8.x + mp.m8.y;
+          mc[0] = mp.c0.x + mp.c0.y;
+          mc[1] = mp.c1.x + mp.c1.y;
+          mc[2] = mp.c2.x + mp.c2.y;
+        } else {
+          // FP64: each pixel's dy exactly as dy0 + ky (dy0 converted once per record)
+          const MT dy0m = (MT)dy[0];
+#pragma unroll
+          for (int p = 0; p < P; ++p)
+            if (bm[p])
+              bwd_pixel<ALPHA, EXACT, F64>(h[p], e[p], dx, dy[p],
+                                           F64 ? dy0m + (MT)(8 * (p >> 1) + 4 * (p & 1))
+                                               : (MT)dy[p],
+                                           r2, r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p],
+                                           m, mc, mb, any);
+        }
         if (!__any_sync(kFull, any)) continue;
         BCNT(3, 1);
         MT mr[kMom];

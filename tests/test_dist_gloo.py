@@ -169,3 +169,58 @@ def test_deterministic_gradbucket_rank_order_sum():
             ref += parts[r][k]
         for r in range(world):
             np.testing.assert_array_equal(got[r][k], ref)
+
+
+def _worker_sets(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    # bench.py's pipelined multi-rank e2e: every buffer set's flat gradient
+    # buffer is summed on its own (reduce_flat), in step order
+    sets = [torch.full((257,), float(10 * k + rank + 1)) for k in range(3)]
+    for k in (0, 1, 2, 0):
+        wdist.reduce_flat(sets[k])
+    det = torch.arange(100, dtype=torch.float32) * (rank + 1)
+    wdist.reduce_flat(det, deterministic=True)
+    q.put((rank, [s.numpy().copy() for s in sets], det.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_reduce_flat_per_buffer_set():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_sets, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict((r, (s, d)) for r, s, d in (q.get(timeout=240) for _ in range(world)))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for r in range(world):
+        sets, det = got[r]
+        # set 0 reduced twice: (1 + 2) -> 3 + 3; sets 1, 2 once
+        assert np.all(sets[0] == 2 * (1 + 2))
+        assert np.all(sets[1] == (11 + 12)) and np.all(sets[2] == (21 + 22))
+        np.testing.assert_array_equal(det, np.arange(100, dtype=np.float32) * 3)
+
+
+def test_bench_sharding_modes():
+    """bench.py's partitioning per config and world size: C2 is
+    one image split by tile rows at N > 1 (replicas only on request), C3 views,
+    C4 frames, C5 tile rows."""
+    import argparse
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    a = argparse.Namespace(replicas=False)
+    assert bench.sharding("c2", 1, a) == (False, False, False)
+    assert bench.sharding("c2", 8, a) == (True, False, True)
+    assert bench.sharding("c2", 8, argparse.Namespace(replicas=True)) == (False, False, False)
+    assert bench.sharding("c3", 8, a) == (False, False, True)
+    assert bench.sharding("c4", 8, a) == (False, True, True)
+    assert bench.sharding("c5", 1, a) == (True, False, True)
