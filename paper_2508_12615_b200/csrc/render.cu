@@ -67,7 +67,7 @@ enum { Q_FWD = 0, Q_BWD = 1, Q_STATS = 2 };
 #define WIPES_FWD_UNROLL 1  // record-loop unroll of the SUM forward (A/B knob)
 #endif
 #ifndef WIPES_FWD_UNROLL_ALPHA
-#define WIPES_FWD_UNROLL_ALPHA 2  // ALPHA forward: C3 render_fwd 2.70 -> 2.62 ms at 2
+#define WIPES_FWD_UNROLL_ALPHA 1  // ALPHA forward (packed pairs): 1 and 2 measure the same (C3 2.51 ms)
 #endif
 #ifndef WIPES_BWD_UNROLL
 #define WIPES_BWD_UNROLL 1  // record-loop unroll of the backward (A/B knob)
@@ -662,7 +662,7 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy,
 }
 
 #ifndef WIPES_BWD_PACK
-#define WIPES_BWD_PACK 1  // FP32 backward: a lane's pixel pairs (rows y, y + 4) in FFMA2/FMUL2
+#define WIPES_BWD_PACK 0  // FP32 backward in FFMA2 pairs: A/B knob, measured slower (register spills), off
 #endif
 
 // Packed moment sums of a lane (FP32 path): .x collects the pairs' first
