@@ -237,16 +237,22 @@ def fit_rate(H, W, N, args, flush, dev):
                         "(preprocess, bin/sort, render, loss, backward, Adam: one CUDA graph)"}
 
 
-def mlp_rate(args, flush, dev, peaks):
+def mlp_rate(args, flush, dev, peaks, precision="bf16x3"):
     """NEXT-4: the D-3DGS-shaped deformation field (8 x 256, skip 4, Lx 10,
     Lt 6) forward + backward on the tcgen05 tensor cores for args.mlp_rows
     rows (C4's 300k primitives x 1 frame, one D-3DGS training iteration),
-    CUDA-event timed over args.steps iterations (L2 flushed between)."""
+    CUDA-event timed over args.steps iterations (L2 flushed between).
+    precision "bf16x3" (default: split-bf16 operands, R38) or "bf16".
+    Roofline: the METHOD's FLOPs (the FP32 network's 2 M sum W K per pass,
+    forward + backward) over the time against the measured bf16 tensor peak —
+    the emulation's own MMA work (3x with bf16x3) is reported beside it; the
+    compulsory HBM bytes (parameters in, frame rows out) are ~100 B per row,
+    far below the ridge, so the tensor pipe is the bound."""
     import torch
     from paper_2508_12615_b200 import gen
     from paper_2508_12615_b200.deform import Deformation
     N = args.mlp_rows
-    d = Deformation(N)
+    d = Deformation(N, precision=precision)
     theta = d.init_theta(seed=args.seed, head_scale=0.1)
     p = gen.gen3d(N, seed=args.seed)
     canon = {k: torch.from_numpy(v).to(dev) for k, v in p.items()}
@@ -277,25 +283,18 @@ def mlp_rate(args, flush, dev, peaks):
     bwd_fl = N * (2 * fl - 2 * d.width * d.layer_in(0))
     peak = float(peaks.get("bf16_tflops", 1695.0))
     ach = (fwd_fl + bwd_fl) / ((fwd + bwd) / 1e3) / 1e12
-    # algorithmic HBM bytes of the layer-by-layer schedule (each GEMM streams its
-    # bf16 operands once and writes its output once; weights are L2-resident)
-    E8 = (d.embed_dim + 7) // 8 * 8
-    kp = [E8 if l == 0 else (E8 + d.width if l == d.skip + 1 else d.width) for l in range(d.depth)]
-    fwd_b = N * (2 * E8 + sum(2 * (k + d.width) for k in kp) + 2 * d.width + 4 * 16)
-    bwd_b = N * (sum(2 * (d.width + k) for k in kp) + sum(6 * d.width for _ in kp[1:])
-                 + 2 * 16 + 2 * d.width + 4 * d.width)
-    hbm = float(peaks.get("hbm_gbs", 6464.9))
-    ach_b = (fwd_b + bwd_b) / ((fwd + bwd) / 1e3) / 1e9
+    mult = 3 if precision == "bf16x3" else 1
     return {"workload": f"NEXT-4 deformation MLP (D-3DGS 8x256, skip 4, PE 10/6), {N} rows, "
-                        "forward + backward, bf16 tcgen05 GEMMs with fp32 accumulation",
+                        f"forward + backward, {precision} operands on tcgen05 GEMMs with fp32 "
+                        "accumulation",
+            "precision": precision,
             "fwd_ms": fwd, "bwd_ms": bwd, "iters_per_s": 1e3 / (fwd + bwd),
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak,
+                         "flops": "the method's (FP32 network) 2 M sum(W K) per pass",
+                         "mma_tflops_executed": ach * mult,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
-            "roofline_hbm": {"bound": "hbm", "achieved": ach_b, "peak": hbm, "unit": "GB/s",
-                             "frac": ach_b / hbm,
-                             "bytes": "per layer GEMM: bf16 inputs read once + output written "
-                                      "once (forward), dW and dIn operands (backward)"}}
+            "compulsory_bytes_per_row": 4 * (3 + 4 + 3 + 3) * 2}
 
 
 def sharding(name, world, args):
@@ -745,6 +744,7 @@ def main():
         line["nvs_c3"] = nvs_subrecord(args, rank, world, dev, flush)
     if not args.no_mlp and (c["kind"] == "6d" or name == "c2"):
         line["mlp"] = mlp_rate(args, flush, dev, peaks)
+        line["mlp_bf16"] = mlp_rate(args, flush, dev, peaks, precision="bf16")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fac, cores = cpu_oracle_sample(c, args.cpu_pixels, seed=123)
         line["cpu_baseline"] = {"value": 1.0 / (dt * fac), "unit": "iters/s", "cores": cores,

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define WIPES_ABI_VERSION 3
+#define WIPES_ABI_VERSION 4
 #define WIPES_MAX_CAMERAS_PER_LAUNCH 128 /* more views are processed in chunks */
 #define WIPES_GRAD_MOMENTS 12            /* see wipes_get_grad_moments */
 
@@ -324,6 +324,12 @@ typedef struct {
   int32_t a_mn_major, b_mn_major, epilogue, split_k;
   float* colsum;      /* optional [N] f32: += column sums of the epilogue result
                          over the rows (atomic; e.g. a bias gradient), or NULL */
+  int64_t split3;     /* bf16 epilogues (ABI v4): 0 = C holds bf16(v); > 0 = C
+                         holds the split-bf16 triple of v (R38):
+                         C[m, n] = C[m, n + split3] = hi = bf16(v),
+                         C[m, n + 2 split3] = lo = bf16(v - hi), so that a
+                         following GEMM over [hi | hi | lo] against weights
+                         [W_hi | W_lo | W_hi] forms hi W_hi + hi W_lo + lo W_hi */
 } wipes_gemm_args;
 wipes_status wipes_gemm_bf16(const wipes_gemm_args* args, void* stream);
 
@@ -344,7 +350,16 @@ typedef struct {
   int32_t depth;   /* >= 1 (D-3DGS: 8)                      */
   int32_t skip;    /* -1 (none) or 0..depth-2 (D-3DGS: 4)    */
   int32_t Lx, Lt;  /* encoding frequencies (D-3DGS: 10, 6)   */
+  int32_t precision; /* ABI v4: WIPES_MLP_BF16X3 (0, default) = every operand
+                      * carried as a split-bf16 pair v = hi + lo (hi = bf16(v),
+                      * lo = bf16(v - hi)) and every product as hi.hi + hi.lo +
+                      * lo.hi on the bf16 tensor cores (one GEMM over
+                      * concatenated [hi | hi | lo] x [W_hi | W_lo | W_hi]
+                      * operands, fp32 accumulation; ~2^-16 relative operands,
+                      * close to the FP32 network of D-3DGS, R38);
+                      * WIPES_MLP_BF16 (1) = single bf16 operands (faster, R36) */
 } wipes_mlp_config;
+enum { WIPES_MLP_BF16X3 = 0, WIPES_MLP_BF16 = 1 };
 
 size_t wipes_mlp_param_count(const wipes_mlp_config* cfg);
 /* Workspace for F*N rows; the forward keeps its activations there for the

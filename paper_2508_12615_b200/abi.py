@@ -65,12 +65,15 @@ class wipes_gemm_args(C.Structure):
                 ("mask", C.c_void_p), ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64), ("ldm", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_mn_major", C.c_int32), ("epilogue", C.c_int32),
-                ("split_k", C.c_int32), ("colsum", C.c_void_p)]
+                ("split_k", C.c_int32), ("colsum", C.c_void_p), ("split3", C.c_int64)]
 
 
 class wipes_mlp_config(C.Structure):
     _fields_ = [("width", C.c_int32), ("depth", C.c_int32), ("skip", C.c_int32),
-                ("Lx", C.c_int32), ("Lt", C.c_int32)]
+                ("Lx", C.c_int32), ("Lt", C.c_int32), ("precision", C.c_int32)]
+
+
+MLP_PRECISION = {"bf16x3": 0, "bf16": 1}
 
 
 GEMM_EPI = {"store_f32": 0, "bias_f32": 1, "bias_relu_bf16": 2, "mask_bf16": 3,

@@ -426,6 +426,9 @@ wipes_status wipes_gemm_bf16(const wipes_gemm_args* g, void* stream) {
       !g->bias)
     return fail(WIPES_EINVAL, "bias is NULL");
   if (g->epilogue == WIPES_GEMM_EPI_MASK_BF16 && !g->mask) return fail(WIPES_EINVAL, "mask is NULL");
+  if (g->split3 < 0 || (g->split3 > 0 && g->epilogue != WIPES_GEMM_EPI_BIAS_RELU_BF16 &&
+                        g->epilogue != WIPES_GEMM_EPI_MASK_BF16))
+    return fail(WIPES_EINVAL, "split3 needs a bf16 epilogue");
   if (g->split_k > 1 && g->epilogue != WIPES_GEMM_EPI_ATOMIC_F32)
     return fail(WIPES_EINVAL, "split_k > 1 needs the atomic epilogue");
   cudaError_t e = launch_gemm(*g, (cudaStream_t)stream);

@@ -290,6 +290,39 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
         for (int i = 0; i < 32; ++i)
           if (i < nv) atomicAdd(cp + i, v[i]);
       }
+    } else if (kBf16Out && g.split3 > 0) {
+      // split-bf16 triple (R38): hi at n and n + split3, lo at n + 2 split3
+      __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(g.C) + m * g.ldc + n;
+      const int64_t s3 = g.split3;
+      if (full && cvec && (s3 % 8) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 uh, ul;
+          uint32_t* wh = reinterpret_cast<uint32_t*>(&uh);
+          uint32_t* wl = reinterpret_cast<uint32_t*>(&ul);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float a = v[8 * q + 2 * h], b = v[8 * q + 2 * h + 1];
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(a, b);
+            const __nv_bfloat162 lo =
+                __floats2bfloat162_rn(a - __low2float(hi), b - __high2float(hi));
+            wh[h] = *reinterpret_cast<const uint32_t*>(&hi);
+            wl[h] = *reinterpret_cast<const uint32_t*>(&lo);
+          }
+          reinterpret_cast<uint4*>(cp)[q] = uh;
+          reinterpret_cast<uint4*>(cp + s3)[q] = uh;
+          reinterpret_cast<uint4*>(cp + 2 * s3)[q] = ul;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nv) {
+            const __nv_bfloat16 hi = __float2bfloat16_rn(v[i]);
+            cp[i] = hi;
+            cp[i + s3] = hi;
+            cp[i + 2 * s3] = __float2bfloat16_rn(v[i] - __bfloat162float(hi));
+          }
+      }
     } else if (kBf16Out) {
       __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(g.C) + m * g.ldc + n;
       if (full && cvec) {
@@ -614,7 +647,7 @@ cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
   std::memset(&P.tc, 0, sizeof(P.tc));
   std::memset(&P.tm, 0, sizeof(P.tm));
   P.tmask = EPI == WIPES_GEMM_EPI_MASK_BF16 && make_out_tmap(&P.tm, g.mask, true, g.M, g.N, g.ldm);
-  P.tstore = EPI != WIPES_GEMM_EPI_ATOMIC_F32 &&
+  P.tstore = EPI != WIPES_GEMM_EPI_ATOMIC_F32 && g.split3 == 0 &&
              make_out_tmap(&P.tc, g.C,
                            EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16 || EPI == WIPES_GEMM_EPI_MASK_BF16,
                            g.M, g.N, g.ldc);

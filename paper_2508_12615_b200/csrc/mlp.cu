@@ -32,6 +32,9 @@ constexpr int kMaxE8 = 3 * (1 + 2 * 16) + (1 + 2 * 16) + 8;  // Lx, Lt <= 16
 
 struct MlpLayout {
   int W, D, skip, Lx, Lt, E, E8, catw;
+  bool x3;     // split-bf16 operands (WIPES_MLP_BF16X3, R38)
+  int R;       // 3 with x3 (every activation buffer holds [hi | hi | lo]), else 1
+  size_t wb3[kMlpMaxDepth], whb3;  // x3: backward weights [W_hi; W_lo; W_hi] (3 rows blocks)
   int64_t M;
   int K[kMlpMaxDepth], Kp[kMlpMaxDepth];
   int64_t thW[kMlpMaxDepth], thb[kMlpMaxDepth], thWh, thbh, P;
@@ -40,7 +43,7 @@ struct MlpLayout {
 };
 
 bool mlp_cfg_ok(const wipes_mlp_config& c) {
-  return c.width >= 16 && c.width <= 256 && c.width % 16 == 0 && c.depth >= 1 &&
+  return (c.precision == WIPES_MLP_BF16X3 || c.precision == WIPES_MLP_BF16) && c.width >= 16 && c.width <= 256 && c.width % 16 == 0 && c.depth >= 1 &&
          c.depth <= kMlpMaxDepth && c.skip >= -1 && c.skip <= c.depth - 2 && c.Lx >= 0 &&
          c.Lx <= 16 && c.Lt >= 0 && c.Lt <= 16;
 }
@@ -50,7 +53,11 @@ MlpLayout mlp_layout(const wipes_mlp_config& c, int64_t M) {
   L.W = c.width; L.D = c.depth; L.skip = c.skip; L.Lx = c.Lx; L.Lt = c.Lt;
   L.E = 3 * (1 + 2 * c.Lx) + (1 + 2 * c.Lt);
   L.E8 = (L.E + 7) / 8 * 8;
-  L.catw = L.E8 + L.W;
+  L.x3 = c.precision == WIPES_MLP_BF16X3;
+  L.R = L.x3 ? 3 : 1;
+  // x3: cat = [e_hi | e_hi | e_lo | h_hi | h_hi | h_lo] (layer 0 reads the first
+  // 3 E8 columns, the layer after the skip all of them)
+  L.catw = L.R * (L.E8 + L.W);
   L.M = M;
   int64_t o = 0;
   for (int l = 0; l < L.D; ++l) {
@@ -65,21 +72,24 @@ MlpLayout mlp_layout(const wipes_mlp_config& c, int64_t M) {
   size_t b = 0;
   auto take = [&](size_t bytes) { size_t r = b; b = align_up(b + bytes, 256); return r; };
   int kmax = 0;
+  const size_t R = (size_t)L.R;
   for (int l = 0; l < L.D; ++l) {
-    L.wbf[l] = take(2 * (size_t)L.W * L.Kp[l]);
+    L.wbf[l] = take(2 * R * (size_t)L.W * L.Kp[l]);
+    L.wb3[l] = L.x3 ? take(2 * R * (size_t)L.W * L.Kp[l]) : 0;
     kmax = L.Kp[l] > kmax ? L.Kp[l] : kmax;
   }
-  L.whbf = take(2 * (size_t)kOutCols * L.W);
+  L.whbf = take(2 * R * (size_t)kOutCols * L.W);
+  L.whb3 = L.x3 ? take(2 * R * (size_t)kOutCols * L.W) : 0;
   L.cat = take(2 * (size_t)M * L.catw);
-  for (int l = 0; l < L.D; ++l) L.h[l] = l == L.skip ? 0 : take(2 * (size_t)M * L.W);
+  for (int l = 0; l < L.D; ++l) L.h[l] = l == L.skip ? 0 : take(2 * R * (size_t)M * L.W);
   L.out = take(4 * (size_t)M * kOutCols);
-  L.dout_bf = take(2 * (size_t)M * kOutCols);
+  L.dout_bf = take(2 * R * (size_t)M * kOutCols);
   L.dout_f = take(4 * (size_t)M * kOutCols);
-  L.dz[0] = take(2 * (size_t)M * L.W);
-  L.dz[1] = take(2 * (size_t)M * L.W);
+  L.dz[0] = take(2 * R * (size_t)M * L.W);
+  L.dz[1] = take(2 * R * (size_t)M * L.W);
   L.dws = take(4 * (size_t)L.W * kmax);
   L.wpart = L.bpart = 0;
-  if (L.W == 256) {
+  if (L.W == 256 && !L.x3) {
     L.wpart = take(4 * (size_t)kMlpBwdMaxGroups * 256 * 256);
     L.bpart = take(4 * (size_t)kMlpBwdMaxGroups * 4 * 256);
   }
@@ -110,10 +120,67 @@ __global__ void k_mlp_weights_all(const float* theta, int E, int E8, const __gri
   }
 }
 
+// x3 (split-bf16, R38): weight w -> hi = bf16(w), lo = bf16(w - hi).
+// Forward layout [rows, 3 Kp]: per input segment (the encoding and, after the
+// skip, the hidden part) three blocks [hi | lo | hi] against activations
+// [hi | hi | lo]; backward layout [3 rows, Kp] = [W_hi; W_lo; W_hi] (the dL/dIn
+// GEMM reduces over the output rows against dL/dz = [hi | hi | lo]).
+struct WeightJobsX3 {
+  int n;
+  struct Job {
+    int64_t thW;
+    int rows, rows_valid, Kp, K;
+    bool has_cat;
+    __nv_bfloat16 *dst, *dstb;
+  } j[kMlpMaxDepth + 1];
+};
+__device__ __forceinline__ float mlp_wsrc(const float* theta, const WeightJobsX3::Job& jb, int E,
+                                          int E8, int j, int c) {
+  if (j >= jb.rows_valid) return 0.f;
+  int src;
+  if (!jb.has_cat) src = c < jb.K ? c : -1;
+  else src = c < E ? c : (c < E8 ? -1 : c - E8 + E);
+  return src >= 0 ? theta[jb.thW + (int64_t)j * jb.K + src] : 0.f;
+}
+__device__ __forceinline__ __nv_bfloat16 split_part(float v, int b) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  return b == 1 ? __float2bfloat16_rn(v - __bfloat162float(hi)) : hi;
+}
+__global__ void k_mlp_weights_x3(const float* theta, int E, int E8,
+                                 const __grid_constant__ WeightJobsX3 w) {
+  const WeightJobsX3::Job& jb = w.j[blockIdx.y];
+  const int Kp3 = 3 * jb.Kp;
+  const int64_t n = (int64_t)jb.rows * Kp3;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    // forward layout: row j, column cc of [rows, 3 Kp]
+    {
+      const int j = (int)(idx / Kp3), cc = (int)(idx - (int64_t)j * Kp3);
+      int b, c;
+      if (!jb.has_cat) {
+        b = cc / jb.Kp; c = cc - b * jb.Kp;
+      } else if (cc < 3 * E8) {
+        b = cc / E8; c = cc - b * E8;
+      } else {
+        const int r = cc - 3 * E8, Wd = jb.Kp - E8;
+        b = r / Wd; c = E8 + (r - b * Wd);
+      }
+      jb.dst[idx] = split_part(mlp_wsrc(theta, jb, E, E8, j, c), b);
+    }
+    // backward layout: row rr of [3 rows, Kp], column c
+    {
+      const int rr = (int)(idx / jb.Kp), c = (int)(idx - (int64_t)rr * jb.Kp);
+      const int b = rr / jb.rows, j = rr - b * jb.rows;
+      jb.dstb[idx] = split_part(mlp_wsrc(theta, jb, E, E8, j, c), b);
+    }
+  }
+}
+
 struct EmbedArgs {
   const float* mean;
   int64_t N, row0, rows;
   int32_t f0, Lx, Lt, E8, catw;
+  int32_t x3;  // write [hi | hi | lo] blocks of E8 columns (the encoding's lo part)
   float t[kMlpMaxFrames];
   __nv_bfloat16* cat;
 };
@@ -165,6 +232,33 @@ __global__ void __launch_bounds__(128) k_mlp_embed(const __grid_constant__ Embed
 #pragma unroll
   for (int v = 0; v < kE8 / 8; ++v)
     if (v < e8 / 8) row[v] = src[v];
+  if (a.x3) {  // second hi block, then lo = bf16(value - hi) recomputed in fp32
+    uint4* row2 = reinterpret_cast<uint4*>(a.cat + m * a.catw + e8);
+#pragma unroll
+    for (int v = 0; v < kE8 / 8; ++v)
+      if (v < e8 / 8) row2[v] = src[v];
+    c = 0;
+    for (int d = 0; d < 3; ++d) { buf[c] = __float2bfloat16_rn(x[d] - __bfloat162float(buf[c])); ++c; }
+    for (int k = 0; k < lx; ++k) {
+      const float sc = (float)(1 << k);
+      float sn[3], cs[3];
+      for (int d = 0; d < 3; ++d) sincosf(sc * x[d], &sn[d], &cs[d]);
+      for (int d = 0; d < 3; ++d) { buf[c] = __float2bfloat16_rn(sn[d] - __bfloat162float(buf[c])); ++c; }
+      for (int d = 0; d < 3; ++d) { buf[c] = __float2bfloat16_rn(cs[d] - __bfloat162float(buf[c])); ++c; }
+    }
+    buf[c] = __float2bfloat16_rn(t - __bfloat162float(buf[c]));
+    ++c;
+    for (int k = 0; k < lt; ++k) {
+      float sn, cs;
+      sincosf((float)(1 << k) * t, &sn, &cs);
+      buf[c] = __float2bfloat16_rn(sn - __bfloat162float(buf[c])); ++c;
+      buf[c] = __float2bfloat16_rn(cs - __bfloat162float(buf[c])); ++c;
+    }
+    uint4* row3 = reinterpret_cast<uint4*>(a.cat + m * a.catw + 2 * e8);
+#pragma unroll
+    for (int v = 0; v < kE8 / 8; ++v)
+      if (v < e8 / 8) row3[v] = src[v];
+  }
 }
 
 struct ApplyArgs {
@@ -200,7 +294,7 @@ __global__ void __launch_bounds__(128) k_mlp_apply(const __grid_constant__ Apply
 // dL/dout = (g_mu_t, g_q_t, g_s_t * s_t, g_f_t) (s_t = s exp(ds)), bf16 + fp32.
 __global__ void __launch_bounds__(128) k_mlp_dout(int64_t N, int64_t M, const float* out,
                                                   const float* scale, wipes_grads g,
-                                                  __nv_bfloat16* dbf, float* df) {
+                                                  __nv_bfloat16* dbf, float* df, int x3) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   const int64_t i = m % N;
@@ -220,9 +314,23 @@ __global__ void __launch_bounds__(128) k_mlp_dout(int64_t N, int64_t M, const fl
     const __nv_bfloat162 pr = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
     w[h] = *reinterpret_cast<const uint32_t*>(&pr);
   }
-  uint4* db = reinterpret_cast<uint4*>(dbf + m * kOutCols);
-  db[0] = u[0];
-  db[1] = u[1];
+  if (x3) {  // [hi | hi | lo] rows of 3 x 16 (R38)
+    uint4 l[2];
+    uint32_t* wl = reinterpret_cast<uint32_t*>(l);
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&w[h]);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(v[2 * h] - __low2float(hi),
+                                                      v[2 * h + 1] - __high2float(hi));
+      wl[h] = *reinterpret_cast<const uint32_t*>(&lo);
+    }
+    uint4* db = reinterpret_cast<uint4*>(dbf + m * 3 * kOutCols);
+    db[0] = u[0]; db[1] = u[1]; db[2] = u[0]; db[3] = u[1]; db[4] = l[0]; db[5] = l[1];
+  } else {
+    uint4* db = reinterpret_cast<uint4*>(dbf + m * kOutCols);
+    db[0] = u[0];
+    db[1] = u[1];
+  }
   float4* d4 = reinterpret_cast<float4*>(df + m * kOutCols);
 #pragma unroll
   for (int q = 0; q < 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -356,9 +464,10 @@ bool mlp_unfused_env() {
 cudaError_t gemm(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                  int64_t lda, int64_t ldb, int64_t ldc, int epi, bool amn, bool bmn,
                  const float* bias, const void* mask, int64_t ldm, int split, cudaStream_t s,
-                 float* colsum = nullptr) {
+                 float* colsum = nullptr, int64_t split3 = 0) {
   wipes_gemm_args g;
   g.colsum = colsum;
+  g.split3 = split3;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.mask = mask;
   g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.ldm = ldm;
   g.a_mn_major = amn; g.b_mn_major = bmn; g.epilogue = epi; g.split_k = split;
@@ -366,6 +475,188 @@ cudaError_t gemm(const void* A, const void* B, void* C, int64_t M, int64_t N, in
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// x3 (WIPES_MLP_BF16X3, R38): the same network with every operand a
+// split-bf16 pair. Activation buffers hold [hi | hi | lo] column blocks (the
+// GEMM epilogue writes them, split3 = width), weights [hi | lo | hi] per input
+// segment, so each layer is ONE bf16 GEMM over K' = 3K forming
+// hi.hi + hi.lo + lo.hi (the lo.lo term, ~2^-18 relative, is dropped) with fp32
+// accumulation. The layer-by-layer generic GEMM only (the fused bf16 kernels of
+// mlp_fused.cu keep single-bf16 layouts).
+// ---------------------------------------------------------------------------
+cudaError_t mlp_forward_x3(const MlpLayout& L, const float* theta, int64_t N, int32_t F,
+                           const float* times, const wipes_params& canon,
+                           const wipes_params& frame, int32_t sh_coeffs, char* ws,
+                           cudaStream_t s) {
+  const int64_t M = L.M;
+  {
+    WeightJobsX3 wj;
+    wj.n = L.D + 1;
+    for (int l = 0; l <= L.D; ++l) {
+      WeightJobsX3::Job& jb = wj.j[l];
+      if (l < L.D) {
+        jb.thW = L.thW[l]; jb.rows = L.W; jb.rows_valid = L.W; jb.Kp = L.Kp[l]; jb.K = L.K[l];
+        jb.has_cat = l == L.skip + 1;
+        jb.dst = (__nv_bfloat16*)(ws + L.wbf[l]); jb.dstb = (__nv_bfloat16*)(ws + L.wb3[l]);
+      } else {
+        jb.thW = L.thWh; jb.rows = kOutCols; jb.rows_valid = 13; jb.Kp = L.W; jb.K = L.W;
+        jb.has_cat = false;
+        jb.dst = (__nv_bfloat16*)(ws + L.whbf); jb.dstb = (__nv_bfloat16*)(ws + L.whb3);
+      }
+    }
+    launch_begin(K_MLP_MISC, s);
+    k_mlp_weights_x3<<<dim3(64, wj.n), 256, 0, s>>>(theta, L.E, L.E8, wj);
+    launch_end(K_MLP_MISC, s);
+  }
+  __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
+  const int64_t E3 = 3 * (int64_t)L.E8, W3 = 3 * (int64_t)L.W;
+  static thread_local EmbedArgs ea;
+  for (int f0 = 0; f0 < F; f0 += kMlpMaxFrames) {
+    const int nf = F - f0 < kMlpMaxFrames ? F - f0 : kMlpMaxFrames;
+    ea.mean = canon.mean; ea.N = N; ea.row0 = (int64_t)f0 * N; ea.rows = (int64_t)nf * N;
+    ea.f0 = f0; ea.Lx = L.Lx; ea.Lt = L.Lt; ea.E8 = L.E8; ea.catw = L.catw; ea.cat = cat;
+    ea.x3 = 1;
+    for (int k = 0; k < nf; ++k) ea.t[k] = times[f0 + k];
+    launch_begin(K_MLP_MISC, s);
+    if (L.Lx == 10 && L.Lt == 6)
+      k_mlp_embed<10, 6><<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
+    else
+      k_mlp_embed<0, 0><<<nblk(ea.rows, 128), 128, 0, s>>>(ea);
+    launch_end(K_MLP_MISC, s);
+  }
+  cudaError_t e = cudaSuccess;
+  for (int l = 0; l < L.D && e == cudaSuccess; ++l) {
+    const void* in;
+    int64_t ldin, K3;
+    if (l == 0) { in = cat; ldin = L.catw; K3 = E3; }
+    else if (l == L.skip + 1) { in = cat; ldin = L.catw; K3 = L.catw; }
+    else if (l - 1 == L.skip) { in = cat + E3; ldin = L.catw; K3 = W3; }
+    else { in = ws + L.h[l - 1]; ldin = W3; K3 = W3; }
+    void* outp = l == L.skip ? (void*)(cat + E3) : (void*)(ws + L.h[l]);
+    const int64_t ldo = l == L.skip ? L.catw : W3;
+    e = gemm(in, ws + L.wbf[l], outp, M, L.W, K3, ldin, 3 * (int64_t)L.Kp[l], ldo,
+             WIPES_GEMM_EPI_BIAS_RELU_BF16, false, false, theta + L.thb[l], nullptr, 0, 1, s,
+             nullptr, L.W);
+  }
+  if (e != cudaSuccess) return e;
+  const int last = L.D - 1;
+  const void* hl = last == L.skip ? (const void*)(cat + E3) : (const void*)(ws + L.h[last]);
+  const int64_t ldh = last == L.skip ? L.catw : W3;
+  e = gemm(hl, ws + L.whbf, ws + L.out, M, 13, W3, ldh, W3, kOutCols, WIPES_GEMM_EPI_BIAS_F32,
+           false, false, theta + L.thbh, nullptr, 0, 1, s);
+  if (e != cudaSuccess) return e;
+  ApplyArgs aa;
+  aa.N = N; aa.M = M; aa.out = (const float*)(ws + L.out); aa.canon = canon; aa.frame = frame;
+  aa.sh_coeffs = sh_coeffs;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_apply<<<nblk(M, 128), 128, 0, s>>>(aa);
+  launch_end(K_MLP_MISC, s);
+  return cudaGetLastError();
+}
+
+// dW (rows x cols, fp32, += into C with leading dimension ldc) = dz^T in over
+// the M rows, split-bf16: dz_hi.in_hi + dz_hi.in_lo + dz_lo.in_hi (three
+// accumulating GEMMs; dz and in are [hi | hi | lo] blocks of width dzw / inw).
+cudaError_t mlp_dw_x3(const __nv_bfloat16* dz, int64_t dzw, const __nv_bfloat16* in, int64_t ldin,
+                      int64_t inw, int64_t cols, int64_t rows, int64_t M, float* C, int64_t ldc,
+                      int split, cudaStream_t s) {
+  const int64_t ldz = 3 * dzw;
+  const __nv_bfloat16* a[3] = {dz, dz, dz + 2 * dzw};
+  const __nv_bfloat16* b[3] = {in, in + 2 * inw, in};
+  for (int t = 0; t < 3; ++t) {
+    cudaError_t e = gemm(a[t], b[t], C, rows, cols, M, ldz, ldin, ldc, WIPES_GEMM_EPI_ATOMIC_F32,
+                         true, true, nullptr, nullptr, 0, split, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t mlp_backward_x3(const MlpLayout& L, const float* theta, int64_t N, int32_t F,
+                            const wipes_params& canon, const wipes_grads& gfr, float* g_theta,
+                            const wipes_grads& gcan, char* ws, cudaStream_t s) {
+  const int64_t M = L.M;
+  cudaError_t e = cudaMemsetAsync(g_theta, 0, sizeof(float) * L.P, s);
+  if (e != cudaSuccess || M == 0) return e;
+  __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
+  const float* out = (const float*)(ws + L.out);
+  __nv_bfloat16* dbf = (__nv_bfloat16*)(ws + L.dout_bf);
+  float* dfp = (float*)(ws + L.dout_f);
+  const int64_t E3 = 3 * (int64_t)L.E8, W3 = 3 * (int64_t)L.W;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_dout<<<nblk(M, 128), 128, 0, s>>>(N, M, out, canon.scale, gfr, dbf, dfp, 1);
+  launch_end(K_MLP_MISC, s);
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_canon<<<nblk(N, 128), 128, 0, s>>>(N, F, out, gfr, gcan);
+  launch_end(K_MLP_MISC, s);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto split_for = [&](int64_t tiles) {
+    int64_t sp = (2 * sms + tiles - 1) / tiles;
+    const int64_t chunks = (M + 63) / 64;
+    return (int)(sp < 1 ? 1 : (sp > chunks ? chunks : sp));
+  };
+  const int last = L.D - 1;
+  const __nv_bfloat16* hl = last == L.skip ? cat + E3 : (const __nv_bfloat16*)(ws + L.h[last]);
+  const int64_t ldh = last == L.skip ? L.catw : W3;
+  float* dws = (float*)(ws + L.dws);
+  // head: dWh = dout^T h_last (13 x W), dbh = colsum(dout), dh_last = dout Wh
+  e = cudaMemsetAsync(dws, 0, sizeof(float) * 13 * L.W, s);
+  if (e != cudaSuccess) return e;
+  e = mlp_dw_x3(dbf, kOutCols, hl, ldh, L.W, L.W, 13, M, dws, L.W,
+                split_for((L.W + 255) / 256), s);
+  if (e != cudaSuccess) return e;
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_unpad<<<nblk(13 * (int64_t)L.W, 256), 256, 0, s>>>(dws, 13, L.W, L.E, L.E8, L.W, false,
+                                                           g_theta + L.thWh);
+  launch_end(K_MLP_MISC, s);
+  launch_begin(K_MLP_MISC, s);
+  k_mlp_dout_colsum<<<2 * sms, 256, 0, s>>>(dfp, M, g_theta + L.thbh);
+  launch_end(K_MLP_MISC, s);
+  __nv_bfloat16* dz = (__nv_bfloat16*)(ws + L.dz[0]);
+  __nv_bfloat16* dz2 = (__nv_bfloat16*)(ws + L.dz[1]);
+  e = gemm(dbf, ws + L.whb3, dz, M, L.W, 3 * kOutCols, 3 * kOutCols, L.W, W3,
+           WIPES_GEMM_EPI_MASK_BF16, false, true, nullptr, hl, ldh, 1, s, g_theta + L.thb[last],
+           L.W);
+  if (e != cudaSuccess) return e;
+  for (int l = last; l >= 0; --l) {
+    e = cudaMemsetAsync(dws, 0, sizeof(float) * (size_t)L.W * L.Kp[l], s);
+    if (e != cudaSuccess) return e;
+    const bool has_cat = l == L.skip + 1;
+    if (l == 0 || has_cat) {  // the encoding segment: dws columns [0, E8)
+      e = mlp_dw_x3(dz, L.W, cat, L.catw, L.E8, L.E8, L.W, M, dws, L.Kp[l],
+                    split_for((L.W + 127) / 128), s);
+      if (e != cudaSuccess) return e;
+    }
+    if (l > 0) {  // the hidden segment
+      const __nv_bfloat16* hin = (l - 1 == L.skip) ? cat + E3
+                                                   : (const __nv_bfloat16*)(ws + L.h[l - 1]);
+      const int64_t ldin = (l - 1 == L.skip) ? L.catw : W3;
+      e = mlp_dw_x3(dz, L.W, hin, ldin, L.W, L.W, L.W, M, dws + (has_cat ? L.E8 : 0), L.Kp[l],
+                    split_for(((L.W + 127) / 128) * ((L.W + 255) / 256)), s);
+      if (e != cudaSuccess) return e;
+    }
+    launch_begin(K_MLP_MISC, s);
+    k_mlp_unpad<<<nblk((int64_t)L.W * L.K[l], 256), 256, 0, s>>>(
+        dws, L.W, L.Kp[l], L.E, L.E8, L.K[l], has_cat, g_theta + L.thW[l]);
+    launch_end(K_MLP_MISC, s);
+    if (l == 0) break;
+    // dz_(l-1) = (dz W_l)[:, hidden part] * (h_(l-1) > 0), split; its column sums
+    // are the bias gradient of layer l-1
+    const __nv_bfloat16* wl = (const __nv_bfloat16*)(ws + L.wb3[l]) + (has_cat ? L.E8 : 0);
+    const void* mask = (l - 1 == L.skip) ? (const void*)(cat + E3) : (const void*)(ws + L.h[l - 1]);
+    const int64_t ldm = (l - 1 == L.skip) ? L.catw : W3;
+    e = gemm(dz, wl, dz2, M, L.W, W3, W3, L.Kp[l], W3, WIPES_GEMM_EPI_MASK_BF16, false, true,
+             nullptr, mask, ldm, 1, s, g_theta + L.thb[l - 1], L.W);
+    if (e != cudaSuccess) return e;
+    __nv_bfloat16* t = dz; dz = dz2; dz2 = t;
+  }
+  return cudaGetLastError();
+}
 
 bool mlp_config_valid(const wipes_mlp_config& c) { return mlp_cfg_ok(c); }
 int64_t mlp_param_count(const wipes_mlp_config& c) { return mlp_layout(c, 0).P; }
@@ -380,6 +671,7 @@ cudaError_t launch_mlp_forward(const wipes_mlp_config& c, const float* theta, in
   const int64_t M = N * (int64_t)F;
   const MlpLayout L = mlp_layout(c, M);
   if (M == 0) return cudaSuccess;
+  if (L.x3) return mlp_forward_x3(L, theta, N, F, times, canon, frame, sh_coeffs, ws, s);
   // bf16 weights (rounded to nearest even)
   {
     WeightJobs wj;
@@ -485,6 +777,7 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
                                 cudaStream_t s) {
   const int64_t M = N * (int64_t)F;
   const MlpLayout L = mlp_layout(c, M);
+  if (L.x3) return mlp_backward_x3(L, theta, N, F, canon, gfr, g_theta, gcan, ws, s);
   cudaError_t e = cudaMemsetAsync(g_theta, 0, sizeof(float) * L.P, s);
   if (e != cudaSuccess || M == 0) return e;
   __nv_bfloat16* cat = (__nv_bfloat16*)(ws + L.cat);
@@ -492,7 +785,7 @@ cudaError_t launch_mlp_backward(const wipes_mlp_config& c, const float* theta, i
   __nv_bfloat16* dbf = (__nv_bfloat16*)(ws + L.dout_bf);
   float* dfp = (float*)(ws + L.dout_f);
   launch_begin(K_MLP_MISC, s);
-  k_mlp_dout<<<nblk(M, 128), 128, 0, s>>>(N, M, out, canon.scale, gfr, dbf, dfp);
+  k_mlp_dout<<<nblk(M, 128), 128, 0, s>>>(N, M, out, canon.scale, gfr, dbf, dfp, L.x3 ? 1 : 0);
   launch_end(K_MLP_MISC, s);
   launch_begin(K_MLP_MISC, s);
   k_mlp_canon<<<nblk(N, 128), 128, 0, s>>>(N, F, out, gfr, gcan);

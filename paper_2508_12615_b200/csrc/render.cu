@@ -101,6 +101,12 @@ __device__ __forceinline__ float rcp_a(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Fire-and-forget float add (RED, no return): atomicAdd here compiled to an
+// ATOMG whose completion the loop then waited on (long-scoreboard stall at the
+// next record's branch: 16% of the C2 backward's stall samples).
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 __device__ __forceinline__ float4 ldg_nc(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -187,28 +193,46 @@ __device__ __forceinline__ bool hits_footprint(const float4& r0, const float4& r
   return cx + rx >= 0.5f && cx - rx <= 7.5f && cy + ry >= 0.5f && cy - ry <= h - 0.5f;
 }
 
-// Exponents of alpha*G for a lane's pixel pair (rows y0 and y0 + 4) — one
-// arithmetic shared by every kernel, so all take the same alpha_min decisions
-// (and, since 8x8 blocks are 8-aligned for every tile size, every pixel is
-// evaluated by the same expression whatever the tiling).
-struct PairPos {
-  float dy0, e0, e1;
+// Exponents of alpha*G for a lane's pixel pair (rows y and y + 4, same column)
+// — one arithmetic shared by every kernel (forward, backward, stats), so all
+// take the same alpha_min decisions (the ALPHA backward's transmittance
+// recovery relies on it); and since 8x8 blocks are 8-aligned for every tile
+// size, every pixel is evaluated by the same expression whatever the tiling.
+// Packed: (dx, dy) = (px - r0.x - r0.z, py - r0.y - r0.w) in one FADD2 pair, the
+// pair's dy = (dy, dy + 4), e = (A dx + B dy) dx + (C dy dy + log2 alpha)
+// elementwise in FFMA2/FMUL2.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+struct PairE {
+  float dx;
+  float2 dy, e;
 };
 
-__device__ __forceinline__ float pair_dx(const float4& r0, float px) {
-  return __fsub_rn(__fsub_rn(px, r0.x), r0.z);
+__device__ __forceinline__ float2 pair_e2(const float4& r1, float dx, float2 dy) {
+  const float2 t = __ffma2_rn(f2(r1.x), f2(dx), __fmul2_rn(f2(r1.y), dy));  // A dx + B dy
+  const float2 cdy = __fmul2_rn(f2(r1.z), dy);                             // C dy
+  return __ffma2_rn(t, f2(dx), __ffma2_rn(cdy, dy, f2(r1.w)));
 }
 
-__device__ __forceinline__ PairPos pair_exponents(const float4& r0, const float4& r1, float dx,
-                                                  float py0) {
-  PairPos p;
-  p.dy0 = __fsub_rn(__fsub_rn(py0, r0.y), r0.w);
-  const float t = __fmaf_rn(r1.x, dx, __fmul_rn(r1.y, p.dy0));  // A dx + B dy
-  const float cdy = __fmul_rn(r1.z, p.dy0);                      // C dy
-  p.e0 = __fmaf_rn(t, dx, __fmaf_rn(cdy, p.dy0, r1.w));
-  // dy1 = dy0 + 4: e1 = e0 + 4 (B dx + 2 C dy0 + 4 C)
-  const float v = __fmaf_rn(r1.y, dx, __fmaf_rn(2.f, cdy, __fmul_rn(4.f, r1.z)));
-  p.e1 = __fmaf_rn(4.f, v, p.e0);
+__device__ __forceinline__ PairE pair_exp(const float4& r0, const float4& r1, float px, float py) {
+  const float2 d = __fadd2_rn(__fadd2_rn(make_float2(px, py), make_float2(-r0.x, -r0.y)),
+                              make_float2(-r0.z, -r0.w));
+  PairE p;
+  p.dx = d.x;
+  p.dy = make_float2(d.y, __fadd_rn(d.y, 4.f));
+  p.e = pair_e2(r1, p.dx, p.dy);
+  return p;
+}
+
+// The same for a further pair of rows of the lane (py' = py + 8k) given dx:
+// dy' = (py' - r0.y) - r0.w, elementwise the expression pair_exp evaluates.
+__device__ __forceinline__ PairE pair_exp_dx(const float4& r0, const float4& r1, float dx,
+                                             float py) {
+  PairE p;
+  p.dx = dx;
+  const float dy = __fadd_rn(__fadd_rn(py, -r0.y), -r0.w);
+  p.dy = make_float2(dy, __fadd_rn(dy, 4.f));
+  p.e = pair_e2(r1, dx, p.dy);
   return p;
 }
 
@@ -220,14 +244,17 @@ __device__ __forceinline__ float pair_weight(float ag, float cs, const float4& r
   return __fmul_rn(ag, __fmaf_rn(r2.w, cs, 0.5f));
 }
 
-__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
-
 // Warp-private staging area: the compacted hits of the current 32-record chunk.
 struct WarpSmem {
   float4 rec[4][32];
   int32_t pid[32];
   int32_t pos[32];
   int32_t dj[32];  // deterministic mode: dup index of the staged record
+};
+
+// Backward: the staging area plus the warp's moment-reduction buffer.
+struct WarpSmemB : WarpSmem {
+  float4 red4[12 * 32 / 4];  // [moment][lane] (16-byte aligned for LDS.128)
 };
 
 // One work item of a warp.
@@ -240,11 +267,28 @@ struct Item {
   int sub;         // footprint index within the tile
 };
 
+// Work items: lane 0 claims the next index from the queue. With
+// WIPES_ITEM_PREFETCH the claim runs one item ahead (`pf` holds the index for
+// the NEXT item, so the atomic's round trip overlaps the current item); on small
+// frames (C2 forward: 1.3 items per warp) claiming ahead unbalances the warps
+// (fwd 60 -> 76 us), so it is off by default. A claimed index >= the item
+// count is dropped (nothing behind it).
+#ifndef WIPES_ITEM_PREFETCH
+#define WIPES_ITEM_PREFETCH 0  // claim items one ahead (A/B knob; see next_item)
+#endif
 template <int TS, int GG = (TS >= 16 ? 2 : 1)>
-__device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chunks, Item& it) {
+__device__ __forceinline__ bool next_item(const RenderArgs& a, int lane, int chunks, Item& it,
+                                          int& pf) {
   using Gm = Geo<TS, GG>;
   int item = 0;
-  if (lane == 0) item = atomicAdd(&a.hdr->work[a.queue], 1);
+  if (lane == 0) {
+    if (WIPES_ITEM_PREFETCH) {
+      item = pf;
+      pf = atomicAdd(&a.hdr->work[a.queue], 1);
+    } else {
+      item = atomicAdd(&a.hdr->work[a.queue], 1);
+    }
+  }
   item = __shfl_sync(kFull, item, 0);
   if ((int64_t)item >= a.BT * Gm::S * chunks) return false;
   const int chunk = item % chunks;
@@ -359,7 +403,8 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
   // ALPHA likewise: the pair's transmittances and colour sums packed; the
   // per-pixel decisions (skip, clamp, stop) stay scalar
   constexpr bool PACKA = ALPHA && !STATS && P == 2 && WIPES_FWD_PACK;
-  while (next_item<TS, GF>(a, lane, 1, it)) {
+  int pf = (WIPES_ITEM_PREFETCH && lane == 0) ? atomicAdd(&a.hdr->work[a.queue], 1) : 0;
+  while (next_item<TS, GF>(a, lane, 1, it, pf)) {
     bool in[P], done[P];
     float C[P][3], T[P];
     float2 Cp[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -391,15 +436,16 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
 #pragma unroll kFwdUnroll
       for (int i = 0; i < cnt; ++i) {
         const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
-        const float dx = pair_dx(r0, px);
         float e[P], dy[P];
         bool h[P];
         uint32_t any = 0, bm[P];
+        const PairE p0 = pair_exp(r0, r1, px, py0);
+        const float dx = p0.dx;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * g);
-          e[2 * g] = pp.e0; e[2 * g + 1] = pp.e1;
-          dy[2 * g] = pp.dy0; dy[2 * g + 1] = pp.dy0 + 4.f;
+          const PairE pp = g == 0 ? p0 : pair_exp_dx(r0, r1, dx, py0 + 8.f * g);
+          e[2 * g] = pp.e.x; e[2 * g + 1] = pp.e.y;
+          dy[2 * g] = pp.dy.x; dy[2 * g + 1] = pp.dy.y;
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -566,6 +612,32 @@ __device__ __forceinline__ mom_t transpose_reduce12(mom_t (&v)[kMom], int lane) 
     v[0] = k + __shfl_xor_sync(kFull, s, 2);
   }
   return v[0] + __shfl_xor_sync(kFull, v[0], 1);
+}
+
+#ifndef WIPES_SMEM_REDUCE
+#define WIPES_SMEM_REDUCE 0  // A/B knob: measured slower (C2 bwd 0.126 vs 0.114 ms, C5 3.07 vs 2.55)
+#endif
+// 12-moment warp reduction through the warp's shared buffer: every lane stores
+// its 12 partial moments moment-major (12 conflict-free STS), then lane 2k + h
+// (k < 12) sums the 16 values of moment k from lanes 16h..16h + 15 (four
+// LDS.128, fixed order) and the pair combines with one shuffle: lane 2k holds
+// moment k. ~35 instructions instead of the transpose-reduce's ~60 (13 SHFL,
+// 24 FSEL, 13 FADD); deterministic order.
+__device__ __forceinline__ float smem_reduce12(const float (&v)[kMom], float4* buf4, int lane) {
+  float* buf = reinterpret_cast<float*>(buf4);
+#pragma unroll
+  for (int k = 0; k < kMom; ++k) buf[k * 32 + lane] = v[k];
+  __syncwarp();
+  float s = 0.f;
+  if (lane < 2 * kMom) {
+    const float4* q = buf4 + (lane >> 1) * 8 + (lane & 1) * 4;
+    const float4 a = q[0], b = q[1], c = q[2], d = q[3];
+    s = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+        (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+  }
+  s += __shfl_xor_sync(kFull, s, 1);
+  __syncwarp();  // the buffer is rewritten by the next record
+  return s;
 }
 
 // Moments of one pair, gw = dL/dw and w already zeroed when the
@@ -736,14 +808,17 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
   constexpr bool PACKB = !F64 && WIPES_BWD_PACK;
-  __shared__ WarpSmem sm_all[kWarpsPerCta];
+  __shared__ WarpSmemB sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  WarpSmem& ws = sm_all[wid];
+  WarpSmemB& ws = sm_all[wid];
+  // which moment this lane holds after the warp reduction (and writes out)
+  constexpr bool SMRED = !F64 && WIPES_SMEM_REDUCE;
   const int q3 = (lane >> 1) & 3;
-  const int my_m = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
-  const bool writer = !(lane & 1) && q3 < 3;
+  const int my_m = SMRED ? (lane >> 1) : 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
+  const bool writer = SMRED ? (!(lane & 1) && lane < 2 * kMom) : (!(lane & 1) && q3 < 3);
   Item it;
-  while (next_item<TS>(a, lane, ALPHA ? 1 : a.chunks, it)) {
+  int pf = (WIPES_ITEM_PREFETCH && lane == 0) ? atomicAdd(&a.hdr->work[a.queue], 1) : 0;
+  while (next_item<TS>(a, lane, ALPHA ? 1 : a.chunks, it, pf)) {
     const int64_t HW = (int64_t)a.H * a.W;
     const float* gp = a.dLdC + it.v * 3 * HW;
     bool in[P];
@@ -801,15 +876,16 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         const int i = ALPHA ? cnt - 1 - ii : ii;
         const int pos = ws.pos[i];  // index within the tile list
         const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
-        const float dx = pair_dx(r0, px);
         float e[P], dy[P];
         bool h[P];
         uint32_t any_h = 0, bm[P];
+        const PairE p0 = pair_exp(r0, r1, px, py0);
+        const float dx = p0.dx;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * gg);
-          e[2 * gg] = pp.e0; e[2 * gg + 1] = pp.e1;
-          dy[2 * gg] = pp.dy0; dy[2 * gg + 1] = pp.dy0 + 4.f;
+          const PairE pp = gg == 0 ? p0 : pair_exp_dx(r0, r1, dx, py0 + 8.f * gg);
+          e[2 * gg] = pp.e.x; e[2 * gg + 1] = pp.e.y;
+          dy[2 * gg] = pp.dy.x; dy[2 * gg + 1] = pp.dy.y;
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -866,7 +942,12 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         BCNT(3, 1);
         MT mr[kMom];
         finish_moments<F64>(mr, m, mc, dx);
-        const float red = (float)transpose_reduce12(mr, lane);
+        float red;
+        if constexpr (SMRED) {
+          red = smem_reduce12(mr, ws.red4, lane);
+        } else {
+          red = (float)transpose_reduce12(mr, lane);
+        }
         if (EXACT) {
 #pragma unroll
           for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
@@ -878,8 +959,8 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
           if (EXACT && lane == 0) sl[kMom] = mb;
           if (lane == 0) a.slotmask[si] = 1;
         } else {
-          if (writer) atomicAdd(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
-          if (EXACT && lane == 0) atomicAdd(a.mom_beta + vN + ws.pid[i], mb);
+          if (writer) red_add(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
+          if (EXACT && lane == 0) red_add(a.mom_beta + vN + ws.pid[i], mb);
         }
       }
       __syncwarp();

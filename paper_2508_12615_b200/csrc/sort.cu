@@ -169,19 +169,25 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   __syncthreads();
   volatile uint32_t* st = a.status;
   st[(int64_t)tile * 256 + tid] = kFlagAgg | sm.thist[tid];
+  // only the last tile has invalid slots (digit 256): full tiles match 8 bits
+  const bool full_tile = base + kSortTile <= n;
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = dig[i];
 #ifdef WIPES_SORT_MATCH
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
 #else
-    // lanes with the same digit: AND over the 9 digit bits (bit 8 marks an
+    // lanes with the same digit: AND over the digit bits (bit 8 marks an
     // invalid slot) of the matching ballots — cheaper than MATCH.ANY
     uint32_t peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 9; ++b) {
+    for (int b = 0; b < 8; ++b) {
       const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
       peers &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+    if (!full_tile) {
+      const uint32_t bb = __ballot_sync(0xffffffffu, d >> 8);
+      peers &= (d >> 8) ? bb : ~bb;
     }
 #endif
     const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;

@@ -29,11 +29,15 @@ def _stream():
 
 class Deformation:
     def __init__(self, N: int, width: int = 256, depth: int = 8, skip: int = 4, Lx: int = 10,
-                 Lt: int = 6, device="cuda"):
+                 Lt: int = 6, device="cuda", precision: str = "bf16x3"):
+        """precision: "bf16x3" (default) carries every operand as a split-bf16
+        pair (~2^-16 relative, near the FP32 D-3DGS network, DESIGN.md R38);
+        "bf16" single bf16 operands (faster, R36)."""
         if not torch.cuda.is_available():
             raise RuntimeError("Deformation needs a CUDA device (no CPU fallback)")
         abi.lib()
-        self.cfg = abi.wipes_mlp_config(width, depth, skip, Lx, Lt)
+        self.precision = precision
+        self.cfg = abi.wipes_mlp_config(width, depth, skip, Lx, Lt, abi.MLP_PRECISION[precision])
         self.P = abi.wipes_mlp_param_count(self.cfg)
         if self.P == 0:
             raise abi.WipesError(abi.WIPES_EINVAL, "wipes_mlp_param_count",

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_strings(L):
-    assert L.wipes_abi_version() == 3
+    assert L.wipes_abi_version() == 4
     assert abi.status_name(abi.WIPES_EINVAL) == "WIPES_EINVAL"
     assert "render_fwd" in abi.kernel_names()
 
