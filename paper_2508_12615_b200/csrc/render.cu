@@ -193,46 +193,30 @@ __device__ __forceinline__ bool hits_footprint(const float4& r0, const float4& r
   return cx + rx >= 0.5f && cx - rx <= 7.5f && cy + ry >= 0.5f && cy - ry <= h - 0.5f;
 }
 
-// Exponents of alpha*G for a lane's pixel pair (rows y and y + 4, same column)
-// — one arithmetic shared by every kernel (forward, backward, stats), so all
-// take the same alpha_min decisions (the ALPHA backward's transmittance
-// recovery relies on it); and since 8x8 blocks are 8-aligned for every tile
-// size, every pixel is evaluated by the same expression whatever the tiling.
-// Packed: (dx, dy) = (px - r0.x - r0.z, py - r0.y - r0.w) in one FADD2 pair, the
-// pair's dy = (dy, dy + 4), e = (A dx + B dy) dx + (C dy dy + log2 alpha)
-// elementwise in FFMA2/FMUL2.
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
-struct PairE {
-  float dx;
-  float2 dy, e;
+// Exponents of alpha*G for a lane's pixel pair (rows y0 and y0 + 4) — one
+// arithmetic shared by every kernel, so all take the same alpha_min decisions
+// (and, since 8x8 blocks are 8-aligned for every tile size, every pixel is
+// evaluated by the same expression whatever the tiling).
+struct PairPos {
+  float dy0, e0, e1;
 };
 
-__device__ __forceinline__ float2 pair_e2(const float4& r1, float dx, float2 dy) {
-  const float2 t = __ffma2_rn(f2(r1.x), f2(dx), __fmul2_rn(f2(r1.y), dy));  // A dx + B dy
-  const float2 cdy = __fmul2_rn(f2(r1.z), dy);                             // C dy
-  return __ffma2_rn(t, f2(dx), __ffma2_rn(cdy, dy, f2(r1.w)));
+__device__ __forceinline__ float pair_dx(const float4& r0, float px) {
+  return __fsub_rn(__fsub_rn(px, r0.x), r0.z);
 }
 
-__device__ __forceinline__ PairE pair_exp(const float4& r0, const float4& r1, float px, float py) {
-  const float2 d = __fadd2_rn(__fadd2_rn(make_float2(px, py), make_float2(-r0.x, -r0.y)),
-                              make_float2(-r0.z, -r0.w));
-  PairE p;
-  p.dx = d.x;
-  p.dy = make_float2(d.y, __fadd_rn(d.y, 4.f));
-  p.e = pair_e2(r1, p.dx, p.dy);
-  return p;
-}
-
-// The same for a further pair of rows of the lane (py' = py + 8k) given dx:
-// dy' = (py' - r0.y) - r0.w, elementwise the expression pair_exp evaluates.
-__device__ __forceinline__ PairE pair_exp_dx(const float4& r0, const float4& r1, float dx,
-                                             float py) {
-  PairE p;
-  p.dx = dx;
-  const float dy = __fadd_rn(__fadd_rn(py, -r0.y), -r0.w);
-  p.dy = make_float2(dy, __fadd_rn(dy, 4.f));
-  p.e = pair_e2(r1, dx, p.dy);
+__device__ __forceinline__ PairPos pair_exponents(const float4& r0, const float4& r1, float dx,
+                                                  float py0) {
+  PairPos p;
+  p.dy0 = __fsub_rn(__fsub_rn(py0, r0.y), r0.w);
+  const float t = __fmaf_rn(r1.x, dx, __fmul_rn(r1.y, p.dy0));  // A dx + B dy
+  const float cdy = __fmul_rn(r1.z, p.dy0);                      // C dy
+  p.e0 = __fmaf_rn(t, dx, __fmaf_rn(cdy, p.dy0, r1.w));
+  // dy1 = dy0 + 4: e1 = e0 + 4 (B dx + 2 C dy0 + 4 C)
+  const float v = __fmaf_rn(r1.y, dx, __fmaf_rn(2.f, cdy, __fmul_rn(4.f, r1.z)));
+  p.e1 = __fmaf_rn(4.f, v, p.e0);
   return p;
 }
 
@@ -436,16 +420,15 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
 #pragma unroll kFwdUnroll
       for (int i = 0; i < cnt; ++i) {
         const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
+        const float dx = pair_dx(r0, px);
         float e[P], dy[P];
         bool h[P];
         uint32_t any = 0, bm[P];
-        const PairE p0 = pair_exp(r0, r1, px, py0);
-        const float dx = p0.dx;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const PairE pp = g == 0 ? p0 : pair_exp_dx(r0, r1, dx, py0 + 8.f * g);
-          e[2 * g] = pp.e.x; e[2 * g + 1] = pp.e.y;
-          dy[2 * g] = pp.dy.x; dy[2 * g + 1] = pp.dy.y;
+          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * g);
+          e[2 * g] = pp.e0; e[2 * g + 1] = pp.e1;
+          dy[2 * g] = pp.dy0; dy[2 * g + 1] = pp.dy0 + 4.f;
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -876,16 +859,15 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         const int i = ALPHA ? cnt - 1 - ii : ii;
         const int pos = ws.pos[i];  // index within the tile list
         const float4 r0 = ws.rec[0][i], r1 = ws.rec[1][i];
+        const float dx = pair_dx(r0, px);
         float e[P], dy[P];
         bool h[P];
         uint32_t any_h = 0, bm[P];
-        const PairE p0 = pair_exp(r0, r1, px, py0);
-        const float dx = p0.dx;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-          const PairE pp = gg == 0 ? p0 : pair_exp_dx(r0, r1, dx, py0 + 8.f * gg);
-          e[2 * gg] = pp.e.x; e[2 * gg + 1] = pp.e.y;
-          dy[2 * gg] = pp.dy.x; dy[2 * gg + 1] = pp.dy.y;
+          const PairPos pp = pair_exponents(r0, r1, dx, py0 + 8.f * gg);
+          e[2 * gg] = pp.e0; e[2 * gg + 1] = pp.e1;
+          dy[2 * gg] = pp.dy0; dy[2 * gg + 1] = pp.dy0 + 4.f;
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
