@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
     if (live && j < a.cap) {
       const int t = (int)(j - so);
       const int row = t / ow, col = t - row * ow;
+      WCHECK(t >= 0 && col >= 0 && col < ow && ox + col < a.GX);
       a.keys[j] = ovt + (uint32_t)(oty + row * dty) * (uint32_t)a.GX + (uint32_t)(ox + col);
       if (a.prevals) {
         a.vals[j] = (uint32_t)j;

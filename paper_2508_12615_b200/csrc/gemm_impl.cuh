@@ -250,7 +250,38 @@ __device__ __forceinline__ void epilogue_tile(const wipes_gemm_args& g, int cb0,
       // (out-of-range rows/columns are clipped by the tensor map bounds)
       if (lane == 0) bulk_wait_read();  // the previous block's store has read the buffer
       __syncwarp();
-      if (kBf16Out) {
+      if (kBf16Out && g.split3 > 0) {
+        // split-bf16 triple through TMA: hi staged at stg, lo at stg + 2 KB
+        uint4* row = reinterpret_cast<uint4*>(stg + lane * 64);
+        uint4* rowl = reinterpret_cast<uint4*>(stg + 2048 + lane * 64);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 uh, ul;
+          uint32_t* wh = reinterpret_cast<uint32_t*>(&uh);
+          uint32_t* wl = reinterpret_cast<uint32_t*>(&ul);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float a = v[8 * q + 2 * h], b = v[8 * q + 2 * h + 1];
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(a, b);
+            const __nv_bfloat162 lo =
+                __floats2bfloat162_rn(a - __low2float(hi), b - __high2float(hi));
+            wh[h] = *reinterpret_cast<const uint32_t*>(&hi);
+            wl[h] = *reinterpret_cast<const uint32_t*>(&lo);
+          }
+          row[q] = uh;
+          rowl[q] = ul;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int rr = (int)(m0 + 32 * ew);
+          tma_store_2d(tcmap, (int)n, rr, stg);
+          tma_store_2d(tcmap, (int)(n + g.split3), rr, stg);
+          tma_store_2d(tcmap, (int)(n + 2 * g.split3), rr, stg + 2048);
+          bulk_commit();
+        }
+        continue;
+      } else if (kBf16Out) {
         uint4* row = reinterpret_cast<uint4*>(stg + lane * 64);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -647,10 +678,13 @@ cudaError_t launch_ws(const wipes_gemm_args& g, cudaStream_t s) {
   std::memset(&P.tc, 0, sizeof(P.tc));
   std::memset(&P.tm, 0, sizeof(P.tm));
   P.tmask = EPI == WIPES_GEMM_EPI_MASK_BF16 && make_out_tmap(&P.tm, g.mask, true, g.M, g.N, g.ldm);
-  P.tstore = EPI != WIPES_GEMM_EPI_ATOMIC_F32 && g.split3 == 0 &&
+  // split3: one map over the three blocks (3 split3 columns); only when the
+  // blocks are whole 32-column boxes (a partial box would spill into the next block)
+  const bool s3ok = g.split3 == 0 || (g.N == g.split3 && g.N % 32 == 0);
+  P.tstore = EPI != WIPES_GEMM_EPI_ATOMIC_F32 && s3ok &&
              make_out_tmap(&P.tc, g.C,
                            EPI == WIPES_GEMM_EPI_BIAS_RELU_BF16 || EPI == WIPES_GEMM_EPI_MASK_BF16,
-                           g.M, g.N, g.ldc);
+                           g.M, g.split3 ? 3 * g.split3 : g.N, g.ldc);
 #ifdef WIPES_GEMM_CPASYNC  // cp.async staging variant (experiments / cross-checks)
   return launch_ws_t<NT, AMN, BMN, EPI, false>(P, s);
 #else

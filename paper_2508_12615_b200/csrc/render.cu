@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs 
         a.T_final[it.v * HW + q] = T[p];
         a.n_contrib[it.v * HW + q] = last[p];
       }
+      WCHECK(q >= 0 && q < HW);
       img[q] = C[p][0]; img[HW + q] = C[p][1]; img[2 * HW + q] = C[p][2];
     }
   }
@@ -936,11 +937,13 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         }
         if (a.slots) {  // deterministic: this warp's slot of (dup, footprint); no atomics
           const int64_t si = (int64_t)ws.dj[i] * a.fps + it.sub;
+          WCHECK(ws.dj[i] >= 0 && it.sub < a.fps);
           float* sl = a.slots + si * a.slotw;
           if (writer) sl[my_m] = red;
           if (EXACT && lane == 0) sl[kMom] = mb;
           if (lane == 0) a.slotmask[si] = 1;
         } else {
+          WCHECK(!writer || (my_m >= 0 && my_m < kMom && ws.pid[i] >= 0 && ws.pid[i] < a.N));
           if (writer) red_add(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
           if (EXACT && lane == 0) red_add(a.mom_beta + vN + ws.pid[i], mb);
         }

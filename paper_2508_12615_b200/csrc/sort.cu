@@ -219,25 +219,32 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   }
 #else
   // look back kLookBack predecessors per round: their status words are loaded
-  // together (independent loads), then consumed in tile order
-  for (int64_t t = (int64_t)tile - 1; t >= 0;) {
-    uint32_t s[kLookBack];
+  // together (independent loads), then consumed in tile order. 32-bit tile
+  // index and one running pointer (the 64-bit index math of every load was a
+  // third of the pass's instructions at C3).
+  {
+    int t = (int)tile - 1;
+    const volatile uint32_t* sp = st + (int64_t)t * 256 + d;
+    while (t >= 0) {
+      uint32_t s[kLookBack];
 #pragma unroll
-    for (int j = 0; j < kLookBack; ++j)
-      s[j] = t - j >= 0 ? st[(t - j) * 256 + d] : (2u << 30);  // before tile 0: inclusive 0
-    int used = 0;
-    bool stop = false;
+      for (int j = 0; j < kLookBack; ++j)
+        s[j] = t - j >= 0 ? sp[-256 * j] : (2u << 30);  // before tile 0: inclusive 0
+      int used = 0;
+      bool stop = false;
 #pragma unroll
-    for (int j = 0; j < kLookBack; ++j) {
-      const uint32_t f = s[j] & ~kValMask;
-      if (stop || used < j || f == 0u) continue;  // unpublished: re-read from here
-      prefix += s[j] & kValMask;
-      ++used;
-      stop = f == kFlagInc;
+      for (int j = 0; j < kLookBack; ++j) {
+        const uint32_t f = s[j] & ~kValMask;
+        if (stop || used < j || f == 0u) continue;  // unpublished: re-read from here
+        prefix += s[j] & kValMask;
+        ++used;
+        stop = f == kFlagInc;
+      }
+      if (stop) break;
+      if (used == 0) __nanosleep(WIPES_SORT_BACKOFF);  // predecessor unpublished: back off
+      t -= used;
+      sp -= 256 * used;
     }
-    if (stop) break;
-    if (used == 0) __nanosleep(WIPES_SORT_BACKOFF);  // predecessor unpublished: back off
-    t -= used;
   }
 #endif
   // flag and value share one 32-bit word: no fence needed between publishes
