@@ -211,6 +211,25 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
                               const float* dL_dimage, const float* T_final,
                               const int32_t* n_contrib, wipes_grads* grads, void* stream);
 
+/* Step 4 in two calls, so a multi-GPU caller can overlap the gradient
+ * all-reduce with the chain rule:
+ * wipes_render_bwd_moments = the render backward into the workspace moments
+ * (same arguments as wipes_render_bwd minus params/cams/grads); then
+ * wipes_preprocess_bwd writes the parameter-gradient rows [row0, row1) —
+ * primitives for a shared parameter set (view_stride = 0, or 2D), (view,
+ * primitive) rows for per-frame sets — and may be called once per row chunk,
+ * each chunk's rows complete when its call's work on `stream` completes.
+ * wipes_render_bwd == moments + preprocess_bwd(0, rows). Rows outside
+ * [row0, row1) are not written. row1 < 0 means all rows. */
+wipes_status wipes_render_bwd_moments(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                                      size_t ws_bytes, int64_t dup_capacity,
+                                      const float* dL_dimage, const float* T_final,
+                                      const int32_t* n_contrib, void* stream);
+wipes_status wipes_preprocess_bwd(const wipes_config* cfg, const wipes_params* params, int64_t N,
+                                  const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
+                                  int64_t dup_capacity, wipes_grads* grads, int64_t row0,
+                                  int64_t row1, void* stream);
+
 /* The 12 per-record gradient MOMENTS [B*N, 12] (float32) accumulated by the
  * last wipes_render_bwd, for tests and inspection. With gw = dL/dw of a valid
  * (pixel, record) pair, w = alpha W, ag = alpha G, d = pixel - mu', sums over

@@ -114,6 +114,10 @@ def lib():
     L.wipes_render_fwd.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp, vp]
     L.wipes_render_bwd.argtypes = [P(wipes_config), P(wipes_params), i64, P(wipes_camera), i32,
                                    vp, sz, i64, vp, vp, vp, P(wipes_grads), vp]
+    L.wipes_render_bwd_moments.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp, vp,
+                                           vp]
+    L.wipes_preprocess_bwd.argtypes = [P(wipes_config), P(wipes_params), i64, P(wipes_camera),
+                                       i32, vp, sz, i64, P(wipes_grads), i64, i64, vp]
     L.wipes_get_grad_moments.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
     L.wipes_render_stats.argtypes = [P(wipes_config), i64, i32, vp, sz, i64, vp, vp]
     L.wipes_train_scratch_bytes.restype = sz
@@ -147,6 +151,7 @@ def lib():
     L.wipes_abi_version.restype = C.c_int
     for fn in ("wipes_preprocess", "wipes_bin_sort", "wipes_check_overflow",
                "wipes_get_preprocess", "wipes_render_fwd", "wipes_render_bwd",
+               "wipes_render_bwd_moments", "wipes_preprocess_bwd",
                "wipes_get_grad_moments", "wipes_timing_collect", "wipes_render_stats",
                "wipes_loss_l2", "wipes_adam_step", "wipes_activate"):
         getattr(L, fn).restype = C.c_int
@@ -156,7 +161,8 @@ def lib():
 
 EXPORTED = ["wipes_workspace_bytes", "wipes_preprocess", "wipes_bin_sort",
             "wipes_check_overflow", "wipes_get_preprocess", "wipes_render_fwd",
-            "wipes_render_bwd", "wipes_get_grad_moments", "wipes_render_stats",
+            "wipes_render_bwd", "wipes_render_bwd_moments", "wipes_preprocess_bwd",
+            "wipes_get_grad_moments", "wipes_render_stats",
             "wipes_train_scratch_bytes", "wipes_loss_l2", "wipes_adam_step", "wipes_activate",
             "wipes_overflow_flag", "wipes_gemm_bf16", "wipes_mlp_param_count",
             "wipes_mlp_workspace_bytes", "wipes_mlp_forward", "wipes_mlp_backward",
@@ -265,6 +271,17 @@ def wipes_render_bwd(cfg, params, N, cams, B, ws, ws_bytes, cap, dLdC, T_final, 
     return lib().wipes_render_bwd(C.byref(cfg), C.byref(params), N,
                                   cams if cams is not None else None, B, ws, ws_bytes, cap,
                                   dLdC, T_final, n_contrib, C.byref(grads), stream)
+
+
+def wipes_render_bwd_moments(cfg, N, B, ws, ws_bytes, cap, dLdC, T_final, n_contrib, stream):
+    return lib().wipes_render_bwd_moments(C.byref(cfg), N, B, ws, ws_bytes, cap, dLdC, T_final,
+                                          n_contrib, stream)
+
+
+def wipes_preprocess_bwd(cfg, params, N, cams, B, ws, ws_bytes, cap, grads, row0, row1, stream):
+    return lib().wipes_preprocess_bwd(C.byref(cfg), C.byref(params), N,
+                                      cams if cams is not None else None, B, ws, ws_bytes, cap,
+                                      C.byref(grads), row0, row1, stream)
 
 
 def wipes_get_grad_moments(cfg, N, B, ws, ws_bytes, cap, out, stream):

@@ -279,24 +279,12 @@ wipes_status wipes_render_fwd(const wipes_config* cfg, int64_t N, int32_t B, voi
   return WIPES_OK;
 }
 
-wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* params, int64_t N,
-                              const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
-                              int64_t dup_capacity, const float* dL_dimage, const float* T_final,
-                              const int32_t* n_contrib, wipes_grads* grads, void* stream) {
-  NvtxRange nvtx_range("wipes_render_bwd");
-  wipes_status st = check_cfg(cfg, N, B);
-  if (st != WIPES_OK) return st;
-  st = check_params(cfg, params, N, B);
-  if (st != WIPES_OK) return st;
-  Layout L = make_layout(*cfg, N, B, dup_capacity);
-  st = check_ws(L, ws, ws_bytes, dup_capacity);
-  if (st != WIPES_OK) return st;
+static wipes_status render_bwd_moments(const wipes_config* cfg, const Layout& L, void* ws,
+                                       const float* dL_dimage, const float* T_final,
+                                       const int32_t* n_contrib, cudaStream_t s) {
   if (!dL_dimage || !aligned(dL_dimage, 4)) return fail(WIPES_EINVAL, "dL_dimage");
   if (cfg->blend == WIPES_BLEND_ALPHA && (!T_final || !n_contrib))
     return fail(WIPES_EINVAL, "ALPHA mode needs T_final and n_contrib");
-  if (!grads) return fail(WIPES_EINVAL, "grads is NULL");
-  if (cfg->prim == WIPES_PRIM_3D && !cams) return fail(WIPES_EINVAL, "cams is NULL (3D)");
-  cudaStream_t s = (cudaStream_t)stream;
   char* w = (char*)ws;
   cudaError_t e = cudaSuccess;
   if (L.BN > 0) {
@@ -314,10 +302,70 @@ wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* param
     e = launch_det_gather(L, w, s);
     if (e != cudaSuccess) return cuda_fail(e, "det_gather launch");
   }
-  e = cfg->prim == WIPES_PRIM_2D ? launch_preprocess2d_bwd(*cfg, *params, L, w, *grads, s)
-                                 : launch_preprocess3d_bwd(*cfg, *params, L, cams, w, *grads, s);
+  return WIPES_OK;
+}
+
+static wipes_status preprocess_bwd(const wipes_config* cfg, const wipes_params* params,
+                                   const wipes_camera* cams, const Layout& L, void* ws,
+                                   wipes_grads* grads, int64_t row0, int64_t row1,
+                                   cudaStream_t s) {
+  if (!grads) return fail(WIPES_EINVAL, "grads is NULL");
+  if (cfg->prim == WIPES_PRIM_3D && !cams) return fail(WIPES_EINVAL, "cams is NULL (3D)");
+  if (row0 < 0 || (row1 >= 0 && row1 < row0)) return fail(WIPES_EINVAL, "row0 / row1");
+  char* w = (char*)ws;
+  cudaError_t e = cfg->prim == WIPES_PRIM_2D
+                      ? launch_preprocess2d_bwd(*cfg, *params, L, w, *grads, s, row0, row1)
+                      : launch_preprocess3d_bwd(*cfg, *params, L, cams, w, *grads, s, row0, row1);
   if (e != cudaSuccess) return cuda_fail(e, "preprocess_bwd launch");
   return WIPES_OK;
+}
+
+wipes_status wipes_render_bwd(const wipes_config* cfg, const wipes_params* params, int64_t N,
+                              const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
+                              int64_t dup_capacity, const float* dL_dimage, const float* T_final,
+                              const int32_t* n_contrib, wipes_grads* grads, void* stream) {
+  NvtxRange nvtx_range("wipes_render_bwd");
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  st = check_params(cfg, params, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  if (!grads) return fail(WIPES_EINVAL, "grads is NULL");
+  if (cfg->prim == WIPES_PRIM_3D && !cams) return fail(WIPES_EINVAL, "cams is NULL (3D)");
+  cudaStream_t s = (cudaStream_t)stream;
+  st = render_bwd_moments(cfg, L, ws, dL_dimage, T_final, n_contrib, s);
+  if (st != WIPES_OK) return st;
+  return preprocess_bwd(cfg, params, cams, L, ws, grads, 0, -1, s);
+}
+
+wipes_status wipes_render_bwd_moments(const wipes_config* cfg, int64_t N, int32_t B, void* ws,
+                                      size_t ws_bytes, int64_t dup_capacity,
+                                      const float* dL_dimage, const float* T_final,
+                                      const int32_t* n_contrib, void* stream) {
+  NvtxRange nvtx_range("wipes_render_bwd_moments");
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  return render_bwd_moments(cfg, L, ws, dL_dimage, T_final, n_contrib, (cudaStream_t)stream);
+}
+
+wipes_status wipes_preprocess_bwd(const wipes_config* cfg, const wipes_params* params, int64_t N,
+                                  const wipes_camera* cams, int32_t B, void* ws, size_t ws_bytes,
+                                  int64_t dup_capacity, wipes_grads* grads, int64_t row0,
+                                  int64_t row1, void* stream) {
+  NvtxRange nvtx_range("wipes_preprocess_bwd");
+  wipes_status st = check_cfg(cfg, N, B);
+  if (st != WIPES_OK) return st;
+  st = check_params(cfg, params, N, B);
+  if (st != WIPES_OK) return st;
+  Layout L = make_layout(*cfg, N, B, dup_capacity);
+  st = check_ws(L, ws, ws_bytes, dup_capacity);
+  if (st != WIPES_OK) return st;
+  return preprocess_bwd(cfg, params, cams, L, ws, grads, row0, row1, (cudaStream_t)stream);
 }
 
 wipes_status wipes_get_grad_moments(const wipes_config* cfg, int64_t N, int32_t B, const void* ws,

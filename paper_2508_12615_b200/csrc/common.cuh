@@ -301,12 +301,15 @@ cudaError_t launch_render_fwd(const wipes_config& c, const Layout& L, char* ws, 
 cudaError_t launch_render_bwd(const wipes_config& c, const Layout& L, char* ws, int final_in_b,
                               const float* dLdC, const float* T_final,
                               const int32_t* n_contrib, cudaStream_t s);
+// Parameter rows [row0, row1) (row1 < 0: all): primitives (2D, view_stride 0)
+// or (view, primitive) rows (per-frame parameter sets).
 cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p,
                                     const Layout& L, char* ws, const wipes_grads& g,
-                                    cudaStream_t s);
+                                    cudaStream_t s, int64_t row0 = 0, int64_t row1 = -1);
 cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p,
                                     const Layout& L, const wipes_camera* cams, char* ws,
-                                    const wipes_grads& g, cudaStream_t s);
+                                    const wipes_grads& g, cudaStream_t s, int64_t row0 = 0,
+                                    int64_t row1 = -1);
 
 inline int final_buffer_is_b(const Layout& L) { return L.passes & 1; }
 

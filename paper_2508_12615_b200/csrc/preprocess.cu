@@ -661,6 +661,7 @@ struct Bwd2DArgs {
   Cfg2 c;
   int32_t cov2;
   int64_t N;
+  int64_t row0, row1;  // parameter rows [row0, row1) of this launch
   const float *cov, *freq, *opacity;
   const uint8_t* flag;
   const float* mom;
@@ -668,8 +669,8 @@ struct Bwd2DArgs {
 };
 
 __global__ void __launch_bounds__(256) k_pre2d_bwd(Bwd2DArgs a) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.N) return;
+  int64_t i = a.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.row1) return;
   bool live = a.flag[i] == 0;
   double g[kRecGrads];
   for (int k = 0; k < kRecGrads; ++k) g[k] = 0.0;
@@ -718,6 +719,7 @@ struct Bwd3DArgs {
   Cfg2 c;
   int32_t ewa_clamp, accumulate;
   int64_t N, view_stride, nrows;
+  int64_t row0;  // first (launch-local) parameter row: rows [row0, row0 + nrows)
   const float *mean, *scale, *quat, *freq;
   const float* opacity;
   const uint8_t* flag;
@@ -738,8 +740,9 @@ struct Bwd3DArgs {
 // and the full 3x3 ray-space covariance Sigma_hat = M3 S3 M3^T.
 template <bool EXACT>
 __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __grid_constant__ Bwd3DArgs a) {
-  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= a.nrows) return;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows) return;
+  const int64_t row = a.row0 + r;
   int v_lo, v_hi;
   int64_t i, pi;
   if (a.view_stride == 0) { v_lo = a.cams.v0; v_hi = a.cams.v0 + a.cams.nv; i = row; pi = row; }
@@ -915,8 +918,9 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
 // (mu, s, q, f: 13), each giving the column J[:, k] of the 8-output Jacobian;
 // phase, colour and opacity pass straight through the record.
 __global__ void __launch_bounds__(128) k_pre3d_bwd_exact(const __grid_constant__ Bwd3DArgs a) {
-  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= a.nrows) return;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows) return;
+  const int64_t row = a.row0 + r;
   int v_lo, v_hi;
   int64_t i, pi;
   if (a.view_stride == 0) { v_lo = a.cams.v0; v_hi = a.cams.v0 + a.cams.nv; i = row; pi = row; }
@@ -985,9 +989,10 @@ template <int DEG, int GV>
 __global__ void __launch_bounds__(128, WIPES_SH_MINB) k_sh_bwd(const __grid_constant__ Bwd3DArgs a) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gid / GV;
+  const int64_t lrow = gid / GV;
+  const int64_t row = a.row0 + lrow;
   const int gl = (int)(gid % GV);
-  const bool active = row < a.nrows;  // whole groups only: no early return (shuffles)
+  const bool active = lrow < a.nrows;  // whole groups only: no early return (shuffles)
   int v_lo = 0, v_hi = 0;
   int64_t i = 0, pi = 0;
   if (active) {
@@ -1154,9 +1159,12 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
 
 cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p,
                                     const Layout& L, char* ws, const wipes_grads& g,
-                                    cudaStream_t s) {
-  if (L.N == 0) return cudaSuccess;
+                                    cudaStream_t s, int64_t row0, int64_t row1) {
+  if (row1 < 0 || row1 > L.N) row1 = L.N;
+  if (L.N == 0 || row1 <= row0) return cudaSuccess;
   Bwd2DArgs a;
+  a.row0 = row0;
+  a.row1 = row1;
   a.c = make_cfg2(c, L);
   a.cov2 = c.cov2;
   a.N = L.N;
@@ -1167,15 +1175,18 @@ cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p
   a.mom = (const float*)(ws + L.rgrad);
   a.g = g;
   launch_begin(K_PRE2D_BWD, s);
-  k_pre2d_bwd<<<(unsigned)((L.N + 255) / 256), 256, 0, s>>>(a);
+  k_pre2d_bwd<<<(unsigned)((row1 - row0 + 255) / 256), 256, 0, s>>>(a);
   launch_end(K_PRE2D_BWD, s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p,
                                     const Layout& L, const wipes_camera* cams, char* ws,
-                                    const wipes_grads& g, cudaStream_t s) {
-  if (L.N == 0) return cudaSuccess;
+                                    const wipes_grads& g, cudaStream_t s, int64_t row0,
+                                    int64_t row1) {
+  const int64_t rows = p.view_stride == 0 ? L.N : (int64_t)L.B * L.N;
+  if (row1 < 0 || row1 > rows) row1 = rows;
+  if (L.N == 0 || row1 <= row0) return cudaSuccess;
   static thread_local Bwd3DArgs a;  // ~9 KB: keep off the host stack
   a.c = make_cfg2(c, L);
   a.ewa_clamp = c.ewa_clamp;
@@ -1195,7 +1206,16 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
     int nv = L.B - v0 < WIPES_MAX_CAMERAS_PER_LAUNCH ? L.B - v0 : WIPES_MAX_CAMERAS_PER_LAUNCH;
     fill_cams(a.cams, cams, v0, nv);
     a.accumulate = (p.view_stride == 0 && v0 > 0) ? 1 : 0;
-    a.nrows = p.view_stride == 0 ? L.N : (int64_t)nv * L.N;
+    if (p.view_stride == 0) {  // primitive rows, every view chunk
+      a.row0 = row0;
+      a.nrows = row1 - row0;
+    } else {  // (view, primitive) rows of this chunk's views within [row0, row1)
+      const int64_t c0 = (int64_t)v0 * L.N, c1 = (int64_t)(v0 + nv) * L.N;
+      const int64_t lo = row0 > c0 ? row0 : c0, hi = row1 < c1 ? row1 : c1;
+      if (hi <= lo) continue;
+      a.row0 = lo - c0;
+      a.nrows = hi - lo;
+    }
     launch_begin(K_PRE3D_BWD, s);
     static const bool dual = getenv("WIPES_EXACT_DUAL") != nullptr;
     if (L.exact && dual)  // forward-mode (dual number) cross-check of the hand adjoint

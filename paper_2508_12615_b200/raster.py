@@ -27,6 +27,15 @@ PARAM_KEYS_3D = ("mean", "scale", "quat", "freq", "phase", "color", "opacity", "
 GRAD_KEYS = ("mean", "cov", "scale", "quat", "freq", "phase", "color", "opacity", "sh")
 
 
+def row_ranges(rows: int, chunks: int) -> list:
+    """[row0, row1) ranges splitting `rows` into `chunks` contiguous pieces
+    (multiples of 64 rows except the last)."""
+    chunks = max(1, min(int(chunks), max(1, -(-rows // 64))))
+    step = -(-rows // chunks)
+    step = -(-step // 64) * 64
+    return [(a, min(rows, a + step)) for a in range(0, rows, step)] or [(0, 0)]
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -162,7 +171,14 @@ class Rasterizer:
         return n, bool(o)
 
     # ------------------------------------------------------------- backward
-    def backward(self, dL_dimage: torch.Tensor, grads: Optional[dict] = None) -> dict:
+    def backward(self, dL_dimage: torch.Tensor, grads: Optional[dict] = None,
+                 row_chunks: int = 1, on_rows=None) -> dict:
+        """Gradients of every parameter group. row_chunks > 1 splits the
+        preprocess backward into that many parameter-row ranges (one launch
+        each, wipes_preprocess_bwd) and calls on_rows(row0, row1) after each is
+        enqueued on the current stream: a multi-GPU caller starts the
+        all-reduce of rows [row0, row1) there, overlapping the next chunk
+        (dist.GradBucket.reduce_rows)."""
         if self._saved is None:
             raise RuntimeError("backward() before forward()")
         _req(dL_dimage, "dL_dimage")
@@ -177,10 +193,29 @@ class Rasterizer:
         g = abi.wipes_grads()
         for k in GRAD_KEYS:
             setattr(g, k, abi.ptr(grads.get(k)))
-        abi.check(abi.wipes_render_bwd(self.cfg, pp, self.N, cp, self.B, self._ws_ptr(),
-                                       self.ws_bytes, self.cap, abi.ptr(dL_dimage), abi.ptr(T),
-                                       abi.ptr(nc), g, _stream()), "wipes_render_bwd")
+        if row_chunks <= 1 and on_rows is None:
+            abi.check(abi.wipes_render_bwd(self.cfg, pp, self.N, cp, self.B, self._ws_ptr(),
+                                           self.ws_bytes, self.cap, abi.ptr(dL_dimage),
+                                           abi.ptr(T), abi.ptr(nc), g, _stream()),
+                      "wipes_render_bwd")
+            return grads
+        abi.check(abi.wipes_render_bwd_moments(self.cfg, self.N, self.B, self._ws_ptr(),
+                                               self.ws_bytes, self.cap, abi.ptr(dL_dimage),
+                                               abi.ptr(T), abi.ptr(nc), _stream()),
+                  "wipes_render_bwd_moments")
+        rows = self.grad_rows()
+        for r0, r1 in row_ranges(rows, row_chunks):
+            abi.check(abi.wipes_preprocess_bwd(self.cfg, pp, self.N, cp, self.B, self._ws_ptr(),
+                                               self.ws_bytes, self.cap, g, r0, r1, _stream()),
+                      "wipes_preprocess_bwd")
+            if on_rows is not None:
+                on_rows(r0, r1)
         return grads
+
+    def grad_rows(self) -> int:
+        """Parameter-gradient rows: primitives (2D or a shared 3D set) or
+        (view, primitive) rows of per-frame sets."""
+        return self.N if (self.prim == "2d" or self._view_stride == 0) else self.B * self.N
 
     # ----------------------------------------------------------- debug/parity
     def get_preprocess(self):

@@ -224,3 +224,58 @@ def test_bench_sharding_modes():
     assert bench.sharding("c3", 8, a) == (False, False, True)
     assert bench.sharding("c4", 8, a) == (False, True, True)
     assert bench.sharding("c5", 1, a) == (True, False, True)
+
+
+def _worker_rows_bucket(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    from paper_2508_12615_b200.raster import row_ranges
+    rng = np.random.default_rng(40 + rank)
+    N = 1000
+    g = {"mean": torch.from_numpy(rng.normal(size=(N, 3)).astype(np.float32)),
+         "quat": torch.from_numpy(rng.normal(size=(N, 4)).astype(np.float32)),
+         "opacity": torch.from_numpy(rng.normal(size=N).astype(np.float32))}
+    full = {k: v.clone() for k, v in g.items()}
+    for v in full.values():
+        dist.all_reduce(v)
+    b = wdist.GradBucket(g)
+    ov = wdist.OverlappedReduce(b)
+    for r0, r1 in row_ranges(N, 3):  # as Rasterizer.backward(row_chunks=3, on_rows=...)
+        ov.on_rows(r0, r1)
+    ov.finish()
+    q.put((rank, {k: v.numpy().copy() for k, v in g.items()},
+           {k: v.numpy().copy() for k, v in full.items()}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_bucketed_row_reduce_equals_full_all_reduce():
+    """The overlapped exchange (dist.OverlappedReduce / GradBucket.reduce_rows):
+    reducing the parameter rows chunk by chunk, every group's slice of each
+    chunk, gives exactly the all-reduce of the whole buffers."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_rows_bucket, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for _, chunked, full in got:
+        for k in full:
+            np.testing.assert_array_equal(chunked[k], full[k])
+
+
+def test_row_ranges_partition():
+    from paper_2508_12615_b200.raster import row_ranges
+    for rows in (1, 63, 64, 1000, 1000000):
+        for k in (1, 2, 3, 4, 7):
+            rr = row_ranges(rows, k)
+            assert rr[0][0] == 0 and rr[-1][1] == rows
+            assert all(a1 == b0 for (_, a1), (b0, _) in zip(rr, rr[1:]))
+            assert all(r0 % 64 == 0 for r0, _ in rr)
