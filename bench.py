@@ -103,35 +103,47 @@ def load_alu_peaks(clk_hz):
 
 def hbm_fractions(kt, steps, L, hbm_gbs):
     """SURVEY §8(d) gate G2: achieved algorithmic bytes / CUDA-event time of the
-    HBM-bound kernels against the measured copy bandwidth. Algorithmic bytes
-    per launch: L = dict(BN, N, dup, BT, passes, param_bytes,
-    grad_bytes)."""
-    BN, dup = L["BN"], L["dup"]
-    per = {
-        # params read once per (view, primitive) set + rect 16, count 4, flag 1, depth 4, record 64
+    HBM-bound kernel groups against the measured copy bandwidth, per STEP (a
+    group may be several launches: camera chunks, sort passes, the ALPHA
+    presort's key kernels). L = dict(BN, dup, BT, alpha, B, param_bytes,
+    grad_bytes). Sort keys and values are 32-bit: one pass reads and writes
+    16 B per element; the ALPHA path first presorts the BN (view, primitive)
+    depth keys (4 depth bytes + the view bytes) and then sorts the dup tile
+    keys."""
+    BN, dup, alpha = L["BN"], L["dup"], L["alpha"]
+    vb = 0
+    while (1 << vb) < L["B"]:
+        vb += 1
+    pre = (4 + (vb + 7) // 8) if alpha else 0
+    tb = 0
+    while (1 << tb) < L["BT"]:
+        tb += 1
+    tile_passes = (tb + 7) // 8
+    per_step = {
+        # params read + rect 16, count 4, flag 1, depth 4, record 64 written per (view, prim)
         "preprocess2d": L["param_bytes"] + 89 * BN,
         "preprocess3d": L["param_bytes"] + 89 * BN,
-        # rect 16 + offset 8 + depth key 4 read per (view, primitive); key 8 + value 4 per dup
-        "duplicate": 28 * BN + 12 * dup,
-        # every digit histogram from one read of the keys (8 B / dup)
-        "radix_hist": 8 * dup,
-        # one onesweep pass: key + value read and written (24 B / dup)
-        "radix_scatter": 24 * dup,
+        # rect 16 + offset 8 + count 4 read per (view, prim); key 4 + value 4 per dup;
+        # ALPHA also the presort key build (4 in, 8 out) and count gather (8 in, 4 out)
+        "duplicate": 28 * BN + 8 * dup + (24 * BN if alpha else 0),
+        # one read of the keys per sort
+        "radix_hist": 4 * dup + (4 * BN if alpha else 0),
+        # per pass: key + value read and written
+        "radix_scatter": 16 * (tile_passes * dup + pre * BN),
         # sorted keys read, CSR offsets written
-        "tile_ranges": 8 * dup + 4 * (L["BT"] + 1),
+        "tile_ranges": 4 * dup + 4 * (L["BT"] + 1),
         # moments (48 B / (view, primitive)) + params read, gradients written
         "preprocess2d_bwd": 48 * BN + L["param_bytes"] + L["grad_bytes"],
         "preprocess3d_bwd": 48 * BN + L["param_bytes"] + L["grad_bytes"],
     }
     out = {}
-    for k, b in per.items():
+    for k, b in per_step.items():
         if k not in kt or not kt[k][1]:
             continue
-        ms, n = kt[k]
-        t = ms / 1e3 / n
+        t = kt[k][0] / 1e3 / steps
         gbs = b / t / 1e9
-        out[k] = {"bytes_per_launch": int(b), "us_per_launch": t * 1e6, "GB/s": gbs,
-                  "frac": gbs / hbm_gbs}
+        out[k] = {"bytes_per_step": int(b), "us_per_step": t * 1e6,
+                  "launches_per_step": kt[k][1] / steps, "GB/s": gbs, "frac": gbs / hbm_gbs}
     return out
 
 
@@ -757,6 +769,7 @@ def main():
             "hbm_kernels": hbm_fractions(
                 kt, args.steps,
                 dict(BN=Bl * N, dup=int(n_tot2), BT=Bl * (-(-W // args.tile)) * (-(-H // args.tile)),
+                     alpha=blend == "alpha", B=Bl,
                      param_bytes=sum(v.numel() * 4 for v in params.values()),
                      grad_bytes=sum(v.numel() * 4 for v in grads.values())),
                 float(peaks.get("hbm_gbs", 6450.9))),
