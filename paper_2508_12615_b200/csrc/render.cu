@@ -999,8 +999,8 @@ cudaError_t launch_fwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
 
 template <int TS>
 cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
-  const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   ra.queue = Q_BWD;
+  const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   void (*k)(RenderArgs);
   if (ra.f64) {
     if (ra.mom_beta)
