@@ -16,10 +16,67 @@ __device__ __forceinline__ int64_t clamp_n(const WsHeader* h, int64_t cap) {
 }
 
 // ---------------------------------------------------------------- scan ----
+// Exclusive scan of nblk block sums in place by one block of NT threads.
+// Optionally publishes the grand total and the capacity-overflow flag into
+// the workspace header and resets its per-frame scheduling state. The sums
+// may have been written by other blocks of the same grid: they are read
+// through L2 (ld.global.cg).
+template <int NT, typename T>
+__device__ __forceinline__ void scan_sums_block(T* blk, int64_t nblk, WsHeader* hdr, int64_t cap) {
+  static_assert(sizeof(T) == 8, "64-bit block sums");
+  constexpr int NW = NT / 32;
+  __shared__ T wt[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (nblk + NT - 1) / NT;
+  const int64_t b0 = (int64_t)tid * per;
+  T s = 0;
+  for (int64_t k = 0; k < per; ++k)
+    if (b0 + k < nblk) s += (T)__ldcg((const long long*)blk + b0 + k);
+  T inc = s;
+  for (int off = 1; off < 32; off <<= 1) {
+    T t = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += t;
+  }
+  if (lane == 31) wt[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T t = lane < NW ? wt[lane] : (T)0;
+    T ti = t;
+    for (int off = 1; off < 32; off <<= 1) {
+      T u = __shfl_up_sync(0xffffffffu, ti, off);
+      if (lane >= off) ti += u;
+    }
+    if (lane < NW) wt[lane] = ti - t;
+    if (lane == 31 && hdr) {
+      hdr->total = (int64_t)ti;
+      hdr->overflow = (int64_t)ti > cap ? 1 : 0;
+    }
+  }
+  if (hdr && wid == 1) {  // reset the per-frame scheduling state
+    hdr->bcount[lane] = 0;
+    hdr->bfill[lane] = 0;
+    if (lane < kQueues) { hdr->work[lane] = 0; hdr->done[lane] = 0; }
+    if (lane >= 1 && lane < 4) hdr->arrive[lane] = 0;
+  }
+  __syncthreads();
+  T run = wt[wid] + inc - s;
+  for (int64_t k = 0; k < per; ++k)
+    if (b0 + k < nblk) {
+      T v = (T)__ldcg((const long long*)blk + b0 + k);
+      blk[b0 + k] = run;
+      run += v;
+    }
+}
+
+// Single-launch exclusive scan: every block scans its kScanTile items and
+// publishes its sum; the last block to arrive (counter `arrive`) scans the
+// block sums. Consumers add loc[i] + blk[i / kScanTile].
 template <typename TIn, typename TOut>
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const TIn* in, int64_t n,
-                                                           TOut* loc, TOut* blk_sum) {
+__global__ void __launch_bounds__(kScanBlock) k_scan(const TIn* in, int64_t n, TOut* loc,
+                                                    TOut* blk_sum, int32_t* arrive,
+                                                    WsHeader* hdr, int64_t cap) {
   __shared__ TOut warp_tot[kScanBlock / 32];
+  __shared__ int is_last;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * kScanItems;
   TOut v[kScanItems];
@@ -48,9 +105,13 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const TIn* in, int64
       if (lane >= off) ti += u;
     }
     if (lane < kScanBlock / 32) warp_tot[lane] = ti - t;  // exclusive
-    if (lane == kScanBlock / 32 - 1) blk_sum[blockIdx.x] = ti;
+    if (lane == kScanBlock / 32 - 1) {
+      blk_sum[blockIdx.x] = ti;
+      __threadfence();  // the sum is visible before this block counts as arrived
+    }
   }
   __syncthreads();
+  if (tid == 0) is_last = atomicAdd(arrive, 1) == (int)gridDim.x - 1;
   TOut run = warp_tot[wid] + inc - s;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
@@ -58,53 +119,12 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const TIn* in, int64
     if (idx < n) loc[idx] = run;
     run += v[k];
   }
-}
-
-// Exclusive scan of the block sums in place (one block). Optionally publishes
-// the grand total and the capacity-overflow flag into the workspace header.
-template <typename T>
-__global__ void __launch_bounds__(1024) k_scan_sums(T* blk, int64_t nblk, WsHeader* hdr,
-                                                   int64_t cap) {
-  __shared__ T wt[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t per = (nblk + 1023) / 1024;
-  const int64_t b0 = (int64_t)tid * per;
-  T s = 0;
-  for (int64_t k = 0; k < per; ++k)
-    if (b0 + k < nblk) s += blk[b0 + k];
-  T inc = s;
-  for (int off = 1; off < 32; off <<= 1) {
-    T t = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc += t;
-  }
-  if (lane == 31) wt[wid] = inc;
   __syncthreads();
-  if (wid == 0) {
-    T t = wt[lane];
-    T ti = t;
-    for (int off = 1; off < 32; off <<= 1) {
-      T u = __shfl_up_sync(0xffffffffu, ti, off);
-      if (lane >= off) ti += u;
-    }
-    wt[lane] = ti - t;
-    if (lane == 31 && hdr) {
-      hdr->total = (int64_t)ti;
-      hdr->overflow = (int64_t)ti > cap ? 1 : 0;
-    }
+  if (is_last) {
+    __threadfence();
+    scan_sums_block<kScanBlock>(blk_sum, gridDim.x, hdr, cap);
+    if (tid == 0) *arrive = 0;  // self-resetting for the next scan of this workspace
   }
-  if (hdr && wid == 1) {  // reset the per-frame scheduling state
-    hdr->bcount[lane] = 0;
-    hdr->bfill[lane] = 0;
-    if (lane < kQueues) { hdr->work[lane] = 0; hdr->done[lane] = 0; }
-  }
-  __syncthreads();
-  T run = wt[wid] + inc - s;
-  for (int64_t k = 0; k < per; ++k)
-    if (b0 + k < nblk) {
-      T v = blk[b0 + k];
-      blk[b0 + k] = run;
-      run += v;
-    }
 }
 
 // ----------------------------------------------------------- duplicate ----
@@ -124,14 +144,32 @@ struct DupArgs {
   uint32_t* keys;
   uint32_t* vals;
   uint32_t* prevals;  // deterministic mode: vals[j] = j, prevals[j] = primitive
+  uint32_t* ghist;    // non-null: also build the radix histogram of the npass
+  int32_t npass;      //   8-bit tile-key digits (sort.cu's k_sort_hist, fused)
 };
+
+// Adds a block's shared histogram into the global one (after the whole block
+// has counted: every warp, including those past the records, reaches here).
+__device__ __forceinline__ void flush_hist(const DupArgs& a, uint32_t (*hist)[256]) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.npass * 256; i += blockDim.x) {
+    const uint32_t c = (&hist[0][0])[i];
+    if (c) atomicAdd(a.ghist + i, c);
+  }
+}
 
 // Warp-cooperative emission: the 32 records of a warp own one contiguous
 // output range (their offsets are consecutive in the scan), so the warp
 // writes it lane-strided — every store instruction covers 32 consecutive
 // pairs — finding each pair's record by a binary search over the lanes'
 // start offsets and its tile from the record's rect.
+template <bool HIST>
 __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
+  __shared__ uint32_t hist[HIST ? kMaxPasses : 1][256];
+  if (HIST) {
+    for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+    __syncthreads();
+  }
   const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   constexpr unsigned kFullMask = 0xffffffffu;
@@ -154,45 +192,62 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
       wdt = r.z - r.x;
     }
   }
-  // the warp's output range [S, E) (lane 0 is always a valid record)
-  if (j0 - lane >= a.BN) return;  // whole warp beyond the records
-  const int64_t S = __shfl_sync(kFullMask, start, 0);
-  int64_t E = j0 < a.BN ? start + n : 0;
+  // (break: the whole warp is beyond the records; it still reaches the flush)
+  do {
+    if (j0 - lane >= a.BN) break;
+    // the warp's output range [S, E) (lane 0 is always a valid record)
+    const int64_t S = __shfl_sync(kFullMask, start, 0);
+    int64_t E = j0 < a.BN ? start + n : 0;
 #pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    const int64_t t = __shfl_xor_sync(kFullMask, E, off);
-    E = t > E ? t : E;
-  }
-  const int dty = a.row_mod > 1 ? a.row_mod : 1;
-  for (int64_t j = S + lane; j - lane < E; j += 32) {
-    const bool live = j < E;
-    // owner = the last lane with start <= j (starts are non-decreasing; a
-    // zero-count lane shares its start with the next lane, which owns it)
-    int owner = 0;
-#pragma unroll
-    for (int step = 16; step; step >>= 1) {
-      const int64_t sv = __shfl_sync(kFullMask, start, owner + step);
-      if (sv <= j) owner += step;
+    for (int off = 16; off; off >>= 1) {
+      const int64_t t = __shfl_xor_sync(kFullMask, E, off);
+      E = t > E ? t : E;
     }
-    const int64_t so = __shfl_sync(kFullMask, start, owner);
-    const int ox = __shfl_sync(kFullMask, r.x, owner);
-    const int ow = __shfl_sync(kFullMask, wdt, owner);
-    const int oty = __shfl_sync(kFullMask, ty0, owner);
-    const uint32_t ovt = __shfl_sync(kFullMask, vt, owner);
-    const uint32_t oi = __shfl_sync(kFullMask, ival, owner);
-    if (live && j < a.cap) {
-      const int t = (int)(j - so);
-      const int row = t / ow, col = t - row * ow;
-      WCHECK(t >= 0 && col >= 0 && col < ow && ox + col < a.GX);
-      a.keys[j] = ovt + (uint32_t)(oty + row * dty) * (uint32_t)a.GX + (uint32_t)(ox + col);
-      if (a.prevals) {
-        a.vals[j] = (uint32_t)j;
-        a.prevals[j] = oi;
-      } else {
-        a.vals[j] = oi;
+    const int dty = a.row_mod > 1 ? a.row_mod : 1;
+    for (int64_t j = S + lane; j - lane < E; j += 32) {
+      const bool live = j < E;
+      // owner = the last lane with start <= j (starts are non-decreasing; a
+      // zero-count lane shares its start with the next lane, which owns it)
+      int owner = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int64_t sv = __shfl_sync(kFullMask, start, owner + step);
+        if (sv <= j) owner += step;
+      }
+      const int64_t so = __shfl_sync(kFullMask, start, owner);
+      const int ox = __shfl_sync(kFullMask, r.x, owner);
+      const int ow = __shfl_sync(kFullMask, wdt, owner);
+      const int oty = __shfl_sync(kFullMask, ty0, owner);
+      const uint32_t ovt = __shfl_sync(kFullMask, vt, owner);
+      const uint32_t oi = __shfl_sync(kFullMask, ival, owner);
+      const bool emit = live && j < a.cap;
+      uint32_t key = 0;
+      if (emit) {
+        const int t = (int)(j - so);
+        const int row = t / ow, col = t - row * ow;
+        WCHECK(t >= 0 && col >= 0 && col < ow && ox + col < a.GX);
+        key = ovt + (uint32_t)(oty + row * dty) * (uint32_t)a.GX + (uint32_t)(ox + col);
+        a.keys[j] = key;
+        if (a.prevals) {
+          a.vals[j] = (uint32_t)j;
+          a.prevals[j] = oi;
+        } else {
+          a.vals[j] = oi;
+        }
+      }
+      if (HIST) {
+        // low digit: mostly distinct across the lanes (consecutive tiles);
+        // higher digits: few distinct values, so one add per distinct digit
+        if (emit) atomicAdd(&hist[0][key & 255u], 1u);
+        for (int p = 1; p < a.npass; ++p) {
+          const uint32_t d = emit ? (key >> (8 * p)) & 255u : 256u;
+          const uint32_t peers = __match_any_sync(kFullMask, d);
+          if (emit && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&hist[p][d], (uint32_t)__popc(peers));
+        }
       }
     }
-  }
+  } while (0);
+  if (HIST) flush_hist(a, hist);
 }
 
 // ALPHA depth presort inputs: key = orderable depth bits, value = o = view*N +
@@ -212,18 +267,6 @@ __global__ void __launch_bounds__(256) k_gather_counts(const uint32_t* order, co
 }
 
 // --------------------------------------------------------- tile ranges ----
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, const WsHeader* hdr,
-                                                     int64_t cap, int64_t BT, int32_t* toff) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = clamp_n(hdr, cap);
-  if (i > n) return;
-  int64_t tp = i == 0 ? -1 : (int64_t)keys[i - 1];
-  int64_t tc = i == n ? BT : (int64_t)keys[i];
-  if (tc > BT) tc = BT;
-  WCHECK(tp >= -1 && tc <= BT && tp <= tc);
-  for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
-}
-
 // 64-bit (tile << 32 | depth bits) keys of the sorted pairs, for parity copies.
 __global__ void __launch_bounds__(256) k_keys64(const uint32_t* keys, const uint32_t* vals,
                                                 const uint32_t* prevals, const uint32_t* dkey,
@@ -279,6 +322,59 @@ __global__ void __launch_bounds__(256) k_tile_order_place(const int32_t* toff, i
   if (u < BT) order[base[b] + r] = (int32_t)u;
 }
 
+#ifndef WIPES_DUP_HIST_MAXB
+#define WIPES_DUP_HIST_MAXB 2048  // duplicate grids up to this size build the sort histogram
+#endif
+#ifndef WIPES_ORDER_FUSE_MAX
+#define WIPES_ORDER_FUSE_MAX 8192  // up to this many tiles, the last ranges block orders them
+#endif
+
+// Per-tile CSR ranges from the sorted keys: entry i writes toff[u] = i for
+// every tile u in (key[i-1], key[i]]. With `order` set (small BT), the last
+// block to finish also builds the longest-first tile order in shared memory,
+// saving the two tile-order launches.
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, WsHeader* hdr,
+                                                     int64_t cap, int64_t BT, int32_t* toff,
+                                                     int32_t* order) {
+  __shared__ int is_last;
+  __shared__ int32_t h[kBuckets], base[kBuckets];
+  const int tid = threadIdx.x;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t n = clamp_n(hdr, cap);
+  if (i <= n) {
+    int64_t tp = i == 0 ? -1 : (int64_t)keys[i - 1];
+    int64_t tc = i == n ? BT : (int64_t)keys[i];
+    if (tc > BT) tc = BT;
+    WCHECK(tp >= -1 && tc <= BT && tp <= tc);
+    for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
+  }
+  if (!order) return;
+  __threadfence();  // this thread's ranges are visible before the block arrives
+  __syncthreads();
+  if (tid == 0) is_last = atomicAdd(&hdr->arrive[2], 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (tid < kBuckets) h[tid] = 0;
+  __syncthreads();
+  for (int64_t u = tid; u < BT; u += blockDim.x) {
+    const int len = __ldcg(toff + u + 1) - __ldcg(toff + u);
+    atomicAdd(&h[len > 0 ? 32 - __clz(len) : 0], 1);
+  }
+  __syncthreads();
+  if (tid < kBuckets) {
+    int off = 0;  // start of bucket tid in descending-bucket order
+    for (int k = kBuckets - 1; k > tid; --k) off += h[k];
+    base[tid] = off;
+  }
+  __syncthreads();
+  for (int64_t u = tid; u < BT; u += blockDim.x) {
+    const int len = __ldcg(toff + u + 1) - __ldcg(toff + u);
+    order[atomicAdd(&base[len > 0 ? 32 - __clz(len) : 0], 1)] = (int32_t)u;
+  }
+  if (tid == 0) hdr->arrive[2] = 0;  // self-resetting (bin_sort may run again)
+}
+
 __global__ void k_offsets(const int64_t* loc, const int64_t* blk, int64_t BN, int64_t* out) {
   int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o < BN) out[o] = loc[o] + blk[o / kScanTile];
@@ -306,18 +402,15 @@ cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, c
 
 cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s) {
   WsHeader* hdr = (WsHeader*)(ws + L.hdr);
-  int64_t* blk = (int64_t*)(ws + L.blk_sum);
-  if (L.BN > 0) {
-    launch_begin(K_SCAN_BLOCKS, s);
-    k_scan_blocks<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
-        (const int32_t*)(ws + L.count), L.BN, (int64_t*)(ws + L.loc_off), blk);
-    launch_end(K_SCAN_BLOCKS, s);
-  } else {
-    cudaMemsetAsync(blk, 0, sizeof(int64_t), s);
+  if (L.BN == 0) {  // no preprocess launch zeroed the arrival counter
+    cudaError_t e = cudaMemsetAsync(hdr->arrive, 0, sizeof(hdr->arrive), s);
+    if (e != cudaSuccess) return e;
   }
-  launch_begin(K_SCAN_SUMS, s);
-  k_scan_sums<int64_t><<<1, 1024, 0, s>>>(blk, L.nblk_scan, hdr, L.cap);
-  launch_end(K_SCAN_SUMS, s);
+  launch_begin(K_SCAN_BLOCKS, s);
+  k_scan<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
+      (const int32_t*)(ws + L.count), L.BN, (int64_t*)(ws + L.loc_off),
+      (int64_t*)(ws + L.blk_sum), &hdr->arrive[0], hdr, L.cap);
+  launch_end(K_SCAN_BLOCKS, s);
   return cudaGetLastError();
 }
 
@@ -360,12 +453,10 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
                                           (int32_t*)(ws + L.cnt2));
       launch_end(K_DUPLICATE, s);
       launch_begin(K_SCAN_BLOCKS, s);
-      k_scan_blocks<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
-          (const int32_t*)(ws + L.cnt2), L.BN, (int64_t*)(ws + L.loc2), (int64_t*)(ws + L.blk2));
+      k_scan<int32_t, int64_t><<<(unsigned)L.nblk_scan, kScanBlock, 0, s>>>(
+          (const int32_t*)(ws + L.cnt2), L.BN, (int64_t*)(ws + L.loc2), (int64_t*)(ws + L.blk2),
+          &hdr->arrive[1], nullptr, 0);
       launch_end(K_SCAN_BLOCKS, s);
-      launch_begin(K_SCAN_SUMS, s);
-      k_scan_sums<int64_t><<<1, 1024, 0, s>>>((int64_t*)(ws + L.blk2), L.nblk_scan, nullptr, 0);
-      launch_end(K_SCAN_SUMS, s);
       loc = (const int64_t*)(ws + L.loc2);
       blk = (const int64_t*)(ws + L.blk2);
     }
@@ -380,23 +471,36 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     d.row_mod = c.row_mod; d.row_rem = c.row_rem;
     d.keys = kA; d.vals = vA;
     d.prevals = L.det ? (uint32_t*)(ws + L.prevals) : nullptr;
+    // small grids build the tile-key histogram while emitting (one launch
+    // less); large ones leave it to k_sort_hist (fewer global atomics)
+    const bool fuse_hist = L.passes > 0 && gBN <= WIPES_DUP_HIST_MAXB;
+    d.ghist = (uint32_t*)(ws + L.sort_hist);
+    d.npass = L.passes;
     launch_begin(K_DUPLICATE, s);
-    k_duplicate<<<gBN, 256, 0, s>>>(d);
+    if (fuse_hist) {
+      e = cudaMemsetAsync(d.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
+      if (e != cudaSuccess) return e;
+      k_duplicate<true><<<gBN, 256, 0, s>>>(d);
+    } else {
+      k_duplicate<false><<<gBN, 256, 0, s>>>(d);
+    }
     launch_end(K_DUPLICATE, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // stable LSD passes over the (view*T + tile) bits only
     int shifts[kMaxPasses];
     for (int p = 0; p < L.passes; ++p) shifts[p] = 8 * p;
-    e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s);
+    e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s, 1, 0,
+                              fuse_hist);
     if (e != cudaSuccess) return e;
   }
   const uint32_t* kf = *final_in_b ? kB : kA;
+  const bool fuse_order = L.BT > 0 && L.BT <= WIPES_ORDER_FUSE_MAX;
   launch_begin(K_TILE_RANGES, s);
-  k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(kf, hdr, L.cap, L.BT,
-                                                                  (int32_t*)(ws + L.toff));
+  k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(
+      kf, hdr, L.cap, L.BT, (int32_t*)(ws + L.toff), fuse_order ? (int32_t*)(ws + L.order) : nullptr);
   launch_end(K_TILE_RANGES, s);
-  if (L.BT > 0) {
+  if (L.BT > 0 && !fuse_order) {
     const unsigned g = (unsigned)((L.BT + 255) / 256);
     // bucket counters must start at zero for every ordering (bin_sort may run
     // more than once per preprocess)

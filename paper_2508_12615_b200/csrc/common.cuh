@@ -77,6 +77,9 @@ struct WsHeader {
   // longest-first tile order: per-bucket counts and fill pointers (zeroed by
   // the count scan of every preprocess)
   int32_t bcount[kBuckets], bfill[kBuckets];
+  // last-block arrival counters of the fused binning kernels (count scan,
+  // ALPHA order scan, tile ranges); zeroed by preprocess, self-resetting
+  int32_t arrive[4];
 };
 static_assert(sizeof(WsHeader) <= 512, "header must fit its slot");
 
@@ -289,7 +292,8 @@ cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
-                        cudaStream_t s, uint32_t vdiv = 1, uint32_t vmask = 0);
+                        cudaStream_t s, uint32_t vdiv = 1, uint32_t vmask = 0,
+                        bool hist_ready = false);
 cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
                           cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);

@@ -34,6 +34,7 @@ struct PreOut {
   uint32_t* dkey;
   float4* rec;
   uint8_t* cull_flags;
+  int32_t* arrive;  // WsHeader::arrive, zeroed here for the binning kernels that follow
 };
 
 __device__ __forceinline__ bool fin(double x) { return isfinite(x); }
@@ -151,6 +152,7 @@ struct Pre2DArgs {
 
 __global__ void __launch_bounds__(256) k_pre2d(Pre2DArgs a) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 4) a.o.arrive[i] = 0;
   if (i >= a.N) return;
   const Cfg2& c = a.c;
   double mux = a.mean[2 * i], muy = a.mean[2 * i + 1];
@@ -525,6 +527,7 @@ struct Pre3DArgs {
 template <bool EXACT, bool SH>
 __global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < 4) a.o.arrive[gid] = 0;
   if (gid >= (int64_t)a.cams.nv * a.N) return;
   // SH with shared parameters: view-minor order, so a primitive's
   // coefficients (48 floats) are read once from HBM for all its views
@@ -1093,6 +1096,7 @@ PreOut make_out(const Layout& L, char* ws, uint8_t* cull) {
   o.dkey = (uint32_t*)(ws + L.dkey);
   o.rec = (float4*)(ws + L.rec);
   o.cull_flags = cull;
+  o.arrive = ((WsHeader*)(ws + L.hdr))->arrive;
   return o;
 }
 

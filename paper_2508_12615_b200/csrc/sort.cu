@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
-                        cudaStream_t s, uint32_t vdiv, uint32_t vmask) {
+                        cudaStream_t s, uint32_t vdiv, uint32_t vmask, bool hist_ready) {
   if (npass == 0 || cap == 0) return cudaSuccess;
   WIPES_SET_SMEM_ONCE(k_sort_pass<K>, (int)sizeof(SortSmem<K>));
   SortArgs<K> a;
@@ -311,15 +311,18 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   a.vdiv = vdiv ? vdiv : 1u;
   a.vmask = vmask;
   for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
-  cudaError_t e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   a.kin = kA; a.vin = vA; a.pass = 0; a.shift = 0;
-  const int64_t hist_blocks = (cap + WIPES_HIST_KEYS - 1) / WIPES_HIST_KEYS;
-  launch_begin(K_RADIX_HIST, s);
-  k_sort_hist<K><<<(unsigned)(hist_blocks < WIPES_HIST_MAXB ? (hist_blocks > 0 ? hist_blocks : 1)
-                                                              : WIPES_HIST_MAXB),
-                   256, 0, s>>>(a);
-  launch_end(K_RADIX_HIST, s);
+  if (!hist_ready) {  // else the producer zeroed ghist + counters and built the histogram
+    e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
+    if (e != cudaSuccess) return e;
+    const int64_t hist_blocks = (cap + WIPES_HIST_KEYS - 1) / WIPES_HIST_KEYS;
+    launch_begin(K_RADIX_HIST, s);
+    k_sort_hist<K><<<(unsigned)(hist_blocks < WIPES_HIST_MAXB ? (hist_blocks > 0 ? hist_blocks : 1)
+                                                                : WIPES_HIST_MAXB),
+                     256, 0, s>>>(a);
+    launch_end(K_RADIX_HIST, s);
+  }
   const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
   for (int p = 0; p < npass; ++p) {
     const bool from_a = (p & 1) == 0;
@@ -340,10 +343,10 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
 
 template cudaError_t launch_sort<uint32_t>(const Layout&, char*, uint32_t*, uint32_t*,
                                            uint32_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t, uint32_t, uint32_t);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool);
 template cudaError_t launch_sort<uint64_t>(const Layout&, char*, uint64_t*, uint32_t*,
                                            uint64_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t, uint32_t, uint32_t);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool);
 
 size_t sort_smem_bytes64() { return sizeof(SortSmem<uint64_t>); }
 
