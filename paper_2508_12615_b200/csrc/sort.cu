@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(256) k_sort_hist(SortArgs<K> a) {
   }
 }
 
+#ifndef WIPES_SORT_RANK
+#define WIPES_SORT_RANK 1  // lanes with equal digits: 0 = 8 ballots, 1 = shared atomicOr masks
+#endif
+
 template <typename K>
 struct SortSmem {
   K keys[kSortTile];
@@ -126,11 +130,46 @@ struct SortSmem {
   uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
   uint32_t gofs[256];          // global output offset of the tile's first key per digit
   uint32_t tile;
+#if WIPES_SORT_RANK == 1
+  uint32_t match[2][kWarps][257];  // per-warp lane masks of each digit (double-buffered)
+#endif
 };
 
 #ifndef WIPES_SORT_MINB
 #define WIPES_SORT_MINB 4
 #endif
+
+#ifndef WIPES_SORT_LOOKBACK2
+#define WIPES_SORT_LOOKBACK2 4  // larger later windows measured slower (C3 scatter 0.88 ms at 4, 0.90 at 8, 0.96 at 16, 1.05 at 32)
+#endif
+constexpr int kLookBack2 = WIPES_SORT_LOOKBACK2;
+
+// One look-back round of W predecessors (t, t - 1, ...; before tile 0 reads as
+// an inclusive 0): adds their values in tile order up to the first inclusive
+// word (returns true) or the first unpublished one (advances t and sp past the
+// aggregates used, backing off if none was).
+template <int W>
+__device__ __forceinline__ bool lookback_round(const volatile uint32_t*& sp, int& t,
+                                               uint32_t& prefix) {
+  uint32_t s[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) s[j] = t - j >= 0 ? sp[-256 * j] : kFlagInc;
+  int used = 0;
+  bool stop = false;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const uint32_t f = s[j] & ~kValMask;
+    if (stop || used < j || f == 0u) continue;  // unpublished: re-read from here
+    prefix += s[j] & kValMask;
+    ++used;
+    stop = f == kFlagInc;
+  }
+  if (stop) return true;
+  if (used == 0) __nanosleep(WIPES_SORT_BACKOFF);  // predecessor unpublished: back off
+  t -= used;
+  sp -= 256 * used;
+  return false;
+}
 
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(SortArgs<K> a) {
@@ -140,6 +179,9 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   const int64_t n = n_keys(a);
   if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
   for (int i = tid; i < kWarps * 256; i += kSortThreads) (&sm.wcnt[0][0])[i] = 0;
+#if WIPES_SORT_RANK == 1
+  for (int i = tid; i < 2 * kWarps * 257; i += kSortThreads) (&sm.match[0][0][0])[i] = 0;
+#endif
   sm.thist[tid] = 0;  // kSortThreads == 256
   __syncthreads();
   const uint32_t tile = sm.tile;
@@ -171,6 +213,33 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   st[(int64_t)tile * 256 + tid] = kFlagAgg | sm.thist[tid];
   // only the last tile has invalid slots (digit 256): full tiles match 8 bits
   const bool full_tile = base + kSortTile <= n;
+#if WIPES_SORT_RANK == 1
+  (void)full_tile;
+  // lanes with the same digit: every lane ORs its bit into its digit's mask
+  // (warp-private shared words) and, after a warp barrier, reads the mask back.
+  // The digit's first lane (the leader) advances the warp's running count after
+  // a second barrier, and clears its mask one step later (two buffers: the
+  // clear falls between the next step's barriers, after every lane has read the
+  // mask and before the buffer's next use).
+  uint32_t prev_d = 256u;
+  bool prev_lead = false;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t d = dig[i];
+    uint32_t* mrow = sm.match[i & 1][wid];
+    atomicOr(&mrow[d], 1u << lane);
+    __syncwarp();
+    if (prev_lead) sm.match[(i + 1) & 1][wid][prev_d] = 0u;  // step i - 1's mask
+    const uint32_t peers = *(volatile uint32_t*)&mrow[d];
+    const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;
+    rank[i] = before + __popc(peers & lt);
+    const bool lead = (peers & lt) == 0;
+    __syncwarp();
+    if (lead && d < 256u) sm.wcnt[wid][d] = before + __popc(peers);
+    prev_d = d;
+    prev_lead = lead;
+  }
+#else
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = dig[i];
@@ -196,6 +265,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     if (d < 256u && (peers & lt) == 0) sm.wcnt[wid][d] = before + __popc(peers);
     __syncwarp();
   }
+#endif
   __syncthreads();
   // ---- per digit (thread tid = digit): warp prefixes, tile count ---------
   const int d = tid;  // kSortThreads == 256
@@ -218,33 +288,18 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     --t;
   }
 #else
-  // look back kLookBack predecessors per round: their status words are loaded
+  // look back over the predecessors: kLookBack status words per first round,
+  // kLookBack2 per later round (the first wave of CTAs starts together, so its
+  // tiles walk back across hundreds of aggregates; later tiles mostly find an
+  // inclusive prefix one or two tiles back). The words of a round are loaded
   // together (independent loads), then consumed in tile order. 32-bit tile
-  // index and one running pointer (the 64-bit index math of every load was a
-  // third of the pass's instructions at C3).
+  // index and one running pointer.
   {
     int t = (int)tile - 1;
     const volatile uint32_t* sp = st + (int64_t)t * 256 + d;
-    while (t >= 0) {
-      uint32_t s[kLookBack];
-#pragma unroll
-      for (int j = 0; j < kLookBack; ++j)
-        s[j] = t - j >= 0 ? sp[-256 * j] : (2u << 30);  // before tile 0: inclusive 0
-      int used = 0;
-      bool stop = false;
-#pragma unroll
-      for (int j = 0; j < kLookBack; ++j) {
-        const uint32_t f = s[j] & ~kValMask;
-        if (stop || used < j || f == 0u) continue;  // unpublished: re-read from here
-        prefix += s[j] & kValMask;
-        ++used;
-        stop = f == kFlagInc;
+    if (t >= 0 && !lookback_round<kLookBack>(sp, t, prefix))
+      while (!lookback_round<kLookBack2>(sp, t, prefix)) {
       }
-      if (stop) break;
-      if (used == 0) __nanosleep(WIPES_SORT_BACKOFF);  // predecessor unpublished: back off
-      t -= used;
-      sp -= 256 * used;
-    }
   }
 #endif
   // flag and value share one 32-bit word: no fence needed between publishes
