@@ -330,23 +330,38 @@ __global__ void __launch_bounds__(256) k_tile_order_place(const int32_t* toff, i
 #endif
 
 // Per-tile CSR ranges from the sorted keys: entry i writes toff[u] = i for
-// every tile u in (key[i-1], key[i]]. With `order` set (small BT), the last
-// block to finish also builds the longest-first tile order in shared memory,
-// saving the two tile-order launches.
+// every tile u in (key[i-1], key[i]] (entry n closes the list with BT). Each
+// thread takes four consecutive entries (one 16-byte key load). With `order`
+// set (small BT), the last block to finish also builds the longest-first tile
+// order in shared memory, saving the two tile-order launches.
 __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, WsHeader* hdr,
                                                      int64_t cap, int64_t BT, int32_t* toff,
                                                      int32_t* order) {
   __shared__ int is_last;
   __shared__ int32_t h[kBuckets], base[kBuckets];
   const int tid = threadIdx.x;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + tid);
   const int64_t n = clamp_n(hdr, cap);
-  if (i <= n) {
-    int64_t tp = i == 0 ? -1 : (int64_t)keys[i - 1];
-    int64_t tc = i == n ? BT : (int64_t)keys[i];
-    if (tc > BT) tc = BT;
-    WCHECK(tp >= -1 && tc <= BT && tp <= tc);
-    for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
+  if (i0 <= n) {
+    uint32_t k[4];
+    if (i0 + 4 <= n) {
+      const uint4 v = *reinterpret_cast<const uint4*>(keys + i0);
+      k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) k[e] = i0 + e < n ? keys[i0 + e] : 0u;
+    }
+    int64_t tp = i0 == 0 ? -1 : (int64_t)keys[i0 - 1];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t i = i0 + e;
+      if (i > n) break;
+      int64_t tc = i == n ? BT : (int64_t)k[e];
+      if (tc > BT) tc = BT;
+      WCHECK(tp >= -1 && tc <= BT && tp <= tc);
+      for (int64_t u = tp + 1; u <= tc; ++u) toff[u] = (int32_t)i;
+      tp = tc;
+    }
   }
   if (!order) return;
   __threadfence();  // this thread's ranges are visible before the block arrives
@@ -497,7 +512,7 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
   const uint32_t* kf = *final_in_b ? kB : kA;
   const bool fuse_order = L.BT > 0 && L.BT <= WIPES_ORDER_FUSE_MAX;
   launch_begin(K_TILE_RANGES, s);
-  k_tile_ranges<<<(unsigned)((L.cap + 1 + 255) / 256), 256, 0, s>>>(
+  k_tile_ranges<<<(unsigned)((L.cap + 1 + 1023) / 1024), 256, 0, s>>>(
       kf, hdr, L.cap, L.BT, (int32_t*)(ws + L.toff), fuse_order ? (int32_t*)(ws + L.order) : nullptr);
   launch_end(K_TILE_RANGES, s);
   if (L.BT > 0 && !fuse_order) {

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     if (prev_lead) sm.match[(i + 1) & 1][wid][prev_d] = 0u;  // step i - 1's mask
     const uint32_t peers = *(volatile uint32_t*)&mrow[d];
     const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;
-    rank[i] = before + __popc(peers & lt);
+    rank[i] = (d << 16) | (before + __popc(peers & lt));  // digit | rank (< 2^16)
     const bool lead = (peers & lt) == 0;
     __syncwarp();
     if (lead && d < 256u) sm.wcnt[wid][d] = before + __popc(peers);
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     }
 #endif
     const uint32_t before = d < 256u ? sm.wcnt[wid][d] : 0u;
-    rank[i] = before + __popc(peers & lt);
+    rank[i] = (d << 16) | (before + __popc(peers & lt));  // digit | rank (< 2^16)
     __syncwarp();
     if (d < 256u && (peers & lt) == 0) sm.wcnt[wid][d] = before + __popc(peers);
     __syncwarp();
@@ -325,9 +325,9 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   // ---- stage in tile-sorted order, then coalesced write-out -----------------
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t dd = dig[i];
+    const uint32_t dd = rank[i] >> 16;
     if (dd < 256u) {
-      const uint32_t loc = sm.bexcl[dd] + sm.wcnt[wid][dd] + rank[i];
+      const uint32_t loc = sm.bexcl[dd] + sm.wcnt[wid][dd] + (rank[i] & 0xffffu);
       WCHECK(loc < (uint32_t)kSortTile);
       sm.keys[loc] = key[i];
       sm.vals[loc] = val[i];
