@@ -129,10 +129,10 @@ struct SortSmem {
   uint32_t thist[256];         // tile digit histogram (published before the ranking)
   uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
   uint32_t gofs[256];          // global output offset of the tile's first key per digit
-  uint32_t tile;
 #if WIPES_SORT_RANK == 1
-  uint32_t match[2][kWarps][257];  // per-warp lane masks of each digit (double-buffered)
+  uint32_t match[2][kWarps][260];  // per-warp lane masks of each digit, 257 used (double-buffered)
 #endif
+  uint32_t tile;
 };
 
 #ifndef WIPES_SORT_MINB
@@ -148,12 +148,23 @@ constexpr int kLookBack2 = WIPES_SORT_LOOKBACK2;
 // an inclusive 0): adds their values in tile order up to the first inclusive
 // word (returns true) or the first unpublished one (advances t and sp past the
 // aggregates used, backing off if none was).
+// Look-back status words: relaxed GPU-scope accesses (flag and value share one
+// word, so no ordering beyond the word itself is needed).
+__device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int W>
-__device__ __forceinline__ bool lookback_round(const volatile uint32_t*& sp, int& t,
+__device__ __forceinline__ bool lookback_round(const uint32_t*& sp, int& t,
                                                uint32_t& prefix) {
   uint32_t s[W];
 #pragma unroll
-  for (int j = 0; j < W; ++j) s[j] = t - j >= 0 ? sp[-256 * j] : kFlagInc;
+  for (int j = 0; j < W; ++j) s[j] = t - j >= 0 ? ld_status(sp - 256 * j) : kFlagInc;
   int used = 0;
   bool stop = false;
 #pragma unroll
@@ -178,11 +189,6 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n = n_keys(a);
   if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
-  for (int i = tid; i < kWarps * 256; i += kSortThreads) (&sm.wcnt[0][0])[i] = 0;
-#if WIPES_SORT_RANK == 1
-  for (int i = tid; i < 2 * kWarps * 257; i += kSortThreads) (&sm.match[0][0][0])[i] = 0;
-#endif
-  sm.thist[tid] = 0;  // kSortThreads == 256
   __syncthreads();
   const uint32_t tile = sm.tile;
   const int64_t base = (int64_t)tile * kSortTile;
@@ -200,17 +206,33 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     const bool valid = idx < n;
     key[i] = valid ? a.kin[idx] : (K)0;
     val[i] = valid ? a.vin[idx] : 0u;
-    const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
-    dig[i] = valid ? (src & 255u) : 256u;
   }
+  // zero the counters (16-byte stores) while the key loads are in flight
+  {
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    uint4* w4 = reinterpret_cast<uint4*>(&sm.wcnt[0][0]);
+    for (int i = tid; i < kWarps * 256 / 4; i += kSortThreads) w4[i] = z;
+#if WIPES_SORT_RANK == 1
+    uint4* m4 = reinterpret_cast<uint4*>(&sm.match[0][0][0]);
+    for (int i = tid; i < 2 * kWarps * 260 / 4; i += kSortThreads) m4[i] = z;
+#endif
+    sm.thist[tid] = 0;  // kSortThreads == 256
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
+    const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
+    dig[i] = idx < n ? (src & 255u) : 256u;
+  }
+  __syncthreads();
   // tile histogram first, so the aggregate is published before the ranking
   // and the successors' look-back rarely has to wait for it
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i)
     if (dig[i] < 256u) atomicAdd(&sm.thist[dig[i]], 1u);
   __syncthreads();
-  volatile uint32_t* st = a.status;
-  st[(int64_t)tile * 256 + tid] = kFlagAgg | sm.thist[tid];
+  uint32_t* st = a.status;
+  st_status(st + (int64_t)tile * 256 + tid, kFlagAgg | sm.thist[tid]);
   // only the last tile has invalid slots (digit 256): full tiles match 8 bits
   const bool full_tile = base + kSortTile <= n;
 #if WIPES_SORT_RANK == 1
@@ -280,7 +302,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   uint32_t prefix = 0;
 #ifdef WIPES_SORT_LB1
   for (int64_t t = (int64_t)tile - 1; t >= 0;) {
-    const uint32_t s = st[t * 256 + d];
+    const uint32_t s = ld_status(st + t * 256 + d);
     const uint32_t f = s & ~kValMask;
     if (f == 0u) continue;  // not yet published: spin
     prefix += s & kValMask;
@@ -296,14 +318,14 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   // index and one running pointer.
   {
     int t = (int)tile - 1;
-    const volatile uint32_t* sp = st + (int64_t)t * 256 + d;
+    const uint32_t* sp = st + (int64_t)t * 256 + d;
     if (t >= 0 && !lookback_round<kLookBack>(sp, t, prefix))
       while (!lookback_round<kLookBack2>(sp, t, prefix)) {
       }
   }
 #endif
   // flag and value share one 32-bit word: no fence needed between publishes
-  st[(int64_t)tile * 256 + d] = kFlagInc | (prefix + cnt);
+  st_status(st + (int64_t)tile * 256 + d, kFlagInc | (prefix + cnt));
   // global digit base = exclusive scan of the pass histogram (block scan)
   const uint32_t gh = a.ghist[a.pass * 256 + d];
   uint32_t incl_g = gh, incl_b = cnt;
