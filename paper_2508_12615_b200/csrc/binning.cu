@@ -79,14 +79,21 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(const TIn* in, int64_t n, T
   __shared__ int is_last;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * kScanItems;
+  static_assert(sizeof(TIn) == 4 && sizeof(TOut) == 8 && kScanItems == 8, "vector path");
   TOut v[kScanItems];
   TOut s = 0;
+  const bool whole = base + kScanItems <= n;  // a thread's 8 items: two 16-byte loads
+  if (whole) {
+    const int4 a0 = reinterpret_cast<const int4*>(in + base)[0];
+    const int4 a1 = reinterpret_cast<const int4*>(in + base)[1];
+    v[0] = (TOut)a0.x; v[1] = (TOut)a0.y; v[2] = (TOut)a0.z; v[3] = (TOut)a0.w;
+    v[4] = (TOut)a1.x; v[5] = (TOut)a1.y; v[6] = (TOut)a1.z; v[7] = (TOut)a1.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t idx = base + k;
-    v[k] = idx < n ? (TOut)in[idx] : (TOut)0;
-    s += v[k];
+    for (int k = 0; k < kScanItems; ++k) v[k] = base + k < n ? (TOut)in[base + k] : (TOut)0;
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) s += v[k];
   // inclusive warp scan of thread sums
   TOut inc = s;
 #pragma unroll
@@ -112,12 +119,19 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(const TIn* in, int64_t n, T
   }
   __syncthreads();
   if (tid == 0) is_last = atomicAdd(arrive, 1) == (int)gridDim.x - 1;
-  TOut run = warp_tot[wid] + inc - s;
+  TOut r[kScanItems];
+  r[0] = warp_tot[wid] + inc - s;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t idx = base + k;
-    if (idx < n) loc[idx] = run;
-    run += v[k];
+  for (int k = 1; k < kScanItems; ++k) r[k] = r[k - 1] + v[k - 1];
+  if (whole) {  // four 16-byte stores
+    longlong2* o = reinterpret_cast<longlong2*>(loc + base);
+#pragma unroll
+    for (int k = 0; k < kScanItems / 2; ++k)
+      o[k] = make_longlong2((long long)r[2 * k], (long long)r[2 * k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (base + k < n) loc[base + k] = r[k];
   }
   __syncthreads();
   if (is_last) {

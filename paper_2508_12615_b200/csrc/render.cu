@@ -784,7 +784,7 @@ __device__ __forceinline__ void bwd_pair(bool h0, bool h1, float e0, float e1, f
   m.c2 = __ffma2_rn(cw, g[2], m.c2);
 }
 
-template <int TS, bool ALPHA, bool EXACT, bool F64>
+template <int TS, bool ALPHA, bool EXACT, bool F64, bool DET>
 __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
                                             : (ALPHA ? WIPES_MINB_BWD_ALPHA : WIPES_MINB_BWD))
     k_render_bwd(RenderArgs a) {
@@ -800,6 +800,10 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
   const int q3 = (lane >> 1) & 3;
   const int my_m = SMRED ? (lane >> 1) : 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
   const bool writer = SMRED ? (!(lane & 1) && lane < 2 * kMom) : (!(lane & 1) && q3 < 3);
+  // the moment this lane writes, kMom if none, held in a register the compiler
+  // cannot rematerialise (it recomputed the lane arithmetic for every record)
+  int wm;
+  asm volatile("mov.b32 %0, %1;" : "=r"(wm) : "r"(writer ? my_m : kMom));
   Item it;
   int pf = (WIPES_ITEM_PREFETCH && lane == 0) ? atomicAdd(&a.hdr->work[a.queue], 1) : 0;
   while (next_item<TS>(a, lane, ALPHA ? 1 : a.chunks, it, pf)) {
@@ -935,7 +939,7 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
 #pragma unroll
           for (int off = 16; off; off >>= 1) mb += __shfl_xor_sync(kFull, mb, off);
         }
-        if (a.slots) {  // deterministic: this warp's slot of (dup, footprint); no atomics
+        if constexpr (DET) {  // deterministic: this warp's slot of (dup, footprint); no atomics
           const int64_t si = (int64_t)ws.dj[i] * a.fps + it.sub;
           WCHECK(ws.dj[i] >= 0 && it.sub < a.fps);
           float* sl = a.slots + si * a.slotw;
@@ -943,8 +947,8 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
           if (EXACT && lane == 0) sl[kMom] = mb;
           if (lane == 0) a.slotmask[si] = 1;
         } else {
-          WCHECK(!writer || (my_m >= 0 && my_m < kMom && ws.pid[i] >= 0 && ws.pid[i] < a.N));
-          if (writer) red_add(a.mom + (vN + ws.pid[i]) * kMom + my_m, red);
+          WCHECK(wm >= kMom || (wm >= 0 && ws.pid[i] >= 0 && ws.pid[i] < a.N));
+          if (wm < kMom) red_add(a.mom + (vN + ws.pid[i]) * kMom + wm, red);
           if (EXACT && lane == 0) red_add(a.mom_beta + vN + ws.pid[i], mb);
         }
       }
@@ -997,22 +1001,27 @@ cudaError_t launch_fwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int TS, bool DET>
+void (*pick_bwd(bool alpha, bool exact, bool f64))(RenderArgs) {
+  if (f64) {
+    if (exact)
+      return alpha ? k_render_bwd<TS, true, true, true, DET> : k_render_bwd<TS, false, true, true, DET>;
+    return alpha ? k_render_bwd<TS, true, false, true, DET> : k_render_bwd<TS, false, false, true, DET>;
+  }
+  if (exact)
+    return alpha ? k_render_bwd<TS, true, true, false, DET> : k_render_bwd<TS, false, true, false, DET>;
+  return alpha ? k_render_bwd<TS, true, false, false, DET> : k_render_bwd<TS, false, false, false, DET>;
+}
+
 template <int TS>
 cudaError_t launch_bwd_ts(bool alpha, RenderArgs ra, cudaStream_t s) {
   ra.queue = Q_BWD;
   const int64_t items = ra.BT * Geo<TS>::S * (alpha ? 1 : ra.chunks);
   void (*k)(RenderArgs);
-  if (ra.f64) {
-    if (ra.mom_beta)
-      k = alpha ? k_render_bwd<TS, true, true, true> : k_render_bwd<TS, false, true, true>;
-    else
-      k = alpha ? k_render_bwd<TS, true, false, true> : k_render_bwd<TS, false, false, true>;
-  } else {
-    if (ra.mom_beta)
-      k = alpha ? k_render_bwd<TS, true, true, false> : k_render_bwd<TS, false, true, false>;
-    else
-      k = alpha ? k_render_bwd<TS, true, false, false> : k_render_bwd<TS, false, false, false>;
-  }
+  if (ra.slots)
+    k = pick_bwd<TS, true>(alpha, ra.mom_beta != nullptr, ra.f64 != 0);
+  else
+    k = pick_bwd<TS, false>(alpha, ra.mom_beta != nullptr, ra.f64 != 0);
   launch_begin(K_RENDER_BWD, s);
   k<<<persistent_grid(k, items), kCta, 0, s>>>(ra);
   launch_end(K_RENDER_BWD, s);
