@@ -22,6 +22,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
           f"-I{os.path.join(ROOT, 'include')}"]
 SOURCES = {
     "preprocess.cu": ["--fmad=false"],
+    "preprocess_bwd.cu": [],
     "binning.cu": [],
     "sort.cu": [],
     "render.cu": [],

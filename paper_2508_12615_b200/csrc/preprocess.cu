@@ -23,6 +23,11 @@ constexpr double kLog2e = 1.4426950408889634;
 #ifndef WIPES_PRE3D_MINB
 #define WIPES_PRE3D_MINB 2  // min CTAs/SM, FP64 3D backward (no spills at 234 registers)
 #endif
+#ifndef WIPES_PRE3D_VMINOR
+#define WIPES_PRE3D_VMINOR 0  // 1: views of a primitive in adjacent threads for flat colour too
+                              // (C3 k_pre3d 0.419 -> 0.452 ms: the scattered record writes cost
+                              // more than the 465 MB of parameter re-reads save)
+#endif
 #ifndef WIPES_PRE3D_FWD_MINB
 #define WIPES_PRE3D_FWD_MINB 8  // min CTAs/SM, FP64 3D forward (measured faster at 64 registers)
 #endif
@@ -150,6 +155,7 @@ struct Pre2DArgs {
   PreOut o;
 };
 
+#ifndef WIPES_PRE_BWD_TU  // forward kernels: this TU is built with --fmad=false (pinned FP64)
 __global__ void __launch_bounds__(256) k_pre2d(Pre2DArgs a) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 4) a.o.arrive[i] = 0;
@@ -186,6 +192,8 @@ __global__ void __launch_bounds__(256) k_pre2d(Pre2DArgs a) {
   else
     zero_record(a.o.rec + 4 * i);
 }
+
+#endif
 
 // ---------------------------------------------------------------- 3D ------
 struct Proj3 {
@@ -524,6 +532,7 @@ struct Pre3DArgs {
   CamBlock cams;
 };
 
+#ifndef WIPES_PRE_BWD_TU  // forward kernels
 template <bool EXACT, bool SH>
 __global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB)
   if (gid >= (int64_t)a.cams.nv * a.N) return;
   // SH with shared parameters: view-minor order, so a primitive's
   // coefficients (48 floats) are read once from HBM for all its views
-  const bool vminor = SH && a.view_stride == 0;
+  const bool vminor = (SH || WIPES_PRE3D_VMINOR) && a.view_stride == 0;
   int vl = vminor ? (int)(gid % a.cams.nv) : (int)(gid / a.N);
   int64_t i = vminor ? gid / a.cams.nv : gid - (int64_t)vl * a.N;
   int v = a.cams.v0 + vl;
@@ -618,6 +627,8 @@ __global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB)
     zero_record(a.o.rec + 4 * o);
 }
 
+#endif
+
 // ------------------------------------------------------------- backward ----
 // conic -> covariance: G_Sigma = -A G_A A, G_A = [[ga, gb/2],[gb/2, gc]];
 // returns (g_xx, g_xy (off-diagonal counted twice), g_yy).
@@ -671,6 +682,7 @@ struct Bwd2DArgs {
   wipes_grads g;
 };
 
+#ifdef WIPES_PRE_BWD_TU  // backward kernels: preprocess_bwd.cu builds them with FMA contraction
 __global__ void __launch_bounds__(256) k_pre2d_bwd(Bwd2DArgs a) {
   int64_t i = a.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.row1) return;
@@ -1077,6 +1089,8 @@ void launch_sh_bwd(const Bwd3DArgs& a, int views_per_row, cudaStream_t s) {
   else go(k_sh_bwd<DEG, 1>, 1);
 }
 
+#endif
+
 Cfg2 make_cfg2(const wipes_config& c, const Layout& L) {
   Cfg2 r;
   r.W = c.width; r.H = c.height; r.tile = c.tile; r.GX = L.GX; r.GY = L.GY;
@@ -1113,6 +1127,7 @@ void fill_cams(CamBlock& cb, const wipes_camera* cams, int v0, int nv) {
 
 }  // namespace
 
+#ifndef WIPES_PRE_BWD_TU  // forward launchers
 cudaError_t launch_preprocess2d(const wipes_config& c, const wipes_params& p, const Layout& L,
                                 char* ws, uint8_t* cull_flags, cudaStream_t s) {
   if (L.N == 0) return cudaSuccess;
@@ -1161,6 +1176,9 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
   return cudaSuccess;
 }
 
+#endif
+
+#ifdef WIPES_PRE_BWD_TU  // backward launchers
 cudaError_t launch_preprocess2d_bwd(const wipes_config& c, const wipes_params& p,
                                     const Layout& L, char* ws, const wipes_grads& g,
                                     cudaStream_t s, int64_t row0, int64_t row1) {
@@ -1245,5 +1263,7 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
   }
   return cudaSuccess;
 }
+
+#endif
 
 }  // namespace wipes
