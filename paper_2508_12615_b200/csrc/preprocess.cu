@@ -214,18 +214,9 @@ __device__ __forceinline__ double s3at(const double* S, int i, int j) {
 
 // O2 steps 1-9 in the pinned order. PINNED = false (backward
 // only, where no integer decision is taken) replaces divisions by reciprocals.
+// The view-independent half: normalised quaternion, rotation and S3 = R S^2 R^T.
 template <bool PINNED = true>
-__device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_clamp,
-                         const double* mu, const double* s, const double* q, const double* f,
-                         Proj3& P) {
-  double Rv[9];
-  for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
-  double t0 = cam[9], t1 = cam[10], t2 = cam[11];
-  double fx = cam[12], fy = cam[13];
-  P.p[0] = ((Rv[0] * mu[0] + Rv[1] * mu[1]) + Rv[2] * mu[2]) + t0;
-  P.p[1] = ((Rv[3] * mu[0] + Rv[4] * mu[1]) + Rv[5] * mu[2]) + t1;
-  P.p[2] = ((Rv[6] * mu[0] + Rv[7] * mu[1]) + Rv[8] * mu[2]) + t2;
-  double x = P.p[0], y = P.p[1], z = P.p[2];
+__device__ __forceinline__ void project3_prim(const double* s, const double* q, Proj3& P) {
   double w = q[0], qx = q[1], qy = q[2], qz = q[3];
   double n = sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
   if (PINNED) {
@@ -251,6 +242,22 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
     for (int j = i; j < 3; ++j)
       P.S3[k++] = (((R[3 * i] * s2[0]) * R[3 * j] + (R[3 * i + 1] * s2[1]) * R[3 * j + 1]) +
                    (R[3 * i + 2] * s2[2]) * R[3 * j + 2]);
+}
+
+// The per-view half (P.S3 from project3_prim): camera-space mean, EWA Jacobian,
+// Sigma' = M S3 M^T and the rotated frequency.
+template <bool PINNED = true>
+__device__ __forceinline__ void project3_view(const float* cam, int32_t W, int32_t H,
+                                              int32_t ewa_clamp, const double* mu,
+                                              const double* f, Proj3& P) {
+  double Rv[9];
+  for (int k = 0; k < 9; ++k) Rv[k] = cam[k];
+  double t0 = cam[9], t1 = cam[10], t2 = cam[11];
+  double fx = cam[12], fy = cam[13];
+  P.p[0] = ((Rv[0] * mu[0] + Rv[1] * mu[1]) + Rv[2] * mu[2]) + t0;
+  P.p[1] = ((Rv[3] * mu[0] + Rv[4] * mu[1]) + Rv[5] * mu[2]) + t1;
+  P.p[2] = ((Rv[6] * mu[0] + Rv[7] * mu[1]) + Rv[8] * mu[2]) + t2;
+  double x = P.p[0], y = P.p[1], z = P.p[2];
   const double rz = PINNED ? 0.0 : 1.0 / z;
   double tx = PINNED ? x / z : x * rz, ty = PINNED ? y / z : y * rz;
   P.clx = P.cly = false;
@@ -289,6 +296,14 @@ __device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_cla
   P.g[0] = ((Rv[0] * f[0] + Rv[1] * f[1]) + Rv[2] * f[2]);
   P.g[1] = ((Rv[3] * f[0] + Rv[4] * f[1]) + Rv[5] * f[2]);
   P.g[2] = ((Rv[6] * f[0] + Rv[7] * f[1]) + Rv[8] * f[2]);
+}
+
+template <bool PINNED = true>
+__device__ void project3(const float* cam, int32_t W, int32_t H, int32_t ewa_clamp,
+                         const double* mu, const double* s, const double* q, const double* f,
+                         Proj3& P) {
+  project3_prim<PINNED>(s, q, P);
+  project3_view<PINNED>(cam, W, H, ewa_clamp, mu, f, P);
 }
 
 // ------------------------------------------------ exact projection (NEXT-1) --
@@ -533,56 +548,29 @@ struct Pre3DArgs {
 };
 
 #ifndef WIPES_PRE_BWD_TU  // forward kernels
-template <bool EXACT, bool SH>
-__global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid < 4) a.o.arrive[gid] = 0;
-  if (gid >= (int64_t)a.cams.nv * a.N) return;
-  // SH with shared parameters: view-minor order, so a primitive's
-  // coefficients (48 floats) are read once from HBM for all its views
-  const bool vminor = (SH || WIPES_PRE3D_VMINOR) && a.view_stride == 0;
-  int vl = vminor ? (int)(gid % a.cams.nv) : (int)(gid / a.N);
-  int64_t i = vminor ? gid / a.cams.nv : gid - (int64_t)vl * a.N;
-  int v = a.cams.v0 + vl;
-  int64_t o = (int64_t)v * a.N + i;
-  int64_t pi = (int64_t)v * a.view_stride + i;
-  const float* cam = a.cams.v[vl];
+// One (view, primitive) record from its loaded parameters. With have_prim the
+// caller has already run project3_prim (once for all views of the primitive);
+// the arithmetic is the same either way (the halves are independent).
+template <bool EXACT>
+__device__ __forceinline__ void pre3d_record(const Pre3DArgs& a, const float* cam, int64_t o,
+                                             bool ok, const double* mu, const double* s,
+                                             const double* q, const double* f, double phi,
+                                             double cr, double cg, double cb, double al,
+                                             bool have_prim, Proj3& P) {
   const Cfg2& c = a.c;
-  double mu[3] = {a.mean[3 * pi], a.mean[3 * pi + 1], a.mean[3 * pi + 2]};
-  double s[3] = {a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2]};
-  double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
-  double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
-  double phi = a.phase ? (double)a.phase[pi] : 0.0;
-  double cr = 0.0, cg = 0.0, cb = 0.0;
-  if (!SH) { cr = a.color[3 * pi]; cg = a.color[3 * pi + 1]; cb = a.color[3 * pi + 2]; }
-  double al = a.opacity[pi];
   int4 rect = make_int4(0, 0, 0, 0);
   int32_t cnt = 0;
   int flag = 0;
   uint32_t dk = 0;
   double conic[3] = {0, 0, 0}, ext[2] = {0, 0};
   double mux = 0, muy = 0, fpx = 0, fpy = 0, beta = 1.0;
-  double qq = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
-  bool ok = fin(mu[0]) && fin(mu[1]) && fin(mu[2]) && fin(s[0]) && fin(s[1]) && fin(s[2]) &&
-            fin(q[0]) && fin(q[1]) && fin(q[2]) && fin(q[3]) && fin(f[0]) && fin(f[1]) &&
-            fin(f[2]) && fin(phi) && fin(al) && fin(cr) && fin(cg) && fin(cb) && (qq > 0.0);
-  if (SH && ok) {  // NEXT-3: view-dependent colour from SH
-    double d[3], Y[16];
-    view_dir(cam, mu, d);
-    sh_basis(a.sh_deg, d[0], d[1], d[2], Y, nullptr);
-    const int K = (a.sh_deg + 1) * (a.sh_deg + 1);
-    const float* shp = a.sh + (int64_t)3 * K * pi;
-    double rgb[3] = {0.5, 0.5, 0.5};
-    for (int k = 0; k < K; ++k)
-      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * (double)shp[3 * k + ch];
-    cr = fmax(rgb[0], 0.0); cg = fmax(rgb[1], 0.0); cb = fmax(rgb[2], 0.0);
-    ok = fin(rgb[0]) && fin(rgb[1]) && fin(rgb[2]);
-  }
   if (!ok) {
     flag = 5;
   } else {
-    Proj3 P;
-    project3(cam, c.W, c.H, a.ewa_clamp, mu, s, q, f, P);
+    if (have_prim)
+      project3_view(cam, c.W, c.H, a.ewa_clamp, mu, f, P);
+    else
+      project3(cam, c.W, c.H, a.ewa_clamp, mu, s, q, f, P);
     double x = P.p[0], y = P.p[1], z = P.p[2];
     double nz = cam[16], fz = cam[17];
     if (!(z >= nz && z <= fz)) {
@@ -625,6 +613,86 @@ __global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB)
     write_record(a.o.rec + 4 * o, mux, muy, conic, al, fpx, fpy, phi, beta, cr, cg, cb, ext);
   else
     zero_record(a.o.rec + 4 * o);
+}
+
+__device__ __forceinline__ bool params_finite(const double* mu, const double* s, const double* q,
+                                              const double* f, double phi, double al, double cr,
+                                              double cg, double cb) {
+  double qq = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+  return fin(mu[0]) && fin(mu[1]) && fin(mu[2]) && fin(s[0]) && fin(s[1]) && fin(s[2]) &&
+         fin(q[0]) && fin(q[1]) && fin(q[2]) && fin(q[3]) && fin(f[0]) && fin(f[1]) &&
+         fin(f[2]) && fin(phi) && fin(al) && fin(cr) && fin(cg) && fin(cb) && (qq > 0.0);
+}
+
+// One thread per (view, primitive) record.
+template <bool EXACT, bool SH>
+__global__ void __launch_bounds__(128, (EXACT || SH) ? 2 : WIPES_PRE3D_FWD_MINB) k_pre3d(const __grid_constant__ Pre3DArgs a) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < 4) a.o.arrive[gid] = 0;
+  if (gid >= (int64_t)a.cams.nv * a.N) return;
+  // SH with shared parameters: view-minor order, so a primitive's
+  // coefficients (48 floats) are read once from HBM for all its views
+  const bool vminor = (SH || WIPES_PRE3D_VMINOR) && a.view_stride == 0;
+  int vl = vminor ? (int)(gid % a.cams.nv) : (int)(gid / a.N);
+  int64_t i = vminor ? gid / a.cams.nv : gid - (int64_t)vl * a.N;
+  int v = a.cams.v0 + vl;
+  int64_t o = (int64_t)v * a.N + i;
+  int64_t pi = (int64_t)v * a.view_stride + i;
+  const float* cam = a.cams.v[vl];
+  double mu[3] = {a.mean[3 * pi], a.mean[3 * pi + 1], a.mean[3 * pi + 2]};
+  double s[3] = {a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2]};
+  double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
+  double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
+  double phi = a.phase ? (double)a.phase[pi] : 0.0;
+  double cr = 0.0, cg = 0.0, cb = 0.0;
+  if (!SH) { cr = a.color[3 * pi]; cg = a.color[3 * pi + 1]; cb = a.color[3 * pi + 2]; }
+  double al = a.opacity[pi];
+  bool ok = params_finite(mu, s, q, f, phi, al, cr, cg, cb);
+  if (SH && ok) {  // NEXT-3: view-dependent colour from SH
+    double d[3], Y[16];
+    view_dir(cam, mu, d);
+    sh_basis(a.sh_deg, d[0], d[1], d[2], Y, nullptr);
+    const int K = (a.sh_deg + 1) * (a.sh_deg + 1);
+    const float* shp = a.sh + (int64_t)3 * K * pi;
+    double rgb[3] = {0.5, 0.5, 0.5};
+    for (int k = 0; k < K; ++k)
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * (double)shp[3 * k + ch];
+    cr = fmax(rgb[0], 0.0); cg = fmax(rgb[1], 0.0); cb = fmax(rgb[2], 0.0);
+    ok = fin(rgb[0]) && fin(rgb[1]) && fin(rgb[2]);
+  }
+  Proj3 P;
+  pre3d_record<EXACT>(a, cam, o, ok, mu, s, q, f, phi, cr, cg, cb, al, false, P);
+}
+
+#ifndef WIPES_PRE3D_LOOP
+#define WIPES_PRE3D_LOOP 1  // shared parameters, flat colour: one thread per primitive
+#endif
+#ifndef WIPES_PRE3D_LOOP_MINB
+#define WIPES_PRE3D_LOOP_MINB 4
+#endif
+
+// Shared parameters (view_stride 0), flat colour: one thread per primitive
+// loads its parameters once, runs the view-independent half of the projection
+// (quaternion normalisation, R, S3) once, and emits the records of all the
+// launch's views in view order (record o = v N + i: coalesced per view).
+template <bool EXACT>
+__global__ void __launch_bounds__(128, WIPES_PRE3D_LOOP_MINB) k_pre3d_loop(const __grid_constant__ Pre3DArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 4) a.o.arrive[i] = 0;
+  if (i >= a.N) return;
+  double mu[3] = {a.mean[3 * i], a.mean[3 * i + 1], a.mean[3 * i + 2]};
+  double s[3] = {a.scale[3 * i], a.scale[3 * i + 1], a.scale[3 * i + 2]};
+  double q[4] = {a.quat[4 * i], a.quat[4 * i + 1], a.quat[4 * i + 2], a.quat[4 * i + 3]};
+  double f[3] = {a.freq[3 * i], a.freq[3 * i + 1], a.freq[3 * i + 2]};
+  const double phi = a.phase ? (double)a.phase[i] : 0.0;
+  const double cr = a.color[3 * i], cg = a.color[3 * i + 1], cb = a.color[3 * i + 2];
+  const double al = a.opacity[i];
+  const bool ok = params_finite(mu, s, q, f, phi, al, cr, cg, cb);
+  Proj3 P;
+  if (ok) project3_prim(s, q, P);
+  for (int vl = 0; vl < a.cams.nv; ++vl)
+    pre3d_record<EXACT>(a, a.cams.v[vl], (int64_t)(a.cams.v0 + vl) * a.N + i, ok, mu, s, q, f,
+                        phi, cr, cg, cb, al, true, P);
 }
 
 #endif
@@ -1165,7 +1233,9 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
     int64_t n = (int64_t)nv * L.N;
     launch_begin(K_PRE3D, s);
     const unsigned gr = (unsigned)((n + 127) / 128);
-    if (a.sh_deg >= 0)
+    if (WIPES_PRE3D_LOOP && a.sh_deg < 0 && a.view_stride == 0)
+      (a.exact ? k_pre3d_loop<true> : k_pre3d_loop<false>)<<<(unsigned)((L.N + 127) / 128), 128, 0, s>>>(a);
+    else if (a.sh_deg >= 0)
       (a.exact ? k_pre3d<true, true> : k_pre3d<false, true>)<<<gr, 128, 0, s>>>(a);
     else
       (a.exact ? k_pre3d<true, false> : k_pre3d<false, false>)<<<gr, 128, 0, s>>>(a);
