@@ -21,7 +21,10 @@ namespace {
 
 constexpr double kLog2e = 1.4426950408889634;
 #ifndef WIPES_PRE3D_MINB
-#define WIPES_PRE3D_MINB 2  // min CTAs/SM, FP64 3D backward (no spills at 234 registers)
+#define WIPES_PRE3D_MINB 3  // min CTAs/SM, FP64 3D backward (168 registers, small spills: C3 0.512 -> 0.441 ms vs 2)
+#endif
+#ifndef WIPES_PRE3D_BWD_PRIM_ONCE
+#define WIPES_PRE3D_BWD_PRIM_ONCE 0  // 1: quaternion/R/S3 once per row (C3 bwd 0.451 vs 0.441 ms per view: registers)
 #endif
 #ifndef WIPES_PRE3D_VMINOR
 #define WIPES_PRE3D_VMINOR 0  // 1: views of a primitive in adjacent threads for flat colour too
@@ -840,12 +843,17 @@ __global__ void __launch_bounds__(128, WIPES_PRE3D_MINB) k_pre3d_bwd(const __gri
   double s[3] = {a.scale[3 * pi], a.scale[3 * pi + 1], a.scale[3 * pi + 2]};
   double q[4] = {a.quat[4 * pi], a.quat[4 * pi + 1], a.quat[4 * pi + 2], a.quat[4 * pi + 3]};
   double f[3] = {a.freq[3 * pi], a.freq[3 * pi + 1], a.freq[3 * pi + 2]};
+  Proj3 P;
+  bool have_prim = false;
   for (int v = v_lo; v < v_hi; ++v) {
     const int64_t o = (int64_t)v * a.N + i;
     if (a.flag[o] != 0) continue;
     const float* cam = a.cams.v[v - a.cams.v0];
-    Proj3 P;
-    project3<false>(cam, a.c.W, a.c.H, a.ewa_clamp, mu, s, q, f, P);
+    if (!have_prim || !WIPES_PRE3D_BWD_PRIM_ONCE) {  // the view-independent half once per row
+      project3_prim<false>(s, q, P);
+      have_prim = true;
+    }
+    project3_view<false>(cam, a.c.W, a.c.H, a.ewa_clamp, mu, f, P);
     double x = P.p[0], y = P.p[1], z = P.p[2];
     double fx = cam[12], fy = cam[13];
     const double rz = 1.0 / z, rz2 = rz * rz, rfx = 1.0 / fx, rfy = 1.0 / fy;
