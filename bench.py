@@ -101,6 +101,14 @@ def load_alu_peaks(clk_hz):
     return sms * 128 * clk_hz, sms * 16 * clk_hz, "unit counts (profiles/peaks.json missing)"
 
 
+def hist_bytes(n, passes, cap, rts_tiles=1024, tile=2048):
+    """Histogram-side bytes of one sort of n keys (capacity cap) over `passes` digits."""
+    tiles = -(-cap // tile)
+    if tiles >= rts_tiles:
+        return passes * (4 * n + 16 * 256 * tiles)
+    return 4 * n
+
+
 def hbm_fractions(kt, steps, L, hbm_gbs):
     """SURVEY §8(d) gate G2: achieved algorithmic bytes / CUDA-event time of the
     HBM-bound kernel groups against the measured copy bandwidth, per STEP (a
@@ -126,8 +134,12 @@ def hbm_fractions(kt, steps, L, hbm_gbs):
         # rect 16 + offset 8 + count 4 read per (view, prim); key 4 + value 4 per dup;
         # ALPHA also the presort key build (4 in, 8 out) and count gather (8 in, 4 out)
         "duplicate": 28 * BN + 8 * dup + (24 * BN if alpha else 0),
-        # one read of the keys per sort
-        "radix_hist": 4 * dup + (4 * BN if alpha else 0),
+        # onesweep sorts: one read of the keys per sort (all passes' histograms);
+        # reduce-then-scan sorts (>= 1024 tiles of 2048 keys, sort.cu): per pass
+        # one key read + the digit-major tile counts (4 B written, 4 B read and
+        # 8 B written by the flat scan per (digit, tile))
+        "radix_hist": sum(hist_bytes(n, p, c) for n, p, c in
+                          ((dup, tile_passes, L.get("cap", dup)),) + (((BN, pre, BN),) if alpha else ())),
         # per pass: key + value read and written
         "radix_scatter": 16 * (tile_passes * dup + pre * BN),
         # sorted keys read, CSR offsets written
@@ -768,7 +780,8 @@ def main():
             "roofline": roof,
             "hbm_kernels": hbm_fractions(
                 kt, args.steps,
-                dict(BN=Bl * N, dup=int(n_tot2), BT=Bl * (-(-W // args.tile)) * (-(-H // args.tile)),
+                dict(BN=Bl * N, dup=int(n_tot2), cap=int(r.cap),
+                     BT=Bl * (-(-W // args.tile)) * (-(-H // args.tile)),
                      alpha=blend == "alpha", B=Bl,
                      param_bytes=sum(v.numel() * 4 for v in params.values()),
                      grad_bytes=sum(v.numel() * 4 for v in grads.values())),

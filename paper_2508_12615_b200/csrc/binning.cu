@@ -443,6 +443,14 @@ cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_flat_scan(const int32_t* in, int64_t n, int64_t* loc, int64_t* blk,
+                             int32_t* arrive, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + kScanTile - 1) / kScanTile);
+  k_scan<int32_t, int64_t><<<g, kScanBlock, 0, s>>>(in, n, loc, blk, arrive, nullptr, 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cudaStream_t s,
                             int* final_in_b) {
   WsHeader* hdr = (WsHeader*)(ws + L.hdr);

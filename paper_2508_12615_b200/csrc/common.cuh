@@ -96,7 +96,8 @@ struct Layout {
   int64_t sort_tiles = 0;  // onesweep tiles of kSortTile keys
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
-         pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, toff = 0,
+         pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, sort_loc = 0,
+         sort_blk = 0, toff = 0,
          order = 0, rgrad = 0, rbeta = 0, rdc = 0, prevals = 0, slots = 0, slotmask = 0, total = 0;
 };
 
@@ -159,6 +160,13 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.blk2 = take(sizeof(int64_t) * (L.alpha ? L.nblk_scan + 1 : 0));
   L.sort_hist = take(sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses));
   L.sort_status = take(sizeof(uint32_t) * 256 * (L.sort_tiles > 0 ? L.sort_tiles : 1));
+  // reduce-then-scan passes (large sorts): the digit-major tile counts reuse
+  // sort_status; their flat exclusive scan goes to sort_loc / sort_blk
+  {
+    const int64_t ent = 256 * (L.sort_tiles > 0 ? L.sort_tiles : 1);
+    L.sort_loc = take(sizeof(int64_t) * ent);
+    L.sort_blk = take(sizeof(int64_t) * ((ent + kScanTile - 1) / kScanTile + 1));
+  }
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
   L.order = take(sizeof(int32_t) * (L.BT + 1));
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
@@ -289,6 +297,10 @@ cudaError_t launch_preprocess3d(const wipes_config& c, const wipes_params& p, co
                                 const wipes_camera* cams, char* ws, uint8_t* cull_flags,
                                 cudaStream_t s);
 cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
+// Flat exclusive scan of n int32 values: out[i] = loc[i] + blk[i / kScanTile]
+// (one launch; `arrive` a zeroed, self-resetting counter in the header).
+cudaError_t launch_flat_scan(const int32_t* in, int64_t n, int64_t* loc, int64_t* blk,
+                             int32_t* arrive, cudaStream_t s);
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,

@@ -50,6 +50,12 @@ struct SortArgs {
   int32_t shifts[kMaxPasses];
   int32_t npass, pass, shift;
   uint32_t vdiv, vmask;  // pass p with bit p of vmask: digit of (value / vdiv), not of key
+  // reduce-then-scan passes: digit-major tile counts [256][tiles] and their
+  // flat exclusive scan (offset of digit d of tile t = loc[i] + blk[i / kScanTile])
+  uint32_t* rts_cnt;
+  const int64_t* rts_loc;
+  const int64_t* rts_blk;
+  int64_t tiles;
 };
 
 template <typename K>
@@ -68,6 +74,18 @@ __device__ __forceinline__ int64_t n_keys(const SortArgs<K>& a) {
 #ifndef WIPES_HIST_UNROLL
 #define WIPES_HIST_UNROLL 4   // independent key loads in flight per thread
 #endif
+
+// Shared-memory histogram add of one digit per lane (d = 256: no key). When
+// the whole warp holds one digit (the high digits of tile keys, whose runs
+// are long), one add of 32 instead of 32 conflicting atomics.
+__device__ __forceinline__ void warp_hist_add(uint32_t* h, uint32_t d) {
+  const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+  if (__all_sync(0xffffffffu, d == d0)) {
+    if ((threadIdx.x & 31) == 0 && d0 < 256u) atomicAdd(&h[d0], 32u);
+  } else if (d < 256u) {
+    atomicAdd(&h[d], 1u);
+  }
+}
 
 template <typename K>
 __global__ void __launch_bounds__(256) k_sort_hist(SortArgs<K> a) {
@@ -98,15 +116,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(SortArgs<K> a) {
         if (p < a.npass) {
           const uint32_t bin = (((a.vmask >> p) & 1u) ? (vq[u] >> a.shifts[p])
                                                       : (uint32_t)(k[u] >> a.shifts[p])) & 255u;
-#ifdef WIPES_HIST_MATCH
-          // lanes adding to the same bin: one add of their count (high digits
-          // of tile keys take few distinct values, so plain adds serialise)
-          const uint32_t peers = __match_any_sync(0xffffffffu, valid ? bin : 256u);
-          if (valid && (peers & ((1u << lane) - 1u)) == 0)
-            atomicAdd(&h[p][bin], (uint32_t)__popc(peers));
-#else
-          if (valid) atomicAdd(&h[p][bin], 1u);
-#endif
+          if (valid) atomicAdd(&h[p][bin], 1u);  // (warp_hist_add measured slower here)
         }
     }
   }
@@ -135,6 +145,9 @@ struct SortSmem {
   uint32_t tile;
 };
 
+#ifndef WIPES_SORT_RTS_TILES
+#define WIPES_SORT_RTS_TILES 1024  // sorts of at least this many 2048-key tiles: reduce-then-scan
+#endif
 #ifndef WIPES_SORT_MINB
 #define WIPES_SORT_MINB 4
 #endif
@@ -182,13 +195,43 @@ __device__ __forceinline__ bool lookback_round(const uint32_t*& sp, int& t,
   return false;
 }
 
+// Reduce-then-scan, reduce step: the digit histogram of every tile, written
+// digit-major so one flat exclusive scan turns it into each (digit, tile)'s
+// global output offset (no look-back). Tiles past the data write zeros.
 template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_sort_up(SortArgs<K> a) {
+  __shared__ uint32_t h[256];
+  const int tid = threadIdx.x;
+  const int64_t n = n_keys(a);
+  h[tid] = 0;  // kSortThreads == 256
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const bool vp = (a.vmask >> a.pass) & 1u;
+  uint32_t dg[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {  // the loads first (independent)
+    const int64_t idx = base + i * kSortThreads + tid;
+    dg[i] = 256u;
+    if (idx < n)
+      dg[i] = (vp ? (a.vin[idx] / a.vdiv) >> a.shift : (uint32_t)(a.kin[idx] >> a.shift)) & 255u;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) warp_hist_add(h, dg[i]);
+  __syncthreads();
+  a.rts_cnt[(int64_t)tid * a.tiles + blockIdx.x] = h[tid];
+}
+
+template <typename K, bool RTS>
 __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(SortArgs<K> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n = n_keys(a);
-  if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
+  if (RTS) {
+    if (tid == 0) sm.tile = blockIdx.x;  // offsets come from the scan: any tile order
+  } else {
+    if (tid == 0) sm.tile = atomicAdd(a.counter + a.pass, 1u);
+  }
   __syncthreads();
   const uint32_t tile = sm.tile;
   const int64_t base = (int64_t)tile * kSortTile;
@@ -227,12 +270,14 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   __syncthreads();
   // tile histogram first, so the aggregate is published before the ranking
   // and the successors' look-back rarely has to wait for it
-#pragma unroll
-  for (int i = 0; i < kSortItems; ++i)
-    if (dig[i] < 256u) atomicAdd(&sm.thist[dig[i]], 1u);
-  __syncthreads();
   uint32_t* st = a.status;
-  st_status(st + (int64_t)tile * 256 + tid, kFlagAgg | sm.thist[tid]);
+  if (!RTS) {  // (reduce-then-scan has its offsets already)
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i)
+      if (dig[i] < 256u) atomicAdd(&sm.thist[dig[i]], 1u);
+    __syncthreads();
+    st_status(st + (int64_t)tile * 256 + tid, kFlagAgg | sm.thist[tid]);
+  }
   // only the last tile has invalid slots (digit 256): full tiles match 8 bits
   const bool full_tile = base + kSortTile <= n;
 #if WIPES_SORT_RANK == 1
@@ -298,6 +343,25 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     sm.wcnt[w][d] = cnt;
     cnt += c;
   }
+  if constexpr (RTS) {
+    // the scanned digit-major counts give the tile's global digit offsets
+    const int64_t e = (int64_t)d * a.tiles + tile;
+    const uint32_t go = (uint32_t)(a.rts_loc[e] + a.rts_blk[e / kScanTile]);
+    uint32_t incl_b = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t tb = __shfl_up_sync(0xffffffffu, incl_b, off);
+      if (lane >= off) incl_b += tb;
+    }
+    __shared__ uint32_t wb2[kWarps];
+    if (lane == 31) wb2[wid] = incl_b;
+    __syncthreads();
+    uint32_t ob = 0;
+    for (int w = 0; w < wid; ++w) ob += wb2[w];
+    sm.bexcl[d] = ob + incl_b - cnt;
+    sm.gofs[d] = go;
+    __syncthreads();
+  } else {
   // look back for the exclusive prefix (the aggregate was published above)
   uint32_t prefix = 0;
 #ifdef WIPES_SORT_LB1
@@ -344,6 +408,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   sm.bexcl[d] = excl_b;
   sm.gofs[d] = excl_g + prefix;
   __syncthreads();
+  }
   // ---- stage in tile-sorted order, then coalesced write-out -----------------
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -376,7 +441,8 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
                         cudaStream_t s, uint32_t vdiv, uint32_t vmask, bool hist_ready) {
   if (npass == 0 || cap == 0) return cudaSuccess;
-  WIPES_SET_SMEM_ONCE(k_sort_pass<K>, (int)sizeof(SortSmem<K>));
+  WIPES_SET_SMEM_ONCE((k_sort_pass<K, false>), (int)sizeof(SortSmem<K>));
+  WIPES_SET_SMEM_ONCE((k_sort_pass<K, true>), (int)sizeof(SortSmem<K>));
   SortArgs<K> a;
   a.hdr = (const WsHeader*)(ws + L.hdr);
   a.n_fixed = n_fixed;
@@ -388,9 +454,18 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   a.vdiv = vdiv ? vdiv : 1u;
   a.vmask = vmask;
   for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
+  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
+  // large sorts: reduce-then-scan passes (no look-back chain across the
+  // hundreds of tiles in flight); small ones: onesweep (one launch per pass)
+  const bool rts = tiles >= WIPES_SORT_RTS_TILES;
+  a.tiles = tiles;
+  a.rts_cnt = a.status;
+  a.rts_loc = (const int64_t*)(ws + L.sort_loc);
+  a.rts_blk = (const int64_t*)(ws + L.sort_blk);
+  int32_t* arrive = &((WsHeader*)(ws + L.hdr))->arrive[3];
   cudaError_t e = cudaSuccess;
   a.kin = kA; a.vin = vA; a.pass = 0; a.shift = 0;
-  if (!hist_ready) {  // else the producer zeroed ghist + counters and built the histogram
+  if (!hist_ready && !rts) {  // else the producer zeroed ghist + counters and built the histogram
     e = cudaMemsetAsync(a.ghist, 0, sizeof(uint32_t) * (kMaxPasses * 256 + kMaxPasses), s);
     if (e != cudaSuccess) return e;
     const int64_t hist_blocks = (cap + WIPES_HIST_KEYS - 1) / WIPES_HIST_KEYS;
@@ -400,17 +475,30 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
                      256, 0, s>>>(a);
     launch_end(K_RADIX_HIST, s);
   }
-  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
   for (int p = 0; p < npass; ++p) {
     const bool from_a = (p & 1) == 0;
     a.kin = from_a ? kA : kB; a.vin = from_a ? vA : vB;
     a.kout = from_a ? kB : kA; a.vout = from_a ? vB : vA;
     a.pass = p;
     a.shift = shifts[p];
+    if (rts) {
+      launch_begin(K_RADIX_HIST, s);
+      k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, s>>>(a);
+      e = launch_flat_scan((const int32_t*)a.rts_cnt, 256 * tiles, (int64_t*)a.rts_loc,
+                           (int64_t*)a.rts_blk, arrive, s);
+      launch_end(K_RADIX_HIST, s);
+      if (e != cudaSuccess) return e;
+      launch_begin(K_RADIX_SCATTER, s);
+      k_sort_pass<K, true><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
+      launch_end(K_RADIX_SCATTER, s);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      continue;
+    }
     e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * 256 * (size_t)tiles, s);
     if (e != cudaSuccess) return e;
     launch_begin(K_RADIX_SCATTER, s);
-    k_sort_pass<K><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
+    k_sort_pass<K, false><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
     launch_end(K_RADIX_SCATTER, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
