@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(const TIn* in, int64_t n, T
 struct DupArgs {
   const int4* rect;
   const int32_t* count;
+  const int32_t* count_sorted;  // ALPHA: count[order[j]] (k_gather_counts)
   const uint32_t* order;  // ALPHA: presorted (view, primitive) ids; SUM: nullptr
   const int64_t* loc;
   const int64_t* blk;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(256) k_duplicate(DupArgs a) {
   if (j0 < a.BN) {
     const int64_t o = a.order ? (int64_t)a.order[j0] : j0;
     WCHECK(o >= 0 && o < a.BN);
-    n = a.count[o];
+    n = a.order ? a.count_sorted[j0] : a.count[o];  // ALPHA: the gathered counts (coalesced)
     start = a.loc[j0] + a.blk[j0 / kScanTile];
     const int64_t v = o / a.N;
     ival = (uint32_t)(o - v * a.N);
@@ -500,6 +501,7 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     DupArgs d;
     d.rect = (const int4*)(ws + L.rect);
     d.count = (const int32_t*)(ws + L.count);
+    d.count_sorted = (const int32_t*)(ws + L.cnt2);
     d.order = order;
     d.loc = loc;
     d.blk = blk;

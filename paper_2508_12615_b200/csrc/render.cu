@@ -257,6 +257,9 @@ struct Item {
 // frames (C2 forward: 1.3 items per warp) claiming ahead unbalances the warps
 // (fwd 60 -> 76 us), so it is off by default. A claimed index >= the item
 // count is dropped (nothing behind it).
+#ifndef WIPES_STAGE_ALL
+#define WIPES_STAGE_ALL 0  // staging: load all four record quads before the footprint tests
+#endif
 #ifndef WIPES_ITEM_PREFETCH
 #define WIPES_ITEM_PREFETCH 0  // claim items one ahead (A/B knob; see next_item)
 #endif
@@ -331,12 +334,18 @@ __device__ __forceinline__ int stage_chunk(const RenderArgs& a, const float4* re
     }
     WCHECK(pid >= 0 && pid < a.N);
     const float4* r = recv + 4 * (int64_t)pid;
-    r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
-    hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G);
-    if (hit) {
-      r1 = ldg_nc(r + 1);
-      hit = ellipse_hits_rect(r0, r1, it.sx0, it.sy0, 8.f * G, a.skip_e - 0.01f);
-      if (hit) r2 = ldg_nc(r + 2);
+    if (WIPES_STAGE_ALL) {  // the whole record at once: one dependent round trip, not three
+      r0 = ldg_nc(r); r1 = ldg_nc(r + 1); r2 = ldg_nc(r + 2); r3 = ldg_nc(r + 3);
+      hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G) &&
+            ellipse_hits_rect(r0, r1, it.sx0, it.sy0, 8.f * G, a.skip_e - 0.01f);
+    } else {
+      r0 = ldg_nc(r); r3 = ldg_nc(r + 3);
+      hit = hits_footprint(r0, r3, it.sx0, it.sy0, 8.f * G);
+      if (hit) {
+        r1 = ldg_nc(r + 1);
+        hit = ellipse_hits_rect(r0, r1, it.sx0, it.sy0, 8.f * G, a.skip_e - 0.01f);
+        if (hit) r2 = ldg_nc(r + 2);
+      }
     }
   }
   const uint32_t bal = __ballot_sync(kFull, hit);
