@@ -39,6 +39,9 @@ constexpr int kMom = kMoments;  // 12
 #ifndef WIPES_MINB_FWD
 #define WIPES_MINB_FWD 8  // __launch_bounds__ min CTAs per SM (register cap), forward
 #endif
+#ifndef WIPES_MINB_FWD_ALPHA
+#define WIPES_MINB_FWD_ALPHA 8  // ... forward, ALPHA
+#endif
 #ifndef WIPES_MINB_BWD
 #define WIPES_MINB_BWD 6  // ... backward, SUM (C2 best at 80 registers)
 #endif
@@ -380,7 +383,7 @@ __device__ __forceinline__ void alpha_step(bool ok, float w, const float4& r3, i
 }
 
 template <int TS, bool ALPHA, bool STATS>
-__global__ void __launch_bounds__(kCta, WIPES_MINB_FWD) k_render_fwd(RenderArgs a) {
+__global__ void __launch_bounds__(kCta, ALPHA ? WIPES_MINB_FWD_ALPHA : WIPES_MINB_FWD) k_render_fwd(RenderArgs a) {
   constexpr int GF = (TS >= 16 ? WIPES_FWD_G : 1);
   constexpr int kFwdUnroll = ALPHA ? WIPES_FWD_UNROLL_ALPHA : WIPES_FWD_UNROLL;
   using Gm = Geo<TS, GF>;
