@@ -122,7 +122,10 @@ def hbm_fractions(kt, steps, L, hbm_gbs):
     vb = 0
     while (1 << vb) < L["B"]:
         vb += 1
-    pre = (4 + (vb + 7) // 8) if alpha else 0
+    # the presort of a large frame runs segmented by view: 4 depth passes, no view pass
+    seg_cap = L["B"] * (-(-(BN // max(L["B"], 1)) // 2048)) * 2048  # B views x whole tiles
+    seg = alpha and seg_cap // 2048 >= 1024
+    pre = (4 if seg else 4 + (vb + 7) // 8) if alpha else 0
     tb = 0
     while (1 << tb) < L["BT"]:
         tb += 1
@@ -139,7 +142,8 @@ def hbm_fractions(kt, steps, L, hbm_gbs):
         # one key read + the digit-major tile counts (4 B written, 4 B read and
         # 8 B written by the flat scan per (digit, tile))
         "radix_hist": sum(hist_bytes(n, p, c) for n, p, c in
-                          ((dup, tile_passes, L.get("cap", dup)),) + (((BN, pre, BN),) if alpha else ())),
+                          ((dup, tile_passes, L.get("cap", dup)),) +
+                          (((BN, pre, seg_cap if seg else BN),) if alpha else ())),
         # per pass: key + value read and written
         "radix_scatter": 16 * (tile_passes * dup + pre * BN),
         # sorted keys read, CSR offsets written

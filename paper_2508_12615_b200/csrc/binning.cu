@@ -475,7 +475,8 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
       launch_begin(K_DUPLICATE, s);
       k_presort_keys<<<gBN, 256, 0, s>>>((const uint32_t*)(ws + L.dkey), L.BN, pkA, pvA);
       launch_end(K_DUPLICATE, s);
-      // 4 depth-byte passes on the key, then the view bytes of value / N
+      // 4 depth-byte passes on the key, then (unsegmented) the view bytes of
+      // value / N; segmented by view, the depth passes alone
       int shifts[kMaxPasses];
       uint32_t vmask = 0;
       for (int p = 0; p < L.pre_passes; ++p) {
@@ -483,7 +484,7 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
         if (p >= 4) vmask |= 1u << p;
       }
       e = launch_sort<uint32_t>(L, ws, pkA, pvA, pkB, pvB, shifts, L.pre_passes, L.BN, L.BN, s,
-                                (uint32_t)L.N, vmask);
+                                (uint32_t)L.N, vmask, false, L.pre_seg ? L.N : 0);
       if (e != cudaSuccess) return e;
       order = (L.pre_passes & 1) ? pvB : pvA;
       launch_begin(K_DUPLICATE, s);

@@ -42,6 +42,9 @@ constexpr int kScanBlock = 256;                // threads per scan block
 constexpr int kScanItems = 8;                  // items per thread
 constexpr int kScanTile = kScanBlock * kScanItems;
 constexpr int kRadixBits = 8;
+#ifndef WIPES_SORT_RTS_TILES
+#define WIPES_SORT_RTS_TILES 1024  // sorts of at least this many 2048-key tiles: reduce-then-scan
+#endif
 constexpr int kSortThreads = 256;              // onesweep CTA (one digit per thread)
 #ifndef WIPES_SORT_ITEMS
 #define WIPES_SORT_ITEMS 8
@@ -87,6 +90,7 @@ struct Layout {
   int64_t N = 0, BN = 0, cap = 0, BT = 0, T = 0;
   int32_t B = 0, GX = 0, GY = 0;
   int32_t hi_bits = 0, passes = 0, pre_passes = 0;  // dup-sort / depth-presort passes
+  int32_t pre_seg = 0;  // depth presort segmented by view (reduce-then-scan, no view pass)
   int32_t alpha = 0;
   int32_t exact = 0;       // 3D exact z-integration: extra beta moment per record
   int32_t det = 0;         // deterministic backward: per-(dup, footprint) moment slots
@@ -131,9 +135,15 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   L.passes = (hb + kRadixBits - 1) / kRadixBits;
   int vb = 0;
   while (((int64_t)1 << vb) < B) ++vb;
-  L.pre_passes = L.alpha ? 4 + (vb + kRadixBits - 1) / kRadixBits : 0;
+  // large presorts run segmented by view (each view's records sorted among
+  // themselves, tiles inside one view): the 4 depth-byte passes keep the views
+  // in order, so no view pass; small ones sort (view, depth) as one key
+  const int64_t seg_tiles = (N + kSortTile - 1) / kSortTile;
+  L.pre_seg = L.alpha && (int64_t)B * seg_tiles >= WIPES_SORT_RTS_TILES;
+  L.pre_passes = L.alpha ? (L.pre_seg ? 4 : 4 + (vb + kRadixBits - 1) / kRadixBits) : 0;
   const int64_t sort_n = L.cap > L.BN ? L.cap : L.BN;
   L.sort_tiles = (sort_n + kSortTile - 1) / kSortTile;
+  if (L.pre_seg && (int64_t)B * seg_tiles > L.sort_tiles) L.sort_tiles = (int64_t)B * seg_tiles;
   L.nblk_scan = (L.BN + kScanTile - 1) / kScanTile;
   if (L.nblk_scan < 1) L.nblk_scan = 1;
   size_t o = 0;
@@ -305,7 +315,7 @@ template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
                         cudaStream_t s, uint32_t vdiv = 1, uint32_t vmask = 0,
-                        bool hist_ready = false);
+                        bool hist_ready = false, int64_t seg_len = 0);
 cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
                           cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);

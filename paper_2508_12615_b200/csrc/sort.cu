@@ -56,7 +56,38 @@ struct SortArgs {
   const int64_t* rts_loc;
   const int64_t* rts_blk;
   int64_t tiles;
+  // segmented reduce-then-scan (ALPHA presort: one segment per view): keys
+  // [s seg_len, (s + 1) seg_len) sort among themselves; tiles never straddle a
+  // segment (seg_tiles per segment) and the counts are laid out
+  // (segment, digit, tile), so the flat scan keeps the segments in order.
+  // seg_len = 0: one segment of n keys.
+  int64_t seg_len, seg_tiles;
 };
+
+// Key range [base, end) of a tile and the count index of its digit d.
+template <typename K>
+__device__ __forceinline__ void tile_span(const SortArgs<K>& a, int64_t tile, int64_t n,
+                                          int64_t& base, int64_t& end) {
+  if (a.seg_len > 0) {
+    const int64_t sg = tile / a.seg_tiles, lt = tile - sg * a.seg_tiles;
+    base = sg * a.seg_len + lt * kSortTile;
+    end = base + kSortTile;
+    const int64_t se = (sg + 1) * a.seg_len;
+    if (end > se) end = se;
+  } else {
+    base = tile * kSortTile;
+    end = base + kSortTile;
+  }
+  if (end > n) end = n;
+}
+template <typename K>
+__device__ __forceinline__ int64_t count_index(const SortArgs<K>& a, int64_t tile, int d) {
+  if (a.seg_len > 0) {
+    const int64_t sg = tile / a.seg_tiles, lt = tile - sg * a.seg_tiles;
+    return (sg * 256 + d) * a.seg_tiles + lt;
+  }
+  return (int64_t)d * a.tiles + tile;
+}
 
 template <typename K>
 __device__ __forceinline__ int64_t n_keys(const SortArgs<K>& a) {
@@ -145,9 +176,6 @@ struct SortSmem {
   uint32_t tile;
 };
 
-#ifndef WIPES_SORT_RTS_TILES
-#define WIPES_SORT_RTS_TILES 1024  // sorts of at least this many 2048-key tiles: reduce-then-scan
-#endif
 #ifndef WIPES_SORT_MINB
 #define WIPES_SORT_MINB 4
 #endif
@@ -205,20 +233,21 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(SortArgs<K> a) {
   const int64_t n = n_keys(a);
   h[tid] = 0;  // kSortThreads == 256
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  int64_t base, end;
+  tile_span(a, blockIdx.x, n, base, end);
   const bool vp = (a.vmask >> a.pass) & 1u;
   uint32_t dg[kSortItems];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {  // the loads first (independent)
     const int64_t idx = base + i * kSortThreads + tid;
     dg[i] = 256u;
-    if (idx < n)
+    if (idx < end)
       dg[i] = (vp ? (a.vin[idx] / a.vdiv) >> a.shift : (uint32_t)(a.kin[idx] >> a.shift)) & 255u;
   }
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) warp_hist_add(h, dg[i]);
   __syncthreads();
-  a.rts_cnt[(int64_t)tid * a.tiles + blockIdx.x] = h[tid];
+  a.rts_cnt[count_index(a, blockIdx.x, tid)] = h[tid];
 }
 
 template <typename K, bool RTS>
@@ -234,8 +263,9 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   }
   __syncthreads();
   const uint32_t tile = sm.tile;
-  const int64_t base = (int64_t)tile * kSortTile;
-  if (base >= n) return;  // beyond the data: nobody waits on this tile
+  int64_t base, end;  // this tile's keys (onesweep: end = min(base + tile, n))
+  tile_span(a, tile, n, base, end);
+  if (base >= end) return;  // beyond the data: nobody waits on this tile
   const int shift = a.shift;
   const bool vp = (a.vmask >> a.pass) & 1u;
   const uint32_t lt = (1u << lane) - 1u;
@@ -246,7 +276,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
-    const bool valid = idx < n;
+    const bool valid = idx < end;
     key[i] = valid ? a.kin[idx] : (K)0;
     val[i] = valid ? a.vin[idx] : 0u;
   }
@@ -265,7 +295,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
     const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
-    dig[i] = idx < n ? (src & 255u) : 256u;
+    dig[i] = idx < end ? (src & 255u) : 256u;
   }
   __syncthreads();
   // tile histogram first, so the aggregate is published before the ranking
@@ -279,7 +309,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     st_status(st + (int64_t)tile * 256 + tid, kFlagAgg | sm.thist[tid]);
   }
   // only the last tile has invalid slots (digit 256): full tiles match 8 bits
-  const bool full_tile = base + kSortTile <= n;
+  const bool full_tile = base + kSortTile <= end;
 #if WIPES_SORT_RANK == 1
   (void)full_tile;
   // lanes with the same digit: every lane ORs its bit into its digit's mask
@@ -345,7 +375,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   }
   if constexpr (RTS) {
     // the scanned digit-major counts give the tile's global digit offsets
-    const int64_t e = (int64_t)d * a.tiles + tile;
+    const int64_t e = count_index(a, tile, d);
     const uint32_t go = (uint32_t)(a.rts_loc[e] + a.rts_blk[e / kScanTile]);
     uint32_t incl_b = cnt;
 #pragma unroll
@@ -421,7 +451,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     }
   }
   __syncthreads();
-  const int64_t rem = n - base;
+  const int64_t rem = end - base;
   const int tn = rem < kSortTile ? (int)rem : kSortTile;
   for (int j = tid; j < tn; j += kSortThreads) {
     const K k = sm.keys[j];
@@ -439,7 +469,8 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
-                        cudaStream_t s, uint32_t vdiv, uint32_t vmask, bool hist_ready) {
+                        cudaStream_t s, uint32_t vdiv, uint32_t vmask, bool hist_ready,
+                        int64_t seg_len) {
   if (npass == 0 || cap == 0) return cudaSuccess;
   WIPES_SET_SMEM_ONCE((k_sort_pass<K, false>), (int)sizeof(SortSmem<K>));
   WIPES_SET_SMEM_ONCE((k_sort_pass<K, true>), (int)sizeof(SortSmem<K>));
@@ -454,10 +485,16 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   a.vdiv = vdiv ? vdiv : 1u;
   a.vmask = vmask;
   for (int p = 0; p < kMaxPasses; ++p) a.shifts[p] = p < npass ? shifts[p] : 0;
-  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
+  // segmented (n_fixed keys in segments of seg_len): tiles never straddle one
+  a.seg_len = seg_len > 0 ? seg_len : 0;
+  a.seg_tiles = seg_len > 0 ? (seg_len + kSortTile - 1) / kSortTile : 0;
+  const int64_t tiles = seg_len > 0 ? (n_fixed / seg_len) * a.seg_tiles
+                                    : (cap + kSortTile - 1) / kSortTile;
   // large sorts: reduce-then-scan passes (no look-back chain across the
-  // hundreds of tiles in flight); small ones: onesweep (one launch per pass)
-  const bool rts = tiles >= WIPES_SORT_RTS_TILES;
+  // hundreds of tiles in flight); small ones: onesweep (one launch per pass).
+  // Segmented sorts are reduce-then-scan only (Layout::pre_seg).
+  const bool rts = seg_len > 0 || tiles >= WIPES_SORT_RTS_TILES;
+  if (seg_len > 0 && (n_fixed % seg_len != 0 || tiles > L.sort_tiles)) return cudaErrorInvalidValue;
   a.tiles = tiles;
   a.rts_cnt = a.status;
   a.rts_loc = (const int64_t*)(ws + L.sort_loc);
@@ -508,10 +545,12 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
 
 template cudaError_t launch_sort<uint32_t>(const Layout&, char*, uint32_t*, uint32_t*,
                                            uint32_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool,
+                                           int64_t);
 template cudaError_t launch_sort<uint64_t>(const Layout&, char*, uint64_t*, uint32_t*,
                                            uint64_t*, uint32_t*, const int*, int, int64_t,
-                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool);
+                                           int64_t, cudaStream_t, uint32_t, uint32_t, bool,
+                                           int64_t);
 
 size_t sort_smem_bytes64() { return sizeof(SortSmem<uint64_t>); }
 
