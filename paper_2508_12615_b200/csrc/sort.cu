@@ -168,7 +168,7 @@ struct SortSmem {
   uint32_t vals[kSortTile];
   uint32_t wcnt[kWarps][256];  // per-warp running counts, then warp-exclusive prefixes
   uint32_t thist[256];         // tile digit histogram (published before the ranking)
-  uint32_t bexcl[256];         // block-exclusive digit offsets (tile-local)
+  uint32_t bexcl[256];         // (unused: the tile-local digit bases are folded into wcnt)
   uint32_t gofs[256];          // global output offset of the tile's first key per digit
 #if WIPES_SORT_RANK == 1
   uint32_t match[2][kWarps][260];  // per-warp lane masks of each digit, 257 used (double-buffered)
@@ -388,8 +388,12 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
     __syncthreads();
     uint32_t ob = 0;
     for (int w = 0; w < wid; ++w) ob += wb2[w];
-    sm.bexcl[d] = ob + incl_b - cnt;
-    sm.gofs[d] = go;
+    const uint32_t bx = ob + incl_b - cnt;
+    // fold the tile-local digit base into the warp prefixes (staging: one load)
+    // and keep gofs - bexcl (write-out: one load; uint32 wrap-around exact)
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sm.wcnt[w][d] += bx;
+    sm.gofs[d] = go - bx;
     __syncthreads();
   } else {
   // look back for the exclusive prefix (the aggregate was published above)
@@ -435,29 +439,46 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   uint32_t og = 0, ob = 0;
   for (int w = 0; w < wid; ++w) { og += wg[w]; ob += wb[w]; }
   const uint32_t excl_g = og + incl_g - gh, excl_b = ob + incl_b - cnt;
-  sm.bexcl[d] = excl_b;
-  sm.gofs[d] = excl_g + prefix;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) sm.wcnt[w][d] += excl_b;
+  sm.gofs[d] = excl_g + prefix - excl_b;
   __syncthreads();
   }
   // ---- stage in tile-sorted order, then coalesced write-out -----------------
+  // 32-bit keys: (key, value) staged as one 8-byte word (one scattered store
+  // and one load per pair instead of two each)
+  constexpr bool kPair = sizeof(K) == 4;
+  uint2* const kv = reinterpret_cast<uint2*>(sm.keys);  // spans keys + vals (16 KB)
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t dd = rank[i] >> 16;
     if (dd < 256u) {
-      const uint32_t loc = sm.bexcl[dd] + sm.wcnt[wid][dd] + (rank[i] & 0xffffu);
+      const uint32_t loc = sm.wcnt[wid][dd] + (rank[i] & 0xffffu);
       WCHECK(loc < (uint32_t)kSortTile);
-      sm.keys[loc] = key[i];
-      sm.vals[loc] = val[i];
+      if constexpr (kPair) {
+        kv[loc] = make_uint2((uint32_t)key[i], val[i]);
+      } else {
+        sm.keys[loc] = key[i];
+        sm.vals[loc] = val[i];
+      }
     }
   }
   __syncthreads();
   const int64_t rem = end - base;
   const int tn = rem < kSortTile ? (int)rem : kSortTile;
   for (int j = tid; j < tn; j += kSortThreads) {
-    const K k = sm.keys[j];
-    const uint32_t v = sm.vals[j];
+    K k;
+    uint32_t v;
+    if constexpr (kPair) {
+      const uint2 p = kv[j];
+      k = (K)p.x;
+      v = p.y;
+    } else {
+      k = sm.keys[j];
+      v = sm.vals[j];
+    }
     const uint32_t dd = (vp ? (v / a.vdiv) >> shift : (uint32_t)(k >> shift)) & 255u;
-    const int64_t pos = (int64_t)sm.gofs[dd] + (j - (int64_t)sm.bexcl[dd]);
+    const int64_t pos = (int64_t)(uint32_t)(sm.gofs[dd] + (uint32_t)j);
     WCHECK(pos >= 0 && pos < n);
     a.kout[pos] = k;
     a.vout[pos] = v;
