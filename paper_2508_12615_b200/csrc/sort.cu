@@ -168,7 +168,6 @@ struct SortSmem {
   uint32_t vals[kSortTile];
   uint32_t wcnt[kWarps][256];  // per-warp running counts, then warp-exclusive prefixes
   uint32_t thist[256];         // tile digit histogram (published before the ranking)
-  uint32_t bexcl[256];         // (unused: the tile-local digit bases are folded into wcnt)
   uint32_t gofs[256];          // global output offset of the tile's first key per digit
 #if WIPES_SORT_RANK == 1
   uint32_t match[2][kWarps][260];  // per-warp lane masks of each digit, 257 used (double-buffered)
