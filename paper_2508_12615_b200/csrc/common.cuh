@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cassert>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -45,6 +46,12 @@ constexpr int kRadixBits = 8;
 #ifndef WIPES_SORT_RTS_TILES
 #define WIPES_SORT_RTS_TILES 1024  // sorts of at least this many 2048-key tiles: reduce-then-scan
 #endif
+// The threshold, overridable at run time (environment WIPES_SORT_RTS_TILES) so
+// the tests can run either sort mode at any size.
+inline int64_t sort_rts_tiles() {
+  const char* e = getenv("WIPES_SORT_RTS_TILES");
+  return (e && *e) ? atoll(e) : (int64_t)WIPES_SORT_RTS_TILES;
+}
 constexpr int kSortThreads = 256;              // onesweep CTA (one digit per thread)
 #ifndef WIPES_SORT_ITEMS
 #define WIPES_SORT_ITEMS 8
@@ -139,7 +146,7 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   // themselves, tiles inside one view): the 4 depth-byte passes keep the views
   // in order, so no view pass; small ones sort (view, depth) as one key
   const int64_t seg_tiles = (N + kSortTile - 1) / kSortTile;
-  L.pre_seg = L.alpha && (int64_t)B * seg_tiles >= WIPES_SORT_RTS_TILES;
+  L.pre_seg = L.alpha && (int64_t)B * seg_tiles >= sort_rts_tiles();
   L.pre_passes = L.alpha ? (L.pre_seg ? 4 : 4 + (vb + kRadixBits - 1) / kRadixBits) : 0;
   const int64_t sort_n = L.cap > L.BN ? L.cap : L.BN;
   L.sort_tiles = (sort_n + kSortTile - 1) / kSortTile;

@@ -513,7 +513,7 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   // large sorts: reduce-then-scan passes (no look-back chain across the
   // hundreds of tiles in flight); small ones: onesweep (one launch per pass).
   // Segmented sorts are reduce-then-scan only (Layout::pre_seg).
-  const bool rts = seg_len > 0 || tiles >= WIPES_SORT_RTS_TILES;
+  const bool rts = seg_len > 0 || tiles >= sort_rts_tiles();
   if (seg_len > 0 && (n_fixed % seg_len != 0 || tiles > L.sort_tiles)) return cudaErrorInvalidValue;
   a.tiles = tiles;
   a.rts_cnt = a.status;

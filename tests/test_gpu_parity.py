@@ -694,3 +694,47 @@ def test_chunked_preprocess_backward_bitwise(case):
     assert all(a1 == b0 for (_, a1), (b0, _) in zip(seen, seen[1:]))
     for k in ref:
         assert torch.equal(ref[k], got[k]), k
+
+
+# ------------------------------------------------------------- sort modes --
+@pytest.mark.parametrize("mode", ["rts", "onesweep"])
+@pytest.mark.parametrize("case", ["c1_sum", "c1_alpha", "p3d", "p6d", "views131"])
+def test_sort_modes_integer_parity(ora, case, mode, monkeypatch):
+    """Both radix-sort modes (sort.cu) at any size: the run-time threshold
+    WIPES_SORT_RTS_TILES = 1 sends every sort through reduce-then-scan (and the
+    ALPHA presort through its view-segmented form, segments of one or a few
+    ragged tiles), a huge one through onesweep with look-back; keys, values and
+    tile ranges stay bit-exact with the oracle and the image within its bound."""
+    monkeypatch.setenv("WIPES_SORT_RTS_TILES", "1" if mode == "rts" else str(1 << 40))
+    if case.startswith("c1"):
+        blend = case.split("_")[1]
+        H = W = 64
+        N, B = 256, 1
+        p = gen.gen2d(H, W, N, seed=0, cov_mode="cholesky", freq_std=0.5, phase=True,
+                      alpha=(0.2, 1.0) if blend == "alpha" else 1.0,
+                      color_max=1.0 if blend == "alpha" else 0.1, depth=(blend == "alpha"))
+        cams, vs, kind = None, 0, "2d"
+    elif case == "views131":
+        N, B, H, W = 60, 131, 32, 32
+        p = gen.gen3d(N, seed=2, scale_mult=20.0)
+        cams = [gen.camera((2.5 * np.cos(a), -0.3, 2.5 * np.sin(a)), W, H)
+                for a in np.linspace(0, 2 * np.pi, B, endpoint=False)]
+        vs, kind, blend = 0, "3d", "alpha"
+    else:
+        c = gen.make_config(case, seed=0)
+        H, W, N, B = c["H"], c["W"], c["N"], c["B"]
+        p, cams, vs, kind, blend = c["params"], c["cams"], c["view_stride"], "3d", "alpha"
+    if kind == "2d":
+        cfg_o = oracle_cfg(ora, "2d", H, W, blend, cov2="cholesky")
+        pr = ora.project2d(cfg_o, p)
+        r = gpu_rasterizer("2d", H, W, blend, cov2="cholesky")
+    else:
+        cfg_o = oracle_cfg(ora, "3d", H, W, blend, use_rect=True)
+        pr = ora.project3d(cfg_o, p, cams, view_stride=vs)
+        r = gpu_rasterizer("3d", H, W, blend)
+    out = r.forward(to_dev(p), cams, vs) if kind == "3d" else r.forward(to_dev(p))
+    torch.cuda.synchronize()
+    _check_integers(ora, cfg_o, pr, r, B, N)
+    ro = ora.render(cfg_o, pr)
+    nbad, namb = pixel_violations(_pixels(_np(out["image"])), ro["color"], ro["margin"])
+    assert nbad == 0, (case, mode, nbad, namb)
