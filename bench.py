@@ -234,17 +234,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU ---
-def fit_rate(H, W, N, args, flush, dev):
+def fit_rate(H, W, N, args, flush, dev, params):
     """NEXT-2: full fitting iterations (render -> L2 loss -> backward -> Adam,
-    one CUDA graph per iteration, raster.Fitter2D) on this frame size, timed
-    with CUDA events over args.steps replays (L2 flushed between)."""
+    one CUDA graph per iteration, raster.Fitter2D) on the bench frame's own
+    primitives (the C2 distribution: the same parameters as the fwd+bwd line,
+    opacity taken as given), timed with CUDA events over args.steps replays
+    (L2 flushed between)."""
     import torch
     from paper_2508_12615_b200 import gen
     from paper_2508_12615_b200.train import Fitter2D
     tgt = gen.smooth_target(H, W, seed=args.seed)
-    p = gen.init2d_from_target(tgt, N, seed=args.seed, freq_std=0.05)
-    fit = Fitter2D(torch.from_numpy(tgt).to(dev), {k: torch.from_numpy(v) for k, v in p.items()},
-                   cov2="cholesky")
+    fit = Fitter2D(torch.from_numpy(tgt).to(dev), {k: torch.from_numpy(v) for k, v in params.items()},
+                   cov2="sigma", opacity_act="none")
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         flush.zero_()
@@ -263,8 +264,9 @@ def fit_rate(H, W, N, args, flush, dev):
     return {"value": args.steps / (ms / 1e3), "unit": "fitting iters/s",
             "ms_per_step": ms / args.steps, "loss": loss, "overflowed": over,
             "steps_applied": fit.steps_taken(),
-            "workload": f"NEXT-2 image fit {W}x{H}, {N} Cholesky primitives, L2 + Adam "
-                        "(preprocess, bin/sort, render, loss, backward, Adam: one CUDA graph)"}
+            "workload": f"NEXT-2 image fit {W}x{H} on the bench frame's {N} primitives (C2 "
+                        "distribution), L2 + Adam (preprocess, bin/sort, render, loss, backward, "
+                        "Adam: one CUDA graph)"}
 
 
 def mlp_rate(args, flush, dev, peaks, precision="bf16x3"):
@@ -793,7 +795,7 @@ def main():
             "paper_context": "render FPS on one A6000: Kodak 1708-1779 (Table 1, PAPER.md:148-149); "
                              "Mip-NeRF360 95.7 (Table 2, PAPER.md:239)"}
     if c["kind"] == "2d" and not rows and not args.no_fit:
-        line["fit"] = fit_rate(H, W, N, args, flush, dev)
+        line["fit"] = fit_rate(H, W, N, args, flush, dev, c["params"])
     if name == "c2" and not args.no_c3:
         line["nvs_c3"] = nvs_subrecord(args, rank, world, dev, flush)
     if not args.no_mlp and (c["kind"] == "6d" or name == "c2"):
