@@ -130,6 +130,15 @@ def hbm_fractions(kt, steps, L, hbm_gbs):
     while (1 << tb) < L["BT"]:
         tb += 1
     tile_passes = (tb + 7) // 8
+    # ALPHA tile sort segmented by view when the view-local tile ids need fewer
+    # passes (Layout::tile_seg; cap-based tile bound >= 1024)
+    T = L["BT"] // max(L["B"], 1)
+    tv = 0
+    while (1 << tv) < T:
+        tv += 1
+    if alpha and L["B"] > 1 and (tv + 7) // 8 < tile_passes and \
+            -(-L.get("cap", dup) // 2048) + L["B"] >= 1024:
+        tile_passes = (tv + 7) // 8
     per_step = {
         # params read + rect 16, count 4, flag 1, depth 4, record 64 written per (view, prim)
         "preprocess2d": L["param_bytes"] + 89 * BN,

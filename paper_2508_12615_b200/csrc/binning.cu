@@ -405,6 +405,74 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, WsHea
   if (tid == 0) hdr->arrive[2] = 0;  // self-resetting (bin_sort may run again)
 }
 
+// View segments of the ALPHA tile sort (Layout::tile_seg): dups are emitted in
+// presorted (view, depth) order, view v's records at presorted positions
+// [v N, (v + 1) N), so view v's dups start at the scanned offset of position
+// v N (clipped to the stored count). One block: off[0..B], and tiles[0..B] =
+// the exclusive prefix of each view's 2048-key tiles.
+__global__ void __launch_bounds__(1024) k_vseg_tables(const int64_t* loc, const int64_t* blk,
+                                                      const WsHeader* hdr, int64_t cap, int64_t N,
+                                                      int B, int64_t* off, int64_t* tiles) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t n = clamp_n(hdr, cap);
+  for (int v = tid; v <= B; v += blockDim.x) {
+    int64_t o = n;
+    if (v < B) {
+      const int64_t p = (int64_t)v * N;
+      o = loc[p] + blk[p / kScanTile];
+      if (o > n) o = n;
+    }
+    off[v] = o;
+  }
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int v0 = 0; v0 <= B; v0 += blockDim.x) {
+    const int v = v0 + tid;
+    const int64_t c = v < B ? (off[v + 1] - off[v] + kSortTile - 1) / kSortTile : 0;
+    int64_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      int64_t ti = t;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, ti, d);
+        if (lane >= d) ti += u;
+      }
+      wsum[lane] = ti - t;
+    }
+    __syncthreads();
+    if (v <= B) tiles[v] = carry + wsum[wid] + inc - c;
+    __syncthreads();
+    if (tid == (int)blockDim.x - 1) carry += wsum[wid] + inc;
+    __syncthreads();
+  }
+}
+
+// Segment of every tile of the view-segmented sort (B past the last one).
+__global__ void k_vseg_map(const int64_t* tiles, int B, int64_t bound, int32_t* map) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= bound) return;
+  int lo = 0, hi = B;  // tiles[lo] <= t < tiles[hi] (tiles[B] = total)
+  if (t >= tiles[B]) {
+    map[t] = B;
+    return;
+  }
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tiles[mid] <= t) lo = mid; else hi = mid;
+  }
+  map[t] = lo;
+}
+
 __global__ void k_offsets(const int64_t* loc, const int64_t* blk, int64_t BN, int64_t* out) {
   int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o < BN) out[o] = loc[o] + blk[o / kScanTile];
@@ -527,11 +595,30 @@ cudaError_t launch_bin_sort(const wipes_config& c, const Layout& L, char* ws, cu
     launch_end(K_DUPLICATE, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // stable LSD passes over the (view*T + tile) bits only
+    // stable LSD passes over the (view*T + tile) bits only; view-segmented
+    // (ALPHA, Layout::tile_seg): over the view-local tile bits
     int shifts[kMaxPasses];
     for (int p = 0; p < L.passes; ++p) shifts[p] = 8 * p;
-    e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s, 1, 0,
-                              fuse_hist);
+    if (L.tile_seg) {
+      VSeg vs;
+      vs.off = (const int64_t*)(ws + L.vseg_off);
+      vs.tiles = (const int64_t*)(ws + L.vseg_tiles);
+      vs.map = (const int32_t*)(ws + L.vseg_map);
+      vs.nseg = L.B;
+      vs.T = (uint32_t)L.T;
+      vs.tile_bound = L.tile_bound;
+      launch_begin(K_RADIX_HIST, s);
+      k_vseg_tables<<<1, 1024, 0, s>>>(loc, blk, hdr, L.cap, L.N, L.B, (int64_t*)(ws + L.vseg_off),
+                                      (int64_t*)(ws + L.vseg_tiles));
+      k_vseg_map<<<(unsigned)((L.tile_bound + 255) / 256), 256, 0, s>>>(
+          (const int64_t*)(ws + L.vseg_tiles), L.B, L.tile_bound, (int32_t*)(ws + L.vseg_map));
+      launch_end(K_RADIX_HIST, s);
+      e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s, 1, 0,
+                                fuse_hist, 0, &vs);
+    } else {
+      e = launch_sort<uint32_t>(L, ws, kA, vA, kB, vB, shifts, L.passes, -1, L.cap, s, 1, 0,
+                                fuse_hist);
+    }
     if (e != cudaSuccess) return e;
   }
   const uint32_t* kf = *final_in_b ? kB : kA;

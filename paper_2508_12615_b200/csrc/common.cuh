@@ -98,6 +98,8 @@ struct Layout {
   int32_t B = 0, GX = 0, GY = 0;
   int32_t hi_bits = 0, passes = 0, pre_passes = 0;  // dup-sort / depth-presort passes
   int32_t pre_seg = 0;  // depth presort segmented by view (reduce-then-scan, no view pass)
+  int32_t tile_seg = 0;  // ALPHA tile sort segmented by view (per-view tile ids: fewer passes)
+  int64_t tile_bound = 0;  // tiles of a view-segmented tile sort (upper bound)
   int32_t alpha = 0;
   int32_t exact = 0;       // 3D exact z-integration: extra beta moment per record
   int32_t det = 0;         // deterministic backward: per-(dup, footprint) moment slots
@@ -108,7 +110,7 @@ struct Layout {
   size_t hdr = 0, rect = 0, count = 0, flag = 0, dkey = 0, rec = 0, loc_off = 0,
          blk_sum = 0, keysA = 0, keysB = 0, valsA = 0, valsB = 0, pkA = 0, pkB = 0, pvA = 0,
          pvB = 0, cnt2 = 0, loc2 = 0, blk2 = 0, sort_hist = 0, sort_status = 0, sort_loc = 0,
-         sort_blk = 0, toff = 0,
+         sort_blk = 0, vseg_off = 0, vseg_tiles = 0, vseg_map = 0, toff = 0,
          order = 0, rgrad = 0, rbeta = 0, rdc = 0, prevals = 0, slots = 0, slotmask = 0, total = 0;
 };
 
@@ -151,6 +153,21 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
   const int64_t sort_n = L.cap > L.BN ? L.cap : L.BN;
   L.sort_tiles = (sort_n + kSortTile - 1) / kSortTile;
   if (L.pre_seg && (int64_t)B * seg_tiles > L.sort_tiles) L.sort_tiles = (int64_t)B * seg_tiles;
+  // ALPHA dups are emitted view-major (presorted order), so sorting each view's
+  // dups by the view-local tile id (key - view*T) keeps the views in order: when
+  // that id needs fewer radix passes than (view*T + tile), the tile sort runs
+  // segmented by view (reduce-then-scan; C4: 13 instead of 20 bits, 2 passes)
+  {
+    int tb = 0;
+    while (((int64_t)1 << tb) < L.T) ++tb;
+    const int seg_passes = (tb + kRadixBits - 1) / kRadixBits;
+    L.tile_bound = (L.cap + kSortTile - 1) / kSortTile + B;
+    L.tile_seg = L.alpha && B > 1 && seg_passes < L.passes && L.tile_bound >= sort_rts_tiles();
+    if (L.tile_seg) {
+      L.passes = seg_passes;
+      if (L.tile_bound > L.sort_tiles) L.sort_tiles = L.tile_bound;
+    }
+  }
   L.nblk_scan = (L.BN + kScanTile - 1) / kScanTile;
   if (L.nblk_scan < 1) L.nblk_scan = 1;
   size_t o = 0;
@@ -184,6 +201,9 @@ inline Layout make_layout(const wipes_config& c, int64_t N, int32_t B, int64_t c
     L.sort_loc = take(sizeof(int64_t) * ent);
     L.sort_blk = take(sizeof(int64_t) * ((ent + kScanTile - 1) / kScanTile + 1));
   }
+  L.vseg_off = take(sizeof(int64_t) * (L.tile_seg ? B + 1 : 0));
+  L.vseg_tiles = take(sizeof(int64_t) * (L.tile_seg ? B + 1 : 0));
+  L.vseg_map = take(sizeof(int32_t) * (L.tile_seg ? L.tile_bound : 0));
   L.toff = take(sizeof(int32_t) * (L.BT + 1));
   L.order = take(sizeof(int32_t) * (L.BT + 1));
   L.rgrad = take(sizeof(float) * kMoments * L.BN);
@@ -318,11 +338,23 @@ cudaError_t launch_scan_counts(const Layout& L, char* ws, cudaStream_t s);
 // (one launch; `arrive` a zeroed, self-resetting counter in the header).
 cudaError_t launch_flat_scan(const int32_t* in, int64_t n, int64_t* loc, int64_t* blk,
                              int32_t* arrive, cudaStream_t s);
+// Variable-length sort segments (the view-segmented ALPHA tile sort): segment
+// v holds keys [off[v], off[v+1]) and tiles [tiles[v], tiles[v+1]); map[t] is
+// tile t's segment (nseg past the last); digits come from key - v * T.
+struct VSeg {
+  const int64_t* off;
+  const int64_t* tiles;
+  const int32_t* map;
+  int32_t nseg;
+  uint32_t T;
+  int64_t tile_bound;
+};
 template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
                         cudaStream_t s, uint32_t vdiv = 1, uint32_t vmask = 0,
-                        bool hist_ready = false, int64_t seg_len = 0);
+                        bool hist_ready = false, int64_t seg_len = 0,
+                        const VSeg* vseg = nullptr);
 cudaError_t launch_keys64(const Layout& L, const char* ws, int final_in_b, uint64_t* out,
                           cudaStream_t s);
 cudaError_t launch_offsets_copy(const Layout& L, const char* ws, int64_t* out, cudaStream_t s);
@@ -345,5 +377,7 @@ cudaError_t launch_preprocess3d_bwd(const wipes_config& c, const wipes_params& p
                                     int64_t row1 = -1);
 
 inline int final_buffer_is_b(const Layout& L) { return L.passes & 1; }
+
+
 
 }  // namespace wipes

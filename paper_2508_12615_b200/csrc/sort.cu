@@ -62,26 +62,45 @@ struct SortArgs {
   // (segment, digit, tile), so the flat scan keeps the segments in order.
   // seg_len = 0: one segment of n keys.
   int64_t seg_len, seg_tiles;
+  VSeg vs;  // variable-length segments (vs.map non-null), else unused
 };
 
-// Key range [base, end) of a tile and the count index of its digit d.
-template <typename K>
-__device__ __forceinline__ void tile_span(const SortArgs<K>& a, int64_t tile, int64_t n,
-                                          int64_t& base, int64_t& end) {
-  if (a.seg_len > 0) {
-    const int64_t sg = tile / a.seg_tiles, lt = tile - sg * a.seg_tiles;
-    base = sg * a.seg_len + lt * kSortTile;
+// Key range [base, end) of a tile, its segment (variable segments: nseg for a
+// tile past the last one; else 0) and the count index of its digit d.
+template <typename K, bool VS>
+__device__ __forceinline__ int tile_span(const SortArgs<K>& a, int64_t tile, int64_t n,
+                                         int64_t& base, int64_t& end) {
+  int sg = 0;
+  if constexpr (VS) {
+    sg = a.vs.map[tile];
+    if (sg >= a.vs.nseg) {
+      base = end = 0;
+      return sg;
+    }
+    base = a.vs.off[sg] + (tile - a.vs.tiles[sg]) * kSortTile;
     end = base + kSortTile;
-    const int64_t se = (sg + 1) * a.seg_len;
+    const int64_t se = a.vs.off[sg + 1];
+    if (end > se) end = se;
+  } else if (a.seg_len > 0) {
+    const int64_t g = tile / a.seg_tiles, lt = tile - g * a.seg_tiles;
+    base = g * a.seg_len + lt * kSortTile;
+    end = base + kSortTile;
+    const int64_t se = (g + 1) * a.seg_len;
     if (end > se) end = se;
   } else {
     base = tile * kSortTile;
     end = base + kSortTile;
   }
   if (end > n) end = n;
+  return sg;
 }
-template <typename K>
-__device__ __forceinline__ int64_t count_index(const SortArgs<K>& a, int64_t tile, int d) {
+template <typename K, bool VS>
+__device__ __forceinline__ int64_t count_index(const SortArgs<K>& a, int64_t tile, int d, int sg) {
+  if constexpr (VS) {
+    if (sg >= a.vs.nseg) return tile * 256 + d;  // past the segments: zero counts
+    const int64_t t0 = a.vs.tiles[sg], nt = a.vs.tiles[sg + 1] - t0;
+    return t0 * 256 + (int64_t)d * nt + (tile - t0);
+  }
   if (a.seg_len > 0) {
     const int64_t sg = tile / a.seg_tiles, lt = tile - sg * a.seg_tiles;
     return (sg * 256 + d) * a.seg_tiles + lt;
@@ -225,7 +244,7 @@ __device__ __forceinline__ bool lookback_round(const uint32_t*& sp, int& t,
 // Reduce-then-scan, reduce step: the digit histogram of every tile, written
 // digit-major so one flat exclusive scan turns it into each (digit, tile)'s
 // global output offset (no look-back). Tiles past the data write zeros.
-template <typename K>
+template <typename K, bool VS>
 __global__ void __launch_bounds__(kSortThreads) k_sort_up(SortArgs<K> a) {
   __shared__ uint32_t h[256];
   const int tid = threadIdx.x;
@@ -233,7 +252,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(SortArgs<K> a) {
   h[tid] = 0;  // kSortThreads == 256
   __syncthreads();
   int64_t base, end;
-  tile_span(a, blockIdx.x, n, base, end);
+  const int sg = tile_span<K, VS>(a, blockIdx.x, n, base, end);
+  const K ksub = VS ? (K)sg * (K)a.vs.T : (K)0;  // view-local tile ids
   const bool vp = (a.vmask >> a.pass) & 1u;
   uint32_t dg[kSortItems];
 #pragma unroll
@@ -241,15 +261,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(SortArgs<K> a) {
     const int64_t idx = base + i * kSortThreads + tid;
     dg[i] = 256u;
     if (idx < end)
-      dg[i] = (vp ? (a.vin[idx] / a.vdiv) >> a.shift : (uint32_t)(a.kin[idx] >> a.shift)) & 255u;
+      dg[i] = (vp ? (a.vin[idx] / a.vdiv) >> a.shift : (uint32_t)((a.kin[idx] - ksub) >> a.shift)) &
+              255u;
   }
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) warp_hist_add(h, dg[i]);
   __syncthreads();
-  a.rts_cnt[count_index(a, blockIdx.x, tid)] = h[tid];
+  a.rts_cnt[count_index<K, VS>(a, blockIdx.x, tid, sg)] = h[tid];
 }
 
-template <typename K, bool RTS>
+template <typename K, bool RTS, bool VS>
 __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(SortArgs<K> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
@@ -263,8 +284,9 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   __syncthreads();
   const uint32_t tile = sm.tile;
   int64_t base, end;  // this tile's keys (onesweep: end = min(base + tile, n))
-  tile_span(a, tile, n, base, end);
+  const int sg = tile_span<K, VS>(a, tile, n, base, end);
   if (base >= end) return;  // beyond the data: nobody waits on this tile
+  const K ksub = VS ? (K)sg * (K)a.vs.T : (K)0;  // view-local tile ids
   const int shift = a.shift;
   const bool vp = (a.vmask >> a.pass) & 1u;
   const uint32_t lt = (1u << lane) - 1u;
@@ -293,7 +315,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + (int64_t)wid * (32 * kSortItems) + i * 32 + lane;
-    const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)(key[i] >> shift);
+    const uint32_t src = vp ? (val[i] / a.vdiv) >> shift : (uint32_t)((key[i] - ksub) >> shift);
     dig[i] = idx < end ? (src & 255u) : 256u;
   }
   __syncthreads();
@@ -374,7 +396,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
   }
   if constexpr (RTS) {
     // the scanned digit-major counts give the tile's global digit offsets
-    const int64_t e = count_index(a, tile, d);
+    const int64_t e = count_index<K, VS>(a, tile, d, sg);
     const uint32_t go = (uint32_t)(a.rts_loc[e] + a.rts_blk[e / kScanTile]);
     uint32_t incl_b = cnt;
 #pragma unroll
@@ -476,7 +498,7 @@ __global__ void __launch_bounds__(kSortThreads, WIPES_SORT_MINB) k_sort_pass(Sor
       k = sm.keys[j];
       v = sm.vals[j];
     }
-    const uint32_t dd = (vp ? (v / a.vdiv) >> shift : (uint32_t)(k >> shift)) & 255u;
+    const uint32_t dd = (vp ? (v / a.vdiv) >> shift : (uint32_t)((k - ksub) >> shift)) & 255u;
     const int64_t pos = (int64_t)(uint32_t)(sm.gofs[dd] + (uint32_t)j);
     WCHECK(pos >= 0 && pos < n);
     a.kout[pos] = k;
@@ -490,10 +512,11 @@ template <typename K>
 cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, uint32_t* vB,
                         const int* shifts, int npass, int64_t n_fixed, int64_t cap,
                         cudaStream_t s, uint32_t vdiv, uint32_t vmask, bool hist_ready,
-                        int64_t seg_len) {
+                        int64_t seg_len, const VSeg* vseg) {
   if (npass == 0 || cap == 0) return cudaSuccess;
-  WIPES_SET_SMEM_ONCE((k_sort_pass<K, false>), (int)sizeof(SortSmem<K>));
-  WIPES_SET_SMEM_ONCE((k_sort_pass<K, true>), (int)sizeof(SortSmem<K>));
+  WIPES_SET_SMEM_ONCE((k_sort_pass<K, false, false>), (int)sizeof(SortSmem<K>));
+  WIPES_SET_SMEM_ONCE((k_sort_pass<K, true, false>), (int)sizeof(SortSmem<K>));
+  WIPES_SET_SMEM_ONCE((k_sort_pass<K, true, true>), (int)sizeof(SortSmem<K>));
   SortArgs<K> a;
   a.hdr = (const WsHeader*)(ws + L.hdr);
   a.n_fixed = n_fixed;
@@ -508,13 +531,16 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
   // segmented (n_fixed keys in segments of seg_len): tiles never straddle one
   a.seg_len = seg_len > 0 ? seg_len : 0;
   a.seg_tiles = seg_len > 0 ? (seg_len + kSortTile - 1) / kSortTile : 0;
-  const int64_t tiles = seg_len > 0 ? (n_fixed / seg_len) * a.seg_tiles
-                                    : (cap + kSortTile - 1) / kSortTile;
+  a.vs = vseg ? *vseg : VSeg{nullptr, nullptr, nullptr, 0, 0u, 0};
+  const int64_t tiles = vseg ? vseg->tile_bound
+                             : seg_len > 0 ? (n_fixed / seg_len) * a.seg_tiles
+                                           : (cap + kSortTile - 1) / kSortTile;
   // large sorts: reduce-then-scan passes (no look-back chain across the
   // hundreds of tiles in flight); small ones: onesweep (one launch per pass).
   // Segmented sorts are reduce-then-scan only (Layout::pre_seg).
-  const bool rts = seg_len > 0 || tiles >= sort_rts_tiles();
+  const bool rts = vseg || seg_len > 0 || tiles >= sort_rts_tiles();
   if (seg_len > 0 && (n_fixed % seg_len != 0 || tiles > L.sort_tiles)) return cudaErrorInvalidValue;
+  if (vseg && tiles > L.sort_tiles) return cudaErrorInvalidValue;
   a.tiles = tiles;
   a.rts_cnt = a.status;
   a.rts_loc = (const int64_t*)(ws + L.sort_loc);
@@ -540,13 +566,19 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
     a.shift = shifts[p];
     if (rts) {
       launch_begin(K_RADIX_HIST, s);
-      k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, s>>>(a);
+      if (vseg)
+        k_sort_up<K, true><<<(unsigned)tiles, kSortThreads, 0, s>>>(a);
+      else
+        k_sort_up<K, false><<<(unsigned)tiles, kSortThreads, 0, s>>>(a);
       e = launch_flat_scan((const int32_t*)a.rts_cnt, 256 * tiles, (int64_t*)a.rts_loc,
                            (int64_t*)a.rts_blk, arrive, s);
       launch_end(K_RADIX_HIST, s);
       if (e != cudaSuccess) return e;
       launch_begin(K_RADIX_SCATTER, s);
-      k_sort_pass<K, true><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
+      if (vseg)
+        k_sort_pass<K, true, true><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
+      else
+        k_sort_pass<K, true, false><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
       launch_end(K_RADIX_SCATTER, s);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
@@ -555,7 +587,7 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
     e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * 256 * (size_t)tiles, s);
     if (e != cudaSuccess) return e;
     launch_begin(K_RADIX_SCATTER, s);
-    k_sort_pass<K, false><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
+    k_sort_pass<K, false, false><<<(unsigned)tiles, kSortThreads, sizeof(SortSmem<K>), s>>>(a);
     launch_end(K_RADIX_SCATTER, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -566,11 +598,11 @@ cudaError_t launch_sort(const Layout& L, char* ws, K* kA, uint32_t* vA, K* kB, u
 template cudaError_t launch_sort<uint32_t>(const Layout&, char*, uint32_t*, uint32_t*,
                                            uint32_t*, uint32_t*, const int*, int, int64_t,
                                            int64_t, cudaStream_t, uint32_t, uint32_t, bool,
-                                           int64_t);
+                                           int64_t, const VSeg*);
 template cudaError_t launch_sort<uint64_t>(const Layout&, char*, uint64_t*, uint32_t*,
                                            uint64_t*, uint32_t*, const int*, int, int64_t,
                                            int64_t, cudaStream_t, uint32_t, uint32_t, bool,
-                                           int64_t);
+                                           int64_t, const VSeg*);
 
 size_t sort_smem_bytes64() { return sizeof(SortSmem<uint64_t>); }
 
