@@ -505,6 +505,9 @@ def main():
     if world > 1:
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         dist.init_process_group(backend)
+        # the process group must report every rank the launcher started
+        if dist.get_world_size() != world:
+            raise RuntimeError(f"{backend} reports {dist.get_world_size()} ranks, WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:
@@ -791,6 +794,8 @@ def main():
                     "host_cpus": f"{len(local_cpus)} cores local to GPU {bus}" if local_cpus
                                  else "no NUMA pinning (sysfs unavailable)"},
             "gpu_launches": int(launches), "cuda_graph": True,
+            "process_group": ({"backend": dist.get_backend(), "ranks": dist.get_world_size()}
+                              if world > 1 else None),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
             "roofline": roof,
             "hbm_kernels": hbm_fractions(
