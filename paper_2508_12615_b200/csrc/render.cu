@@ -610,6 +610,74 @@ __device__ __forceinline__ mom_t transpose_reduce12(mom_t (&v)[kMom], int lane) 
   return v[0] + __shfl_xor_sync(kFull, v[0], 1);
 }
 
+// Column-first reduction of a lane's 8 dx-free moment sums (m0, m2, m5, m6, m8,
+// c0, c1, c2): lanes l ^ 8 and l ^ 16 hold the same pixel column (lane & 7, one
+// dx), so the first two transposing levels sum each column's 8 values over its 4
+// lanes, the dx products are formed once per column on the column sums
+// (M1 = M0 dx, M3 = M1 dx, M4 = M2 dx, M7 = M6 dx: exact factorisations, as in
+// finish_moments), and three more levels sum the 8 columns. 10 SHFL, 18 FSEL,
+// 10 FADD and 2 FMUL per record instead of finish_moments + transpose_reduce12's
+// 4 FMUL, 13 SHFL, 24 FSEL and 13 FADD. After the reduction lane l holds the
+// moment col_first_moment(l) (kMom for a pad slot).
+__device__ __forceinline__ int col_first_moment(int lane) {
+  // group (b4, b3) -> its four outputs o0..o3 (o = 2 b2 + b1), one nibble each:
+  // (0,0): M0 M9 M1 M3 | (0,1): M2 M5 M4 - | (1,0): M6 M8 M7 - | (1,1): M10 M11 - -
+  static_assert(kMoments == 12, "nibble table");
+  const int idx = ((lane >> 3) & 3) * 4 + ((lane >> 1) & 3);
+  return (int)((0xccbac786c4523190ull >> (4 * idx)) & 0xfull);
+}
+template <typename mom_t>
+__device__ __forceinline__ mom_t col_first_reduce(const mom_t (&m)[9], const mom_t (&mc)[3],
+                                                  float dx, int lane) {
+  // level A (xor 16): b4 = 0 keeps {m0, c0, m2, m5}, b4 = 1 keeps {m6, m8, c1, c2}
+  const mom_t s0[4] = {m[0], mc[0], m[2], m[5]};
+  const mom_t s1[4] = {m[6], m[8], mc[1], mc[2]};
+  mom_t t[4];
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const mom_t send = up ? s0[j] : s1[j];
+      const mom_t keep = up ? s1[j] : s0[j];
+      t[j] = keep + __shfl_xor_sync(kFull, send, 16);
+    }
+  }
+  // level B (xor 8): b3 = 0 keeps t0, t1; b3 = 1 keeps t2, t3 -> column sums
+  // (0,0): (M0, M9), (0,1): (M2, M5), (1,0): (M6, M8), (1,1): (M10, M11)
+  mom_t o[4];
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const mom_t send = up ? t[j] : t[j + 2];
+      const mom_t keep = up ? t[j + 2] : t[j];
+      o[j] = keep + __shfl_xor_sync(kFull, send, 8);
+    }
+  }
+  const mom_t d = (mom_t)dx;
+  o[2] = o[0] * d;  // M1 | M4 | M7 | pad
+  o[3] = o[2] * d;  // M3 | pad ...
+  {  // level C (xor 4): b2 = 0 keeps o0, o1; b2 = 1 keeps o2, o3
+    const bool up = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const mom_t send = up ? o[j] : o[j + 2];
+      const mom_t keep = up ? o[j + 2] : o[j];
+      o[j] = keep + __shfl_xor_sync(kFull, send, 4);
+    }
+  }
+  {  // level D (xor 2)
+    const bool up = lane & 2;
+    const mom_t send = up ? o[0] : o[1];
+    const mom_t keep = up ? o[1] : o[0];
+    o[0] = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  return o[0] + __shfl_xor_sync(kFull, o[0], 1);
+}
+
+#ifndef WIPES_COLFIRST
+#define WIPES_COLFIRST 1  // column-first moment reduction (0: finish_moments + transpose_reduce12)
+#endif
 #ifndef WIPES_SMEM_REDUCE
 #define WIPES_SMEM_REDUCE 0  // A/B knob: measured slower (C2 bwd 0.126 vs 0.114 ms, C5 3.07 vs 2.55)
 #endif
@@ -703,20 +771,21 @@ __device__ __forceinline__ void bwd_pixel(bool h, float e, float dx, float dy,
                                           const float4& r3, const float (&g)[3], float amin,
                                           float amax, float& T, float& sdg,
                                           typename MomT<F64>::T (&m)[9], float (&mc)[3],
-                                          float& mb, bool& any) {
+                                          float& mb, float& any) {
   const float ag = ex2(e);
   const float th = pair_theta(r2, dx, dy);
   const float cs = cos_a(th), sn = sin_a(th);
   const float w = pair_weight(ag, cs, r2);
   const bool ok = h && w >= amin;
-  any = any || ok;
   const float gdc = __fmaf_rn(r3.x, g[0], __fmaf_rn(r3.y, g[1], __fmul_rn(r3.z, g[2])));
   if (!ALPHA) {
     const float we = ok ? w : 0.f;
+    any += we;  // > 0 iff some pair contributed (w >= alpha_min > 0): one FADD, no bool
     add_moments<F64>(m, mc, ok ? gdc : 0.f, we, ag, sn, dym, we * g[0], we * g[1], we * g[2]);
     if (EXACT) mb = __fmaf_rn(ok ? gdc * ag : 0.f, cs, mb);
   } else {
     const float al = ok ? fminf(amax, w) : 0.f;
+    any += al;
     const float ri = rcp_a(1.f - al);  // exactly 1 when al = 0
     const float Tk = T * ri;
     const float dLda = __fmaf_rn(Tk, gdc, -sdg * ri);
@@ -749,26 +818,27 @@ __device__ __forceinline__ void bwd_pair(bool h0, bool h1, float e0, float e1, f
                                          float2 dy, const float4& r2, const float4& r3,
                                          const float2 (&g)[3], float amin, float amax,
                                          float2& T, float2& sdg, MomPack& m, float& mb,
-                                         bool& any) {
+                                         float& any) {
   const float2 ag = make_float2(ex2(e0), ex2(e1));
   const float2 th = __ffma2_rn(f2(r2.x), f2(dx), __ffma2_rn(f2(r2.y), dy, f2(r2.z)));
   const float2 cs = make_float2(cos_a(th.x), cos_a(th.y));
   const float2 sn = make_float2(sin_a(th.x), sin_a(th.y));
   const float2 w = __fmul2_rn(ag, __ffma2_rn(f2(r2.w), cs, f2(0.5f)));
   const bool ok0 = h0 && w.x >= amin, ok1 = h1 && w.y >= amin;
-  any = any || ok0 || ok1;
   const float2 gdc = __ffma2_rn(f2(r3.x), g[0], __ffma2_rn(f2(r3.y), g[1], __fmul2_rn(f2(r3.z), g[2])));
   float2 gw, wm, cw;
   if (!ALPHA) {
     wm = make_float2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
     gw = make_float2(ok0 ? gdc.x : 0.f, ok1 ? gdc.y : 0.f);
     cw = wm;
+    any += wm.x + wm.y;
     if (EXACT) {
       mb = __fmaf_rn(gw.x * ag.x, cs.x, mb);
       mb = __fmaf_rn(gw.y * ag.y, cs.y, mb);
     }
   } else {
     const float2 al = make_float2(ok0 ? fminf(amax, w.x) : 0.f, ok1 ? fminf(amax, w.y) : 0.f);
+    any += al.x + al.y;
     const float2 ri = make_float2(rcp_a(1.f - al.x), rcp_a(1.f - al.y));  // 1 when al = 0
     const float2 Tk = __fmul2_rn(T, ri);
     const float2 dLda = __ffma2_rn(Tk, gdc, __fmul2_rn(make_float2(-sdg.x, -sdg.y), ri));
@@ -809,9 +879,13 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
   WarpSmemB& ws = sm_all[wid];
   // which moment this lane holds after the warp reduction (and writes out)
   constexpr bool SMRED = !F64 && WIPES_SMEM_REDUCE;
+  constexpr bool COLF = !SMRED && WIPES_COLFIRST;
   const int q3 = (lane >> 1) & 3;
-  const int my_m = SMRED ? (lane >> 1) : 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3;
-  const bool writer = SMRED ? (!(lane & 1) && lane < 2 * kMom) : (!(lane & 1) && q3 < 3);
+  const int my_m = SMRED ? (lane >> 1)
+                         : (COLF ? col_first_moment(lane)
+                                 : 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + q3);
+  const bool writer = SMRED ? (!(lane & 1) && lane < 2 * kMom)
+                            : (COLF ? (!(lane & 1) && my_m < kMom) : (!(lane & 1) && q3 < 3));
   // the moment this lane writes, kMom if none, held in a register the compiler
   // cannot rematerialise (it recomputed the lane arithmetic for every record)
   int wm;
@@ -906,7 +980,7 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
         float mc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < 9; ++k) m[k] = 0;
-        bool any = false;
+        float any = 0.f;  // sum of the contributing pairs' weights (> 0 iff any)
         float mb = 0.f;
         if constexpr (PACKB) {
           MomPack mp;
@@ -937,15 +1011,20 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
                                            r2, r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p],
                                            m, mc, mb, any);
         }
-        if (!__any_sync(kFull, any)) continue;
+        if (!__any_sync(kFull, any > 0.f)) continue;
         BCNT(3, 1);
-        MT mr[kMom];
-        finish_moments<F64>(mr, m, mc, dx);
         float red;
-        if constexpr (SMRED) {
-          red = smem_reduce12(mr, ws.red4, lane);
+        if constexpr (COLF) {
+          const MT mcm[3] = {(MT)mc[0], (MT)mc[1], (MT)mc[2]};
+          red = (float)col_first_reduce<MT>(m, mcm, dx, lane);
         } else {
-          red = (float)transpose_reduce12(mr, lane);
+          MT mr[kMom];
+          finish_moments<F64>(mr, m, mc, dx);
+          if constexpr (SMRED) {
+            red = smem_reduce12(mr, ws.red4, lane);
+          } else {
+            red = (float)transpose_reduce12(mr, lane);
+          }
         }
         if (EXACT) {
 #pragma unroll

@@ -1,7 +1,7 @@
 #!/bin/bash
 # quick check: build, render parity tests, C2/C3 bench kernel times (experiment helper)
 python paper_2508_12615_b200/build.py > /dev/null || exit 1
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_train.py -x -q 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_train.py -x -q 2>&1 | grep -E "^(FAILED|E |>|tests/|[0-9]+ (passed|failed))|Error|assert" | head -40
 for c in "$@"; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-fit --no-mlp > gpurun_out/q_$c.json 2>/dev/null
   tail -1 gpurun_out/q_$c.json | python -c "
