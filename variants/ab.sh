@@ -2,7 +2,7 @@
 # A/B of library variants on C2/C3/C5 (experiment helper): bash variants/ab.sh base v1 v2 ...
 for v in "$@"; do
   if [ "$v" = "base" ]; then unset WIPES_LIB; else export WIPES_LIB=$PWD/variants/$v.so; fi
-  for c in c2 c3 c5; do
+  for c in ${AB_CFGS:-c2 c3 c5}; do
     timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-fit --no-mlp 2>/dev/null | tail -1 | python -c "
 import json,sys
 try:
