@@ -386,9 +386,15 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, WsHea
   if (!is_last) return;
   __threadfence();
   if (tid < kBuckets) h[tid] = 0;
+  // the whole CSR array into shared memory first: every load in flight at once
+  // (the two passes below then read shared memory instead of two dependent L2
+  // round trips per iteration)
+  __shared__ int32_t s_toff[WIPES_ORDER_FUSE_MAX + 1];
+#pragma unroll 8
+  for (int u = tid; u <= (int)BT; u += 256) s_toff[u] = __ldcg(toff + u);
   __syncthreads();
-  for (int64_t u = tid; u < BT; u += blockDim.x) {
-    const int len = __ldcg(toff + u + 1) - __ldcg(toff + u);
+  for (int u = tid; u < (int)BT; u += 256) {
+    const int len = s_toff[u + 1] - s_toff[u];
     atomicAdd(&h[len > 0 ? 32 - __clz(len) : 0], 1);
   }
   __syncthreads();
@@ -398,8 +404,8 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, WsHea
     base[tid] = off;
   }
   __syncthreads();
-  for (int64_t u = tid; u < BT; u += blockDim.x) {
-    const int len = __ldcg(toff + u + 1) - __ldcg(toff + u);
+  for (int u = tid; u < (int)BT; u += 256) {
+    const int len = s_toff[u + 1] - s_toff[u];
     order[atomicAdd(&base[len > 0 ? 32 - __clz(len) : 0], 1)] = (int32_t)u;
   }
   if (tid == 0) hdr->arrive[2] = 0;  // self-resetting (bin_sort may run again)
