@@ -57,8 +57,9 @@ def parse():
     ap.add_argument("--c3-steps", type=int, default=5)
     ap.add_argument("--grad-chunks", type=int, default=4,
                     help="N > 1: parameter-row buckets of the overlapped gradient all_reduce")
-    ap.add_argument("--e2e-sets", type=int, default=2,
-                    help="device buffer sets the pipelined e2e loop rotates through")
+    ap.add_argument("--e2e-sets", type=int, default=None,
+                    help="device buffer sets the pipelined e2e loop rotates through "
+                         "(default 3, or 2 when a step moves >= 1 GB: C4)")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-fit", action="store_true",
@@ -338,6 +339,40 @@ def mlp_rate(args, flush, dev, peaks, precision="bf16x3"):
             "compulsory_bytes_per_row": 4 * (3 + 4 + 3 + 3) * 2}
 
 
+def host_link(hp, hdl, hg, dp, ddl, dg, s_up, s_down, e2e_ms, reps=10):
+    """The lease's host copy path, measured on the e2e buffers: the step's
+    uploads alone, its download alone, and both directions together (their
+    own streams, as in the e2e pipeline). Context for `e2e`: a step cannot
+    finish faster than its copies, and the copy rate differs between leases."""
+    import torch
+
+    def timed(up, down):
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s_up)
+        b0.record(s_down)
+        for _ in range(reps):
+            if up:
+                with torch.cuda.stream(s_up):
+                    dp.copy_(hp, non_blocking=True)
+                    ddl.copy_(hdl, non_blocking=True)
+            if down:
+                with torch.cuda.stream(s_down):
+                    hg.copy_(dg, non_blocking=True)
+        a1.record(s_up)
+        b1.record(s_down)
+        torch.cuda.synchronize()
+        return max(a0.elapsed_time(a1) if up else 0.0, b0.elapsed_time(b1) if down else 0.0) / reps
+    up_b = (hp.numel() + hdl.numel()) * 4
+    dn_b = hg.numel() * 4
+    t_up, t_dn, t_both = timed(True, False), timed(False, True), timed(True, True)
+    return {"h2d_GBps": up_b / t_up / 1e6, "d2h_GBps": dn_b / t_dn / 1e6,
+            "both_ms_per_step": t_both, "e2e_ms_per_step": e2e_ms,
+            "note": "the step's uploads and download alone and together on this lease; "
+                    "e2e per step >= both_ms_per_step"}
+
+
 def sharding(name, world, args):
     """(rows, frames, shared) of a config at this world size."""
     from paper_2508_12615_b200 import gen
@@ -514,7 +549,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    from paper_2508_12615_b200 import abi, build, gen
+    from paper_2508_12615_b200 import abi, build, gen, hostmem
     from paper_2508_12615_b200.raster import FrameGraph, Rasterizer
     from paper_2508_12615_b200 import dist as wdist
     if rank == 0:
@@ -655,9 +690,12 @@ def main():
     saved_aff = os.sched_getaffinity(0)
     if local_cpus:
         os.sched_setaffinity(0, local_cpus)
-    host_params = {k: torch.from_numpy(v).pin_memory() for k, v in c["params"].items()}
-    host_dL = torch.from_numpy(dL_host).pin_memory()
-    host_grads = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in grads.items()}
+    # page-locked in place after a first touch on this thread (hostmem.py: torch's
+    # pin_memory() buffers uploaded at 10-21 GB/s on some leases, these at ~53)
+    host_params = {k: torch.from_numpy(v) for k, v in c["params"].items()}
+    host_dL = hostmem.pinned_empty(dL_host.shape)
+    host_dL.copy_(torch.from_numpy(dL_host))
+    host_grads = {k: torch.empty(v.shape, dtype=torch.float32) for k, v in grads.items()}
     h2d = sum(v.numel() * 4 for v in host_params.values()) + host_dL.numel() * 4
     d2h = sum(v.numel() * 4 for v in host_grads.values())
     n_e2e = max(50, args.steps)  # at least 50 pipelined steps: host enqueue jitter averages out
@@ -674,9 +712,8 @@ def main():
         for k, n in sizes.items():
             offs[k] = o
             o += (n + 3) // 4 * 4  # 16-byte aligned groups
-        buf = torch.zeros(o, dtype=torch.float32, device=device)
-        if pin:
-            buf = buf.pin_memory()
+        buf = (hostmem.pinned_empty((o,)) if pin
+               else torch.zeros(o, dtype=torch.float32, device=device))
         return buf, {k: buf[offs[k]:offs[k] + sizes[k]].view(shapes[k]) for k in shapes}
 
     pshapes = {k: tuple(v.shape) for k, v in host_params.items()}
@@ -685,7 +722,9 @@ def main():
     for kk, v in host_params.items():
         hp[kk].copy_(v)
     sets, gflats = [], []
-    nsets = max(2, args.e2e_sets)
+    # three sets: step k+1's upload no longer waits for step k-1's download
+    # (C5 e2e 180 -> 219 iters/s; C2/C3 unchanged); two for C4's 3.7 GB steps
+    nsets = max(2, args.e2e_sets if args.e2e_sets else (3 if h2d < 1e9 else 2))
     for _ in range(nsets):
         pflat, pv = flat_views(pshapes, dev)
         pflat.copy_(host_pflat)
@@ -728,7 +767,15 @@ def main():
                 done[b].record(s_back)
         s_copy.wait_stream(s_back)
 
-    pipeline(max(3, args.warmup))  # untimed: first-touch costs of the copy path
+    # untimed warm-up of the copy path, at least 0.1 s of it: right after the
+    # device-only phases the first uploads ran at ~21 GB/s and only then at ~50
+    # (tools/h2d_probe.py: 20 x 7.8 MB at 20.8 GB/s, the next 20 at 49.2 GB/s)
+    # (a step count, not a deadline, so every rank issues the same collectives)
+    est_ms = max(ms_per_step, h2d / 20e6)  # the step, or its upload at the slow rate
+    n_w = torch.tensor([max(3, args.warmup, math.ceil(100.0 / est_ms))], device=dev)
+    if world > 1:
+        dist.all_reduce(n_w, op=dist.ReduceOp.MAX)
+    pipeline(int(n_w.item()))
     torch.cuda.synchronize()
     flush.zero_()
     torch.cuda.synchronize()
@@ -745,6 +792,8 @@ def main():
     e2e_mode = ("pipelined: step k+1's inputs uploaded (H2D stream) and step k-1's "
                 "gradients downloaded (D2H stream) while step k computes"
                 + (" (its gradient all_reduce on the compute stream)" if exchange else ""))
+    link = host_link(host_pflat, host_dL, host_g[0], sets[0][0], sets[0][1], gflats[0],
+                     s_copy, s_back, e2e_total / n_e2e)
     os.sched_setaffinity(0, saved_aff)
     te = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
     if world > 1:
@@ -790,7 +839,7 @@ def main():
             "render_fps": render_fps,
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "mode": e2e_mode,
+                    "d2h_bytes_per_step": d2h, "mode": e2e_mode, "host_link": link,
                     "host_cpus": f"{len(local_cpus)} cores local to GPU {bus}" if local_cpus
                                  else "no NUMA pinning (sysfs unavailable)"},
             "gpu_launches": int(launches), "cuda_graph": True,
