@@ -58,8 +58,7 @@ def parse():
     ap.add_argument("--grad-chunks", type=int, default=4,
                     help="N > 1: parameter-row buckets of the overlapped gradient all_reduce")
     ap.add_argument("--e2e-sets", type=int, default=None,
-                    help="device buffer sets the pipelined e2e loop rotates through "
-                         "(default 3, or 2 when a step moves >= 1 GB: C4)")
+                    help="device buffer sets the pipelined e2e loop rotates through (default 3)")
     ap.add_argument("--cpu-pixels", type=int, default=65536)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-fit", action="store_true",
@@ -723,8 +722,8 @@ def main():
         hp[kk].copy_(v)
     sets, gflats = [], []
     # three sets: step k+1's upload no longer waits for step k-1's download
-    # (C5 e2e 180 -> 219 iters/s; C2/C3 unchanged); two for C4's 3.7 GB steps
-    nsets = max(2, args.e2e_sets if args.e2e_sets else (3 if h2d < 1e9 else 2))
+    # (C5 e2e 180 -> 219 iters/s, C4 11.3 -> 14.1; C2/C3 unchanged)
+    nsets = max(2, args.e2e_sets or 3)
     for _ in range(nsets):
         pflat, pv = flat_views(pshapes, dev)
         pflat.copy_(host_pflat)
