@@ -27,6 +27,7 @@
 #include <cuda_fp16.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -43,7 +44,7 @@ constexpr int kMom = kMoments;  // 12
 #define WIPES_MINB_FWD_ALPHA 8  // ... forward, ALPHA
 #endif
 #ifndef WIPES_MINB_BWD
-#define WIPES_MINB_BWD 6  // ... backward, SUM (C2 best at 80 registers)
+#define WIPES_MINB_BWD 7  // ... backward, SUM (72 registers with dL/dC in shared memory)
 #endif
 #ifndef WIPES_MINB_BWD_ALPHA
 #define WIPES_MINB_BWD_ALPHA 7  // ... backward, ALPHA (72 registers: C3 -6% against 6)
@@ -242,6 +243,17 @@ struct WarpSmem {
 // Backward: the staging area plus the warp's moment-reduction buffer.
 struct WarpSmemB : WarpSmem {
   float4 red4[12 * 32 / 4];  // [moment][lane] (16-byte aligned for LDS.128)
+};
+// SUM backward: each lane's dL/dC values live in warp-private shared memory
+// (lane-private slots: written and read by the same lane, no barrier) instead
+// of 12 registers, which lets the kernel run 7 CTAs/SM without spills (C2 bwd
+// 0.1037 -> 0.1028 ms, C5 2.268 -> 2.205 ms); the ALPHA backward measured
+// slower this way (C3 4.61 -> 4.77 ms, also at 8 CTAs/SM) and keeps registers.
+#ifndef WIPES_BWD_GSMEM
+#define WIPES_BWD_GSMEM 1
+#endif
+struct WarpSmemBG : WarpSmemB {
+  float4 g4[4][32];  // [pixel][lane] (dL/dC r, g, b, -)
 };
 
 // One work item of a warp.
@@ -874,9 +886,11 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
   using Gm = Geo<TS>;
   constexpr int G = Gm::G, P = Gm::P;
   constexpr bool PACKB = !F64 && WIPES_BWD_PACK;
-  __shared__ WarpSmemB sm_all[kWarpsPerCta];
+  constexpr bool GSM = !ALPHA && WIPES_BWD_GSMEM;
+  using WS = std::conditional_t<GSM, WarpSmemBG, WarpSmemB>;
+  __shared__ WS sm_all[kWarpsPerCta];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  WarpSmemB& ws = sm_all[wid];
+  WS& ws = sm_all[wid];
   // which moment this lane holds after the warp reduction (and writes out)
   constexpr bool SMRED = !F64 && WIPES_SMEM_REDUCE;
   constexpr bool COLF = !SMRED && WIPES_COLFIRST;
@@ -917,6 +931,7 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
           ml = max(ml, last[p]);
         }
       }
+      if constexpr (GSM) ws.g4[p][lane] = make_float4(g[p][0], g[p][1], g[p][2], 0.f);
     }
     // packed per-pair state of the FP32 path (pair gg = pixels 2gg, 2gg + 1)
     float2 g2[G][3], T2[G], sdg2[G];
@@ -1004,12 +1019,20 @@ __global__ void __launch_bounds__(kCta, F64 ? WIPES_MINB_BWD_F64
           const MT dy0m = (MT)dy[0];
 #pragma unroll
           for (int p = 0; p < P; ++p)
-            if (bm[p])
+            if (bm[p]) {
+              float gl[3];
+              if constexpr (GSM) {
+                const float4 gv = ws.g4[p][lane];
+                gl[0] = gv.x; gl[1] = gv.y; gl[2] = gv.z;
+              } else {
+                gl[0] = g[p][0]; gl[1] = g[p][1]; gl[2] = g[p][2];
+              }
               bwd_pixel<ALPHA, EXACT, F64>(h[p], e[p], dx, dy[p],
                                            F64 ? dy0m + (MT)(8 * (p >> 1) + 4 * (p & 1))
                                                : (MT)dy[p],
-                                           r2, r3, g[p], a.alpha_min, a.alpha_max, T[p], sdg[p],
+                                           r2, r3, gl, a.alpha_min, a.alpha_max, T[p], sdg[p],
                                            m, mc, mb, any);
+            }
         }
         if (!__any_sync(kFull, any > 0.f)) continue;
         BCNT(3, 1);
